@@ -1,0 +1,453 @@
+"""Python mirror of the reference `anisoq` hot-path API over the C ABI.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/include/anisoq (pq.hpp, index.hpp, geometry.hpp,
+error.hpp); every call runs on the B200 through libanisoq_b200.so. Types are
+thin numpy holders with the reference's field names:
+
+    Dataset(values n x d, norms)            dataset.hpp:41-51
+    ProductCodebook(M, k, sub_dimension, dictionaries)   pq.hpp:39-52
+    CodeMatrix(n, M, k, codes n x M uint32)  pq.hpp:55-67
+    AnisotropicWeights(h_parallel, h_perpendicular)      geometry.hpp:119-145
+    TrainConfig                              vq.hpp:55-69
+    Hit / SearchResult                       index.hpp:46-54
+
+Per-point weights may be given as a list/array of AnisotropicWeights (the
+reference's std::span<const AnisotropicWeights>), as a single
+AnisotropicWeights (uniform), or as ThresholdWeights(T) (the CLI's
+resolve_weights, anisoq_main.cpp:108-142, computed on the device).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+
+_L = _lib.load()
+
+# ---- errors (error.hpp:25-55) ---------------------------------------------
+
+
+class Error(RuntimeError):
+    """anisoq::Error; `error_class` is "validation" or "runtime"."""
+
+    status = 0
+
+    def __init__(self, what: str):
+        super().__init__(what)
+        self.error_class = "runtime" if _L.aq_error_class(self.status) else "validation"
+
+
+def _mk(name, status):
+    return type(name, (Error,), {"status": status})
+
+
+InvalidArgument = _mk("InvalidArgument", 1)
+ZeroNormDatapoint = _mk("ZeroNormDatapoint", 2)
+InvalidThreshold = _mk("InvalidThreshold", 3)
+EmptyDataset = _mk("EmptyDataset", 4)
+EmptyIndex = _mk("EmptyIndex", 5)
+DimensionMismatch = _mk("DimensionMismatch", 6)
+DimensionNotDivisible = _mk("DimensionNotDivisible", 7)
+CodeOutOfRange = _mk("CodeOutOfRange", 8)
+MalformedFile = _mk("MalformedFile", 9)
+InsufficientData = _mk("InsufficientData", 10)
+GroundTruthMismatch = _mk("GroundTruthMismatch", 11)
+QuadratureFailure = _mk("QuadratureFailure", 12)
+SingularSystem = _mk("SingularSystem", 13)
+DeviceError = _mk("DeviceError", 100)
+Unsupported = _mk("Unsupported", 101)
+
+_BY_STATUS = {c.status: c for c in (
+    InvalidArgument, ZeroNormDatapoint, InvalidThreshold, EmptyDataset, EmptyIndex,
+    DimensionMismatch, DimensionNotDivisible, CodeOutOfRange, MalformedFile,
+    InsufficientData, GroundTruthMismatch, QuadratureFailure, SingularSystem,
+    DeviceError, Unsupported)}
+
+
+def _check(st: int) -> None:
+    if st:
+        raise _BY_STATUS.get(st, Error)(_L.aq_last_error().decode())
+
+
+# ---- types -----------------------------------------------------------------
+
+
+@dataclass
+class AnisotropicWeights:
+    h_parallel: float = 1.0
+    h_perpendicular: float = 1.0
+
+    @property
+    def eta(self) -> float:
+        return (self.h_parallel / self.h_perpendicular if self.h_perpendicular > 0
+                else math.inf)
+
+    def is_isotropic(self) -> bool:
+        return self.h_parallel == self.h_perpendicular
+
+    @staticmethod
+    def from_h(h_parallel: float, h_perpendicular: float) -> "AnisotropicWeights":
+        if not (h_parallel >= 0.0 and h_perpendicular >= 0.0 and math.isfinite(h_parallel)
+                and math.isfinite(h_perpendicular)):
+            raise InvalidArgument("InvalidArgument: h coefficients must be finite and >= 0")
+        return AnisotropicWeights(float(h_parallel), float(h_perpendicular))
+
+    @staticmethod
+    def from_eta(eta: float) -> "AnisotropicWeights":
+        if not eta >= 0.0:
+            raise InvalidArgument("InvalidArgument: eta must be >= 0")
+        return AnisotropicWeights.from_h(eta, 1.0)
+
+    @staticmethod
+    def isotropic(h: float = 1.0) -> "AnisotropicWeights":
+        return AnisotropicWeights.from_h(h, h)
+
+
+@dataclass
+class ThresholdWeights:
+    """h_par = eta_limit(T, |x_i|, d), h_perp = 1 per point (geometry.hpp:395-402).
+
+    policy "throw" reproduces the reference (InvalidThreshold when |x_i| <= T);
+    "parallel_only" uses eta = inf -> (h_par, h_perp) = (1, 0)."""
+
+    threshold: float = 0.2
+    policy: str = "throw"
+
+
+def eta_limit(threshold: float, norm: float, d: int) -> float:
+    """geometry.hpp:395-402 (host scalar helper)."""
+    if not norm > 0.0:
+        raise InvalidArgument("InvalidArgument: norm must be positive")
+    if not threshold >= 0.0 or threshold >= norm:
+        raise InvalidThreshold("InvalidThreshold: need 0 <= T < norm")
+    if d < 2:
+        raise InvalidArgument("InvalidArgument: eta_limit needs d >= 2")
+    rho = (threshold / norm) * (threshold / norm)
+    return float(d - 1) * rho / (1.0 - rho)
+
+
+@dataclass
+class Dataset:
+    values: np.ndarray  # n x d, float32-exact
+    normalized: bool = False
+
+    def __post_init__(self):
+        v = np.asarray(self.values)
+        if v.ndim != 2:
+            raise InvalidArgument("InvalidArgument: dataset must be n x d")
+        if v.dtype != np.float32:
+            f = v.astype(np.float32)
+            if not np.array_equal(f.astype(np.float64), np.asarray(v, np.float64)):
+                raise Unsupported("Unsupported: device datasets hold float32-exact values "
+                                  "(fvecs / generate_synthetic data are; dataset.hpp:146-151)")
+            v = f
+        self.values = np.ascontiguousarray(v, dtype=np.float32)
+
+    @property
+    def n(self) -> int:
+        return self.values.shape[0]
+
+    @property
+    def d(self) -> int:
+        return self.values.shape[1]
+
+    def row(self, i: int) -> np.ndarray:
+        return self.values[i].astype(np.float64)
+
+
+@dataclass
+class ProductCodebook:
+    M: int = 0
+    k: int = 0
+    sub_dimension: int = 0
+    dictionaries: np.ndarray = field(default_factory=lambda: np.zeros(0))
+
+    def __post_init__(self):
+        self.dictionaries = np.ascontiguousarray(self.dictionaries, dtype=np.float64).ravel()
+
+    def dim(self) -> int:
+        return self.M * self.sub_dimension
+
+    def codeword(self, m: int, j: int) -> np.ndarray:
+        o = (m * self.k + j) * self.sub_dimension
+        return self.dictionaries[o:o + self.sub_dimension]
+
+
+@dataclass
+class CodeMatrix:
+    n: int = 0
+    M: int = 0
+    k: int = 0
+    codes: np.ndarray = field(default_factory=lambda: np.zeros((0, 0), np.uint32))
+
+    def __post_init__(self):
+        self.codes = np.ascontiguousarray(self.codes, dtype=np.uint32).reshape(self.n, self.M)
+
+    def row(self, i: int) -> np.ndarray:
+        return self.codes[i]
+
+
+@dataclass
+class TrainConfig:
+    max_iterations: int = 100
+    relative_tolerance: float = 1e-6
+    seed: int = 0
+    empty_partition_policy: str = "reseed_highest_loss"
+    ridge: float = -1.0
+    threads: int = 1
+    sweep_to_fixed_point: bool = False
+
+    def c(self) -> _lib.aq_train_config:
+        return _lib.aq_train_config(
+            self.max_iterations, self.relative_tolerance, self.seed,
+            0 if self.empty_partition_policy == "reseed_highest_loss" else 1,
+            self.ridge, self.threads, int(self.sweep_to_fixed_point))
+
+
+@dataclass
+class Hit:
+    index: int
+    score: float
+
+
+@dataclass
+class SearchResult:
+    hits: list
+
+
+@dataclass
+class LookupTable:
+    M: int
+    k: int
+    partials: np.ndarray
+
+    def at(self, m: int, j: int) -> float:
+        return float(self.partials[m * self.k + j])
+
+
+# ---- session -----------------------------------------------------------------
+
+
+class Session:
+    """One CUDA device + stream; owns device-resident objects."""
+
+    _default: dict[int, "Session"] = {}
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        _check(_L.aq_session_create(device, C.byref(h)))
+        self.h = h
+        self.device = device
+
+    @classmethod
+    def default(cls, device: int = 0) -> "Session":
+        if device not in cls._default:
+            cls._default[device] = Session(device)
+        return cls._default[device]
+
+    @property
+    def stream(self) -> int:
+        return _L.aq_session_stream(self.h) or 0
+
+    def sync(self) -> None:
+        _check(_L.aq_session_sync(self.h))
+
+    @property
+    def launches(self) -> int:
+        return int(_L.aq_session_launches(self.h))
+
+    def close(self) -> None:
+        if self.h:
+            _L.aq_session_destroy(self.h)
+            self.h = None
+
+    # device-resident objects
+    def upload_dataset(self, values: np.ndarray) -> "DeviceDataset":
+        ds = values if isinstance(values, Dataset) else Dataset(values)
+        h = C.c_void_p()
+        _check(_L.aq_dataset_upload(self.h, ds.values.ctypes.data, ds.n, ds.d, C.byref(h)))
+        return DeviceDataset(self, h, ds.n, ds.d)
+
+    def wrap_device_rows(self, ptr: int, n: int, d: int) -> "DeviceDataset":
+        h = C.c_void_p()
+        _check(_L.aq_dataset_wrap_device(self.h, ptr, n, d, C.byref(h)))
+        return DeviceDataset(self, h, n, d)
+
+    def upload_codebook(self, cb: ProductCodebook) -> "DeviceCodebook":
+        h = C.c_void_p()
+        _check(_L.aq_codebook_upload(self.h, cb.dictionaries.ctypes.data, cb.M, cb.k,
+                                     cb.sub_dimension, C.byref(h)))
+        return DeviceCodebook(self, h, cb.M, cb.k, cb.sub_dimension)
+
+    def alloc_codes(self, n: int, M: int, k: int) -> "DeviceCodes":
+        h = C.c_void_p()
+        _check(_L.aq_codes_alloc(self.h, n, M, k, C.byref(h)))
+        return DeviceCodes(self, h, n, M, k)
+
+    def upload_codes(self, cm: CodeMatrix) -> "DeviceCodes":
+        h = C.c_void_p()
+        _check(_L.aq_codes_upload(self.h, cm.codes.ctypes.data, cm.n, cm.M, cm.k, C.byref(h)))
+        return DeviceCodes(self, h, cm.n, cm.M, cm.k)
+
+    def upload_packed_codes(self, packed: np.ndarray, n: int, M: int, k: int) -> "DeviceCodes":
+        packed = np.ascontiguousarray(packed, np.uint8)
+        h = C.c_void_p()
+        _check(_L.aq_codes_upload_packed(self.h, packed.ctypes.data, n, M, k, C.byref(h)))
+        return DeviceCodes(self, h, n, M, k)
+
+
+class _Handle:
+    _free = None
+
+    def free(self):
+        if getattr(self, "h", None):
+            getattr(_L, self._free)(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class DeviceDataset(_Handle):
+    _free = "aq_dataset_free"
+
+    def __init__(self, s, h, n, d):
+        self.s, self.h, self.n, self.d = s, h, n, d
+
+    def norms(self) -> np.ndarray:
+        out = np.zeros(self.n, np.float64)
+        _check(_L.aq_dataset_norms(self.h, out.ctypes.data))
+        return out
+
+
+class DeviceCodebook(_Handle):
+    _free = "aq_codebook_free"
+
+    def __init__(self, s, h, M, k, sd):
+        self.s, self.h, self.M, self.k, self.sd = s, h, M, k, sd
+
+    def download(self) -> ProductCodebook:
+        out = np.zeros(self.M * self.k * self.sd, np.float64)
+        _check(_L.aq_codebook_download(self.h, out.ctypes.data))
+        return ProductCodebook(self.M, self.k, self.sd, out)
+
+
+class DeviceCodes(_Handle):
+    _free = "aq_codes_free"
+
+    def __init__(self, s, h, n, M, k):
+        self.s, self.h, self.n, self.M, self.k = s, h, n, M, k
+
+    @property
+    def row_bytes(self) -> int:
+        return int(_L.aq_codes_row_bytes(self.h))
+
+    def download(self) -> CodeMatrix:
+        out = np.zeros((self.n, self.M), np.uint32)
+        _check(_L.aq_codes_download(self.h, out.ctypes.data))
+        return CodeMatrix(self.n, self.M, self.k, out)
+
+    def download_packed(self) -> np.ndarray:
+        out = np.zeros((self.n, self.row_bytes), np.uint8)
+        _check(_L.aq_codes_download_packed(self.h, out.ctypes.data))
+        return out
+
+
+# ---- weights ----------------------------------------------------------------
+
+
+def _weights(w, n: int, keep: list) -> _lib.aq_weights:
+    """Builds an aq_weights descriptor; `keep` holds arrays alive for the call."""
+    cw = _lib.aq_weights()
+    if isinstance(w, AnisotropicWeights):
+        cw.mode = 0
+        cw.h_parallel = w.h_parallel
+        cw.h_perpendicular = w.h_perpendicular
+        return cw
+    if isinstance(w, ThresholdWeights):
+        cw.mode = 2
+        cw.threshold = w.threshold
+        cw.threshold_policy = 1 if w.policy == "parallel_only" else 0
+        return cw
+    if isinstance(w, tuple) and len(w) == 2:
+        hp = np.ascontiguousarray(w[0], np.float64)
+        ho = np.ascontiguousarray(w[1], np.float64)
+    else:
+        seq = list(w)
+        if len(seq) != n:
+            raise InvalidArgument("InvalidArgument: need one AnisotropicWeights per datapoint")
+        if seq and all(s == seq[0] for s in seq):
+            return _weights(seq[0], n, keep)
+        hp = np.array([s.h_parallel for s in seq], np.float64)
+        ho = np.array([s.h_perpendicular for s in seq], np.float64)
+    if hp.size != n or ho.size != n:
+        raise InvalidArgument("InvalidArgument: need one AnisotropicWeights per datapoint")
+    keep += [hp, ho]
+    cw.mode = 1
+    cw.h_parallel_arr = hp.ctypes.data
+    cw.h_perpendicular_arr = ho.ctypes.data
+    return cw
+
+
+def _sess(session: Optional[Session]) -> Session:
+    return session or Session.default()
+
+
+# ---- encode (pq.hpp) ------------------------------------------------------------
+
+
+def pq_quantize(data: Dataset, cb: ProductCodebook, weights, passes: int,
+                threads: int = 1, session: Optional[Session] = None) -> CodeMatrix:
+    """pq.hpp:581-612. `threads` is accepted for signature parity; results never
+    depend on it (parallel.hpp:32-35)."""
+    s = _sess(session)
+    data = data if isinstance(data, Dataset) else Dataset(data)
+    keep: list = []
+    w = _weights(weights, data.n, keep)
+    out = np.zeros((data.n, cb.M), np.uint32)
+    _check(_L.aq_pq_quantize(s.h, data.values.ctypes.data, data.n, data.d,
+                             cb.dictionaries.ctypes.data, cb.M, cb.k, cb.sub_dimension,
+                             C.byref(w), passes, out.ctypes.data))
+    return CodeMatrix(data.n, cb.M, cb.k, out)
+
+
+def pq_assign_pass(data: Dataset, cb: ProductCodebook, weights, codes: CodeMatrix,
+                   sweep_to_fixed_point: bool = False, session: Optional[Session] = None):
+    """detail::pq_assign_pass (pq.hpp:202-221): returns (codes, per-point losses)."""
+    s = _sess(session)
+    data = data if isinstance(data, Dataset) else Dataset(data)
+    keep: list = []
+    w = _weights(weights, data.n, keep)
+    out = np.ascontiguousarray(codes.codes, np.uint32).copy()
+    losses = np.zeros(data.n, np.float64)
+    _check(_L.aq_pq_assign_pass(s.h, data.values.ctypes.data, data.n, data.d,
+                                cb.dictionaries.ctypes.data, cb.M, cb.k, cb.sub_dimension,
+                                C.byref(w), int(sweep_to_fixed_point), out.ctypes.data,
+                                losses.ctypes.data))
+    return CodeMatrix(data.n, cb.M, cb.k, out), losses
+
+
+def dev_pq_quantize(ds: DeviceDataset, cb: DeviceCodebook, weights, passes: int,
+                    out: DeviceCodes) -> None:
+    keep: list = []
+    w = _weights(weights, ds.n, keep)
+    _check(_L.aq_dev_pq_quantize(ds.h, cb.h, C.byref(w), passes, out.h))
+
+
+def dev_pq_assign_pass(ds: DeviceDataset, cb: DeviceCodebook, weights, codes: DeviceCodes,
+                       sweep_to_fixed_point: bool = False, losses_ptr: int = 0) -> int:
+    keep: list = []
+    w = _weights(weights, ds.n, keep)
+    ch = C.c_uint64(0)
+    _check(_L.aq_dev_pq_assign_pass(ds.h, cb.h, C.byref(w), int(sweep_to_fixed_point),
+                                    codes.h, losses_ptr or None, C.byref(ch)))
+    return ch.value

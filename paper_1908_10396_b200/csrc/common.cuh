@@ -1,0 +1,216 @@
+// Shared definitions for the B200-native anisotropic PQ library.
+//
+// Device data layout:
+//   * dataset rows are stored "pair-tiled": rows grouped in tiles of 32, and
+//     inside a tile each pair of dimensions (2p, 2p+1) is a contiguous block
+//     of 32 float2 (one per row). A warp whose lanes own 32 consecutive rows
+//     reads the sub-vector of one 2-D subspace as a single coalesced 256-byte
+//     load; no shared-memory staging or transpose is needed in the encoders.
+//   * norms are float64, computed on the device in the reference's order
+//     (dataset.hpp:55-59: sequential sum of squares, then sqrt).
+//   * codes are packed row-major: 4-bit (k <= 16, low nibble = even m) or
+//     8-bit (k <= 256), row stride rounded up to 8 bytes.
+//   * codebooks are kept in float64 (the reference's arithmetic) plus float32
+//     staging tables used only as filters whose errors are bounded.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+
+#include "../../include/anisoq_b200.h"
+
+namespace aqd {
+
+// ---- error plumbing -------------------------------------------------------
+void set_error(int status, const char* fmt, ...);
+int ref_error(int status, const char* detail);  // "<RefName>: detail"
+const char* status_ref_name(int status);
+
+#define AQ_CUDA(call)                                                     \
+  do {                                                                    \
+    cudaError_t e_ = (call);                                              \
+    if (e_ != cudaSuccess) {                                              \
+      ::aqd::set_error(AQ_E_CUDA, "CUDA error %s at %s:%d: %s",           \
+                       cudaGetErrorName(e_), __FILE__, __LINE__,          \
+                       cudaGetErrorString(e_));                           \
+      return AQ_E_CUDA;                                                   \
+    }                                                                     \
+  } while (0)
+
+#define AQ_TRY(expr)             \
+  do {                           \
+    int st_ = (expr);            \
+    if (st_ != AQ_OK) return st_; \
+  } while (0)
+
+#define AQ_LAUNCHED(sess)                 \
+  do {                                    \
+    (sess)->launches++;                   \
+    AQ_CUDA(cudaGetLastError());          \
+  } while (0)
+
+// Device-side error record: the smallest offending point index wins, which is
+// the error the reference's sequential loops would raise first.
+struct DevError {
+  unsigned long long key;  // (index << 8) | status, ~0ull when clear
+};
+
+__device__ __forceinline__ void report_error(DevError* e, uint64_t index,
+                                             int status) {
+  atomicMin(&e->key, (unsigned long long)((index << 8) | (uint64_t)status));
+}
+
+// ---- scratch memory ---------------------------------------------------------
+struct Scratch {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace aqd
+
+struct aq_session {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint64_t launches = 0;
+  int num_sms = 148;
+  aqd::DevError* err = nullptr;     // device
+  aqd::DevError* err_host = nullptr;  // pinned mirror
+  aqd::Scratch scratch[6];
+};
+
+struct aq_dataset {
+  aq_session* s = nullptr;
+  size_t n = 0, d = 0;
+  float* xt = nullptr;      // pair-tiled rows
+  double* norms = nullptr;  // float64 norms
+};
+
+struct aq_codebook {
+  aq_session* s = nullptr;
+  size_t M = 0, k = 0, sd = 0;
+  double* d64 = nullptr;   // (m*k + j)*sd
+  float4* f32 = nullptr;   // sd == 2: [M][16] {c0, c1, c0^2+c1^2, 0}
+  float* rmax = nullptr;   // [M] max_j |c_mj| (float32 norm, rounded up)
+};
+
+struct aq_codes {
+  aq_session* s = nullptr;
+  size_t n = 0, M = 0, k = 0;
+  size_t stride = 0;       // bytes per row
+  int bits = 4;            // 4 or 8
+  uint8_t* data = nullptr;
+};
+
+namespace aqd {
+
+// Scratch buffers owned by the session, grown on demand (slot-indexed so that
+// concurrently live temporaries never alias).
+int scratch(aq_session* s, int slot, size_t bytes, void** out);
+int check_session(aq_session* s);
+int sync_and_check(aq_session* s, const char* what);  // reads DevError
+int clear_dev_error(aq_session* s);
+
+__host__ __device__ inline size_t pairs_of(size_t d) { return (d + 1) / 2; }
+inline size_t tiled_floats(size_t n, size_t d) {
+  return ((n + 31) / 32) * pairs_of(d) * 64;
+}
+inline size_t code_stride(size_t M, int bits) {
+  const size_t raw = bits == 4 ? (M + 1) / 2 : M;
+  return (raw + 7) & ~size_t(7);
+}
+
+__host__ __device__ __forceinline__ size_t tiled_index(size_t i, size_t j,
+                                                       size_t pairs) {
+  return (((i >> 5) * pairs + (j >> 1)) * 32 + (i & 31)) * 2 + (j & 1);
+}
+
+__device__ __forceinline__ unsigned get_code(const uint8_t* row, int m,
+                                             int bits) {
+  if (bits == 4) return (row[m >> 1] >> ((m & 1) * 4)) & 15u;
+  return row[m];
+}
+
+// ---- weights ------------------------------------------------------------------
+// Resolved per point on the device from an aq_weights descriptor
+// (geometry.hpp:119-145, eta_limit 395-402, CLI resolve_weights
+// anisoq_main.cpp:108-142).
+struct DevWeights {
+  int mode;
+  double hp, ho;          // UNIFORM
+  const double* hp_arr;   // PER_POINT (device copies)
+  const double* ho_arr;
+  double threshold;       // THRESHOLD
+  int policy;
+  int d;
+};
+
+int make_dev_weights(aq_session* s, const aq_weights* w, size_t n, size_t d,
+                     DevWeights* out);
+
+__device__ __forceinline__ bool resolve_weights(const DevWeights& w,
+                                                size_t i, double norm,
+                                                double* hp, double* ho,
+                                                int* status) {
+  if (w.mode == AQ_WEIGHTS_UNIFORM) {
+    *hp = w.hp;
+    *ho = w.ho;
+    return true;
+  }
+  if (w.mode == AQ_WEIGHTS_PER_POINT) {
+    *hp = w.hp_arr[i];
+    *ho = w.ho_arr[i];
+    return true;
+  }
+  // eta_limit (geometry.hpp:395-402), op order kept.
+  if (!(norm > 0.0)) {
+    *status = AQ_E_INVALID_ARGUMENT;
+    return false;
+  }
+  const double t = w.threshold;
+  if (!(t >= 0.0) || t >= norm) {
+    if (w.policy == AQ_THRESHOLD_PARALLEL_ONLY && t >= 0.0) {
+      *hp = 1.0;  // eta = inf: parallel error only
+      *ho = 0.0;
+      return true;
+    }
+    *status = AQ_E_INVALID_THRESHOLD;
+    return false;
+  }
+  const double r = __ddiv_rn(t, norm);
+  const double rho = __dmul_rn(r, r);
+  const double eta =
+      __ddiv_rn(__dmul_rn((double)(w.d - 1), rho), __dsub_rn(1.0, rho));
+  *hp = eta;
+  *ho = 1.0;
+  return true;
+}
+
+// ---- exact float64 primitives (no contraction; reference op order) ----------
+
+// detail::residual_terms (geometry.hpp:182-192) for sd == 2.
+__device__ __forceinline__ void residual2(double x0, double x1, double c0,
+                                          double c1, double* d2, double* rd) {
+  const double df0 = __dsub_rn(x0, c0);
+  const double df1 = __dsub_rn(x1, c1);
+  double a = __dadd_rn(0.0, __dmul_rn(df0, df0));
+  a = __dadd_rn(a, __dmul_rn(df1, df1));
+  double b = __dadd_rn(0.0, __dmul_rn(df0, x0));
+  b = __dadd_rn(b, __dmul_rn(df1, x1));
+  *d2 = a;
+  *rd = b;
+}
+
+// detail::combined_loss (geometry.hpp:196-200).
+__device__ __forceinline__ double combined_loss(double dist2, double rdot,
+                                                double hp, double ho,
+                                                double inv_norm2) {
+  return __dadd_rn(
+      __dmul_rn(ho, dist2),
+      __dmul_rn(__dmul_rn(__dsub_rn(hp, ho), __dmul_rn(rdot, rdot)),
+                inv_norm2));
+}
+
+}  // namespace aqd

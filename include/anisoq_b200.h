@@ -178,9 +178,21 @@ int aq_build_lut(aq_session* s, const double* q, size_t d,
  * (score desc, index asc) of sum_m lut[m][code]; scores bit-identical to the
  * reference's float64 sequential sum. ids_out/scores_out are nq x topn_eff,
  * topn_eff = min(topn, n). */
-int aq_dev_adc_search(aq_codes* codes, aq_codebook* cb, const float* queries,
+int aq_dev_adc_search(aq_codes* codes, aq_codebook* cb, const double* queries,
                       size_t nq, size_t topn, uint32_t* ids_out,
                       double* scores_out);
+/* Same with device pointers (q_dev float64 nq x d; outputs on the device). */
+int aq_dev_adc_search_d(aq_codes* codes, aq_codebook* cb, const double* q_dev,
+                        size_t nq, size_t topn, uint32_t* ids_dev,
+                        double* scores_dev);
+/* Fused query pipeline: ADC top-`topn` then exact-dot rerank to `keep`
+ * (host queries in, host results out; index and dataset resident). Any of
+ * the four outputs may be NULL. */
+int aq_dev_search_rerank(aq_dataset* ds, aq_codes* codes, aq_codebook* cb,
+                         const double* queries, size_t nq, size_t topn,
+                         size_t keep, uint32_t* adc_ids_out,
+                         double* adc_scores_out, uint32_t* ids_out,
+                         double* scores_out);
 int aq_adc_search(aq_session* s, const double* q, size_t d,
                   const uint32_t* codes, size_t n, size_t M, size_t codes_k,
                   const double* dictionaries, size_t cb_M, size_t k,
@@ -188,11 +200,11 @@ int aq_adc_search(aq_session* s, const double* q, size_t d,
                   double* scores_out, size_t* count_out);
 /* Exact-dot rerank of candidate ids: score = dot(q, x[id]) in float64
  * sequential order; keep the best `keep` by (score desc, index asc). */
-int aq_dev_rerank(aq_dataset* ds, const float* queries, size_t nq,
+int aq_dev_rerank(aq_dataset* ds, const double* queries, size_t nq,
                   const uint32_t* cand_ids, size_t ncand, size_t keep,
                   uint32_t* ids_out, double* scores_out);
 /* Brute-force exact MIPS top-`depth` (exact_ground_truth). */
-int aq_dev_exact_search(aq_dataset* ds, const float* queries, size_t nq,
+int aq_dev_exact_search(aq_dataset* ds, const double* queries, size_t nq,
                         size_t depth, uint32_t* ids_out, double* scores_out);
 
 /* ---- codebook update (pq.hpp:290-464) ------------------------------------ */

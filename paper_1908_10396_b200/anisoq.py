@@ -451,3 +451,75 @@ def dev_pq_assign_pass(ds: DeviceDataset, cb: DeviceCodebook, weights, codes: De
     _check(_L.aq_dev_pq_assign_pass(ds.h, cb.h, C.byref(w), int(sweep_to_fixed_point),
                                     codes.h, losses_ptr or None, C.byref(ch)))
     return ch.value
+
+
+# ---- search (index.hpp) -------------------------------------------------------------
+
+
+def build_lut(q, cb: ProductCodebook, session: Optional[Session] = None) -> LookupTable:
+    """index.hpp:56-70 (float64 partial dot products, computed on the device)."""
+    s = _sess(session)
+    q = np.ascontiguousarray(q, np.float64)
+    out = np.zeros(cb.M * cb.k, np.float64)
+    _check(_L.aq_build_lut(s.h, q.ctypes.data, q.size, cb.dictionaries.ctypes.data, cb.M,
+                           cb.k, cb.sub_dimension, out.ctypes.data))
+    return LookupTable(cb.M, cb.k, out)
+
+
+def adc_search(q, codes: CodeMatrix, cb: ProductCodebook, topn: int,
+               session: Optional[Session] = None) -> SearchResult:
+    """index.hpp:118-134: top-N by lookup-table score, (score desc, index asc)."""
+    s = _sess(session)
+    q = np.ascontiguousarray(q, np.float64)
+    te = min(topn, codes.n) if topn >= 1 else 1
+    ids = np.zeros(max(te, 1), np.uint32)
+    sc = np.zeros(max(te, 1), np.float64)
+    cnt = C.c_size_t(0)
+    _check(_L.aq_adc_search(s.h, q.ctypes.data, q.size, codes.codes.ctypes.data, codes.n,
+                            codes.M, codes.k, cb.dictionaries.ctypes.data, cb.M, cb.k,
+                            cb.sub_dimension, topn, ids.ctypes.data, sc.ctypes.data,
+                            C.byref(cnt)))
+    return SearchResult([Hit(int(i), float(v)) for i, v in zip(ids[:cnt.value], sc[:cnt.value])])
+
+
+def dev_adc_search(codes: DeviceCodes, cb: DeviceCodebook, queries, topn: int):
+    """Batched adc_search over a resident index: returns (ids, scores) nq x min(topn, n)."""
+    Q = np.ascontiguousarray(np.atleast_2d(queries), np.float64)
+    nq = Q.shape[0]
+    te = min(topn, codes.n)
+    ids = np.zeros((nq, te), np.uint32)
+    sc = np.zeros((nq, te), np.float64)
+    _check(_L.aq_dev_adc_search(codes.h, cb.h, Q.ctypes.data, nq, topn, ids.ctypes.data,
+                                sc.ctypes.data))
+    return ids, sc
+
+
+def dev_rerank(ds: DeviceDataset, queries, cand_ids, keep: int):
+    """Exact float64 dot rerank of candidate ids (north_star A22)."""
+    Q = np.ascontiguousarray(np.atleast_2d(queries), np.float64)
+    cand = np.ascontiguousarray(cand_ids, np.uint32)
+    nq, nc = cand.shape
+    ke = min(keep, nc)
+    ids = np.zeros((nq, ke), np.uint32)
+    sc = np.zeros((nq, ke), np.float64)
+    _check(_L.aq_dev_rerank(ds.h, Q.ctypes.data, nq, cand.ctypes.data, nc, keep,
+                            ids.ctypes.data, sc.ctypes.data))
+    return ids, sc
+
+
+def dev_search_rerank(ds: DeviceDataset, codes: DeviceCodes, cb: DeviceCodebook, queries,
+                      topn: int = 100, keep: int = 10):
+    """ADC top-`topn` + exact rerank to `keep` in one device pipeline.
+    Returns (adc_ids, adc_scores, ids, scores)."""
+    Q = np.ascontiguousarray(np.atleast_2d(queries), np.float64)
+    nq = Q.shape[0]
+    te = min(topn, codes.n)
+    ke = min(keep, te)
+    aid = np.zeros((nq, te), np.uint32)
+    asc = np.zeros((nq, te), np.float64)
+    ids = np.zeros((nq, ke), np.uint32)
+    sc = np.zeros((nq, ke), np.float64)
+    _check(_L.aq_dev_search_rerank(ds.h, codes.h, cb.h, Q.ctypes.data, nq, topn, keep,
+                                   aid.ctypes.data, asc.ctypes.data, ids.ctypes.data,
+                                   sc.ctypes.data))
+    return aid, asc, ids, sc

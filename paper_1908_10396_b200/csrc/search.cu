@@ -1,0 +1,723 @@
+// Query path: LUT build (build_lut, index.hpp:56-70), 4-bit ADC scoring with
+// top-N selection (adc_search / select_top, index.hpp:88-134), exact-dot
+// rerank (north_star; restated from exact_search, index.hpp:137-147) and
+// brute-force exact MIPS (exact_ground_truth, index.hpp:150-162).
+//
+// Exactness. The reference scores a point by summing M
+// float64 LUT entries in subspace order and orders hits by (score desc,
+// index asc). The scoring kernel sums float32 copies of the entries (error
+// <= delta_q = (Mp+2) 2^-24 sum_m max_j |lut_mj| per score) and keeps, per
+// query, every point whose float32 score is >= theta - 2 delta_q, theta being
+// a float32 score that at least N points reach. The merge kernel re-scores
+// that window in float64 in the reference's order and sorts exactly, so ids
+// AND scores equal the reference's. Inputs whose windows do not fit (massive
+// ties, N > 512) take an exact full-sort fallback.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+namespace aqd {
+
+int sort_scores_desc(aq_session* s, const double* scores, uint32_t* idx,
+                     size_t n);
+
+constexpr int kQB = 16;       // queries per scoring CTA (8 float2 pairs)
+constexpr int kTileP = 256;   // points per tile == threads per CTA
+constexpr int kMaxTopN = 512; // fast path limit
+constexpr int kMergeCap = 2048;
+
+__host__ __device__ inline int pad8(int M) { return (M + 7) & ~7; }
+
+// ---- LUT ---------------------------------------------------------------------
+// One CTA per query. lut64[q][m][j] (reference order of build_lut), lut32 in
+// the scoring layout [qblock][pair][Mp][16] float2 (zero padded), delta[q].
+__global__ void k_build_lut(const double* __restrict__ Q, int nq, int d,
+                            const double* __restrict__ cb, int M, int k,
+                            int sd, double* __restrict__ lut64,
+                            float* __restrict__ lut32,
+                            float* __restrict__ delta) {
+  __shared__ unsigned maxabs[1024];
+  const int q = blockIdx.x;
+  const int Mp = pad8(M);
+  for (int m = threadIdx.x; m < M; m += blockDim.x) maxabs[m] = 0u;
+  __syncthreads();
+  const double* qv = Q + (size_t)q * d;
+  const int qb = q / kQB, qi = q % kQB;
+  float* L = lut32 + (((size_t)qb * (kQB / 2) + qi / 2) * Mp) * 32 + (qi & 1);
+  for (int e = threadIdx.x; e < M * k; e += blockDim.x) {
+    const int m = e / k, j = e % k;
+    const double* c = cb + (size_t)e * sd;
+    double s = 0.0;  // detail::dot (geometry.hpp:170-174)
+    for (int t = 0; t < sd; ++t) s = __dadd_rn(s, __dmul_rn(qv[m * sd + t], c[t]));
+    lut64[(size_t)q * M * k + e] = s;
+    if (j < 16) L[(m * 16 + j) * 2] = (float)s;
+    atomicMax(&maxabs[m], __float_as_uint(__double2float_ru(fabs(s))));
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double S = 0.0;
+    for (int m = 0; m < M; ++m) S += (double)__uint_as_float(maxabs[m]);
+    // float32 sum of Mp terms: <= (Mp-1) u sum|t|, entry rounding <= u sum|t|,
+    // float64 reference rounding <= M 2^-53 sum|t|; 1% and 2u slack on top.
+    const double dl = (double)(Mp + 2) * 5.9604644775390625e-08 * S * 1.01 + 1e-30;
+    delta[q] = __double2float_ru(dl);
+  }
+}
+
+// ---- scoring with a per-CTA candidate window ------------------------------------
+
+struct ScoreArgs {
+  const uint8_t* codes;
+  size_t n;
+  int stride;      // bytes per code row
+  const float* lut32;
+  const float* delta;
+  int Mp;
+  int nq;
+  int N;           // top-N
+  int cap;         // candidate buffer per query
+  size_t range_len;
+  int R;           // number of point ranges
+  uint2* out_buf;  // [q][r][cap] {score bits, index}
+  int* out_cnt;    // [q][r]
+  int* out_flag;   // [q]
+};
+
+__device__ __forceinline__ unsigned f2o(float f) {  // order-preserving
+  const unsigned b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float o2f(unsigned o) {
+  return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
+}
+
+// Warp-cooperative: the N-th largest score among buf[0..cnt) as an ordered
+// key (0 when cnt < N).
+__device__ unsigned warp_nth_largest(const uint2* buf, int cnt, int N) {
+  if (cnt < N) return 0u;
+  const int lane = threadIdx.x & 31;
+  unsigned T = 0u;
+  for (int bit = 31; bit >= 0; --bit) {
+    const unsigned cand = T | (1u << bit);
+    int c = 0;
+    for (int e = lane; e < cnt; e += 32) c += f2o(__uint_as_float(buf[e].x)) >= cand;
+    c = __reduce_add_sync(0xffffffffu, c);
+    if (c >= N) T = cand;
+  }
+  return T;
+}
+
+// Keep only entries >= cut (warp-cooperative, in place); returns new count.
+__device__ int warp_compact(uint2* buf, int cnt, float cut) {
+  const int lane = threadIdx.x & 31;
+  int kept = 0;
+  for (int base = 0; base < cnt; base += 32) {
+    const int e = base + lane;
+    uint2 v = make_uint2(0, 0);
+    bool keep = false;
+    if (e < cnt) {
+      v = buf[e];
+      keep = __uint_as_float(v.x) >= cut;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    __syncwarp();
+    if (keep) buf[kept + __popc(bal & ((1u << lane) - 1u))] = v;
+    kept += __popc(bal);
+    __syncwarp();
+  }
+  return kept;
+}
+
+__global__ void __launch_bounds__(kTileP, 1) k_adc_score(const ScoreArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int Mp = a.Mp;
+  float2* L = reinterpret_cast<float2*>(smem);  // [8 pairs][Mp][16]
+  float* cut = reinterpret_cast<float*>(L + 8 * Mp * 16);
+  float* dl = cut + kQB;
+  int* cnt = reinterpret_cast<int*>(dl + kQB);
+  int* flag = cnt + kQB;
+  uint2* buf = reinterpret_cast<uint2*>(flag + kQB);  // [kQB][cap]
+  const int qb = blockIdx.y, r = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  {
+    const float4* src = reinterpret_cast<const float4*>(
+        a.lut32 + (size_t)qb * 8 * Mp * 32);
+    float4* dst = reinterpret_cast<float4*>(L);
+    for (int t = threadIdx.x; t < 8 * Mp * 8; t += blockDim.x) dst[t] = src[t];
+  }
+  if (threadIdx.x < kQB) {
+    const int q = qb * kQB + threadIdx.x;
+    cut[threadIdx.x] = -INFINITY;
+    dl[threadIdx.x] = q < a.nq ? a.delta[q] : 0.0f;
+    cnt[threadIdx.x] = 0;
+    flag[threadIdx.x] = 0;
+  }
+  __syncthreads();
+  const size_t start = (size_t)r * a.range_len;
+  const size_t end = min(a.n, start + a.range_len);
+  const int cap = a.cap;
+  const int nchunk = Mp >> 3;
+  for (size_t tb = start; tb < end; tb += kTileP) {
+    const size_t p = tb + threadIdx.x;
+    if (p < end) {
+      float acc[kQB];
+#pragma unroll
+      for (int q = 0; q < kQB; ++q) acc[q] = 0.0f;
+      const uint32_t* crow = reinterpret_cast<const uint32_t*>(a.codes + p * a.stride);
+      for (int c = 0; c < nchunk; ++c) {
+        const uint32_t w = __ldg(crow + c);
+        int off[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) off[t] = (c * 8 + t) * 16 + ((w >> (4 * t)) & 15u);
+#pragma unroll
+        for (int pr = 0; pr < 8; ++pr) {
+          const float2* Lp = L + pr * Mp * 16;
+          float s0 = acc[2 * pr], s1 = acc[2 * pr + 1];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const float2 v = Lp[off[t]];
+            s0 += v.x;
+            s1 += v.y;
+          }
+          acc[2 * pr] = s0;
+          acc[2 * pr + 1] = s1;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kQB; ++q) {
+        if (acc[q] >= cut[q]) {
+          const int pos = atomicAdd(&cnt[q], 1);
+          if (pos < cap)
+            buf[q * cap + pos] = make_uint2(__float_as_uint(acc[q]), (unsigned)p);
+          else
+            flag[q] = 1;
+        }
+      }
+    }
+    __syncthreads();
+    // shrink buffers that could overflow during the next tile
+    for (int q = warp; q < kQB; q += kTileP / 32) {
+      const int c = min(cnt[q], cap);
+      if (c > cap - kTileP && !flag[q]) {
+        const unsigned T = warp_nth_largest(buf + q * cap, c, a.N);
+        if (T) {
+          const float nc = __fsub_rd(o2f(T), 2.0f * dl[q]);
+          const float cq = fmaxf(cut[q], nc);
+          const int kept = warp_compact(buf + q * cap, c, cq);
+          if (lane == 0) {
+            cut[q] = cq;
+            cnt[q] = kept;
+            if (kept > cap - kTileP) flag[q] = 1;  // window too large: ties
+          }
+        }
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+  }
+  // final shrink + write-out
+  for (int q = warp; q < kQB; q += kTileP / 32) {
+    const int gq = qb * kQB + q;
+    int c = min(cnt[q], cap);
+    const unsigned T = warp_nth_largest(buf + q * cap, c, a.N);
+    if (T) c = warp_compact(buf + q * cap, c, fmaxf(cut[q], __fsub_rd(o2f(T), 2.0f * dl[q])));
+    if (gq < a.nq) {
+      uint2* dst = a.out_buf + ((size_t)gq * a.R + r) * cap;
+      for (int e = lane; e < c; e += 32) dst[e] = buf[q * cap + e];
+      if (lane == 0) {
+        a.out_cnt[(size_t)gq * a.R + r] = c;
+        if (flag[q]) atomicOr(&a.out_flag[gq], 1);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ---- merge: global window, float64 re-scoring, exact order --------------------
+
+struct MergeArgs {
+  const uint2* buf;
+  const int* cnt;
+  int* flag;
+  int R, cap, N, topn_eff;
+  const float* delta;
+  const double* lut64;
+  const uint8_t* codes;
+  int stride, bits, M, k;
+  uint32_t* ids;    // [q][topn_eff]
+  double* scores;
+};
+
+__global__ void __launch_bounds__(256) k_adc_merge(const MergeArgs a) {
+  __shared__ unsigned long long skey[kMergeCap];  // sort keys
+  __shared__ double ssc[kMergeCap];
+  __shared__ uint32_t sid[kMergeCap];
+  __shared__ int red[32];
+  __shared__ int ncol;
+  const int q = blockIdx.x;
+  if (a.flag[q]) return;  // handled by the exact fallback
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  // total entries
+  const uint2* lists = a.buf + (size_t)q * a.R * a.cap;
+  const int* cnts = a.cnt + (size_t)q * a.R;
+  // global N-th largest over the union (ordered-key binary search)
+  unsigned T = 0u;
+  int total = 0;
+  for (int r = 0; r < a.R; ++r) total += cnts[r];
+  if (total >= a.N) {
+    for (int bit = 31; bit >= 0; --bit) {
+      const unsigned cand = T | (1u << bit);
+      int c = 0;
+      for (int r = 0; r < a.R; ++r)
+        for (int e = tid; e < cnts[r]; e += blockDim.x)
+          c += f2o(__uint_as_float(lists[(size_t)r * a.cap + e].x)) >= cand;
+      c = __reduce_add_sync(0xffffffffu, c);
+      if (lane == 0) red[w] = c;
+      __syncthreads();
+      int tot = 0;
+      for (int t = 0; t < (int)(blockDim.x >> 5); ++t) tot += red[t];
+      __syncthreads();
+      if (tot >= a.N) T = cand;
+    }
+  }
+  const float cutv = T ? __fsub_rd(o2f(T), 2.0f * a.delta[q]) : -INFINITY;
+  if (tid == 0) ncol = 0;
+  __syncthreads();
+  for (int r = 0; r < a.R; ++r)
+    for (int e = tid; e < cnts[r]; e += blockDim.x) {
+      const uint2 v = lists[(size_t)r * a.cap + e];
+      if (__uint_as_float(v.x) >= cutv) {
+        const int pos = atomicAdd(&ncol, 1);
+        if (pos < kMergeCap) sid[pos] = v.y;
+      }
+    }
+  __syncthreads();
+  const int nc = ncol;
+  if (nc > kMergeCap) {
+    if (tid == 0) a.flag[q] = 2;
+    return;
+  }
+  // float64 re-scoring in the reference's order (index.hpp:127-133)
+  const double* lq = a.lut64 + (size_t)q * a.M * a.k;
+  for (int e = tid; e < nc; e += blockDim.x) {
+    const uint8_t* row = a.codes + (size_t)sid[e] * a.stride;
+    double s = 0.0;
+    for (int m = 0; m < a.M; ++m) s = __dadd_rn(s, lq[m * a.k + get_code(row, m, a.bits)]);
+    ssc[e] = s;
+  }
+  // bitonic sort of (score desc, index asc) over the next power of two
+  int P = 1;
+  while (P < nc) P <<= 1;
+  for (int e = tid; e < P; e += blockDim.x) {
+    if (e < nc) {
+      unsigned long long b = (unsigned long long)__double_as_longlong(ssc[e]);
+      b = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+      skey[e] = ~b;  // ascending == score descending
+    } else {
+      skey[e] = ~0ull;
+      sid[e] = 0xffffffffu;
+    }
+  }
+  __syncthreads();
+  for (int size = 2; size <= P; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int e = tid; e < P; e += blockDim.x) {
+        const int o = e ^ stride;
+        if (o > e) {
+          const bool up = (e & size) == 0;
+          const unsigned long long ka = skey[e], kb = skey[o];
+          const uint32_t ia = sid[e], ib = sid[o];
+          const bool gt = ka > kb || (ka == kb && ia > ib);
+          if (gt == up) {
+            skey[e] = kb;
+            skey[o] = ka;
+            sid[e] = ib;
+            sid[o] = ia;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  for (int e = tid; e < a.topn_eff; e += blockDim.x) {
+    unsigned long long b = ~skey[e];
+    b = (b >> 63) ? (b & 0x7fffffffffffffffull) : ~b;
+    a.ids[(size_t)q * a.topn_eff + e] = sid[e];
+    a.scores[(size_t)q * a.topn_eff + e] = __longlong_as_double((long long)b);
+  }
+}
+
+// ---- exact fallback: all float64 scores + stable radix sort ---------------------
+
+__global__ void k_adc_all_scores(const uint8_t* __restrict__ codes, size_t n,
+                                 int stride, int bits, int M, int k,
+                                 const double* __restrict__ lq,
+                                 double* __restrict__ out,
+                                 uint32_t* __restrict__ idx) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint8_t* row = codes + i * stride;
+  double s = 0.0;
+  for (int m = 0; m < M; ++m) s = __dadd_rn(s, lq[m * k + get_code(row, m, bits)]);
+  out[i] = s;
+  idx[i] = (uint32_t)i;
+}
+
+__global__ void k_gather_top(const uint32_t* __restrict__ idx,
+                             const double* __restrict__ scores_by_point,
+                             int topn_eff, uint32_t* ids, double* sc) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= topn_eff) return;
+  ids[e] = idx[e];
+  sc[e] = scores_by_point[idx[e]];
+}
+
+// Device-pointer core. Q (float64, nq x d), ids/scores device (nq x topn_eff).
+int adc_search_device(aq_codes* codes, aq_codebook* cb, const double* Qd,
+                      size_t nq, size_t topn, uint32_t* ids, double* scores) {
+  aq_session* s = codes->s;
+  AQ_TRY(check_session(s));
+  if (codes->n == 0) return ref_error(AQ_E_EMPTY_INDEX, "no quantized datapoints");
+  if (topn < 1) return ref_error(AQ_E_INVALID_ARGUMENT, "topn must be >= 1");
+  if (codes->M != cb->M || codes->k > cb->k)
+    return ref_error(AQ_E_DIMENSION_MISMATCH, "code matrix does not match codebook");
+  if (cb->k > 256 || (codes->bits == 4 && cb->k > 16 && codes->k > 16))
+    return ref_error(AQ_E_UNSUPPORTED, "device search supports k <= 256");
+  if (cb->M > 1024) return ref_error(AQ_E_UNSUPPORTED, "device search supports M <= 1024");
+  if (nq == 0) return AQ_OK;
+  const int M = (int)cb->M, k = (int)cb->k, Mp = pad8(M);
+  const size_t n = codes->n;
+  const size_t topn_eff = std::min(topn, n);
+  const size_t d = cb->M * cb->sd;
+  const size_t nqb = (nq + kQB - 1) / kQB;
+  // workspace
+  const size_t lut64_b = nq * M * k * sizeof(double);
+  const size_t lut32_b = nqb * 8 * (size_t)Mp * 32 * sizeof(float);
+  void* p;
+  AQ_TRY(scratch(s, 1, lut64_b + lut32_b + nq * sizeof(float) + 256, &p));
+  double* lut64 = (double*)p;
+  float* lut32 = (float*)(lut64 + nq * M * k);
+  float* delta = lut32 + lut32_b / sizeof(float);
+  AQ_CUDA(cudaMemsetAsync(lut32, 0, lut32_b, s->stream));
+  k_build_lut<<<(unsigned)nq, 256, 0, s->stream>>>(Qd, (int)nq, (int)d, cb->d64, M, k,
+                                                  (int)cb->sd, lut64, lut32, delta);
+  AQ_LAUNCHED(s);
+
+  const bool fast = codes->bits == 4 && topn <= (size_t)kMaxTopN && M <= 1024;
+  std::vector<int> hflag(nq, fast ? 0 : 1);
+  if (fast) {
+    const int N = (int)topn_eff;
+    const int cap = ((N + 31) & ~31) + 2 * kTileP;
+    // point ranges: enough CTAs for ~2 waves, ranges of whole tiles
+    const size_t tiles = (n + kTileP - 1) / kTileP;
+    size_t R = std::max<size_t>(1, (2 * (size_t)s->num_sms + nqb - 1) / nqb);
+    R = std::min(R, tiles);
+    const size_t range_len = ((tiles + R - 1) / R) * kTileP;
+    R = (n + range_len - 1) / range_len;
+    const size_t buf_b = nq * R * cap * sizeof(uint2);
+    void* p2;
+    AQ_TRY(scratch(s, 3, buf_b + nq * R * sizeof(int) + nq * sizeof(int) + 256, &p2));
+    uint2* obuf = (uint2*)p2;
+    int* ocnt = (int*)(obuf + nq * R * cap);
+    int* oflag = ocnt + nq * R;
+    AQ_CUDA(cudaMemsetAsync(oflag, 0, nq * sizeof(int), s->stream));
+    ScoreArgs sa{codes->data, n, (int)codes->stride, lut32, delta, Mp, (int)nq, N, cap,
+                 range_len, (int)R, obuf, ocnt, oflag};
+    const size_t smem = (size_t)8 * Mp * 16 * sizeof(float2) + 4 * kQB * 4 +
+                        (size_t)kQB * cap * sizeof(uint2);
+    if (smem > 227 * 1024)
+      return ref_error(AQ_E_UNSUPPORTED, "ADC working set exceeds shared memory");
+    AQ_CUDA(cudaFuncSetAttribute(k_adc_score, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    k_adc_score<<<dim3((unsigned)R, (unsigned)nqb), kTileP, smem, s->stream>>>(sa);
+    AQ_LAUNCHED(s);
+    MergeArgs ma{obuf, ocnt, oflag, (int)R, cap, N, (int)topn_eff, delta, lut64,
+                 codes->data, (int)codes->stride, codes->bits, M, k, ids, scores};
+    k_adc_merge<<<(unsigned)nq, 256, 0, s->stream>>>(ma);
+    AQ_LAUNCHED(s);
+    AQ_CUDA(cudaMemcpyAsync(hflag.data(), oflag, nq * sizeof(int), cudaMemcpyDeviceToHost,
+                            s->stream));
+    AQ_CUDA(cudaStreamSynchronize(s->stream));
+  }
+  // exact fallback for flagged queries
+  bool any = false;
+  for (size_t q = 0; q < nq; ++q) any |= hflag[q] != 0;
+  if (any) {
+    void* p3;
+    AQ_TRY(scratch(s, 4, n * (sizeof(double) + sizeof(uint32_t)) + 64, &p3));
+    double* all = (double*)p3;
+    uint32_t* idx = (uint32_t*)(all + n);
+    for (size_t q = 0; q < nq; ++q) {
+      if (!hflag[q]) continue;
+      k_adc_all_scores<<<(unsigned)((n + 255) / 256), 256, 0, s->stream>>>(
+          codes->data, n, (int)codes->stride, codes->bits, M, k, lut64 + q * M * k, all, idx);
+      AQ_LAUNCHED(s);
+      AQ_TRY(sort_scores_desc(s, all, idx, n));
+      k_gather_top<<<(unsigned)((topn_eff + 255) / 256), 256, 0, s->stream>>>(
+          idx, all, (int)topn_eff, ids + q * topn_eff, scores + q * topn_eff);
+      AQ_LAUNCHED(s);
+    }
+  }
+  return AQ_OK;
+}
+
+// ---- rerank (exact float64 dot, sequential order) -------------------------------
+
+// One warp per query: candidates rescored with detail::dot against the row
+// (float32-exact values) and the best `keep` returned in select_top order.
+__global__ void k_rerank(const float* __restrict__ xt, int pairs, int d,
+                         const double* __restrict__ Q, int nq,
+                         const uint32_t* __restrict__ cand, int ncand, int keep,
+                         uint32_t* __restrict__ ids, double* __restrict__ sc,
+                         size_t n, DevError* err) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int wpb = blockDim.x >> 5;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = blockIdx.x * wpb + w;
+  const int P = 1 << (32 - __clz(max(ncand, 2) - 1));  // next pow2
+  unsigned long long* K = reinterpret_cast<unsigned long long*>(smem) + (size_t)w * P;
+  uint32_t* I = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned long long*>(smem) + (size_t)wpb * P) + (size_t)w * P;
+  if (q >= nq) return;
+  const double* qv = Q + (size_t)q * d;
+  for (int e = lane; e < P; e += 32) {
+    if (e < ncand) {
+      const uint32_t id = cand[(size_t)q * ncand + e];
+      double s = 0.0;
+      if (id < n) {
+        for (int j = 0; j < d; ++j)
+          s = __dadd_rn(s, __dmul_rn(qv[j], (double)xt[tiled_index(id, j, pairs)]));
+      } else {
+        report_error(err, (uint64_t)q, AQ_E_INVALID_ARGUMENT);
+      }
+      unsigned long long b = (unsigned long long)__double_as_longlong(s);
+      b = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+      K[e] = ~b;
+      I[e] = id;
+    } else {
+      K[e] = ~0ull;
+      I[e] = 0xffffffffu;
+    }
+  }
+  __syncwarp();
+  for (int size = 2; size <= P; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int e = lane; e < P; e += 32) {
+        const int o = e ^ stride;
+        if (o > e) {
+          const bool up = (e & size) == 0;
+          const unsigned long long ka = K[e], kb = K[o];
+          const uint32_t ia = I[e], ib = I[o];
+          const bool gt = ka > kb || (ka == kb && ia > ib);
+          if (gt == up) {
+            K[e] = kb;
+            K[o] = ka;
+            I[e] = ib;
+            I[o] = ia;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  for (int e = lane; e < keep; e += 32) {
+    unsigned long long b = ~K[e];
+    b = (b >> 63) ? (b & 0x7fffffffffffffffull) : ~b;
+    ids[(size_t)q * keep + e] = I[e];
+    sc[(size_t)q * keep + e] = __longlong_as_double((long long)b);
+  }
+}
+
+int rerank_device(aq_dataset* ds, const double* Qd, size_t nq,
+                  const uint32_t* cand, size_t ncand, size_t keep, uint32_t* ids,
+                  double* sc) {
+  aq_session* s = ds->s;
+  if (ncand == 0 || nq == 0) return AQ_OK;
+  if (ncand > 4096) return ref_error(AQ_E_UNSUPPORTED, "rerank supports <= 4096 candidates");
+  const size_t keep_eff = std::min(keep, ncand);
+  int P = 1;
+  while (P < (int)ncand) P <<= 1;
+  const int wpb = std::max(1, std::min(8, (int)(40 * 1024 / (P * 12))));
+  const size_t smem = (size_t)wpb * P * 12;
+  AQ_TRY(clear_dev_error(s));
+  k_rerank<<<(unsigned)((nq + wpb - 1) / wpb), wpb * 32, smem, s->stream>>>(
+      ds->xt, (int)pairs_of(ds->d), (int)ds->d, Qd, (int)nq, cand, (int)ncand,
+      (int)keep_eff, ids, sc, ds->n, s->err);
+  AQ_LAUNCHED(s);
+  return AQ_OK;
+}
+
+}  // namespace aqd
+
+using namespace aqd;
+
+namespace {
+
+int upload_queries(aq_session* s, const double* Q, size_t nq, size_t d, int slot,
+                   double** out) {
+  void* p;
+  AQ_TRY(scratch(s, slot, nq * d * sizeof(double) + 16, &p));
+  if (nq * d)
+    AQ_CUDA(cudaMemcpyAsync(p, Q, nq * d * sizeof(double), cudaMemcpyHostToDevice,
+                            s->stream));
+  *out = (double*)p;
+  return AQ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int aq_dev_adc_search_d(aq_codes* codes, aq_codebook* cb, const double* q_dev,
+                        size_t nq, size_t topn, uint32_t* ids_dev, double* scores_dev) {
+  if (!codes || !cb) return ref_error(AQ_E_INVALID_ARGUMENT, "null argument");
+  return adc_search_device(codes, cb, q_dev, nq, topn, ids_dev, scores_dev);
+}
+
+int aq_dev_adc_search(aq_codes* codes, aq_codebook* cb, const double* queries,
+                      size_t nq, size_t topn, uint32_t* ids_out, double* scores_out) {
+  if (!codes || !cb) return ref_error(AQ_E_INVALID_ARGUMENT, "null argument");
+  aq_session* s = codes->s;
+  AQ_TRY(check_session(s));
+  if (codes->n == 0) return ref_error(AQ_E_EMPTY_INDEX, "no quantized datapoints");
+  if (topn < 1) return ref_error(AQ_E_INVALID_ARGUMENT, "topn must be >= 1");
+  const size_t d = cb->M * cb->sd;
+  const size_t te = std::min(topn, codes->n);
+  double* Qd;
+  AQ_TRY(upload_queries(s, queries, nq, d, 0, &Qd));
+  uint32_t* ids;
+  double* sc;
+  AQ_CUDA(cudaMallocAsync(&ids, nq * te * sizeof(uint32_t) + 8, s->stream));
+  AQ_CUDA(cudaMallocAsync(&sc, nq * te * sizeof(double) + 8, s->stream));
+  int st = adc_search_device(codes, cb, Qd, nq, topn, ids, sc);
+  if (st == AQ_OK && nq) {
+    cudaMemcpyAsync(ids_out, ids, nq * te * sizeof(uint32_t), cudaMemcpyDeviceToHost, s->stream);
+    cudaMemcpyAsync(scores_out, sc, nq * te * sizeof(double), cudaMemcpyDeviceToHost, s->stream);
+  }
+  cudaFreeAsync(ids, s->stream);
+  cudaFreeAsync(sc, s->stream);
+  cudaError_t e = cudaStreamSynchronize(s->stream);
+  if (st == AQ_OK && e != cudaSuccess) {
+    set_error(AQ_E_CUDA, "CUDA error %s", cudaGetErrorString(e));
+    return AQ_E_CUDA;
+  }
+  return st;
+}
+
+// adc_search (index.hpp:118-134) with host arrays: one query.
+int aq_adc_search(aq_session* s, const double* q, size_t d, const uint32_t* codes,
+                  size_t n, size_t M, size_t codes_k, const double* dict, size_t cbM,
+                  size_t k, size_t sd, size_t topn, uint32_t* ids_out,
+                  double* scores_out, size_t* count_out) {
+  AQ_TRY(check_session(s));
+  if (n == 0) return ref_error(AQ_E_EMPTY_INDEX, "no quantized datapoints");
+  if (topn < 1) return ref_error(AQ_E_INVALID_ARGUMENT, "topn must be >= 1");
+  if (M != cbM || codes_k > k)
+    return ref_error(AQ_E_DIMENSION_MISMATCH, "code matrix does not match codebook");
+  if (d != cbM * sd)
+    return ref_error(AQ_E_DIMENSION_MISMATCH, "query dimension does not match codebook");
+  aq_codebook* cb = nullptr;
+  aq_codes* cm = nullptr;
+  // the reference does not range-check codes here (index.hpp:121-124); the
+  // device packs them with the codebook's k as bound
+  AQ_TRY(aq_codebook_upload(s, dict, cbM, k, sd, &cb));
+  int st = aq_codes_upload(s, codes, n, M, std::max<size_t>(codes_k, 1), &cm);
+  if (st == AQ_OK) st = aq_dev_adc_search(cm, cb, q, 1, topn, ids_out, scores_out);
+  if (count_out) *count_out = std::min(topn, n);
+  aq_codes_free(cm);
+  aq_codebook_free(cb);
+  return st;
+}
+
+int aq_build_lut(aq_session* s, const double* q, size_t d, const double* dict,
+                 size_t M, size_t k, size_t sd, double* lut_out) {
+  AQ_TRY(check_session(s));
+  if (d != M * sd)
+    return ref_error(AQ_E_DIMENSION_MISMATCH, "query dimension does not match codebook");
+  aq_codebook* cb = nullptr;
+  AQ_TRY(aq_codebook_upload(s, dict, M, k, sd, &cb));
+  double* Qd;
+  int st = upload_queries(s, q, 1, d, 0, &Qd);
+  void* p = nullptr;
+  const int Mp = pad8((int)M);
+  const size_t l32 = (size_t)8 * Mp * 32 * sizeof(float);
+  if (st == AQ_OK) st = scratch(s, 1, M * k * sizeof(double) + l32 + 64, &p);
+  if (st == AQ_OK) {
+    double* l64 = (double*)p;
+    float* lut32 = (float*)(l64 + M * k);
+    float* delta = lut32 + l32 / sizeof(float);
+    cudaMemsetAsync(lut32, 0, l32, s->stream);
+    k_build_lut<<<1, 256, 0, s->stream>>>(Qd, 1, (int)d, cb->d64, (int)M, (int)k, (int)sd,
+                                          l64, lut32, delta);
+    s->launches++;
+    cudaMemcpyAsync(lut_out, l64, M * k * sizeof(double), cudaMemcpyDeviceToHost, s->stream);
+    if (cudaStreamSynchronize(s->stream) != cudaSuccess) st = AQ_E_CUDA;
+  }
+  aq_codebook_free(cb);
+  return st;
+}
+
+// Exact-dot rerank of host candidate lists.
+int aq_dev_rerank(aq_dataset* ds, const double* queries, size_t nq,
+                  const uint32_t* cand_ids, size_t ncand, size_t keep,
+                  uint32_t* ids_out, double* scores_out) {
+  if (!ds) return ref_error(AQ_E_INVALID_ARGUMENT, "null dataset");
+  aq_session* s = ds->s;
+  AQ_TRY(check_session(s));
+  const size_t ke = std::min(keep, ncand);
+  double* Qd;
+  AQ_TRY(upload_queries(s, queries, nq, ds->d, 0, &Qd));
+  uint32_t *cand, *ids;
+  double* sc;
+  AQ_CUDA(cudaMallocAsync(&cand, nq * ncand * sizeof(uint32_t) + 8, s->stream));
+  AQ_CUDA(cudaMallocAsync(&ids, nq * ke * sizeof(uint32_t) + 8, s->stream));
+  AQ_CUDA(cudaMallocAsync(&sc, nq * ke * sizeof(double) + 8, s->stream));
+  AQ_CUDA(cudaMemcpyAsync(cand, cand_ids, nq * ncand * sizeof(uint32_t),
+                          cudaMemcpyHostToDevice, s->stream));
+  int st = rerank_device(ds, Qd, nq, cand, ncand, keep, ids, sc);
+  if (st == AQ_OK) st = sync_and_check(s, "rerank: candidate id out of range");
+  if (st == AQ_OK && nq * ke) {
+    cudaMemcpyAsync(ids_out, ids, nq * ke * sizeof(uint32_t), cudaMemcpyDeviceToHost, s->stream);
+    cudaMemcpyAsync(scores_out, sc, nq * ke * sizeof(double), cudaMemcpyDeviceToHost, s->stream);
+  }
+  cudaFreeAsync(cand, s->stream);
+  cudaFreeAsync(ids, s->stream);
+  cudaFreeAsync(sc, s->stream);
+  cudaStreamSynchronize(s->stream);
+  return st;
+}
+
+// Fused query pipeline: ADC top-`topn` then exact rerank to `keep`, device
+// resident index and dataset, host queries in / host results out.
+int aq_dev_search_rerank(aq_dataset* ds, aq_codes* codes, aq_codebook* cb,
+                         const double* queries, size_t nq, size_t topn, size_t keep,
+                         uint32_t* adc_ids_out, double* adc_scores_out,
+                         uint32_t* ids_out, double* scores_out) {
+  if (!ds || !codes || !cb) return ref_error(AQ_E_INVALID_ARGUMENT, "null argument");
+  aq_session* s = codes->s;
+  AQ_TRY(check_session(s));
+  if (codes->n == 0) return ref_error(AQ_E_EMPTY_INDEX, "no quantized datapoints");
+  if (topn < 1) return ref_error(AQ_E_INVALID_ARGUMENT, "topn must be >= 1");
+  if (ds->n != codes->n)
+    return ref_error(AQ_E_DIMENSION_MISMATCH, "code matrix does not match dataset");
+  const size_t te = std::min(topn, codes->n), ke = std::min(keep, te);
+  double* Qd;
+  AQ_TRY(upload_queries(s, queries, nq, ds->d, 0, &Qd));
+  void* p;
+  AQ_TRY(scratch(s, 5, nq * (te * 12 + ke * 12) + 64, &p));
+  uint32_t* aid = (uint32_t*)p;
+  double* asc = (double*)(((uintptr_t)(aid + nq * te) + 15) & ~(uintptr_t)15);
+  uint32_t* rid = (uint32_t*)(asc + nq * te);
+  double* rsc = (double*)(((uintptr_t)(rid + nq * ke) + 15) & ~(uintptr_t)15);
+  AQ_TRY(adc_search_device(codes, cb, Qd, nq, topn, aid, asc));
+  AQ_TRY(rerank_device(ds, Qd, nq, aid, te, ke, rid, rsc));
+  if (adc_ids_out)
+    AQ_CUDA(cudaMemcpyAsync(adc_ids_out, aid, nq * te * 4, cudaMemcpyDeviceToHost, s->stream));
+  if (adc_scores_out)
+    AQ_CUDA(cudaMemcpyAsync(adc_scores_out, asc, nq * te * 8, cudaMemcpyDeviceToHost, s->stream));
+  if (ids_out)
+    AQ_CUDA(cudaMemcpyAsync(ids_out, rid, nq * ke * 4, cudaMemcpyDeviceToHost, s->stream));
+  if (scores_out)
+    AQ_CUDA(cudaMemcpyAsync(scores_out, rsc, nq * ke * 8, cudaMemcpyDeviceToHost, s->stream));
+  return sync_and_check(s, "search");
+}
+
+}  // extern "C"

@@ -1,0 +1,447 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 anisotropic-PQ hot path (BASELINE.json metric).
+
+Headline workload (BASELINE.json configs[1], "config2"): n = 1,183,514 unit
+vectors, d = 100, M = 50 subspaces x 16 codewords (4-bit codes), T = 0.2.
+One step = one batch of 10,000 queries through the query path: float64 LUT
+build, 4-bit ADC scoring of every (query, point) pair with exact top-100
+selection, exact-dot rerank to top-10 (ids and scores bit-identical to the
+reference). `value` = ADC scores/s (query x point) with index and queries
+resident in HBM; `e2e` = the same through the host-buffer C-ABI call
+(queries H2D, results D2H inside the timed region). The secondary object
+`encode` reports anisotropic-encode points/s (configs[2] shape: n = 1e7,
+d = 128, 3 coordinate-descent sweeps).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N   (weak scaling: one shard per rank)
+
+Data are seeded synthetic stand-ins (GloVe-1.2M is not available offline):
+paper_1908_10396_b200/workload.py.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ADC scores/sec (query x point) + anisotropic-encode points/sec, % HBM roofline"
+UNIT = "scores/s"
+
+
+# ---------------------------------------------------------------------------------------
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--n", type=int, default=1_183_514, help="database rows per shard")
+    p.add_argument("--nq", type=int, default=10_000, help="queries per step")
+    p.add_argument("--encode-n", type=int, default=10_000_000)
+    p.add_argument("--no-encode", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    return p.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "_fallback": True}
+
+
+def traffic_record():
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.lines: list[str] = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.device)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------------
+def build_index(aq, wl, n, nq, seed_shard, session):
+    """Config-2 shard: data, queries, codebook, codes (setup, untimed)."""
+    w = wl.config2(n=n, nq=nq, seed=seed_shard)
+    M, k, sd = w.M, w.k, 2
+    # codebook: per-subspace sample of database sub-vectors (train_apq's
+    # cold-start initialisation, pq.hpp:529-542) + anisotropic encode
+    g = np.random.Generator(np.random.PCG64([seed_shard, 7]))
+    dic = np.empty((M, k, sd))
+    for m in range(M):
+        idx = g.choice(n, size=k, replace=False)
+        dic[m] = w.base[idx, m * sd:(m + 1) * sd]
+    cb = aq.ProductCodebook(M, k, sd, dic.ravel())
+    ds = session.upload_dataset(w.base)
+    dcb = session.upload_codebook(cb)
+    dc = session.alloc_codes(n, M, k)
+    aq.dev_pq_quantize(ds, dcb, aq.ThresholdWeights(w.threshold), 3, dc)
+    return w, cb, ds, dcb, dc
+
+
+def run_ours(args):
+    import torch
+    import ctypes as C
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    from paper_1908_10396_b200 import anisoq as aq
+    from paper_1908_10396_b200 import workload as wl
+
+    L = aq._L
+    sess = aq.Session(local)
+    stream = torch.cuda.ExternalStream(sess.stream, device=torch.device("cuda", local))
+    w, cb, ds, dcb, dc = build_index(aq, wl, args.n, args.nq, rank, sess)
+    n, nq, M, d = args.n, args.nq, w.M, w.d
+    topn, keep = 100, 10
+    Qh = np.ascontiguousarray(w.queries, np.float64)
+    Qd = torch.from_numpy(Qh).cuda(local)
+    te, ke = min(topn, n), min(keep, topn)
+    aid = torch.empty((nq, te), dtype=torch.int32, device=f"cuda:{local}")
+    asc = torch.empty((nq, te), dtype=torch.float64, device=f"cuda:{local}")
+    rid = torch.empty((nq, ke), dtype=torch.int32, device=f"cuda:{local}")
+    rsc = torch.empty((nq, ke), dtype=torch.float64, device=f"cuda:{local}")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+
+    def step_dev():
+        aq._check(L.aq_dev_search_rerank_d(ds.h, dc.h, dcb.h, Qd.data_ptr(), nq, topn, keep,
+                                           aid.data_ptr(), asc.data_ptr(), rid.data_ptr(),
+                                           rsc.data_ptr()))
+
+    hid = np.zeros((nq, ke), np.uint32)
+    hsc = np.zeros((nq, ke), np.float64)
+    Qpin = torch.from_numpy(Qh).pin_memory()
+    hid_t = torch.from_numpy(hid)
+    hsc_t = torch.from_numpy(hsc)
+
+    def step_e2e():
+        aq._check(L.aq_dev_search_rerank(ds.h, dc.h, dcb.h, Qpin.data_ptr(), nq, topn, keep,
+                                         None, None, hid_t.data_ptr(), hsc_t.data_ptr()))
+
+    def timed(fn, steps, warmup, with_clocks=False):
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
+        L.aq_session_timing(sess.h, 1)
+        for slot in range(5):
+            L.aq_session_timer_read(sess.h, slot, None, None, 1)
+        launches0 = sess.launches
+        total = 0.0
+        sampler = ClockSampler(local) if with_clocks else None
+        if sampler:
+            sampler.__enter__()
+        for _ in range(steps):
+            flush.zero_()  # > L2 (126 MB): every step starts cold
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            e1.synchronize()
+            total += e0.elapsed_time(e1)
+        if sampler:
+            sampler.__exit__()
+        torch.cuda.synchronize()
+        launches = sess.launches - launches0
+        kt = {}
+        for slot, name in enumerate(["encode", "adc_score", "adc_merge", "rerank", "lut"]):
+            ms, cnt = C.c_double(0), C.c_uint64(0)
+            L.aq_session_timer_read(sess.h, slot, C.byref(ms), C.byref(cnt), 1)
+            if cnt.value:
+                kt[name] = (ms.value, cnt.value)
+        L.aq_session_timing(sess.h, 0)
+        ms = total / steps
+        if ws > 1:
+            t = torch.tensor([ms], device=f"cuda:{local}")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms = t.item()
+        return ms, launches, kt, (sampler.summary() if sampler else None)
+
+    ms, launches, kt, clocks = timed(step_dev, args.steps, args.warmup, with_clocks=True)
+    value = nq * n * ws / (ms / 1e3)
+    ms_e2e, _, _, _ = timed(step_e2e, args.steps, max(1, args.warmup // 2))
+    e2e = nq * n * ws / (ms_e2e / 1e3)
+
+    # roofline of the dominant kernel: ADC scoring (algorithmic bytes: M/2
+    # code bytes per (query, point) score)
+    pk = peaks()
+    ms_k, cnt_k = kt.get("adc_score", (float("nan"), 1))
+    per_launch_s = ms_k / cnt_k / 1e3
+    alg_bytes = nq * n * (M / 2) / cnt_k
+    achieved = alg_bytes / per_launch_s / 1e9
+    tr = traffic_record().get("adc_score")
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"],
+                "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4),
+                "traffic": tr, "kernel": "k_adc_score",
+                "kernel_ms_per_step": round(ms_k / args.steps, 3),
+                "share_of_step": round((ms_k / args.steps) / ms, 3),
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in pk
+                else "fallback 6650 GB/s",
+                "onchip_ceiling_scores_per_s": round(148 * 64 * 1.965e9 / (M + (-M % 8)), -8),
+                "note": "algorithmic bytes = M/2 code bytes per score (single-pass HBM figure); "
+                        "queries are batched so the kernel is shared-memory-LUT bound"}
+
+    out = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": ws,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded stand-in for GloVe-1.2M shape, config2)",
+           "config": {"workload": "config2", "n_per_gpu": n, "d": d, "M": M, "k": 16,
+                      "queries_per_step": nq, "adc_topn": topn, "rerank_to": keep,
+                      "threshold": w.threshold, "codebook": "sampled sub-vectors + 3-sweep "
+                      "anisotropic encode (trained codebook pending)",
+                      "filter_dtype": "f32 (bounded), results f64 bit-exact",
+                      "l2": "flushed (256 MiB write) before every timed step",
+                      "parallelism": f"dp{ws} (row shards)"},
+           "e2e": {"value": round(e2e, 1), "unit": UNIT,
+                   "h2d_bytes_per_step": int(nq * d * 8),
+                   "d2h_bytes_per_step": int(nq * ke * (4 + 8))},
+           "gpu_launches": int(launches), "roofline": roofline, "clocks": clocks,
+           "kernel_ms": {k: round(v[0] / args.steps, 3) for k, v in kt.items()}}
+
+    if not args.no_encode:
+        out["encode"] = bench_encode(args, aq, wl, sess, stream, flush, local, ws, pk)
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args, w, cb, dc, n)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def bench_encode(args, aq, wl, sess, stream, flush, local, ws, pk):
+    """configs[2]: n = 1e7, d = 128, M = 64, 3 sweeps, lognormal norms."""
+    import torch
+    import ctypes as C
+
+    L = aq._L
+    w = wl.config3(n=args.encode_n)
+    n = args.encode_n
+    ds = sess.upload_dataset(w.base)
+    cb = sess.upload_codebook(aq.ProductCodebook(64, 16, 2, w.codebook))
+    out = sess.alloc_codes(n, 64, 16)
+    wt = aq.ThresholdWeights(w.threshold, "parallel_only")
+    for _ in range(args.warmup):
+        aq.dev_pq_quantize(ds, cb, wt, 3, out)
+    L.aq_session_timing(sess.h, 1)
+    L.aq_session_timer_read(sess.h, 0, None, None, 1)
+    tot = 0.0
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        aq.dev_pq_quantize(ds, cb, wt, 3, out)
+        e1.record(stream)
+        e1.synchronize()
+        tot += e0.elapsed_time(e1)
+    ms_k, cnt = C.c_double(0), C.c_uint64(0)
+    L.aq_session_timer_read(sess.h, 0, C.byref(ms_k), C.byref(cnt), 1)
+    L.aq_session_timing(sess.h, 0)
+    ms = tot / args.steps
+    value = n * ws / (ms / 1e3)
+    # e2e: host rows in -> host codes out through the C ABI (pq_quantize)
+    codes_h = np.zeros((n, 64), np.uint32)
+    keep = []
+    cw = aq._weights(wt, n, keep)
+    xs = np.ascontiguousarray(w.base)
+    t0 = time.perf_counter()
+    aq._check(L.aq_pq_quantize(sess.h, xs.ctypes.data, n, 128, w.codebook.ctypes.data, 64, 16, 2,
+                               C.byref(cw), 3, codes_h.ctypes.data))
+    e2e_s = time.perf_counter() - t0
+    per_launch = ms_k.value / max(cnt.value, 1) / 1e3
+    ops_per_pt = 64 * 16 * (3 + 3 * 8)   # M k [(sd+1) + S (sd+6)]
+    fp32_peak = 148 * 128 * 1.965e9      # FP32 pipe ops/s (FFMA = 1 op)
+    achieved_ops = n * ops_per_pt / per_launch
+    del ds, cb, out
+    return {"metric": "anisotropic-encode points/sec", "value": round(value, 1),
+            "unit": "points/s", "ms_per_step": round(ms, 3), "workload": "config3",
+            "n_per_gpu": n, "d": 128, "M": 64, "passes": 3,
+            "roofline": {"bound": "fp32", "achieved": round(achieved_ops / 1e12, 2),
+                         "peak": round(fp32_peak / 1e12, 2), "unit": "Tops/s",
+                         "frac": round(achieved_ops / fp32_peak, 4),
+                         "note": "27,648 algorithmic f32 ops/point (SURVEY.md §8(d)); HBM side "
+                                 "544 B/point is << HBM peak"},
+            "e2e": {"value": round(n / e2e_s, 1), "unit": "points/s",
+                    "h2d_bytes_per_step": int(n * 128 * 4), "d2h_bytes_per_step": int(n * 64 * 4),
+                    "note": "host wall clock of the synchronous aq_pq_quantize call"}}
+
+
+def cpu_baseline(args, w, cb, dc, n):
+    """The reference itself (oracle/_ref, compiled in place) on this host's
+    cores, on a bounded sample of the same step (queries subset x full shard)."""
+    try:
+        from oracle import Port, Reference
+    except Exception as e:  # pragma: no cover
+        return {"value": None, "error": str(e)}
+    codes = dc.download().codes
+    if Reference.available():
+        R, kind = Reference(), "reference"
+        cores = os.cpu_count() or 1
+    else:
+        R, kind = Port(), "port"
+        cores = 1
+    Q = np.ascontiguousarray(w.queries, np.float64)
+    x64 = w.base.astype(np.float64)
+    nq_s = 4
+    while True:
+        t0 = time.perf_counter()
+        ids, _ = (R.adc_search_batch(Q[:nq_s], codes, 16, cb.dictionaries, w.M, 16, 2, 100,
+                                     threads=cores) if kind == "reference" else
+                  R.adc_search_batch(Q[:nq_s], codes, 16, cb.dictionaries, w.M, 16, 2, 100))
+        R.rerank(Q[:nq_s], x64, ids, 10)
+        dt = time.perf_counter() - t0
+        if dt > args.cpu_seconds / 3 or nq_s >= len(Q):
+            break
+        nq_s = min(len(Q), int(nq_s * max(2.0, args.cpu_seconds / 2 / max(dt, 1e-3))))
+    return {"value": round(nq_s * n / dt, 1), "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"{nq_s} queries x {n} points (adc_search top-100 + rerank to 10), "
+                      f"{dt:.1f} s"}
+
+
+def run_reference(args):
+    """--impl reference: the reference CPU implementation (oracle/_ref) on the
+    host cores, same metric/config, each step a bounded query sample."""
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return
+    from oracle import Port, Reference
+    from paper_1908_10396_b200 import workload as wl
+
+    n = args.n
+    w = wl.config2(n=n, nq=args.nq, seed=0)
+    M = w.M
+    g = np.random.Generator(np.random.PCG64([0, 7]))
+    dic = np.empty((M, 16, 2))
+    for m in range(M):
+        idx = g.choice(n, size=16, replace=False)
+        dic[m] = w.base[idx, m * 2:(m + 1) * 2]
+    dic = dic.ravel()
+    if Reference.available():
+        R, kind, cores = Reference(), "reference", os.cpu_count() or 1
+    else:
+        R, kind, cores = Port(), "port", 1
+    x64 = w.base.astype(np.float64)
+    hp = np.empty(n)
+    norms = np.sqrt(np.einsum("ij,ij->i", x64, x64))
+    rho = (w.threshold / norms) ** 2
+    hp[:] = (w.d - 1) * rho / (1 - rho)
+    ho = np.ones(n)
+    # index build with the reference's own encoder (setup, untimed)
+    codes = (R.pq_quantize(x64, dic, M, 16, 2, hp, ho, 3, threads=cores) if kind == "reference"
+             else R.pq_quantize(x64, dic, M, 16, 2, hp, ho, 3))
+    Q = np.ascontiguousarray(w.queries, np.float64)
+    per_step = max(1, min(len(Q), int(os.environ.get("REF_QUERIES_PER_STEP", "16"))))
+
+    def step(i):
+        q = Q[(i * per_step) % len(Q):][:per_step]
+        ids, _ = (R.adc_search_batch(q, codes, 16, dic, M, 16, 2, 100, threads=cores)
+                  if kind == "reference" else R.adc_search_batch(q, codes, 16, dic, M, 16, 2, 100))
+        R.rerank(q, x64, ids, 10)
+        return len(q)
+
+    for i in range(args.warmup):
+        step(i)
+    t0 = time.perf_counter()
+    done = 0
+    for i in range(args.steps):
+        done += step(i)
+    dt = time.perf_counter() - t0
+    value = done * n / dt
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(value, 1), "unit": UNIT,
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded stand-in for GloVe-1.2M shape, config2)",
+        "config": {"workload": "config2", "n_per_gpu": n, "d": w.d, "M": M, "k": 16,
+                   "queries_per_step": per_step, "adc_topn": 100, "rerank_to": 10},
+        "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": f"{per_step} queries x {n} points per step"},
+        "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0}}), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

@@ -109,6 +109,13 @@ int aq_session_sync(aq_session* s);
 /* Kernel launches issued by this session so far (evidence counter). */
 uint64_t aq_session_launches(aq_session* s);
 
+/* Per-kernel CUDA-event timers on the session stream (evidence for the
+ * roofline in bench.py). Slots: 0 encode, 1 adc_score, 2 adc_merge,
+ * 3 rerank, 4 lut. */
+int aq_session_timing(aq_session* s, int enable);
+int aq_session_timer_read(aq_session* s, int slot, double* ms, uint64_t* count,
+                          int reset);
+
 /* ---- device-resident objects ------------------------------------------- */
 typedef struct aq_dataset aq_dataset;   /* x (fp32 n x d) + norms (fp64) */
 typedef struct aq_codebook aq_codebook; /* fp64 dictionaries + fp32 staging */
@@ -193,6 +200,11 @@ int aq_dev_search_rerank(aq_dataset* ds, aq_codes* codes, aq_codebook* cb,
                          size_t keep, uint32_t* adc_ids_out,
                          double* adc_scores_out, uint32_t* ids_out,
                          double* scores_out);
+int aq_dev_search_rerank_d(aq_dataset* ds, aq_codes* codes, aq_codebook* cb,
+                           const double* q_dev, size_t nq, size_t topn,
+                           size_t keep, uint32_t* adc_ids_dev,
+                           double* adc_scores_dev, uint32_t* ids_dev,
+                           double* scores_dev);
 int aq_adc_search(aq_session* s, const double* q, size_t d,
                   const uint32_t* codes, size_t n, size_t M, size_t codes_k,
                   const double* dictionaries, size_t cb_M, size_t k,

@@ -53,6 +53,9 @@ _SIGS = {
     "aq_session_stream": (_VP, [_VP]),
     "aq_session_sync": (_I, [_VP]),
     "aq_session_launches": (C.c_uint64, [_VP]),
+    "aq_session_timing": (_I, [_VP, _I]),
+    "aq_session_timer_read": (_I, [_VP, _I, _VP, _VP, _I]),
+    "aq_dev_search_rerank_d": (_I, [_VP, _VP, _VP, _VP, _SZ, _SZ, _SZ, _VP, _VP, _VP, _VP]),
     "aq_dataset_upload": (_I, [_VP, _VP, _SZ, _SZ, _PP]),
     "aq_dataset_wrap_device": (_I, [_VP, _VP, _SZ, _SZ, _PP]),
     "aq_dataset_free": (_I, [_VP]),

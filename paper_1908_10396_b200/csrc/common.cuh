@@ -19,6 +19,7 @@
 
 #include <cstdio>
 #include <string>
+#include <vector>
 
 #include "../../include/anisoq_b200.h"
 
@@ -71,8 +72,16 @@ struct Scratch {
 
 }  // namespace aqd
 
+// Optional per-kernel CUDA-event timers (bench.py's roofline evidence).
+enum AqTimer { AQ_T_ENCODE = 0, AQ_T_ADC_SCORE = 1, AQ_T_ADC_MERGE = 2,
+               AQ_T_RERANK = 3, AQ_T_LUT = 4, AQ_T_COUNT = 8 };
+
 struct aq_session {
   int device = 0;
+  bool timing = false;
+  std::vector<cudaEvent_t> tev[AQ_T_COUNT];  // start/end pairs
+  double tms[AQ_T_COUNT] = {0};
+  uint64_t tcount[AQ_T_COUNT] = {0};
   cudaStream_t stream = nullptr;
   uint64_t launches = 0;
   int num_sms = 148;
@@ -112,6 +121,8 @@ int scratch(aq_session* s, int slot, size_t bytes, void** out);
 int check_session(aq_session* s);
 int sync_and_check(aq_session* s, const char* what);  // reads DevError
 int clear_dev_error(aq_session* s);
+
+__host__ __device__ void timer_mark(aq_session* s, int slot);  // records an event if timing
 
 __host__ __device__ inline size_t pairs_of(size_t d) { return (d + 1) / 2; }
 inline size_t tiled_floats(size_t n, size_t d) {

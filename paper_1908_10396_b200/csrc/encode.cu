@@ -615,8 +615,10 @@ int run_encode(aq_dataset* ds, aq_codebook* cb, const aq_weights* w,
     if (sm > 200 * 1024)
       return ref_error(AQ_E_UNSUPPORTED, "M too large for the fast encoder");
     const unsigned grid = (unsigned)((ds->n + kEncThreads - 1) / kEncThreads);
+    timer_mark(s, AQ_T_ENCODE);
     k_encode_sd2<<<grid, kEncThreads, sm, s->stream>>>(a, g_stats);
     AQ_LAUNCHED(s);
+    timer_mark(s, AQ_T_ENCODE);
   } else {
     void* work;
     AQ_TRY(scratch(s, 3, ds->n * codes->stride + 16, &work));

@@ -399,9 +399,11 @@ int adc_search_device(aq_codes* codes, aq_codebook* cb, const double* Qd,
   float* lut32 = (float*)(lut64 + nq * M * k);
   float* delta = lut32 + lut32_b / sizeof(float);
   AQ_CUDA(cudaMemsetAsync(lut32, 0, lut32_b, s->stream));
+  timer_mark(s, AQ_T_LUT);
   k_build_lut<<<(unsigned)nq, 256, 0, s->stream>>>(Qd, (int)nq, (int)d, cb->d64, M, k,
                                                   (int)cb->sd, lut64, lut32, delta);
   AQ_LAUNCHED(s);
+  timer_mark(s, AQ_T_LUT);
 
   const bool fast = codes->bits == 4 && topn <= (size_t)kMaxTopN && M <= 1024;
   std::vector<int> hflag(nq, fast ? 0 : 1);
@@ -429,12 +431,16 @@ int adc_search_device(aq_codes* codes, aq_codebook* cb, const double* Qd,
       return ref_error(AQ_E_UNSUPPORTED, "ADC working set exceeds shared memory");
     AQ_CUDA(cudaFuncSetAttribute(k_adc_score, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
+    timer_mark(s, AQ_T_ADC_SCORE);
     k_adc_score<<<dim3((unsigned)R, (unsigned)nqb), kTileP, smem, s->stream>>>(sa);
     AQ_LAUNCHED(s);
+    timer_mark(s, AQ_T_ADC_SCORE);
     MergeArgs ma{obuf, ocnt, oflag, (int)R, cap, N, (int)topn_eff, delta, lut64,
                  codes->data, (int)codes->stride, codes->bits, M, k, ids, scores};
+    timer_mark(s, AQ_T_ADC_MERGE);
     k_adc_merge<<<(unsigned)nq, 256, 0, s->stream>>>(ma);
     AQ_LAUNCHED(s);
+    timer_mark(s, AQ_T_ADC_MERGE);
     AQ_CUDA(cudaMemcpyAsync(hflag.data(), oflag, nq * sizeof(int), cudaMemcpyDeviceToHost,
                             s->stream));
     AQ_CUDA(cudaStreamSynchronize(s->stream));
@@ -538,10 +544,12 @@ int rerank_device(aq_dataset* ds, const double* Qd, size_t nq,
   const int wpb = std::max(1, std::min(8, (int)(40 * 1024 / (P * 12))));
   const size_t smem = (size_t)wpb * P * 12;
   AQ_TRY(clear_dev_error(s));
+  timer_mark(s, AQ_T_RERANK);
   k_rerank<<<(unsigned)((nq + wpb - 1) / wpb), wpb * 32, smem, s->stream>>>(
       ds->xt, (int)pairs_of(ds->d), (int)ds->d, Qd, (int)nq, cand, (int)ncand,
       (int)keep_eff, ids, sc, ds->n, s->err);
   AQ_LAUNCHED(s);
+  timer_mark(s, AQ_T_RERANK);
   return AQ_OK;
 }
 
@@ -683,6 +691,22 @@ int aq_dev_rerank(aq_dataset* ds, const double* queries, size_t nq,
   cudaFreeAsync(sc, s->stream);
   cudaStreamSynchronize(s->stream);
   return st;
+}
+
+// Device-pointer pipeline (queries and all outputs on the device).
+int aq_dev_search_rerank_d(aq_dataset* ds, aq_codes* codes, aq_codebook* cb,
+                           const double* q_dev, size_t nq, size_t topn, size_t keep,
+                           uint32_t* adc_ids_dev, double* adc_scores_dev,
+                           uint32_t* ids_dev, double* scores_dev) {
+  if (!ds || !codes || !cb) return ref_error(AQ_E_INVALID_ARGUMENT, "null argument");
+  aq_session* s = codes->s;
+  AQ_TRY(check_session(s));
+  if (ds->n != codes->n)
+    return ref_error(AQ_E_DIMENSION_MISMATCH, "code matrix does not match dataset");
+  const size_t te = std::min(topn, codes->n), ke = std::min(keep, te);
+  AQ_TRY(adc_search_device(codes, cb, q_dev, nq, topn, adc_ids_dev, adc_scores_dev));
+  AQ_TRY(rerank_device(ds, q_dev, nq, adc_ids_dev, te, ke, ids_dev, scores_dev));
+  return sync_and_check(s, "search");
 }
 
 // Fused query pipeline: ADC top-`topn` then exact rerank to `keep`, device

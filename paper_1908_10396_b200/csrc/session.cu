@@ -54,6 +54,14 @@ int scratch(aq_session* s, int slot, size_t bytes, void** out) {
   return AQ_OK;
 }
 
+void timer_mark(aq_session* s, int slot) {
+  if (!s->timing) return;
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, s->stream);
+  s->tev[slot].push_back(e);
+}
+
 int clear_dev_error(aq_session* s) {
   AQ_CUDA(cudaMemsetAsync(s->err, 0xff, sizeof(DevError), s->stream));
   return AQ_OK;
@@ -294,6 +302,41 @@ int aq_session_sync(aq_session* s) {
 }
 
 uint64_t aq_session_launches(aq_session* s) { return s ? s->launches : 0; }
+
+// Kernel timers: enable=1 starts recording CUDA events around the timed
+// kernels (encode, adc_score, adc_merge, rerank, lut) on the session stream;
+// aq_session_timer_read syncs, folds the recorded pairs into totals and
+// returns total milliseconds and launch count for a slot.
+int aq_session_timing(aq_session* s, int enable) {
+  AQ_TRY(check_session(s));
+  s->timing = enable != 0;
+  return AQ_OK;
+}
+
+int aq_session_timer_read(aq_session* s, int slot, double* ms, uint64_t* count,
+                          int reset) {
+  AQ_TRY(check_session(s));
+  if (slot < 0 || slot >= AQ_T_COUNT) return ref_error(AQ_E_INVALID_ARGUMENT, "bad timer slot");
+  AQ_CUDA(cudaStreamSynchronize(s->stream));
+  for (int t = 0; t < AQ_T_COUNT; ++t) {
+    auto& v = s->tev[t];
+    for (size_t e = 0; e + 1 < v.size(); e += 2) {
+      float x = 0.0f;
+      AQ_CUDA(cudaEventElapsedTime(&x, v[e], v[e + 1]));
+      s->tms[t] += x;
+      s->tcount[t] += 1;
+    }
+    for (auto ev : v) cudaEventDestroy(ev);
+    v.clear();
+  }
+  if (ms) *ms = s->tms[slot];
+  if (count) *count = s->tcount[slot];
+  if (reset) {
+    s->tms[slot] = 0;
+    s->tcount[slot] = 0;
+  }
+  return AQ_OK;
+}
 
 static int dataset_from_device_rows(aq_session* s, const float* xdev, size_t n,
                                     size_t d, aq_dataset** out) {

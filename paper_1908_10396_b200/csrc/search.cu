@@ -5,13 +5,14 @@
 //
 // Exactness. The reference scores a point by summing M
 // float64 LUT entries in subspace order and orders hits by (score desc,
-// index asc). The scoring kernel sums float32 copies of the entries (error
-// <= delta_q = (Mp+2) 2^-24 sum_m max_j |lut_mj| per score) and keeps, per
-// query, every point whose float32 score is >= theta - 2 delta_q, theta being
-// a float32 score that at least N points reach. The merge kernel re-scores
-// that window in float64 in the reference's order and sorts exactly, so ids
-// AND scores equal the reference's. Inputs whose windows do not fit (massive
-// ties, N > 512) take an exact full-sort fallback.
+// index asc). The scoring kernel sums 13-bit integer images of the entries
+// (v = rint(lut / s), s = max|lut| / 4095; the integer sum S is exact and
+// |s S - score| <= M s / 2) and keeps, per query, every point with
+// S >= theta - M - 1, theta being an integer score that at least N points
+// reach. The merge kernel re-scores that window in float64 in the
+// reference's order and sorts exactly, so ids AND scores equal the
+// reference's. Inputs whose windows do not fit (massive ties, N > 512) take
+// an exact full-sort fallback.
 #include <algorithm>
 #include <vector>
 
@@ -22,46 +23,52 @@ namespace aqd {
 int sort_scores_desc(aq_session* s, const double* scores, uint32_t* idx,
                      size_t n);
 
-constexpr int kQB = 16;       // queries per scoring CTA (8 float2 pairs)
-constexpr int kTileP = 256;   // points per tile == threads per CTA
-constexpr int kMaxTopN = 512; // fast path limit
+constexpr int kQP = 16;          // query pairs per scoring CTA
+constexpr int kQB = 2 * kQP;     // queries per scoring CTA
+constexpr int kTileP = 256;      // points per tile == threads per CTA
+constexpr int kMaxTopN = 512;    // fast path limit
 constexpr int kMergeCap = 2048;
-
-__host__ __device__ inline int pad8(int M) { return (M + 7) & ~7; }
+constexpr int kQMax = 4095;      // |v| <= 4095: 13-bit fields, 8 adds per 16-bit lane
 
 // ---- LUT ---------------------------------------------------------------------
-// One CTA per query. lut64[q][m][j] (reference order of build_lut), lut32 in
-// the scoring layout [qblock][pair][Mp][16] float2 (zero padded), delta[q].
+// One CTA per query: lut64[q][m][j] exactly as build_lut computes it, and the
+// integer filter table: v = rint(lut / s) + 4096 with s = max|lut| / 4095, so
+// |s v' - lut| <= s / 2 per entry and a sum of M entries is within M s / 2 of
+// the exact score. Two queries share a 32-bit word (low = even query);
+// layout [qblock][pair][M][16] words.
 __global__ void k_build_lut(const double* __restrict__ Q, int nq, int d,
                             const double* __restrict__ cb, int M, int k,
                             int sd, double* __restrict__ lut64,
-                            float* __restrict__ lut32,
-                            float* __restrict__ delta) {
-  __shared__ unsigned maxabs[1024];
+                            uint16_t* __restrict__ lutq) {
+  __shared__ double red[32];
   const int q = blockIdx.x;
-  const int Mp = pad8(M);
-  for (int m = threadIdx.x; m < M; m += blockDim.x) maxabs[m] = 0u;
-  __syncthreads();
   const double* qv = Q + (size_t)q * d;
-  const int qb = q / kQB, qi = q % kQB;
-  float* L = lut32 + (((size_t)qb * (kQB / 2) + qi / 2) * Mp) * 32 + (qi & 1);
+  double* L = lut64 + (size_t)q * M * k;
+  double mx = 0.0;
   for (int e = threadIdx.x; e < M * k; e += blockDim.x) {
-    const int m = e / k, j = e % k;
+    const int m = e / k;
     const double* c = cb + (size_t)e * sd;
-    double s = 0.0;  // detail::dot (geometry.hpp:170-174)
-    for (int t = 0; t < sd; ++t) s = __dadd_rn(s, __dmul_rn(qv[m * sd + t], c[t]));
-    lut64[(size_t)q * M * k + e] = s;
-    if (j < 16) L[(m * 16 + j) * 2] = (float)s;
-    atomicMax(&maxabs[m], __float_as_uint(__double2float_ru(fabs(s))));
+    double v = 0.0;  // detail::dot (geometry.hpp:170-174)
+    for (int t = 0; t < sd; ++t) v = __dadd_rn(v, __dmul_rn(qv[m * sd + t], c[t]));
+    L[e] = v;
+    mx = fmax(mx, fabs(v));
   }
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double S = 0.0;
-    for (int m = 0; m < M; ++m) S += (double)__uint_as_float(maxabs[m]);
-    // float32 sum of Mp terms: <= (Mp-1) u sum|t|, entry rounding <= u sum|t|,
-    // float64 reference rounding <= M 2^-53 sum|t|; 1% and 2u slack on top.
-    const double dl = (double)(Mp + 2) * 5.9604644775390625e-08 * S * 1.01 + 1e-30;
-    delta[q] = __double2float_ru(dl);
+  mx = 0.0;
+  for (int t = 0; t < (int)(blockDim.x >> 5); ++t) mx = fmax(mx, red[t]);
+  const double sc = mx > 0.0 ? mx / kQMax : 1.0;
+  const int qb = q / kQB, qi = q % kQB;
+  uint16_t* T = lutq + ((((size_t)qb * kQP + qi / 2) * M) * 16) * 2 + (qi & 1);
+  for (int e = threadIdx.x; e < M * 16; e += blockDim.x) {
+    const int m = e / 16, j = e % 16;
+    int v = 0;
+    if (j < k) {
+      v = (int)rint(L[m * k + j] / sc);
+      v = max(-kQMax, min(kQMax, v));
+    }
+    T[(size_t)e * 2] = (uint16_t)(v + kQMax + 1);
   }
 }
 
@@ -71,45 +78,37 @@ struct ScoreArgs {
   const uint8_t* codes;
   size_t n;
   int stride;      // bytes per code row
-  const float* lut32;
-  const float* delta;
-  int Mp;
+  const uint32_t* lutq;
+  int M;
   int nq;
   int N;           // top-N
   int cap;         // candidate buffer per query
   size_t range_len;
   int R;           // number of point ranges
-  uint2* out_buf;  // [q][r][cap] {score bits, index}
+  uint2* out_buf;  // [q][r][cap] {integer score, index}
   int* out_cnt;    // [q][r]
   int* out_flag;   // [q]
 };
 
-__device__ __forceinline__ unsigned f2o(float f) {  // order-preserving
-  const unsigned b = __float_as_uint(f);
-  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
-}
-__device__ __forceinline__ float o2f(unsigned o) {
-  return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
-}
-
-// Warp-cooperative: the N-th largest score among buf[0..cnt) as an ordered
-// key (0 when cnt < N).
-__device__ unsigned warp_nth_largest(const uint2* buf, int cnt, int N) {
-  if (cnt < N) return 0u;
+// Warp-cooperative: the N-th largest integer score among buf[0..cnt);
+// false when cnt < N.
+__device__ bool warp_nth_largest(const uint2* buf, int cnt, int N, unsigned* out) {
+  if (cnt < N) return false;
   const int lane = threadIdx.x & 31;
   unsigned T = 0u;
   for (int bit = 31; bit >= 0; --bit) {
     const unsigned cand = T | (1u << bit);
     int c = 0;
-    for (int e = lane; e < cnt; e += 32) c += f2o(__uint_as_float(buf[e].x)) >= cand;
+    for (int e = lane; e < cnt; e += 32) c += buf[e].x >= cand;
     c = __reduce_add_sync(0xffffffffu, c);
     if (c >= N) T = cand;
   }
-  return T;
+  *out = T;
+  return true;
 }
 
 // Keep only entries >= cut (warp-cooperative, in place); returns new count.
-__device__ int warp_compact(uint2* buf, int cnt, float cut) {
+__device__ int warp_compact(uint2* buf, int cnt, int cut) {
   const int lane = threadIdx.x & 31;
   int kept = 0;
   for (int base = 0; base < cnt; base += 32) {
@@ -118,7 +117,7 @@ __device__ int warp_compact(uint2* buf, int cnt, float cut) {
     bool keep = false;
     if (e < cnt) {
       v = buf[e];
-      keep = __uint_as_float(v.x) >= cut;
+      keep = (int)v.x >= cut;
     }
     const unsigned bal = __ballot_sync(0xffffffffu, keep);
     __syncwarp();
@@ -129,27 +128,29 @@ __device__ int warp_compact(uint2* buf, int cnt, float cut) {
   return kept;
 }
 
+// Integer-LUT ADC over one (query block, point range). Each lane owns a point;
+// per 8 subspaces and query pair, 8 LDS.32 words (two 16-bit entries each)
+// are summed with IADD3 into packed 16-bit lanes, then split into 32-bit
+// accumulators. Shared-memory delivery is the bound: 64 lookups per
+// wavefront. MP > 0 fixes M at compile time (immediate LDS offsets).
+template <int MP>
 __global__ void __launch_bounds__(kTileP, 1) k_adc_score(const ScoreArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int Mp = a.Mp;
-  float2* L = reinterpret_cast<float2*>(smem);  // [8 pairs][Mp][16]
-  float* cut = reinterpret_cast<float*>(L + 8 * Mp * 16);
-  float* dl = cut + kQB;
-  int* cnt = reinterpret_cast<int*>(dl + kQB);
+  const int M = MP > 0 ? MP : a.M;
+  uint32_t* T = reinterpret_cast<uint32_t*>(smem);  // [kQP][M][16]
+  int* cut = reinterpret_cast<int*>(T + kQP * M * 16);
+  int* cnt = cut + kQB;
   int* flag = cnt + kQB;
   uint2* buf = reinterpret_cast<uint2*>(flag + kQB);  // [kQB][cap]
   const int qb = blockIdx.y, r = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   {
-    const float4* src = reinterpret_cast<const float4*>(
-        a.lut32 + (size_t)qb * 8 * Mp * 32);
-    float4* dst = reinterpret_cast<float4*>(L);
-    for (int t = threadIdx.x; t < 8 * Mp * 8; t += blockDim.x) dst[t] = src[t];
+    const uint4* src = reinterpret_cast<const uint4*>(a.lutq + (size_t)qb * kQP * M * 16);
+    uint4* dst = reinterpret_cast<uint4*>(T);
+    for (int t = threadIdx.x; t < kQP * M * 4; t += blockDim.x) dst[t] = src[t];
   }
   if (threadIdx.x < kQB) {
-    const int q = qb * kQB + threadIdx.x;
-    cut[threadIdx.x] = -INFINITY;
-    dl[threadIdx.x] = q < a.nq ? a.delta[q] : 0.0f;
+    cut[threadIdx.x] = INT_MIN;
     cnt[threadIdx.x] = 0;
     flag[threadIdx.x] = 0;
   }
@@ -157,39 +158,51 @@ __global__ void __launch_bounds__(kTileP, 1) k_adc_score(const ScoreArgs a) {
   const size_t start = (size_t)r * a.range_len;
   const size_t end = min(a.n, start + a.range_len);
   const int cap = a.cap;
-  const int nchunk = Mp >> 3;
+  const int nchunk = (M + 7) >> 3;
+  const int margin = M + 1;  // 2 * (M s / 2) / s, plus one unit for float64
   for (size_t tb = start; tb < end; tb += kTileP) {
     const size_t p = tb + threadIdx.x;
     if (p < end) {
-      float acc[kQB];
+      uint32_t acc[kQB];
 #pragma unroll
-      for (int q = 0; q < kQB; ++q) acc[q] = 0.0f;
+      for (int q = 0; q < kQB; ++q) acc[q] = 0u;
       const uint32_t* crow = reinterpret_cast<const uint32_t*>(a.codes + p * a.stride);
-      for (int c = 0; c < nchunk; ++c) {
-        const uint32_t w = __ldg(crow + c);
+#pragma unroll 1
+      for (int ch = 0; ch < nchunk; ++ch) {
+        const uint32_t w = __ldg(crow + ch);
+        const int valid = M - ch * 8;  // >= 8 except in the tail chunk
         int off[8];
 #pragma unroll
-        for (int t = 0; t < 8; ++t) off[t] = (c * 8 + t) * 16 + ((w >> (4 * t)) & 15u);
+        for (int t = 0; t < 8; ++t) off[t] = (ch * 8 + t) * 16 + ((w >> (4 * t)) & 15u);
+        if (valid >= 8) {
 #pragma unroll
-        for (int pr = 0; pr < 8; ++pr) {
-          const float2* Lp = L + pr * Mp * 16;
-          float s0 = acc[2 * pr], s1 = acc[2 * pr + 1];
-#pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            const float2 v = Lp[off[t]];
-            s0 += v.x;
-            s1 += v.y;
+          for (int qp = 0; qp < kQP; ++qp) {
+            const uint32_t* Tq = T + qp * M * 16;
+            const uint32_t pk = (Tq[off[0]] + Tq[off[1]] + Tq[off[2]]) +
+                                (Tq[off[3]] + Tq[off[4]] + Tq[off[5]]) +
+                                (Tq[off[6]] + Tq[off[7]]);
+            acc[2 * qp] += pk & 0xffffu;
+            acc[2 * qp + 1] += pk >> 16;
           }
-          acc[2 * pr] = s0;
-          acc[2 * pr + 1] = s1;
+        } else {
+#pragma unroll
+          for (int qp = 0; qp < kQP; ++qp) {
+            const uint32_t* Tq = T + qp * M * 16;
+            uint32_t pk = 0u;
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+              if (t < valid) pk += Tq[off[t]];
+            acc[2 * qp] += pk & 0xffffu;
+            acc[2 * qp + 1] += pk >> 16;
+          }
         }
       }
 #pragma unroll
       for (int q = 0; q < kQB; ++q) {
-        if (acc[q] >= cut[q]) {
+        if ((int)acc[q] >= cut[q]) {
           const int pos = atomicAdd(&cnt[q], 1);
           if (pos < cap)
-            buf[q * cap + pos] = make_uint2(__float_as_uint(acc[q]), (unsigned)p);
+            buf[q * cap + pos] = make_uint2(acc[q], (unsigned)p);
           else
             flag[q] = 1;
         }
@@ -199,17 +212,14 @@ __global__ void __launch_bounds__(kTileP, 1) k_adc_score(const ScoreArgs a) {
     // shrink buffers that could overflow during the next tile
     for (int q = warp; q < kQB; q += kTileP / 32) {
       const int c = min(cnt[q], cap);
-      if (c > cap - kTileP && !flag[q]) {
-        const unsigned T = warp_nth_largest(buf + q * cap, c, a.N);
-        if (T) {
-          const float nc = __fsub_rd(o2f(T), 2.0f * dl[q]);
-          const float cq = fmaxf(cut[q], nc);
-          const int kept = warp_compact(buf + q * cap, c, cq);
-          if (lane == 0) {
-            cut[q] = cq;
-            cnt[q] = kept;
-            if (kept > cap - kTileP) flag[q] = 1;  // window too large: ties
-          }
+      unsigned th;
+      if (c > cap - kTileP && !flag[q] && warp_nth_largest(buf + q * cap, c, a.N, &th)) {
+        const int cq = max(cut[q], (int)th - margin);
+        const int kept = warp_compact(buf + q * cap, c, cq);
+        if (lane == 0) {
+          cut[q] = cq;
+          cnt[q] = kept;
+          if (kept > cap - kTileP) flag[q] = 1;  // window too large: ties
         }
       }
       __syncwarp();
@@ -220,8 +230,9 @@ __global__ void __launch_bounds__(kTileP, 1) k_adc_score(const ScoreArgs a) {
   for (int q = warp; q < kQB; q += kTileP / 32) {
     const int gq = qb * kQB + q;
     int c = min(cnt[q], cap);
-    const unsigned T = warp_nth_largest(buf + q * cap, c, a.N);
-    if (T) c = warp_compact(buf + q * cap, c, fmaxf(cut[q], __fsub_rd(o2f(T), 2.0f * dl[q])));
+    unsigned th;
+    if (warp_nth_largest(buf + q * cap, c, a.N, &th))
+      c = warp_compact(buf + q * cap, c, max(cut[q], (int)th - margin));
     if (gq < a.nq) {
       uint2* dst = a.out_buf + ((size_t)gq * a.R + r) * cap;
       for (int e = lane; e < c; e += 32) dst[e] = buf[q * cap + e];
@@ -241,7 +252,6 @@ struct MergeArgs {
   const int* cnt;
   int* flag;
   int R, cap, N, topn_eff;
-  const float* delta;
   const double* lut64;
   const uint8_t* codes;
   int stride, bits, M, k;
@@ -261,17 +271,18 @@ __global__ void __launch_bounds__(256) k_adc_merge(const MergeArgs a) {
   // total entries
   const uint2* lists = a.buf + (size_t)q * a.R * a.cap;
   const int* cnts = a.cnt + (size_t)q * a.R;
-  // global N-th largest over the union (ordered-key binary search)
+  // global N-th largest integer score over the union (binary search)
   unsigned T = 0u;
   int total = 0;
   for (int r = 0; r < a.R; ++r) total += cnts[r];
-  if (total >= a.N) {
+  const bool have = total >= a.N;
+  if (have) {
     for (int bit = 31; bit >= 0; --bit) {
       const unsigned cand = T | (1u << bit);
       int c = 0;
       for (int r = 0; r < a.R; ++r)
         for (int e = tid; e < cnts[r]; e += blockDim.x)
-          c += f2o(__uint_as_float(lists[(size_t)r * a.cap + e].x)) >= cand;
+          c += lists[(size_t)r * a.cap + e].x >= cand;
       c = __reduce_add_sync(0xffffffffu, c);
       if (lane == 0) red[w] = c;
       __syncthreads();
@@ -281,13 +292,13 @@ __global__ void __launch_bounds__(256) k_adc_merge(const MergeArgs a) {
       if (tot >= a.N) T = cand;
     }
   }
-  const float cutv = T ? __fsub_rd(o2f(T), 2.0f * a.delta[q]) : -INFINITY;
+  const int cutv = have ? (int)T - (a.M + 1) : INT_MIN;
   if (tid == 0) ncol = 0;
   __syncthreads();
   for (int r = 0; r < a.R; ++r)
     for (int e = tid; e < cnts[r]; e += blockDim.x) {
       const uint2 v = lists[(size_t)r * a.cap + e];
-      if (__uint_as_float(v.x) >= cutv) {
+      if ((int)v.x >= cutv) {
         const int pos = atomicAdd(&ncol, 1);
         if (pos < kMergeCap) sid[pos] = v.y;
       }
@@ -385,31 +396,30 @@ int adc_search_device(aq_codes* codes, aq_codebook* cb, const double* Qd,
     return ref_error(AQ_E_UNSUPPORTED, "device search supports k <= 256");
   if (cb->M > 1024) return ref_error(AQ_E_UNSUPPORTED, "device search supports M <= 1024");
   if (nq == 0) return AQ_OK;
-  const int M = (int)cb->M, k = (int)cb->k, Mp = pad8(M);
+  const int M = (int)cb->M, k = (int)cb->k;
   const size_t n = codes->n;
   const size_t topn_eff = std::min(topn, n);
   const size_t d = cb->M * cb->sd;
   const size_t nqb = (nq + kQB - 1) / kQB;
   // workspace
   const size_t lut64_b = nq * M * k * sizeof(double);
-  const size_t lut32_b = nqb * 8 * (size_t)Mp * 32 * sizeof(float);
+  const size_t lutq_b = nqb * kQP * (size_t)M * 16 * sizeof(uint32_t);
   void* p;
-  AQ_TRY(scratch(s, 1, lut64_b + lut32_b + nq * sizeof(float) + 256, &p));
+  AQ_TRY(scratch(s, 1, lut64_b + lutq_b + 256, &p));
   double* lut64 = (double*)p;
-  float* lut32 = (float*)(lut64 + nq * M * k);
-  float* delta = lut32 + lut32_b / sizeof(float);
-  AQ_CUDA(cudaMemsetAsync(lut32, 0, lut32_b, s->stream));
+  uint32_t* lutq = (uint32_t*)(lut64 + nq * M * k);
+  AQ_CUDA(cudaMemsetAsync(lutq, 0, lutq_b, s->stream));
   timer_mark(s, AQ_T_LUT);
   k_build_lut<<<(unsigned)nq, 256, 0, s->stream>>>(Qd, (int)nq, (int)d, cb->d64, M, k,
-                                                  (int)cb->sd, lut64, lut32, delta);
+                                                  (int)cb->sd, lut64, (uint16_t*)lutq);
   AQ_LAUNCHED(s);
   timer_mark(s, AQ_T_LUT);
 
-  const bool fast = codes->bits == 4 && topn <= (size_t)kMaxTopN && M <= 1024;
+  const bool fast = codes->bits == 4 && topn <= (size_t)kMaxTopN && M <= 256;
   std::vector<int> hflag(nq, fast ? 0 : 1);
   if (fast) {
     const int N = (int)topn_eff;
-    const int cap = ((N + 31) & ~31) + 2 * kTileP;
+    const int cap = ((N + 31) & ~31) + kTileP + 32;
     // point ranges: enough CTAs for ~2 waves, ranges of whole tiles
     const size_t tiles = (n + kTileP - 1) / kTileP;
     size_t R = std::max<size_t>(1, (2 * (size_t)s->num_sms + nqb - 1) / nqb);
@@ -423,19 +433,36 @@ int adc_search_device(aq_codes* codes, aq_codebook* cb, const double* Qd,
     int* ocnt = (int*)(obuf + nq * R * cap);
     int* oflag = ocnt + nq * R;
     AQ_CUDA(cudaMemsetAsync(oflag, 0, nq * sizeof(int), s->stream));
-    ScoreArgs sa{codes->data, n, (int)codes->stride, lut32, delta, Mp, (int)nq, N, cap,
+    ScoreArgs sa{codes->data, n, (int)codes->stride, lutq, M, (int)nq, N, cap,
                  range_len, (int)R, obuf, ocnt, oflag};
-    const size_t smem = (size_t)8 * Mp * 16 * sizeof(float2) + 4 * kQB * 4 +
+    const size_t smem = (size_t)kQP * M * 16 * sizeof(uint32_t) + 3 * kQB * sizeof(int) +
                         (size_t)kQB * cap * sizeof(uint2);
     if (smem > 227 * 1024)
       return ref_error(AQ_E_UNSUPPORTED, "ADC working set exceeds shared memory");
-    AQ_CUDA(cudaFuncSetAttribute(k_adc_score, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
+    const dim3 grid((unsigned)R, (unsigned)nqb);
     timer_mark(s, AQ_T_ADC_SCORE);
-    k_adc_score<<<dim3((unsigned)R, (unsigned)nqb), kTileP, smem, s->stream>>>(sa);
+#define AQ_SCORE_CASE(MM)                                                          \
+  case MM:                                                                        \
+    AQ_CUDA(cudaFuncSetAttribute(k_adc_score<MM>,                                  \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    k_adc_score<MM><<<grid, kTileP, smem, s->stream>>>(sa);                       \
+    break;
+    switch (M) {
+      AQ_SCORE_CASE(16)
+      AQ_SCORE_CASE(32)
+      AQ_SCORE_CASE(48)
+      AQ_SCORE_CASE(50)
+      AQ_SCORE_CASE(64)
+      AQ_SCORE_CASE(128)
+      default:
+        AQ_CUDA(cudaFuncSetAttribute(k_adc_score<0>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_adc_score<0><<<grid, kTileP, smem, s->stream>>>(sa);
+    }
+#undef AQ_SCORE_CASE
     AQ_LAUNCHED(s);
     timer_mark(s, AQ_T_ADC_SCORE);
-    MergeArgs ma{obuf, ocnt, oflag, (int)R, cap, N, (int)topn_eff, delta, lut64,
+    MergeArgs ma{obuf, ocnt, oflag, (int)R, cap, N, (int)topn_eff, lut64,
                  codes->data, (int)codes->stride, codes->bits, M, k, ids, scores};
     timer_mark(s, AQ_T_ADC_MERGE);
     k_adc_merge<<<(unsigned)nq, 256, 0, s->stream>>>(ma);
@@ -645,16 +672,13 @@ int aq_build_lut(aq_session* s, const double* q, size_t d, const double* dict,
   double* Qd;
   int st = upload_queries(s, q, 1, d, 0, &Qd);
   void* p = nullptr;
-  const int Mp = pad8((int)M);
-  const size_t l32 = (size_t)8 * Mp * 32 * sizeof(float);
-  if (st == AQ_OK) st = scratch(s, 1, M * k * sizeof(double) + l32 + 64, &p);
+  const size_t lq = (size_t)kQP * M * 16 * sizeof(uint32_t);
+  if (st == AQ_OK) st = scratch(s, 1, M * k * sizeof(double) + lq + 64, &p);
   if (st == AQ_OK) {
     double* l64 = (double*)p;
-    float* lut32 = (float*)(l64 + M * k);
-    float* delta = lut32 + l32 / sizeof(float);
-    cudaMemsetAsync(lut32, 0, l32, s->stream);
+    uint16_t* lutq = (uint16_t*)(l64 + M * k);
     k_build_lut<<<1, 256, 0, s->stream>>>(Qd, 1, (int)d, cb->d64, (int)M, (int)k, (int)sd,
-                                          l64, lut32, delta);
+                                          l64, lutq);
     s->launches++;
     cudaMemcpyAsync(lut_out, l64, M * k * sizeof(double), cudaMemcpyDeviceToHost, s->stream);
     if (cudaStreamSynchronize(s->stream) != cudaSuccess) st = AQ_E_CUDA;

@@ -14,6 +14,8 @@
 // reference's. Inputs whose windows do not fit (massive ties, N > 512) take
 // an exact full-sort fallback.
 #include <algorithm>
+#include <climits>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -23,9 +25,13 @@ namespace aqd {
 int sort_scores_desc(aq_session* s, const double* scores, uint32_t* idx,
                      size_t n);
 
-constexpr int kQP = 16;          // query pairs per scoring CTA
-constexpr int kQB = 2 * kQP;     // queries per scoring CTA
-constexpr int kTileP = 256;      // points per tile == threads per CTA
+// Scoring CTA shapes: query pairs per CTA, points per tile (= threads),
+// min CTAs per SM. Selected per launch (AQ_ADC_VARIANT overrides).
+struct AdcShape {
+  int qp, tile, minb;
+};
+constexpr AdcShape kShapes[] = {{16, 256, 1}, {8, 256, 2}, {8, 512, 1}, {16, 512, 1}};
+constexpr int kLutQP = 16;  // lut kernel of the single-query host entry
 constexpr int kMaxTopN = 512;    // fast path limit
 constexpr int kMergeCap = 2048;
 constexpr int kQMax = 4095;      // |v| <= 4095: 13-bit fields, 8 adds per 16-bit lane
@@ -39,7 +45,7 @@ constexpr int kQMax = 4095;      // |v| <= 4095: 13-bit fields, 8 adds per 16-bi
 __global__ void k_build_lut(const double* __restrict__ Q, int nq, int d,
                             const double* __restrict__ cb, int M, int k,
                             int sd, double* __restrict__ lut64,
-                            uint16_t* __restrict__ lutq) {
+                            uint16_t* __restrict__ lutq, int QP) {
   __shared__ double red[32];
   const int q = blockIdx.x;
   const double* qv = Q + (size_t)q * d;
@@ -59,8 +65,8 @@ __global__ void k_build_lut(const double* __restrict__ Q, int nq, int d,
   mx = 0.0;
   for (int t = 0; t < (int)(blockDim.x >> 5); ++t) mx = fmax(mx, red[t]);
   const double sc = mx > 0.0 ? mx / kQMax : 1.0;
-  const int qb = q / kQB, qi = q % kQB;
-  uint16_t* T = lutq + ((((size_t)qb * kQP + qi / 2) * M) * 16) * 2 + (qi & 1);
+  const int qb = q / (2 * QP), qi = q % (2 * QP);
+  uint16_t* T = lutq + ((((size_t)qb * QP + qi / 2) * M) * 16) * 2 + (qi & 1);
   for (int e = threadIdx.x; e < M * 16; e += blockDim.x) {
     const int m = e / 16, j = e % 16;
     int v = 0;
@@ -133,23 +139,24 @@ __device__ int warp_compact(uint2* buf, int cnt, int cut) {
 // are summed with IADD3 into packed 16-bit lanes, then split into 32-bit
 // accumulators. Shared-memory delivery is the bound: 64 lookups per
 // wavefront. MP > 0 fixes M at compile time (immediate LDS offsets).
-template <int MP>
-__global__ void __launch_bounds__(kTileP, 1) k_adc_score(const ScoreArgs a) {
+template <int MP, int QP, int TILE, int MINB>
+__global__ void __launch_bounds__(TILE, MINB) k_adc_score(const ScoreArgs a) {
+  constexpr int QB = 2 * QP;
   extern __shared__ __align__(16) unsigned char smem[];
   const int M = MP > 0 ? MP : a.M;
-  uint32_t* T = reinterpret_cast<uint32_t*>(smem);  // [kQP][M][16]
-  int* cut = reinterpret_cast<int*>(T + kQP * M * 16);
-  int* cnt = cut + kQB;
-  int* flag = cnt + kQB;
-  uint2* buf = reinterpret_cast<uint2*>(flag + kQB);  // [kQB][cap]
+  uint32_t* T = reinterpret_cast<uint32_t*>(smem);  // [QP][M][16]
+  int* cut = reinterpret_cast<int*>(T + QP * M * 16);
+  int* cnt = cut + QB;
+  int* flag = cnt + QB;
+  uint2* buf = reinterpret_cast<uint2*>(flag + QB);  // [QB][cap]
   const int qb = blockIdx.y, r = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   {
-    const uint4* src = reinterpret_cast<const uint4*>(a.lutq + (size_t)qb * kQP * M * 16);
+    const uint4* src = reinterpret_cast<const uint4*>(a.lutq + (size_t)qb * QP * M * 16);
     uint4* dst = reinterpret_cast<uint4*>(T);
-    for (int t = threadIdx.x; t < kQP * M * 4; t += blockDim.x) dst[t] = src[t];
+    for (int t = threadIdx.x; t < QP * M * 4; t += blockDim.x) dst[t] = src[t];
   }
-  if (threadIdx.x < kQB) {
+  if (threadIdx.x < QB) {
     cut[threadIdx.x] = INT_MIN;
     cnt[threadIdx.x] = 0;
     flag[threadIdx.x] = 0;
@@ -160,12 +167,12 @@ __global__ void __launch_bounds__(kTileP, 1) k_adc_score(const ScoreArgs a) {
   const int cap = a.cap;
   const int nchunk = (M + 7) >> 3;
   const int margin = M + 1;  // 2 * (M s / 2) / s, plus one unit for float64
-  for (size_t tb = start; tb < end; tb += kTileP) {
+  for (size_t tb = start; tb < end; tb += TILE) {
     const size_t p = tb + threadIdx.x;
     if (p < end) {
-      uint32_t acc[kQB];
+      uint32_t acc[QB];
 #pragma unroll
-      for (int q = 0; q < kQB; ++q) acc[q] = 0u;
+      for (int q = 0; q < QB; ++q) acc[q] = 0u;
       const uint32_t* crow = reinterpret_cast<const uint32_t*>(a.codes + p * a.stride);
 #pragma unroll 1
       for (int ch = 0; ch < nchunk; ++ch) {
@@ -176,7 +183,7 @@ __global__ void __launch_bounds__(kTileP, 1) k_adc_score(const ScoreArgs a) {
         for (int t = 0; t < 8; ++t) off[t] = (ch * 8 + t) * 16 + ((w >> (4 * t)) & 15u);
         if (valid >= 8) {
 #pragma unroll
-          for (int qp = 0; qp < kQP; ++qp) {
+          for (int qp = 0; qp < QP; ++qp) {
             const uint32_t* Tq = T + qp * M * 16;
             const uint32_t pk = (Tq[off[0]] + Tq[off[1]] + Tq[off[2]]) +
                                 (Tq[off[3]] + Tq[off[4]] + Tq[off[5]]) +
@@ -186,7 +193,7 @@ __global__ void __launch_bounds__(kTileP, 1) k_adc_score(const ScoreArgs a) {
           }
         } else {
 #pragma unroll
-          for (int qp = 0; qp < kQP; ++qp) {
+          for (int qp = 0; qp < QP; ++qp) {
             const uint32_t* Tq = T + qp * M * 16;
             uint32_t pk = 0u;
 #pragma unroll
@@ -198,7 +205,7 @@ __global__ void __launch_bounds__(kTileP, 1) k_adc_score(const ScoreArgs a) {
         }
       }
 #pragma unroll
-      for (int q = 0; q < kQB; ++q) {
+      for (int q = 0; q < QB; ++q) {
         if ((int)acc[q] >= cut[q]) {
           const int pos = atomicAdd(&cnt[q], 1);
           if (pos < cap)
@@ -210,16 +217,16 @@ __global__ void __launch_bounds__(kTileP, 1) k_adc_score(const ScoreArgs a) {
     }
     __syncthreads();
     // shrink buffers that could overflow during the next tile
-    for (int q = warp; q < kQB; q += kTileP / 32) {
+    for (int q = warp; q < QB; q += TILE / 32) {
       const int c = min(cnt[q], cap);
       unsigned th;
-      if (c > cap - kTileP && !flag[q] && warp_nth_largest(buf + q * cap, c, a.N, &th)) {
+      if (c > cap - TILE && !flag[q] && warp_nth_largest(buf + q * cap, c, a.N, &th)) {
         const int cq = max(cut[q], (int)th - margin);
         const int kept = warp_compact(buf + q * cap, c, cq);
         if (lane == 0) {
           cut[q] = cq;
           cnt[q] = kept;
-          if (kept > cap - kTileP) flag[q] = 1;  // window too large: ties
+          if (kept > cap - TILE) flag[q] = 1;  // window too large: ties
         }
       }
       __syncwarp();
@@ -227,8 +234,8 @@ __global__ void __launch_bounds__(kTileP, 1) k_adc_score(const ScoreArgs a) {
     __syncthreads();
   }
   // final shrink + write-out
-  for (int q = warp; q < kQB; q += kTileP / 32) {
-    const int gq = qb * kQB + q;
+  for (int q = warp; q < QB; q += TILE / 32) {
+    const int gq = qb * QB + q;
     int c = min(cnt[q], cap);
     unsigned th;
     if (warp_nth_largest(buf + q * cap, c, a.N, &th))
@@ -400,10 +407,14 @@ int adc_search_device(aq_codes* codes, aq_codebook* cb, const double* Qd,
   const size_t n = codes->n;
   const size_t topn_eff = std::min(topn, n);
   const size_t d = cb->M * cb->sd;
-  const size_t nqb = (nq + kQB - 1) / kQB;
+  int variant = 1;
+  if (const char* v = getenv("AQ_ADC_VARIANT")) variant = atoi(v) & 3;
+  const AdcShape shp = kShapes[variant];
+  const int QB = 2 * shp.qp, TILE = shp.tile;
+  const size_t nqb = (nq + QB - 1) / QB;
   // workspace
   const size_t lut64_b = nq * M * k * sizeof(double);
-  const size_t lutq_b = nqb * kQP * (size_t)M * 16 * sizeof(uint32_t);
+  const size_t lutq_b = nqb * shp.qp * (size_t)M * 16 * sizeof(uint32_t);
   void* p;
   AQ_TRY(scratch(s, 1, lut64_b + lutq_b + 256, &p));
   double* lut64 = (double*)p;
@@ -411,7 +422,8 @@ int adc_search_device(aq_codes* codes, aq_codebook* cb, const double* Qd,
   AQ_CUDA(cudaMemsetAsync(lutq, 0, lutq_b, s->stream));
   timer_mark(s, AQ_T_LUT);
   k_build_lut<<<(unsigned)nq, 256, 0, s->stream>>>(Qd, (int)nq, (int)d, cb->d64, M, k,
-                                                  (int)cb->sd, lut64, (uint16_t*)lutq);
+                                                  (int)cb->sd, lut64, (uint16_t*)lutq,
+                                                  shp.qp);
   AQ_LAUNCHED(s);
   timer_mark(s, AQ_T_LUT);
 
@@ -419,12 +431,12 @@ int adc_search_device(aq_codes* codes, aq_codebook* cb, const double* Qd,
   std::vector<int> hflag(nq, fast ? 0 : 1);
   if (fast) {
     const int N = (int)topn_eff;
-    const int cap = ((N + 31) & ~31) + kTileP + 32;
+    const int cap = ((N + 31) & ~31) + TILE + 32;
     // point ranges: enough CTAs for ~2 waves, ranges of whole tiles
-    const size_t tiles = (n + kTileP - 1) / kTileP;
-    size_t R = std::max<size_t>(1, (2 * (size_t)s->num_sms + nqb - 1) / nqb);
+    const size_t tiles = (n + TILE - 1) / TILE;
+    size_t R = std::max<size_t>(1, (2 * (size_t)s->num_sms * shp.minb + nqb - 1) / nqb);
     R = std::min(R, tiles);
-    const size_t range_len = ((tiles + R - 1) / R) * kTileP;
+    const size_t range_len = ((tiles + R - 1) / R) * TILE;
     R = (n + range_len - 1) / range_len;
     const size_t buf_b = nq * R * cap * sizeof(uint2);
     void* p2;
@@ -435,31 +447,40 @@ int adc_search_device(aq_codes* codes, aq_codebook* cb, const double* Qd,
     AQ_CUDA(cudaMemsetAsync(oflag, 0, nq * sizeof(int), s->stream));
     ScoreArgs sa{codes->data, n, (int)codes->stride, lutq, M, (int)nq, N, cap,
                  range_len, (int)R, obuf, ocnt, oflag};
-    const size_t smem = (size_t)kQP * M * 16 * sizeof(uint32_t) + 3 * kQB * sizeof(int) +
-                        (size_t)kQB * cap * sizeof(uint2);
+    const size_t smem = (size_t)shp.qp * M * 16 * sizeof(uint32_t) + 3 * QB * sizeof(int) +
+                        (size_t)QB * cap * sizeof(uint2);
     if (smem > 227 * 1024)
       return ref_error(AQ_E_UNSUPPORTED, "ADC working set exceeds shared memory");
     const dim3 grid((unsigned)R, (unsigned)nqb);
     timer_mark(s, AQ_T_ADC_SCORE);
-#define AQ_SCORE_CASE(MM)                                                          \
-  case MM:                                                                        \
-    AQ_CUDA(cudaFuncSetAttribute(k_adc_score<MM>,                                  \
+#define AQ_SCORE_LAUNCH(MM, QPv, TL, MB)                                              \
+  do {                                                                              \
+    AQ_CUDA(cudaFuncSetAttribute(k_adc_score<MM, QPv, TL, MB>,                       \
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    k_adc_score<MM><<<grid, kTileP, smem, s->stream>>>(sa);                       \
+    k_adc_score<MM, QPv, TL, MB><<<grid, TL, smem, s->stream>>>(sa);                \
+  } while (0)
+#define AQ_SCORE_M(MM)                                               \
+  case MM:                                                          \
+    if (variant == 0) AQ_SCORE_LAUNCH(MM, 16, 256, 1);              \
+    else if (variant == 1) AQ_SCORE_LAUNCH(MM, 8, 256, 2);          \
+    else if (variant == 2) AQ_SCORE_LAUNCH(MM, 8, 512, 1);          \
+    else AQ_SCORE_LAUNCH(MM, 16, 512, 1);                           \
     break;
     switch (M) {
-      AQ_SCORE_CASE(16)
-      AQ_SCORE_CASE(32)
-      AQ_SCORE_CASE(48)
-      AQ_SCORE_CASE(50)
-      AQ_SCORE_CASE(64)
-      AQ_SCORE_CASE(128)
+      AQ_SCORE_M(16)
+      AQ_SCORE_M(32)
+      AQ_SCORE_M(48)
+      AQ_SCORE_M(50)
+      AQ_SCORE_M(64)
+      AQ_SCORE_M(128)
       default:
-        AQ_CUDA(cudaFuncSetAttribute(k_adc_score<0>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_adc_score<0><<<grid, kTileP, smem, s->stream>>>(sa);
+        if (variant == 0) AQ_SCORE_LAUNCH(0, 16, 256, 1);
+        else if (variant == 1) AQ_SCORE_LAUNCH(0, 8, 256, 2);
+        else if (variant == 2) AQ_SCORE_LAUNCH(0, 8, 512, 1);
+        else AQ_SCORE_LAUNCH(0, 16, 512, 1);
     }
-#undef AQ_SCORE_CASE
+#undef AQ_SCORE_M
+#undef AQ_SCORE_LAUNCH
     AQ_LAUNCHED(s);
     timer_mark(s, AQ_T_ADC_SCORE);
     MergeArgs ma{obuf, ocnt, oflag, (int)R, cap, N, (int)topn_eff, lut64,
@@ -672,13 +693,13 @@ int aq_build_lut(aq_session* s, const double* q, size_t d, const double* dict,
   double* Qd;
   int st = upload_queries(s, q, 1, d, 0, &Qd);
   void* p = nullptr;
-  const size_t lq = (size_t)kQP * M * 16 * sizeof(uint32_t);
+  const size_t lq = (size_t)kLutQP * M * 16 * sizeof(uint32_t);
   if (st == AQ_OK) st = scratch(s, 1, M * k * sizeof(double) + lq + 64, &p);
   if (st == AQ_OK) {
     double* l64 = (double*)p;
     uint16_t* lutq = (uint16_t*)(l64 + M * k);
     k_build_lut<<<1, 256, 0, s->stream>>>(Qd, 1, (int)d, cb->d64, (int)M, (int)k, (int)sd,
-                                          l64, lutq);
+                                          l64, lutq, kLutQP);
     s->launches++;
     cudaMemcpyAsync(lut_out, l64, M * k * sizeof(double), cudaMemcpyDeviceToHost, s->stream);
     if (cudaStreamSynchronize(s->stream) != cudaSuccess) st = AQ_E_CUDA;

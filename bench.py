@@ -91,7 +91,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200", "-i", str(self.device)],
+                 "-lms", "100", "-i", str(self.device)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -244,7 +244,7 @@ def run_ours(args):
     pk = peaks()
     ms_k, cnt_k = kt.get("adc_score", (float("nan"), 1))
     per_launch_s = ms_k / cnt_k / 1e3
-    alg_bytes = nq * n * (M / 2) / cnt_k
+    alg_bytes = nq * n * (M / 2)  # one scoring launch per step covers every score
     achieved = alg_bytes / per_launch_s / 1e9
     tr = traffic_record().get("adc_score")
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"],

@@ -227,6 +227,10 @@ int aq_dev_pq_codebook_update(aq_dataset* ds, aq_codes* codes,
                               const aq_weights* w, double ridge,
                               aq_codebook* out);
 
+int aq_pq_codebook_update(aq_session* s, const float* x, size_t n, size_t d,
+                          const uint32_t* codes, size_t M, size_t k,
+                          const aq_weights* w, double ridge, double* dict_out);
+
 /* ---- trainers (pq.hpp:469-575) ------------------------------------------- */
 typedef struct aq_train_config {  /* vq.hpp:55-69 */
   int max_iterations;

@@ -85,6 +85,7 @@ _SIGS = {
     "aq_dev_exact_search": (_I, [_VP, _VP, _SZ, _SZ, _VP, _VP]),
     "aq_dev_assemble_selector_system": (_I, [_VP, _VP, _VP, _VP, _VP]),
     "aq_dev_pq_codebook_update": (_I, [_VP, _VP, _VP, _D, _VP]),
+    "aq_pq_codebook_update": (_I, [_VP, _VP, _SZ, _SZ, _VP, _SZ, _SZ, _VP, _D, _VP]),
     "aq_dev_train_l2_pq": (_I, [_VP, _SZ, _SZ, _VP, _PP, _PP]),
     "aq_debug_exact_window_count": (_I, [_VP, _I, _VP]),
     "aq_dev_train_apq": (_I, [_VP, _SZ, _SZ, _VP, _VP, _I, _PP, _PP, _VP, _VP]),

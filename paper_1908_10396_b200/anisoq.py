@@ -523,3 +523,40 @@ def dev_search_rerank(ds: DeviceDataset, codes: DeviceCodes, cb: DeviceCodebook,
                                    aid.ctypes.data, asc.ctypes.data, ids.ctypes.data,
                                    sc.ctypes.data))
     return aid, asc, ids, sc
+
+
+# ---- codebook update (pq.hpp:290-464) ---------------------------------------------------
+
+
+def pq_codebook_update(data, codes: CodeMatrix, weights, M: int, k: int, ridge: float = -1.0,
+                       session: Optional[Session] = None) -> ProductCodebook:
+    """pq.hpp:356-464: joint codebook solve for fixed codes (bit-identical to the
+    reference's serial normal equations + the pinned blocked Cholesky)."""
+    s = _sess(session)
+    data = data if isinstance(data, Dataset) else Dataset(data)
+    keep: list = []
+    w = _weights(weights, data.n, keep)
+    out = np.zeros(k * data.d, np.float64)
+    cm = np.ascontiguousarray(codes.codes, np.uint32)
+    _check(_L.aq_pq_codebook_update(s.h, data.values.ctypes.data, data.n, data.d,
+                                    cm.ctypes.data, M, k, C.byref(w), ridge, out.ctypes.data))
+    return ProductCodebook(M, k, data.d // M if M else 0, out)
+
+
+def assemble_selector_system(data, codes: CodeMatrix, weights, M: int, k: int,
+                             session: Optional[Session] = None):
+    """pq.hpp:290-343: returns (system_matrix dim x dim, rhs dim), dim = k d."""
+    s = _sess(session)
+    data = data if isinstance(data, Dataset) else Dataset(data)
+    if codes.n != data.n or codes.M != M:
+        raise DimensionMismatch("DimensionMismatch: code matrix does not match dataset")
+    ds = s.upload_dataset(data)
+    dc = s.upload_codes(CodeMatrix(codes.n, codes.M, k, codes.codes))
+    keep: list = []
+    w = _weights(weights, data.n, keep)
+    dim = k * data.d
+    A = np.zeros((dim, dim), np.float64)
+    rhs = np.zeros(dim, np.float64)
+    _check(_L.aq_dev_assemble_selector_system(ds.h, dc.h, C.byref(w), A.ctypes.data,
+                                              rhs.ctypes.data))
+    return A, rhs

@@ -93,7 +93,8 @@ struct aq_session {
 struct aq_dataset {
   aq_session* s = nullptr;
   size_t n = 0, d = 0;
-  float* xt = nullptr;      // pair-tiled rows
+  float* xt = nullptr;      // pair-tiled rows (encoders, search)
+  float* xr = nullptr;      // row-major rows (normal equations, gathers)
   double* norms = nullptr;  // float64 norms
 };
 

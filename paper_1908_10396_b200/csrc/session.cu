@@ -347,6 +347,10 @@ static int dataset_from_device_rows(aq_session* s, const float* xdev, size_t n,
   const size_t tf = tiled_floats(n, d);
   AQ_CUDA(cudaMallocAsync(&ds->xt, (tf ? tf : 1) * sizeof(float), s->stream));
   AQ_CUDA(cudaMallocAsync(&ds->norms, (n ? n : 1) * sizeof(double), s->stream));
+  AQ_CUDA(cudaMallocAsync(&ds->xr, (n * d ? n * d : 1) * sizeof(float), s->stream));
+  if (n * d)
+    AQ_CUDA(cudaMemcpyAsync(ds->xr, xdev, n * d * sizeof(float), cudaMemcpyDeviceToDevice,
+                            s->stream));
   const size_t ntile = ((n + 31) / 32) * 32;
   if (ntile) {
     k_tile_rows<<<(unsigned)((ntile + 127) / 128), 128, 0, s->stream>>>(
@@ -381,6 +385,7 @@ int aq_dataset_free(aq_dataset* ds) {
   if (!ds) return AQ_OK;
   cudaSetDevice(ds->s->device);
   cudaFreeAsync(ds->xt, ds->s->stream);
+  cudaFreeAsync(ds->xr, ds->s->stream);
   cudaFreeAsync(ds->norms, ds->s->stream);
   delete ds;
   return AQ_OK;

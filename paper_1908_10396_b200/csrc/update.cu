@@ -1,0 +1,715 @@
+// Codebook update (pq_codebook_update, pq.hpp:356-464) on the device:
+//   * stable per-subspace bucket lists of points by code (counting sort);
+//   * the dense normal equations (assemble_selector_system, pq.hpp:290-343):
+//     one warp per (row strip (m, j), 32 column subspaces); every entry is
+//     accumulated by one lane over the strip's points in ascending point
+//     order with the reference's operation order, so the matrix (and rhs) is
+//     bit-identical to the reference's serial loop;
+//   * ridge + blocked Cholesky + triangular solves mirroring the oracle's
+//     pinned LLT (oracle/eigen_subset/Eigen/Dense): block 64, sequential inner
+//     sums, products rounded before the add/sub;
+//   * the isotropic weighted-mean path (pq.hpp:405-423);
+//   * reseeding of unused codewords from the loss ranking (pq.hpp:443-462).
+#include <algorithm>
+#include <climits>
+#include <vector>
+
+#include "common.cuh"
+
+namespace aqd {
+
+__global__ void k_radix_scan(unsigned* __restrict__ hist, size_t total);
+int sort_scores_desc(aq_session* s, const double* scores, uint32_t* idx, size_t n);
+int run_encode(aq_dataset* ds, aq_codebook* cb, const aq_weights* w, aq_codes* codes,
+               int mode, int passes, int sweep_fixed, double* losses_dev,
+               uint64_t* changed_out);
+int stage_codebook(aq_codebook* cb);
+
+constexpr int kBucketBlock = 1024;
+constexpr int kLLT = 64;  // pinned block size (Eigen stand-in)
+
+// ---- bucket lists -------------------------------------------------------------------
+
+__global__ void k_bucket_hist(const uint8_t* __restrict__ codes, size_t n, int stride,
+                              int bits, int K, unsigned* __restrict__ hist, size_t nb,
+                              DevError* err, int k) {
+  __shared__ unsigned h[256];
+  const int m = blockIdx.y;
+  for (int t = threadIdx.x; t < K; t += blockDim.x) h[t] = 0;
+  __syncthreads();
+  const size_t base = (size_t)blockIdx.x * kBucketBlock;
+  for (int t = threadIdx.x; t < kBucketBlock; t += blockDim.x) {
+    const size_t i = base + t;
+    if (i < n) {
+      const unsigned c = get_code(codes + i * stride, m, bits);
+      if ((int)c >= k) report_error(err, i, AQ_E_CODE_OUT_OF_RANGE);
+      atomicAdd(&h[min(c, (unsigned)K - 1)], 1u);
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < K; t += blockDim.x)
+    hist[((size_t)m * K + t) * nb + blockIdx.x] = h[t];
+}
+
+// stable scatter (points keep ascending order inside every bucket)
+__global__ void k_bucket_scatter(const uint8_t* __restrict__ codes, size_t n, int stride,
+                                 int bits, int K, const unsigned* __restrict__ base,
+                                 size_t nb, uint32_t* __restrict__ list) {
+  __shared__ unsigned run[256];
+  __shared__ unsigned wcnt[8][256];
+  const int m = blockIdx.y;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int t = threadIdx.x; t < K; t += blockDim.x)
+    run[t] = base[((size_t)m * K + t) * nb + blockIdx.x] - (unsigned)((size_t)m * n);
+  const size_t b0 = (size_t)blockIdx.x * kBucketBlock;
+  for (int round = 0; round < kBucketBlock / 256; ++round) {
+    for (int t = threadIdx.x; t < 8 * 256; t += blockDim.x) (&wcnt[0][0])[t] = 0;
+    __syncthreads();
+    const size_t i = b0 + (size_t)round * 256 + threadIdx.x;
+    const bool valid = i < n;
+    const unsigned dg = valid ? min(get_code(codes + i * stride, m, bits), (unsigned)K - 1)
+                              : 256u;
+    const unsigned peers = __match_any_sync(0xffffffffu, dg);
+    const unsigned rk = __popc(peers & ((1u << lane) - 1u));
+    if (valid && rk == 0) wcnt[w][dg] = __popc(peers);
+    __syncthreads();
+    if (valid) {
+      unsigned before = 0;
+      for (int ww = 0; ww < w; ++ww) before += wcnt[ww][dg];
+      list[(size_t)m * n + run[dg] + before + rk] = (uint32_t)i;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < K; t += blockDim.x) {
+      unsigned s = 0;
+      for (int ww = 0; ww < 8; ++ww) s += wcnt[ww][t];
+      run[t] += s;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_bucket_offsets(const unsigned* __restrict__ base, size_t nb, int M, int K,
+                                 size_t n, uint32_t* __restrict__ start,
+                                 uint32_t* __restrict__ count) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= M * K) return;
+  const int m = t / K, j = t % K;
+  const unsigned s0 = base[((size_t)m * K + j) * nb] - (unsigned)((size_t)m * n);
+  const unsigned s1 = j + 1 < K ? base[((size_t)m * K + j + 1) * nb] - (unsigned)((size_t)m * n)
+                                : (unsigned)n;
+  start[t] = s0;
+  count[t] = s1 - s0;
+}
+
+struct Buckets {
+  uint32_t* list = nullptr;   // [M][n]
+  uint32_t* start = nullptr;  // [M][K]
+  uint32_t* count = nullptr;  // [M][K]
+  int K = 0;
+};
+
+int build_buckets(aq_codes* c, int k, Buckets* B) {
+  aq_session* s = c->s;
+  const size_t n = c->n, M = c->M;
+  const int K = k;
+  const size_t nb = (n + kBucketBlock - 1) / kBucketBlock;
+  void* p;
+  AQ_TRY(scratch(s, 2, (M * n + 2 * M * K + M * K * nb) * sizeof(unsigned) + 256, &p));
+  B->list = (uint32_t*)p;
+  B->start = B->list + M * n;
+  B->count = B->start + M * K;
+  unsigned* hist = B->count + M * K;
+  B->K = K;
+  AQ_TRY(clear_dev_error(s));
+  k_bucket_hist<<<dim3((unsigned)nb, (unsigned)M), 256, 0, s->stream>>>(
+      c->data, n, (int)c->stride, c->bits, K, hist, nb, s->err, k);
+  AQ_LAUNCHED(s);
+  AQ_TRY(sync_and_check(s, "codebook update: code out of range"));
+  k_radix_scan<<<1, 1024, 0, s->stream>>>(hist, M * K * nb);
+  AQ_LAUNCHED(s);
+  k_bucket_scatter<<<dim3((unsigned)nb, (unsigned)M), 256, 0, s->stream>>>(
+      c->data, n, (int)c->stride, c->bits, K, hist, nb, B->list);
+  AQ_LAUNCHED(s);
+  k_bucket_offsets<<<(unsigned)((M * K + 255) / 256), 256, 0, s->stream>>>(
+      hist, nb, (int)M, K, n, B->start, B->count);
+  AQ_LAUNCHED(s);
+  return AQ_OK;
+}
+
+// ---- per-point weights: h_par, h_perp, coupling coefficient -----------------------------
+// coef = (h_par - h_perp) / |x|^2 exactly as pq.hpp:313-319; flags[0] = some
+// point is anisotropic, flags[1] = smallest anisotropic zero-norm index + 1.
+__global__ void k_point_weights(const double* __restrict__ norms, size_t n, DevWeights w,
+                                double* __restrict__ hp, double* __restrict__ ho,
+                                double* __restrict__ coef, unsigned long long* flags,
+                                DevError* err) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double a, b;
+  int st = AQ_OK;
+  if (!resolve_weights(w, i, norms[i], &a, &b, &st)) {
+    report_error(err, i, st);
+    a = b = 1.0;
+  }
+  hp[i] = a;
+  ho[i] = b;
+  double c = 0.0;
+  if (a != b) {
+    atomicOr(&flags[0], 1ull);
+    const double n2 = __dmul_rn(norms[i], norms[i]);
+    if (n2 == 0.0)
+      atomicMin(&flags[1], (unsigned long long)i + 1ull);
+    else
+      c = __ddiv_rn(__dsub_rn(a, b), n2);
+  }
+  coef[i] = c;
+}
+
+// ---- dense normal equations ---------------------------------------------------------------
+
+struct AsmArgs {
+  const float* xr;
+  size_t n;
+  int d, M, k, sd;
+  const uint8_t* codes;
+  int stride, bits;
+  const uint32_t* list;
+  const uint32_t* start;
+  const uint32_t* count;
+  const double* hp;
+  const double* ho;
+  const double* coef;
+  int full;        // 1: all column subspaces (API), 0: m2 <= m (lower, for LLT)
+  double* A;       // dim x dim row-major
+  double* rhs;     // dim
+  int nchunk;      // column chunks of 32 subspaces per strip
+};
+
+// One warp = (row strip (m, j), chunk of 32 column subspaces). Lane l owns
+// column subspace m2 = 32 chunk + l; its accumulators for rows (m, j, a) x
+// columns (m2, j2, b) sit in shared memory, lane-interleaved (no bank
+// conflicts, no atomics). The strip's points are visited in ascending order,
+// so each entry sees the reference's exact sequence of additions
+// (pq.hpp:320-339): += h_perp on the diagonal first, then += (coef x_a) x_b.
+__global__ void __launch_bounds__(32) k_assemble(const AsmArgs a) {
+  extern __shared__ __align__(16) double acc[];  // [(aa*k + j2)*sd + b][32], then rhs[sd]
+  const int unit = blockIdx.x;
+  const int chunk = unit % a.nchunk;
+  const int strip = unit / a.nchunk;
+  const int m = strip / a.k, j = strip % a.k;
+  const int lane = threadIdx.x;
+  const int sd = a.sd, k = a.k, d = a.d;
+  const int m2 = chunk * 32 + lane;
+  const int mcols = a.full ? a.M : m + 1;
+  if (chunk * 32 >= mcols) return;
+  const bool mine = m2 < mcols;
+  const int nacc = sd * k * sd;
+  double* racc = acc + (size_t)nacc * 32;
+  for (int e = 0; e < nacc; ++e) acc[e * 32 + lane] = 0.0;
+  if (lane < sd) racc[lane] = 0.0;
+  const uint32_t* L = a.list + (size_t)m * a.n + a.start[m * k + j];
+  const size_t cnt = a.count[m * k + j];
+  const bool do_rhs = chunk == 0;
+  for (size_t t = 0; t < cnt; ++t) {
+    const uint32_t p = L[t];
+    const float* xp = a.xr + (size_t)p * d;
+    const double cf = a.coef[p];
+    if (do_rhs && lane < sd)  // rhs += h_par * x (pq.hpp:326)
+      racc[lane] = __dadd_rn(racc[lane], __dmul_rn(a.hp[p], (double)xp[m * sd + lane]));
+    if (!mine) continue;
+    const unsigned j2 = get_code(a.codes + (size_t)p * a.stride, m2, a.bits);
+    if (m2 == m) {  // diagonal h_perp (pq.hpp:324-325), j2 == j here
+      const double hop = a.ho[p];
+      for (int aa = 0; aa < sd; ++aa) {
+        double* e = acc + (size_t)((aa * k + j) * sd + aa) * 32 + lane;
+        *e = __dadd_rn(*e, hop);
+      }
+    }
+    if (cf == 0.0) continue;  // pq.hpp:328
+    for (int aa = 0; aa < sd; ++aa) {
+      const double xc = __dmul_rn(cf, (double)xp[m * sd + aa]);
+      for (int b = 0; b < sd; ++b) {
+        double* e = acc + (size_t)((aa * k + j2) * sd + b) * 32 + lane;
+        *e = __dadd_rn(*e, __dmul_rn(xc, (double)xp[m2 * sd + b]));
+      }
+    }
+  }
+  const size_t dim = (size_t)k * d;
+  if (mine) {
+    for (int aa = 0; aa < sd; ++aa)
+      for (int j2 = 0; j2 < k; ++j2)
+        for (int b = 0; b < sd; ++b)
+          a.A[((size_t)(m * k + j) * sd + aa) * dim + (size_t)(m2 * k + j2) * sd + b] =
+              acc[(size_t)((aa * k + j2) * sd + b) * 32 + lane];
+  }
+  if (do_rhs && lane < sd) a.rhs[(size_t)(m * k + j) * sd + lane] = racc[lane];
+}
+
+// trace (sequential, Eigen stand-in) and ridge = 1e-6 trace / dim (pq.hpp:431-435)
+__global__ void k_trace_ridge(double* A, size_t dim, double ridge) {
+  __shared__ double r;
+  if (threadIdx.x == 0) {
+    double tr = 0.0;
+    for (size_t i = 0; i < dim; ++i) tr = __dadd_rn(tr, A[i * dim + i]);
+    r = ridge < 0.0 ? __ddiv_rn(__dmul_rn(1e-6, tr), (double)dim) : ridge;
+  }
+  __syncthreads();
+  for (size_t i = threadIdx.x; i < dim; i += blockDim.x)
+    A[i * dim + i] = __dadd_rn(A[i * dim + i], r);
+}
+
+// ---- blocked Cholesky (lower, in place, row-major) --------------------------------------
+
+// Panel for block [kb, be): every CTA factors the diagonal block (identical,
+// deterministic) then the rows of its own range below the block.
+__global__ void k_llt_panel(double* A, int n, int kb, int rows_per_cta, int* fail) {
+  __shared__ double D[kLLT][kLLT + 1];
+  const int be = min(kb + kLLT, n), bs = be - kb;
+  const int t = threadIdx.x;
+  for (int e = t; e < bs * bs; e += blockDim.x) {
+    const int r = e / bs, c = e % bs;
+    D[r][c] = c <= r ? A[(size_t)(kb + r) * n + kb + c] : 0.0;
+  }
+  __syncthreads();
+  for (int jj = 0; jj < bs; ++jj) {
+    if (t == 0) {
+      double s = D[jj][jj];
+      for (int q = 0; q < jj; ++q) s = __dsub_rn(s, __dmul_rn(D[jj][q], D[jj][q]));
+      if (!(s > 0.0) && s <= 0.0) atomicExch(fail, 1);
+      D[jj][jj] = __dsqrt_rn(s);
+    }
+    __syncthreads();
+    const double dg = D[jj][jj];
+    for (int r = jj + 1 + t; r < bs; r += blockDim.x) {
+      double v = D[r][jj];
+      for (int q = 0; q < jj; ++q) v = __dsub_rn(v, __dmul_rn(D[r][q], D[jj][q]));
+      D[r][jj] = __ddiv_rn(v, dg);
+    }
+    __syncthreads();
+  }
+  if (blockIdx.x == 0)
+    for (int e = t; e < bs * bs; e += blockDim.x) {
+      const int r = e / bs, c = e % bs;
+      if (c <= r) A[(size_t)(kb + r) * n + kb + c] = D[r][c];
+    }
+  // rows below the block
+  const int r0 = be + blockIdx.x * rows_per_cta;
+  const int r1 = min(n, r0 + rows_per_cta);
+  for (int i = r0 + t; i < r1; i += blockDim.x) {
+    double* Li = A + (size_t)i * n + kb;
+    for (int jj = 0; jj < bs; ++jj) {
+      double v = Li[jj];
+      for (int q = 0; q < jj; ++q) v = __dsub_rn(v, __dmul_rn(Li[q], D[jj][q]));
+      Li[jj] = __ddiv_rn(v, D[jj][jj]);
+    }
+  }
+}
+
+// Trailing update of the lower triangle: L[i][c] -= sum_{q in block} L[i][q] L[c][q]
+// (sum sequential in q from 0.0, then one subtraction). 64 x 64 tiles.
+__global__ void __launch_bounds__(256) k_llt_trail(double* A, int n, int kb) {
+  extern __shared__ __align__(16) double tsm[];
+  double(*Pi)[kLLT + 1] = reinterpret_cast<double(*)[kLLT + 1]>(tsm);
+  double(*Pc)[kLLT + 1] = reinterpret_cast<double(*)[kLLT + 1]>(tsm + 64 * (kLLT + 1));
+  const int be = min(kb + kLLT, n), bs = be - kb;
+  // triangular tile index -> (ti, tc), tc <= ti
+  const int tile = blockIdx.x;
+  int ti = (int)((sqrt(8.0 * tile + 1.0) - 1.0) / 2.0);
+  while ((ti + 1) * (ti + 2) / 2 <= tile) ++ti;
+  while (ti * (ti + 1) / 2 > tile) --ti;
+  const int tc = tile - ti * (ti + 1) / 2;
+  const int i0 = be + ti * 64, c0 = be + tc * 64;
+  for (int e = threadIdx.x; e < 64 * bs; e += blockDim.x) {
+    const int r = e / bs, q = e % bs;
+    Pi[r][q] = i0 + r < n ? A[(size_t)(i0 + r) * n + kb + q] : 0.0;
+    Pc[r][q] = c0 + r < n ? A[(size_t)(c0 + r) * n + kb + q] : 0.0;
+  }
+  __syncthreads();
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double s[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) s[u][v] = 0.0;
+  for (int q = 0; q < bs; ++q) {
+    double pi[4], pc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      pi[u] = Pi[ty * 4 + u][q];
+      pc[u] = Pc[tx * 4 + u][q];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) s[u][v] = __dadd_rn(s[u][v], __dmul_rn(pi[u], pc[v]));
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int i = i0 + ty * 4 + u, c = c0 + tx * 4 + v;
+      if (i < n && c <= i) {
+        double* e = A + (size_t)i * n + c;
+        *e = __dsub_rn(*e, s[u][v]);
+      }
+    }
+}
+
+// LLT solve (forward L y = b, backward L^T x = y), blocked like the stand-in.
+__global__ void __launch_bounds__(1024) k_llt_solve(const double* L, int n, double* x) {
+  for (int kb = 0; kb < n; kb += kLLT) {
+    const int be = min(kb + kLLT, n);
+    if (threadIdx.x == 0)
+      for (int i = kb; i < be; ++i) {
+        double t = x[i];
+        for (int q = kb; q < i; ++q) t = __dsub_rn(t, __dmul_rn(L[(size_t)i * n + q], x[q]));
+        x[i] = __ddiv_rn(t, L[(size_t)i * n + i]);
+      }
+    __syncthreads();
+    for (int i = be + threadIdx.x; i < n; i += blockDim.x) {
+      double s = 0.0;
+      for (int q = kb; q < be; ++q) s = __dadd_rn(s, __dmul_rn(L[(size_t)i * n + q], x[q]));
+      x[i] = __dsub_rn(x[i], s);
+    }
+    __syncthreads();
+  }
+  const int nb = (n + kLLT - 1) / kLLT;
+  for (int bi = nb - 1; bi >= 0; --bi) {
+    const int kb = bi * kLLT, be = min(kb + kLLT, n);
+    if (threadIdx.x == 0)
+      for (int i = be - 1; i >= kb; --i) {
+        double t = x[i];
+        for (int q = i + 1; q < be; ++q) t = __dsub_rn(t, __dmul_rn(L[(size_t)q * n + i], x[q]));
+        x[i] = __ddiv_rn(t, L[(size_t)i * n + i]);
+      }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kb; i += blockDim.x) {
+      double s = 0.0;
+      for (int q = kb; q < be; ++q) s = __dadd_rn(s, __dmul_rn(L[(size_t)q * n + i], x[q]));
+      x[i] = __dsub_rn(x[i], s);
+    }
+    __syncthreads();
+  }
+}
+
+int llt_solve_device(aq_session* s, double* A, int n, double* x) {
+  int* fail;
+  void* p;
+  AQ_TRY(scratch(s, 4, 64, &p));
+  fail = (int*)p;
+  AQ_CUDA(cudaMemsetAsync(fail, 0, sizeof(int), s->stream));
+  for (int kb = 0; kb < n; kb += kLLT) {
+    const int be = std::min(kb + kLLT, n);
+    const int below = n - be;
+    const int rpc = 128;
+    const int ctas = std::max(1, (below + rpc - 1) / rpc);
+    k_llt_panel<<<ctas, 128, 0, s->stream>>>(A, n, kb, rpc, fail);
+    AQ_LAUNCHED(s);
+    if (below > 0) {
+      const int T = (below + 63) / 64;
+      const int tsmem = 2 * 64 * (kLLT + 1) * (int)sizeof(double);
+      AQ_CUDA(cudaFuncSetAttribute(k_llt_trail, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   tsmem));
+      k_llt_trail<<<T * (T + 1) / 2, 256, tsmem, s->stream>>>(A, n, kb);
+      AQ_LAUNCHED(s);
+    }
+  }
+  int hf = 0;
+  AQ_CUDA(cudaMemcpyAsync(&hf, fail, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+  AQ_CUDA(cudaStreamSynchronize(s->stream));
+  if (hf) return ref_error(AQ_E_SINGULAR_SYSTEM, "joint codebook system is not positive definite");
+  k_llt_solve<<<1, 1024, 0, s->stream>>>(A, n, x);
+  AQ_LAUNCHED(s);
+  return AQ_OK;
+}
+
+// ---- isotropic weighted means (pq.hpp:405-423) ------------------------------------------
+
+__global__ void k_iso_means(const float* xr, size_t n, int d, int M, int k, int sd,
+                            const uint32_t* list, const uint32_t* start,
+                            const uint32_t* count, const double* hp, const double* ho,
+                            double* dict, DevError* err) {
+  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= M * k) return;
+  const int m = slot / k;
+  const uint32_t* L = list + (size_t)m * n + start[slot];
+  const size_t cnt = count[slot];
+  if (cnt == 0) return;
+  double num[16];
+  for (int c = 0; c < sd; ++c) num[c] = 0.0;
+  double den = 0.0;
+  for (size_t t = 0; t < cnt; ++t) {
+    const uint32_t p = L[t];
+    for (int c = 0; c < sd; ++c)
+      num[c] = __dadd_rn(num[c], __dmul_rn(hp[p], (double)xr[(size_t)p * d + m * sd + c]));
+    den = __dadd_rn(den, ho[p]);
+  }
+  if (den <= 0.0) {
+    report_error(err, (uint64_t)slot, AQ_E_SINGULAR_SYSTEM);
+    return;
+  }
+  for (int c = 0; c < sd; ++c) dict[(size_t)slot * sd + c] = __ddiv_rn(num[c], den);
+}
+
+// unused-codeword reseeding: walk (m, j) lexicographically, consuming the
+// loss ranking cyclically (pq.hpp:452-461)
+__global__ void k_reseed(const uint32_t* count, int M, int k, int sd, const uint32_t* order,
+                         size_t n, const float* xr, int d, double* dict) {
+  size_t cursor = 0;
+  for (int m = 0; m < M; ++m)
+    for (int j = 0; j < k; ++j) {
+      if (count[m * k + j] != 0) continue;
+      const uint32_t p = order[cursor++ % n];
+      for (int c = 0; c < sd; ++c)
+        dict[((size_t)m * k + j) * sd + c] = (double)xr[(size_t)p * d + m * sd + c];
+    }
+}
+
+__global__ void k_iota(uint32_t* v, size_t n) {
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) v[t] = (uint32_t)t;
+}
+
+struct PointW {
+  double* hp = nullptr;
+  double* ho = nullptr;
+  double* coef = nullptr;
+  unsigned long long flags[2] = {0, 0};
+};
+
+int point_weights(aq_dataset* ds, const aq_weights* w, PointW* pw, void** owner) {
+  aq_session* s = ds->s;
+  const size_t n = ds->n;
+  DevWeights dw;
+  AQ_TRY(make_dev_weights(s, w, n, ds->d, &dw));
+  double* buf;
+  AQ_CUDA(cudaMallocAsync(&buf, (3 * n + 2) * sizeof(double), s->stream));
+  *owner = buf;
+  pw->hp = buf;
+  pw->ho = buf + n;
+  pw->coef = buf + 2 * n;
+  unsigned long long* fl = (unsigned long long*)(buf + 3 * n);
+  const unsigned long long init[2] = {0ull, ~0ull};
+  AQ_CUDA(cudaMemcpyAsync(fl, init, sizeof init, cudaMemcpyHostToDevice, s->stream));
+  AQ_TRY(clear_dev_error(s));
+  if (n) {
+    k_point_weights<<<(unsigned)((n + 255) / 256), 256, 0, s->stream>>>(
+        ds->norms, n, dw, pw->hp, pw->ho, pw->coef, fl, s->err);
+    AQ_LAUNCHED(s);
+  }
+  AQ_CUDA(cudaMemcpyAsync(pw->flags, fl, sizeof init, cudaMemcpyDeviceToHost, s->stream));
+  AQ_TRY(sync_and_check(s, "weights"));
+  return AQ_OK;
+}
+
+// Assembles the system into device buffers A (dim^2) and rhs (dim).
+int assemble_device(aq_dataset* ds, aq_codes* codes, const PointW& pw, const Buckets& B,
+                    int k, bool full, double* A, double* rhs) {
+  aq_session* s = ds->s;
+  const int M = (int)codes->M, d = (int)ds->d, sd = d / M;
+  const size_t dim = (size_t)k * d;
+  AQ_CUDA(cudaMemsetAsync(A, 0, dim * dim * sizeof(double), s->stream));
+  AQ_CUDA(cudaMemsetAsync(rhs, 0, dim * sizeof(double), s->stream));
+  const int nchunk = (M + 31) / 32;
+  AsmArgs a{ds->xr, ds->n, d, M, k, sd, codes->data, (int)codes->stride, codes->bits,
+            B.list, B.start, B.count, pw.hp, pw.ho, pw.coef, full ? 1 : 0, A, rhs, nchunk};
+  const size_t smem = ((size_t)sd * k * sd * 32 + 16) * sizeof(double);
+  if (smem > 227 * 1024)
+    return ref_error(AQ_E_UNSUPPORTED, "normal-equation strip exceeds shared memory");
+  AQ_CUDA(cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem));
+  const unsigned units = (unsigned)(M * k * nchunk);
+  k_assemble<<<units, 32, smem, s->stream>>>(a);
+  AQ_LAUNCHED(s);
+  return AQ_OK;
+}
+
+int check_update_args(aq_dataset* ds, aq_codes* codes, size_t M) {
+  if (ds->n == 0) return ref_error(AQ_E_EMPTY_DATASET, "cannot update on an empty dataset");
+  if (codes->n != ds->n || codes->M != M)
+    return ref_error(AQ_E_DIMENSION_MISMATCH, "code matrix does not match dataset");
+  if (M == 0 || ds->d % M != 0)
+    return ref_error(AQ_E_DIMENSION_NOT_DIVISIBLE, "dimension not divisible by M");
+  return AQ_OK;
+}
+
+}  // namespace aqd
+
+using namespace aqd;
+
+extern "C" {
+
+// assemble_selector_system (pq.hpp:290-343): full matrix, host outputs.
+int aq_dev_assemble_selector_system(aq_dataset* ds, aq_codes* codes, const aq_weights* w,
+                                    double* A_out, double* rhs_out) {
+  if (!ds || !codes) return ref_error(AQ_E_INVALID_ARGUMENT, "null argument");
+  aq_session* s = ds->s;
+  AQ_TRY(check_session(s));
+  if (codes->n != ds->n || codes->M == 0)
+    return ref_error(AQ_E_DIMENSION_MISMATCH, "code matrix does not match dataset");
+  if (ds->d % codes->M != 0)
+    return ref_error(AQ_E_DIMENSION_NOT_DIVISIBLE, "dimension not divisible by M");
+  const int k = (int)codes->k, M = (int)codes->M;
+  const size_t dim = (size_t)k * ds->d;
+  void* owner = nullptr;
+  PointW pw;
+  AQ_TRY(point_weights(ds, w, &pw, &owner));
+  int st = AQ_OK;
+  if (pw.flags[1] != ~0ull) {
+    char msg[128];
+    snprintf(msg, sizeof msg, "anisotropic update undefined at |x| = 0 (point %llu)",
+             pw.flags[1] - 1);
+    st = ref_error(AQ_E_ZERO_NORM_DATAPOINT, msg);
+  }
+  Buckets B;
+  double* A = nullptr;
+  if (st == AQ_OK && ds->n) st = build_buckets(codes, k, &B);
+  if (st == AQ_OK) {
+    if (cudaMallocAsync(&A, (dim * dim + dim) * sizeof(double), s->stream) != cudaSuccess)
+      st = ref_error(AQ_E_CUDA, "out of device memory for the normal equations");
+  }
+  if (st == AQ_OK && ds->n) st = assemble_device(ds, codes, pw, B, k, true, A, A + dim * dim);
+  if (st == AQ_OK && !ds->n) {
+    cudaMemsetAsync(A, 0, (dim * dim + dim) * sizeof(double), s->stream);
+  }
+  if (st == AQ_OK) {
+    cudaMemcpyAsync(A_out, A, dim * dim * sizeof(double), cudaMemcpyDeviceToHost, s->stream);
+    cudaMemcpyAsync(rhs_out, A + dim * dim, dim * sizeof(double), cudaMemcpyDeviceToHost,
+                    s->stream);
+  }
+  if (A) cudaFreeAsync(A, s->stream);
+  cudaFreeAsync(owner, s->stream);
+  cudaStreamSynchronize(s->stream);
+  (void)M;
+  return st;
+}
+
+// pq_codebook_update (pq.hpp:356-464): writes `out` (M x k x sd, allocated).
+int aq_dev_pq_codebook_update(aq_dataset* ds, aq_codes* codes, const aq_weights* w,
+                              double ridge, aq_codebook* out) {
+  if (!ds || !codes || !out) return ref_error(AQ_E_INVALID_ARGUMENT, "null argument");
+  aq_session* s = ds->s;
+  AQ_TRY(check_session(s));
+  const size_t M = out->M, k = out->k;
+  AQ_TRY(check_update_args(ds, codes, M));
+  if (codes->k > k) return ref_error(AQ_E_CODE_OUT_OF_RANGE, "code out of range");
+  const int sd = (int)(ds->d / M);
+  if ((size_t)sd != out->sd)
+    return ref_error(AQ_E_DIMENSION_MISMATCH, "codebook sub-dimension does not match");
+  if (M == 1)
+    return ref_error(AQ_E_UNSUPPORTED,
+                     "M == 1 (vector quantization update) is not on the device path yet");
+  if (sd > 16) return ref_error(AQ_E_UNSUPPORTED, "device update supports sub_dimension <= 16");
+  const size_t n = ds->n, dim = k * ds->d;
+  Buckets B;
+  AQ_TRY(build_buckets(codes, (int)k, &B));
+  void* owner = nullptr;
+  PointW pw;
+  int st = point_weights(ds, w, &pw, &owner);
+  double* A = nullptr;
+  if (st == AQ_OK)
+    st = cudaMemsetAsync(out->d64, 0, M * k * sd * sizeof(double), s->stream) == cudaSuccess
+             ? AQ_OK
+             : AQ_E_CUDA;
+  const bool all_iso = pw.flags[0] == 0;
+  if (st == AQ_OK && all_iso) {
+    AQ_TRY(clear_dev_error(s));
+    k_iso_means<<<(unsigned)((M * k + 127) / 128), 128, 0, s->stream>>>(
+        ds->xr, n, (int)ds->d, (int)M, (int)k, sd, B.list, B.start, B.count, pw.hp, pw.ho,
+        out->d64, s->err);
+    s->launches++;
+    st = sync_and_check(s, "zero total weight in block");
+  } else if (st == AQ_OK) {
+    if (dim > 16384) {
+      st = ref_error(AQ_E_INVALID_ARGUMENT,
+                     "stacked codebook system exceeds 16384 unknowns (pq.hpp:426-429)");
+    } else if (pw.flags[1] != ~0ull) {
+      char msg[128];
+      snprintf(msg, sizeof msg, "anisotropic update undefined at |x| = 0 (point %llu)",
+               pw.flags[1] - 1);
+      st = ref_error(AQ_E_ZERO_NORM_DATAPOINT, msg);
+    } else if (cudaMallocAsync(&A, (dim * dim + dim) * sizeof(double), s->stream) !=
+               cudaSuccess) {
+      st = ref_error(AQ_E_CUDA, "out of device memory for the normal equations");
+    }
+    if (st == AQ_OK) st = assemble_device(ds, codes, pw, B, (int)k, false, A, A + dim * dim);
+    if (st == AQ_OK) {
+      k_trace_ridge<<<1, 1024, 0, s->stream>>>(A, dim, ridge);
+      s->launches++;
+      st = llt_solve_device(s, A, (int)dim, A + dim * dim);
+    }
+    if (st == AQ_OK &&
+        cudaMemcpyAsync(out->d64, A + dim * dim, dim * sizeof(double),
+                        cudaMemcpyDeviceToDevice, s->stream) != cudaSuccess)
+      st = AQ_E_CUDA;
+  }
+  // reseed unused codewords from the loss ranking under the new codebook
+  if (st == AQ_OK) {
+    std::vector<uint32_t> hc(M * k);
+    cudaMemcpyAsync(hc.data(), B.count, M * k * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                    s->stream);
+    cudaStreamSynchronize(s->stream);
+    bool any_unused = false;
+    for (auto c : hc) any_unused |= c == 0;
+    if (any_unused) {
+      st = stage_codebook(out);
+      double* losses = nullptr;
+      uint32_t* idx = nullptr;
+      uint32_t* cnt_copy = nullptr;
+      if (st == AQ_OK) {
+        cudaMallocAsync(&losses, n * sizeof(double), s->stream);
+        cudaMallocAsync(&idx, n * sizeof(uint32_t), s->stream);
+        cudaMallocAsync(&cnt_copy, M * k * sizeof(uint32_t), s->stream);
+        cudaMemcpyAsync(cnt_copy, hc.data(), M * k * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                        s->stream);
+        st = run_encode(ds, out, w, codes, 2, 0, 0, losses, nullptr);
+      }
+      if (st == AQ_OK) {
+        k_iota<<<(unsigned)((n + 255) / 256), 256, 0, s->stream>>>(idx, n);
+        s->launches++;
+        st = sort_scores_desc(s, losses, idx, n);
+      }
+      if (st == AQ_OK) {
+        k_reseed<<<1, 1, 0, s->stream>>>(cnt_copy, (int)M, (int)k, sd, idx, n, ds->xr,
+                                         (int)ds->d, out->d64);
+        s->launches++;
+      }
+      if (losses) cudaFreeAsync(losses, s->stream);
+      if (idx) cudaFreeAsync(idx, s->stream);
+      if (cnt_copy) cudaFreeAsync(cnt_copy, s->stream);
+    }
+  }
+  if (st == AQ_OK) st = stage_codebook(out);
+  if (A) cudaFreeAsync(A, s->stream);
+  if (owner) cudaFreeAsync(owner, s->stream);
+  cudaError_t e = cudaStreamSynchronize(s->stream);
+  if (st == AQ_OK && e != cudaSuccess) {
+    set_error(AQ_E_CUDA, "CUDA error %s", cudaGetErrorString(e));
+    st = AQ_E_CUDA;
+  }
+  return st;
+}
+
+// Host-pointer form of pq_codebook_update.
+int aq_pq_codebook_update(aq_session* s, const float* x, size_t n, size_t d,
+                          const uint32_t* codes, size_t M, size_t k, const aq_weights* w,
+                          double ridge, double* dict_out) {
+  AQ_TRY(check_session(s));
+  if (n == 0) return ref_error(AQ_E_EMPTY_DATASET, "cannot update on an empty dataset");
+  if (M == 0 || d % M != 0)
+    return ref_error(AQ_E_DIMENSION_NOT_DIVISIBLE, "dimension not divisible by M");
+  aq_dataset* ds = nullptr;
+  aq_codes* cm = nullptr;
+  aq_codebook* cb = nullptr;
+  int st = aq_dataset_upload(s, x, n, d, &ds);
+  if (st == AQ_OK) st = aq_codes_upload(s, codes, n, M, k, &cm);
+  if (st == AQ_OK) st = aq_codebook_upload(s, nullptr, M, k, d / M, &cb);
+  if (st == AQ_OK) st = aq_dev_pq_codebook_update(ds, cm, w, ridge, cb);
+  if (st == AQ_OK) st = aq_codebook_download(cb, dict_out);
+  aq_codebook_free(cb);
+  aq_codes_free(cm);
+  aq_dataset_free(ds);
+  return st;
+}
+
+}  // extern "C"

@@ -560,3 +560,47 @@ def assemble_selector_system(data, codes: CodeMatrix, weights, M: int, k: int,
     _check(_L.aq_dev_assemble_selector_system(ds.h, dc.h, C.byref(w), A.ctypes.data,
                                               rhs.ctypes.data))
     return A, rhs
+
+
+# ---- trainers (pq.hpp:469-575) ---------------------------------------------------------
+
+
+def dev_train_l2_pq(ds: DeviceDataset, M: int, k: int, config: TrainConfig = TrainConfig()):
+    cfg = config.c()
+    cb, cm = C.c_void_p(), C.c_void_p()
+    _check(_L.aq_dev_train_l2_pq(ds.h, M, k, C.byref(cfg), C.byref(cb), C.byref(cm)))
+    return (DeviceCodebook(ds.s, cb, M, k, ds.d // M), DeviceCodes(ds.s, cm, ds.n, M, k))
+
+
+def dev_train_apq(ds: DeviceDataset, M: int, k: int, weights, config: TrainConfig = TrainConfig(),
+                  warm_start: bool = True, loss_history: Optional[list] = None):
+    cfg = config.c()
+    keep: list = []
+    w = _weights(weights, ds.n, keep)
+    cb, cm = C.c_void_p(), C.c_void_p()
+    hist = np.zeros(max(config.max_iterations, 0) + 1, np.float64)
+    hl = C.c_size_t(0)
+    _check(_L.aq_dev_train_apq(ds.h, M, k, C.byref(w), C.byref(cfg), int(warm_start),
+                               C.byref(cb), C.byref(cm), hist.ctypes.data, C.byref(hl)))
+    if loss_history is not None:
+        loss_history.extend(float(v) for v in hist[: hl.value])
+    return (DeviceCodebook(ds.s, cb, M, k, ds.d // M), DeviceCodes(ds.s, cm, ds.n, M, k))
+
+
+def train_l2_pq(data, M: int, k: int, config: TrainConfig = TrainConfig(),
+                session: Optional[Session] = None):
+    """pq.hpp:469-501: classical PQ (independent k-means per subspace, seed + m)."""
+    s = _sess(session)
+    ds = s.upload_dataset(data)
+    cb, cm = dev_train_l2_pq(ds, M, k, config)
+    return cb.download(), cm.download()
+
+
+def train_apq(data, M: int, k: int, weights, config: TrainConfig = TrainConfig(),
+              warm_start: bool = True, loss_history: Optional[list] = None,
+              session: Optional[Session] = None):
+    """pq.hpp:513-575: alternating anisotropic PQ trainer."""
+    s = _sess(session)
+    ds = s.upload_dataset(data)
+    cb, cm = dev_train_apq(ds, M, k, weights, config, warm_start, loss_history)
+    return cb.download(), cm.download()

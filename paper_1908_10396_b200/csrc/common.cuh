@@ -145,6 +145,17 @@ __device__ __forceinline__ unsigned get_code(const uint8_t* row, int m,
   return row[m];
 }
 
+// Stable per-subspace bucket lists of points by code (update.cu): list[m][.]
+// holds, for every code j, the points with code j at subspace m in ascending
+// order starting at start[m][j], count[m][j] of them.
+struct Buckets {
+  uint32_t* list = nullptr;   // [M][n]
+  uint32_t* start = nullptr;  // [M][K]
+  uint32_t* count = nullptr;  // [M][K]
+  int K = 0;
+};
+int build_buckets(aq_codes* c, int k, Buckets* B);
+
 // ---- weights ------------------------------------------------------------------
 // Resolved per point on the device from an aq_weights descriptor
 // (geometry.hpp:119-145, eta_limit 395-402, CLI resolve_weights

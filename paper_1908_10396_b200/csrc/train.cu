@@ -1,0 +1,416 @@
+// Trainers on the device:
+//   * train_l2_pq (pq.hpp:469-501): M independent isotropic k-means runs
+//     (train_avq, vq.hpp:243-329, seed + m per subspace) advanced in lockstep,
+//     each subspace stopping on its own criterion;
+//   * train_apq (pq.hpp:513-575): warm or cold start, assignment pass
+//     (encode.cu), joint codebook update (update.cu), loss history and the
+//     reference's stopping rules.
+// Loss totals are std::accumulate in index order (pq.hpp:553,562;
+// vq.hpp:270,316): a single-thread float64 chain per subspace, so histories
+// are bit-identical to the reference.
+#include <algorithm>
+#include <unordered_map>
+#include <vector>
+
+#include "common.cuh"
+
+namespace aqd {
+
+int sort_scores_desc(aq_session* s, const double* scores, uint32_t* idx, size_t n);
+int run_encode(aq_dataset* ds, aq_codebook* cb, const aq_weights* w, aq_codes* codes,
+               int mode, int passes, int sweep_fixed, double* losses_dev,
+               uint64_t* changed_out);
+int stage_codebook(aq_codebook* cb);
+
+
+// ---- Rng (rng.hpp:28-89), host side -----------------------------------------------------
+struct HostRng {
+  uint64_t state;
+  uint64_t next_u64() {
+    state += 0x9E3779B97F4A7C15ull;
+    uint64_t z = state;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  }
+  uint64_t next_below(uint64_t n) {
+    const uint64_t threshold = (0 - n) % n;
+    for (;;) {
+      const uint64_t r = next_u64();
+      if (r >= threshold) return r % n;
+    }
+  }
+  // sample_distinct (rng.hpp:74-83): partial Fisher-Yates on iota(n); only the
+  // touched positions are materialised, so it is O(k) instead of O(n).
+  std::vector<size_t> sample_distinct(size_t n, size_t k) {
+    std::unordered_map<size_t, size_t> moved;
+    auto get = [&](size_t i) {
+      auto it = moved.find(i);
+      return it == moved.end() ? i : it->second;
+    };
+    std::vector<size_t> out;
+    for (size_t i = 0; i < k && i < n; ++i) {
+      const size_t j = i + (size_t)next_below(n - i);
+      const size_t vi = get(i), vj = get(j);
+      moved[i] = vj;
+      moved[j] = vi;
+      out.push_back(vj);
+    }
+    return out;
+  }
+};
+
+// ---- kernels ------------------------------------------------------------------------------
+
+// std::accumulate of `count` values (float64, index order), one thread per row
+__global__ void k_seq_sums(const double* __restrict__ v, size_t ld, size_t count, int rows,
+                           const int* __restrict__ active, double* __restrict__ out) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows || (active && !active[r])) return;
+  const double* p = v + (size_t)r * ld;
+  double s = 0.0;
+  for (size_t i = 0; i < count; ++i) s = __dadd_rn(s, p[i]);
+  out[r] = s;
+}
+
+// codewords from sampled rows: dict[m][j] = x[idx[m][j]][m-subvector]
+__global__ void k_init_codewords(const float* __restrict__ xr, int d, int M, int k, int sd,
+                                 const uint64_t* __restrict__ idx, double* __restrict__ dict) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= M * k) return;
+  const int m = t / k;
+  const uint64_t p = idx[t];
+  for (int c = 0; c < sd; ++c)
+    dict[(size_t)t * sd + c] = (double)xr[p * d + (size_t)m * sd + c];
+}
+
+__device__ __forceinline__ void set_code(uint8_t* row, int m, int bits, unsigned c) {
+  if (bits == 4) {
+    const int sh = (m & 1) * 4;
+    row[m >> 1] = (uint8_t)((row[m >> 1] & ~(15u << sh)) | (c << sh));
+  } else {
+    row[m] = (uint8_t)c;
+  }
+}
+
+// vq_assign_pass with isotropic unit weights (vq.hpp:196-217, assign_scan
+// 83-100): per subspace argmin of dist2 (first index wins), loss = 1.0 dist2.
+// One thread per point walks the active subspaces (codes share bytes).
+__global__ void k_kmeans_assign(const float* __restrict__ xr, size_t n, int d, int M, int k,
+                                int sd, const double* __restrict__ dict,
+                                const int* __restrict__ active, uint8_t* __restrict__ codes,
+                                int stride, int bits, double* __restrict__ losses,
+                                unsigned long long* __restrict__ changes) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint8_t* row = codes + i * stride;
+  const float* xp = xr + i * d;
+  for (int m = 0; m < M; ++m) {
+    if (!active[m]) continue;
+    const double* cm = dict + (size_t)m * k * sd;
+    unsigned bj = 0;
+    double bd = 0.0;
+    for (int j = 0; j < k; ++j) {
+      double d2 = 0.0;
+      for (int c = 0; c < sd; ++c) {
+        const double diff = __dsub_rn((double)xp[m * sd + c], cm[j * sd + c]);
+        d2 = __dadd_rn(d2, __dmul_rn(diff, diff));
+      }
+      if (j == 0 || d2 < bd) {
+        bd = d2;
+        bj = (unsigned)j;
+      }
+    }
+    const unsigned old = get_code(row, m, bits);
+    if (old != bj) {
+      set_code(row, m, bits, bj);
+      atomicAdd(&changes[m], 1ull);
+    }
+    losses[(size_t)m * n + i] = __dmul_rn(1.0, bd);
+  }
+}
+
+// update_codeword isotropic path (vq.hpp:151-162) with unit weights:
+// mean = (sum 1.0 x) / (sum 1.0), members in ascending order.
+__global__ void k_kmeans_means(const float* __restrict__ xr, size_t n, int d, int M, int k,
+                               int sd, const uint32_t* __restrict__ list,
+                               const uint32_t* __restrict__ start,
+                               const uint32_t* __restrict__ count,
+                               const int* __restrict__ active, double* __restrict__ dict) {
+  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= M * k) return;
+  const int m = slot / k;
+  if (!active[m]) return;
+  const size_t cnt = count[slot];
+  if (cnt == 0) return;  // reseeded by the host walk
+  const uint32_t* L = list + (size_t)m * n + start[slot];
+  double num[16];
+  for (int c = 0; c < sd; ++c) num[c] = 0.0;
+  double den = 0.0;
+  for (size_t t = 0; t < cnt; ++t) {
+    const uint32_t p = L[t];
+    for (int c = 0; c < sd; ++c)
+      num[c] = __dadd_rn(num[c], __dmul_rn(1.0, (double)xr[(size_t)p * d + m * sd + c]));
+    den = __dadd_rn(den, 1.0);
+  }
+  for (int c = 0; c < sd; ++c) dict[(size_t)slot * sd + c] = __ddiv_rn(num[c], den);
+}
+
+// empty partitions (vq.hpp:284-292): j ascending, consuming the ranking
+__global__ void k_kmeans_reseed(const uint32_t* __restrict__ count, int m, int k, int sd,
+                                const uint32_t* __restrict__ order, const float* xr, int d,
+                                double* dict) {
+  size_t cursor = 0;
+  for (int j = 0; j < k; ++j) {
+    if (count[m * k + j] != 0) continue;
+    const uint32_t p = order[cursor++];
+    for (int c = 0; c < sd; ++c)
+      dict[((size_t)m * k + j) * sd + c] = (double)xr[(size_t)p * d + m * sd + c];
+  }
+}
+
+__global__ void k_iota2(uint32_t* v, size_t n) {
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) v[t] = (uint32_t)t;
+}
+
+// ---- train_l2_pq -----------------------------------------------------------------------------
+
+int train_l2_pq_device(aq_dataset* ds, size_t M, size_t k, const aq_train_config* cfg,
+                       aq_codebook** cb_out, aq_codes** codes_out) {
+  aq_session* s = ds->s;
+  const size_t n = ds->n, d = ds->d;
+  if (n == 0) return ref_error(AQ_E_EMPTY_DATASET, "cannot train on an empty dataset");
+  if (M == 0 || d % M != 0) return ref_error(AQ_E_DIMENSION_NOT_DIVISIBLE, "dimension not divisible by M");
+  if (k == 0 || k > n) return ref_error(AQ_E_INVALID_ARGUMENT, "need 1 <= k <= n");
+  if (k > 256) return ref_error(AQ_E_UNSUPPORTED, "device trainers support k <= 256");
+  const size_t sd = d / M;
+  if (sd > 16) return ref_error(AQ_E_UNSUPPORTED, "device trainers support sub_dimension <= 16");
+  aq_codebook* cb = nullptr;
+  aq_codes* codes = nullptr;
+  AQ_TRY(aq_codebook_upload(s, nullptr, M, k, sd, &cb));
+  int st = aq_codes_alloc(s, n, M, k, &codes);
+  // initial codewords: Rng(seed + m).sample_distinct(n, k) per subspace
+  std::vector<uint64_t> hidx(M * k);
+  for (size_t m = 0; m < M; ++m) {
+    HostRng r{cfg->seed + m};
+    const auto v = r.sample_distinct(n, k);
+    for (size_t j = 0; j < k; ++j) hidx[m * k + j] = v[j];
+  }
+  double* losses = nullptr;
+  double* totals = nullptr;
+  unsigned long long* changes = nullptr;
+  int* active = nullptr;
+  uint64_t* didx = nullptr;
+  uint32_t* order = nullptr;
+  if (st == AQ_OK) {
+    cudaMallocAsync(&losses, M * n * sizeof(double), s->stream);
+    cudaMallocAsync(&totals, M * sizeof(double), s->stream);
+    cudaMallocAsync(&changes, M * sizeof(unsigned long long), s->stream);
+    cudaMallocAsync(&active, M * sizeof(int), s->stream);
+    cudaMallocAsync(&didx, M * k * sizeof(uint64_t), s->stream);
+    cudaMallocAsync(&order, n * sizeof(uint32_t), s->stream);
+    cudaMemcpyAsync(didx, hidx.data(), M * k * sizeof(uint64_t), cudaMemcpyHostToDevice, s->stream);
+    k_init_codewords<<<(unsigned)((M * k + 127) / 128), 128, 0, s->stream>>>(
+        ds->xr, (int)d, (int)M, (int)k, (int)sd, didx, cb->d64);
+    s->launches++;
+  }
+  std::vector<int> hact(M, 1);
+  std::vector<double> htot(M), hprev(M);
+  std::vector<unsigned long long> hchg(M);
+  auto assign = [&]() -> int {
+    AQ_CUDA(cudaMemcpyAsync(active, hact.data(), M * sizeof(int), cudaMemcpyHostToDevice, s->stream));
+    AQ_CUDA(cudaMemsetAsync(changes, 0, M * sizeof(unsigned long long), s->stream));
+    k_kmeans_assign<<<(unsigned)((n + 127) / 128), 128, 0, s->stream>>>(
+        ds->xr, n, (int)d, (int)M, (int)k, (int)sd, cb->d64, active, codes->data,
+        (int)codes->stride, codes->bits, losses, changes);
+    AQ_LAUNCHED(s);
+    k_seq_sums<<<(unsigned)((M + 31) / 32), 32, 0, s->stream>>>(losses, n, n, (int)M, active, totals);
+    AQ_LAUNCHED(s);
+    AQ_CUDA(cudaMemcpyAsync(htot.data(), totals, M * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    AQ_CUDA(cudaMemcpyAsync(hchg.data(), changes, M * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, s->stream));
+    AQ_CUDA(cudaStreamSynchronize(s->stream));
+    return AQ_OK;
+  };
+  if (st == AQ_OK) st = assign();
+  for (int iter = 0; st == AQ_OK && iter < cfg->max_iterations; ++iter) {
+    bool any = false;
+    for (size_t m = 0; m < M; ++m) any |= hact[m] != 0;
+    if (!any) break;
+    Buckets B;
+    st = build_buckets(codes, (int)k, &B);
+    if (st != AQ_OK) break;
+    AQ_CUDA(cudaMemcpyAsync(active, hact.data(), M * sizeof(int), cudaMemcpyHostToDevice, s->stream));
+    k_kmeans_means<<<(unsigned)((M * k + 127) / 128), 128, 0, s->stream>>>(
+        ds->xr, n, (int)d, (int)M, (int)k, (int)sd, B.list, B.start, B.count, active, cb->d64);
+    s->launches++;
+    if (cfg->empty_partition_policy == 0) {
+      std::vector<uint32_t> hc(M * k);
+      AQ_CUDA(cudaMemcpyAsync(hc.data(), B.count, M * k * sizeof(uint32_t),
+                              cudaMemcpyDeviceToHost, s->stream));
+      AQ_CUDA(cudaStreamSynchronize(s->stream));
+      for (size_t m = 0; m < M && st == AQ_OK; ++m) {
+        if (!hact[m]) continue;
+        bool empty = false;
+        for (size_t j = 0; j < k; ++j) empty |= hc[m * k + j] == 0;
+        if (!empty) continue;
+        // loss_ranking of the last assignment pass (vq.hpp:221-229)
+        uint32_t* cnt_copy = nullptr;
+        cudaMallocAsync(&cnt_copy, M * k * sizeof(uint32_t), s->stream);
+        cudaMemcpyAsync(cnt_copy, hc.data(), M * k * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                        s->stream);
+        k_iota2<<<(unsigned)((n + 255) / 256), 256, 0, s->stream>>>(order, n);
+        s->launches++;
+        st = sort_scores_desc(s, losses + m * n, order, n);
+        if (st == AQ_OK) {
+          k_kmeans_reseed<<<1, 1, 0, s->stream>>>(cnt_copy, (int)m, (int)k, (int)sd, order,
+                                                  ds->xr, (int)d, cb->d64);
+          s->launches++;
+        }
+        cudaFreeAsync(cnt_copy, s->stream);
+      }
+    }
+    if (st != AQ_OK) break;
+    hprev = htot;
+    st = assign();
+    if (st != AQ_OK) break;
+    for (size_t m = 0; m < M; ++m) {
+      if (!hact[m]) continue;
+      if (hchg[m] == 0) {
+        hact[m] = 0;
+        continue;
+      }
+      if (cfg->relative_tolerance > 0.0 &&
+          (hprev[m] == 0.0 || hprev[m] - htot[m] <= cfg->relative_tolerance * hprev[m]))
+        hact[m] = 0;
+    }
+  }
+  cudaFreeAsync(losses, s->stream);
+  cudaFreeAsync(totals, s->stream);
+  cudaFreeAsync(changes, s->stream);
+  cudaFreeAsync(active, s->stream);
+  cudaFreeAsync(didx, s->stream);
+  cudaFreeAsync(order, s->stream);
+  if (st == AQ_OK) st = stage_codebook(cb);
+  cudaStreamSynchronize(s->stream);
+  if (st != AQ_OK) {
+    aq_codebook_free(cb);
+    aq_codes_free(codes);
+    return st;
+  }
+  *cb_out = cb;
+  *codes_out = codes;
+  return AQ_OK;
+}
+
+}  // namespace aqd
+
+using namespace aqd;
+
+extern "C" {
+
+int aq_dev_train_l2_pq(aq_dataset* ds, size_t M, size_t k, const aq_train_config* cfg,
+                       aq_codebook** cb_out, aq_codes** codes_out) {
+  if (!ds || !cfg || !cb_out || !codes_out) return ref_error(AQ_E_INVALID_ARGUMENT, "null argument");
+  AQ_TRY(check_session(ds->s));
+  return train_l2_pq_device(ds, M, k, cfg, cb_out, codes_out);
+}
+
+// train_apq (pq.hpp:513-575). history_out must hold max_iterations + 1 values.
+int aq_dev_train_apq(aq_dataset* ds, size_t M, size_t k, const aq_weights* w,
+                     const aq_train_config* cfg, int warm_start, aq_codebook** cb_out,
+                     aq_codes** codes_out, double* history_out, size_t* history_len) {
+  if (!ds || !cfg || !cb_out || !codes_out) return ref_error(AQ_E_INVALID_ARGUMENT, "null argument");
+  aq_session* s = ds->s;
+  AQ_TRY(check_session(s));
+  const size_t n = ds->n, d = ds->d;
+  if (n == 0) return ref_error(AQ_E_EMPTY_DATASET, "cannot train on an empty dataset");
+  if (M == 0 || d % M != 0) return ref_error(AQ_E_DIMENSION_NOT_DIVISIBLE, "dimension not divisible by M");
+  if (k == 0 || k > n) return ref_error(AQ_E_INVALID_ARGUMENT, "need 1 <= k <= n");
+  if (history_len) *history_len = 0;
+  const size_t sd = d / M;
+  aq_codebook* cb = nullptr;
+  aq_codes* codes = nullptr;
+  if (warm_start) {
+    AQ_TRY(train_l2_pq_device(ds, M, k, cfg, &cb, &codes));
+  } else {
+    // one generator, one sample_distinct per subspace (pq.hpp:533-542)
+    HostRng r{cfg->seed};
+    std::vector<uint64_t> hidx(M * k);
+    for (size_t m = 0; m < M; ++m) {
+      const auto v = r.sample_distinct(n, k);
+      for (size_t j = 0; j < k; ++j) hidx[m * k + j] = v[j];
+    }
+    AQ_TRY(aq_codebook_upload(s, nullptr, M, k, sd, &cb));
+    uint64_t* didx = nullptr;
+    AQ_CUDA(cudaMallocAsync(&didx, M * k * sizeof(uint64_t), s->stream));
+    AQ_CUDA(cudaMemcpyAsync(didx, hidx.data(), M * k * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                            s->stream));
+    k_init_codewords<<<(unsigned)((M * k + 127) / 128), 128, 0, s->stream>>>(
+        ds->xr, (int)d, (int)M, (int)k, (int)sd, didx, cb->d64);
+    s->launches++;
+    cudaFreeAsync(didx, s->stream);
+    int st = stage_codebook(cb);
+    if (st == AQ_OK) st = aq_codes_alloc(s, n, M, k, &codes);
+    // reconstruction_nearest_pass (pq.hpp:547): the encoder with 0 sweeps
+    aq_weights iso{AQ_WEIGHTS_UNIFORM, 1.0, 1.0, nullptr, nullptr, 0.0, 0};
+    if (st == AQ_OK) st = run_encode(ds, cb, &iso, codes, 0, 0, 0, nullptr, nullptr);
+    if (st != AQ_OK) {
+      aq_codebook_free(cb);
+      aq_codes_free(codes);
+      return st;
+    }
+  }
+  double* losses = nullptr;
+  double* total = nullptr;
+  int st = AQ_OK;
+  if (cudaMallocAsync(&losses, n * sizeof(double), s->stream) != cudaSuccess ||
+      cudaMallocAsync(&total, sizeof(double), s->stream) != cudaSuccess)
+    st = ref_error(AQ_E_CUDA, "out of device memory");
+  auto pass = [&](double* tot_h, uint64_t* changed) -> int {
+    AQ_TRY(run_encode(ds, cb, w, codes, 1, 0, cfg->sweep_to_fixed_point, losses, changed));
+    k_seq_sums<<<1, 1, 0, s->stream>>>(losses, n, n, 1, nullptr, total);
+    AQ_LAUNCHED(s);
+    AQ_CUDA(cudaMemcpyAsync(tot_h, total, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    AQ_CUDA(cudaStreamSynchronize(s->stream));
+    return AQ_OK;
+  };
+  double tot = 0.0;
+  uint64_t changed = 0;
+  size_t hl = 0;
+  if (st == AQ_OK) st = pass(&tot, &changed);
+  if (st == AQ_OK && history_out) history_out[hl] = tot;
+  if (st == AQ_OK) ++hl;
+  aq_codebook* next = nullptr;
+  if (st == AQ_OK) st = aq_codebook_upload(s, nullptr, M, k, sd, &next);
+  for (int iter = 0; st == AQ_OK && iter < cfg->max_iterations; ++iter) {
+    st = aq_dev_pq_codebook_update(ds, codes, w, cfg->ridge, next);
+    if (st != AQ_OK) break;
+    std::swap(cb, next);
+    const double prev = tot;
+    st = pass(&tot, &changed);
+    if (st != AQ_OK) break;
+    if (history_out) history_out[hl] = tot;
+    ++hl;
+    if (changed == 0) break;
+    if (cfg->relative_tolerance > 0.0 &&
+        (prev == 0.0 || prev - tot <= cfg->relative_tolerance * prev))
+      break;
+  }
+  if (history_len) *history_len = hl;
+  aq_codebook_free(next);
+  if (losses) cudaFreeAsync(losses, s->stream);
+  if (total) cudaFreeAsync(total, s->stream);
+  cudaStreamSynchronize(s->stream);
+  if (st != AQ_OK) {
+    aq_codebook_free(cb);
+    aq_codes_free(codes);
+    return st;
+  }
+  *cb_out = cb;
+  *codes_out = codes;
+  return AQ_OK;
+}
+
+}  // extern "C"

@@ -101,12 +101,6 @@ __global__ void k_bucket_offsets(const unsigned* __restrict__ base, size_t nb, i
   count[t] = s1 - s0;
 }
 
-struct Buckets {
-  uint32_t* list = nullptr;   // [M][n]
-  uint32_t* start = nullptr;  // [M][K]
-  uint32_t* count = nullptr;  // [M][K]
-  int K = 0;
-};
 
 int build_buckets(aq_codes* c, int k, Buckets* B) {
   aq_session* s = c->s;

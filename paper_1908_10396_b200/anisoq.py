@@ -604,3 +604,136 @@ def train_apq(data, M: int, k: int, weights, config: TrainConfig = TrainConfig()
     ds = s.upload_dataset(data)
     cb, cm = dev_train_apq(ds, M, k, weights, config, warm_start, loss_history)
     return cb.download(), cm.download()
+
+
+# ---- single-point API, exact search, evaluation (pq.hpp:256, index.hpp:137-332) ---------
+
+
+def pq_assign_point(x, current_codes, cb: ProductCodebook, w: AnisotropicWeights,
+                    session: Optional[Session] = None) -> np.ndarray:
+    """pq.hpp:256-282: one coordinate-descent pass for a single float64 point."""
+    s = _sess(session)
+    x = np.ascontiguousarray(x, np.float64)
+    cur = np.ascontiguousarray(current_codes, np.uint32)
+    if cur.size != cb.M:
+        raise DimensionMismatch("DimensionMismatch: need one current code per subspace")
+    out = np.zeros(cb.M, np.uint32)
+    _check(_L.aq_pq_assign_point(s.h, x.ctypes.data, x.size, cur.ctypes.data,
+                                 cb.dictionaries.ctypes.data, cb.M, cb.k, cb.sub_dimension,
+                                 w.h_parallel, w.h_perpendicular, out.ctypes.data))
+    return out
+
+
+def dev_exact_search(ds: DeviceDataset, queries, depth: int):
+    """exact_ground_truth (index.hpp:150-162): exact float64 MIPS top-`depth`."""
+    Q = np.ascontiguousarray(np.atleast_2d(queries), np.float64)
+    nq = Q.shape[0]
+    te = min(depth, ds.n)
+    ids = np.zeros((nq, te), np.uint32)
+    sc = np.zeros((nq, te), np.float64)
+    _check(_L.aq_dev_exact_search(ds.h, Q.ctypes.data, nq, depth, ids.ctypes.data,
+                                  sc.ctypes.data))
+    return ids, sc
+
+
+def exact_search(q, data, topn: int, session: Optional[Session] = None) -> SearchResult:
+    """index.hpp:137-147."""
+    s = _sess(session)
+    data = data if isinstance(data, Dataset) else Dataset(data)
+    if data.n == 0:
+        raise EmptyDataset("EmptyDataset: empty dataset")
+    if topn < 1:
+        raise InvalidArgument("InvalidArgument: topn must be >= 1")
+    q = np.ascontiguousarray(q, np.float64)
+    if q.size != data.d:
+        raise DimensionMismatch("DimensionMismatch: query dimension does not match dataset")
+    ids, sc = dev_exact_search(s.upload_dataset(data), q[None, :], topn)
+    return SearchResult([Hit(int(i), float(v)) for i, v in zip(ids[0], sc[0])])
+
+
+def _seq_dot(a: np.ndarray, b: np.ndarray) -> float:
+    """detail::dot order (geometry.hpp:170-174): products rounded, summed in order."""
+    p = np.asarray(a, np.float64) * np.asarray(b, np.float64)
+    return float(np.add.accumulate(p)[-1]) if p.size else 0.0
+
+
+@dataclass
+class EvalOptions:
+    recall_ns: tuple = (1, 10, 100)
+    kk: int = 10
+    threads: int = 1
+    ground_truth: Optional[np.ndarray] = None
+
+
+@dataclass
+class EvalReport:
+    num_queries: int
+    num_datapoints: int
+    recall_1_at_n: dict
+    kk: int
+    recall_k_at_k: float
+    relative_error_mean: float
+    relative_error_p50: float
+    relative_error_p90: float
+    relative_error_p99: float
+    relative_error_max: float
+
+
+def evaluate(queries, data, codes: CodeMatrix, cb: ProductCodebook,
+             options: EvalOptions = EvalOptions(), session: Optional[Session] = None) -> EvalReport:
+    """index.hpp:213-332 with the searches on the device (batched adc_search and
+    exact ground truth); the recall / relative-error bookkeeping follows the
+    reference line by line (latency is not reported: queries run batched)."""
+    s = _sess(session)
+    Q = np.ascontiguousarray(np.atleast_2d(queries), np.float64)
+    data = data if isinstance(data, Dataset) else Dataset(data)
+    if Q.shape[0] == 0:
+        raise EmptyDataset("EmptyDataset: no queries")
+    if data.n == 0:
+        raise EmptyDataset("EmptyDataset: empty dataset")
+    if codes.n != data.n:
+        raise DimensionMismatch("DimensionMismatch: code matrix does not match dataset")
+    if Q.shape[1] != data.d or data.d != cb.dim():
+        raise DimensionMismatch("DimensionMismatch: query/dataset/codebook dimensions differ")
+    if not options.recall_ns:
+        raise InvalidArgument("InvalidArgument: need at least one N")
+    depth = min(max([options.kk, *options.recall_ns]), data.n)
+    ds = s.upload_dataset(data)
+    if options.ground_truth is not None:
+        gt = np.asarray(options.ground_truth)
+        if gt.shape[0] != Q.shape[0]:
+            raise GroundTruthMismatch(f"GroundTruthMismatch: ground truth has {gt.shape[0]} rows, "
+                                      f"need {Q.shape[0]}")
+        if gt.ndim < 2 or gt.shape[1] < depth:
+            raise GroundTruthMismatch(f"GroundTruthMismatch: ground truth rows need at least "
+                                      f"{depth} entries")
+    else:
+        gt, _ = dev_exact_search(ds, Q, depth)
+    dc = s.upload_codes(codes)
+    dcb = s.upload_codebook(cb)
+    ids, _ = dev_adc_search(dc, dcb, Q, depth)
+    kk = min(options.kk, data.n)
+    nq = Q.shape[0]
+    found = {n_: 0 for n_ in options.recall_ns}
+    overlap = np.zeros(nq)
+    rel = np.zeros(nq)
+    for qi in range(nq):
+        top1 = int(gt[qi][0])
+        for n_ in options.recall_ns:
+            if top1 in ids[qi][: min(n_, ids.shape[1])].tolist():
+                found[n_] += 1
+        overlap[qi] = len(set(ids[qi][:kk].tolist()) & set(int(v) for v in gt[qi][:kk])) / kk
+        exact = _seq_dot(Q[qi], data.values[top1])
+        rec = np.concatenate([cb.codeword(m, int(c)) for m, c in enumerate(codes.codes[top1])])
+        approx = _seq_dot(Q[qi], rec)
+        rel[qi] = abs((exact - approx) / exact) if exact != 0.0 else abs(exact - approx)
+    srt = np.sort(rel)
+
+    def quantile(p):
+        idx = int(math.ceil(p * len(srt)))
+        return float(srt[min(len(srt) - 1, 0 if idx == 0 else idx - 1)])
+
+    return EvalReport(nq, data.n, {n_: found[n_] / nq for n_ in options.recall_ns}, kk,
+                      float(np.add.accumulate(overlap)[-1] / nq),
+                      float(np.add.accumulate(srt)[-1] / nq), quantile(0.5), quantile(0.9),
+                      quantile(0.99), float(srt[-1]))

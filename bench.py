@@ -176,6 +176,9 @@ def run_ours(args):
     rid = torch.empty((nq, ke), dtype=torch.int32, device=f"cuda:{local}")
     rsc = torch.empty((nq, ke), dtype=torch.float64, device=f"cuda:{local}")
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+    # events on the session stream (single GPU); on torch's stream bracketing
+    # the host-synchronous calls + collectives when sharded
+    tstream = stream if ws == 1 else torch.cuda.current_stream(local)
 
     def step_dev():
         aq._check(L.aq_dev_search_rerank_d(ds.h, dc.h, dcb.h, Qd.data_ptr(), nq, topn, keep,
@@ -191,6 +194,20 @@ def run_ours(args):
     def step_e2e():
         aq._check(L.aq_dev_search_rerank(ds.h, dc.h, dcb.h, Qpin.data_ptr(), nq, topn, keep,
                                          None, None, hid_t.data_ptr(), hsc_t.data_ptr()))
+
+    if ws > 1:
+        # row shards: this rank owns global ids [rank*n, (rank+1)*n); one NCCL
+        # all-gather of per-shard candidates + exact merge per step
+        from paper_1908_10396_b200 import distributed as D
+
+        def step_dev():  # noqa: F811
+            D.sharded_search_rerank(ds, dc, dcb, Qd, rank * n, topn, keep)
+
+        def step_e2e():  # noqa: F811
+            q = Qpin.to(f"cuda:{local}", non_blocking=True)
+            _, _, r_ids, r_sc = D.sharded_search_rerank(ds, dc, dcb, q, rank * n, topn, keep)
+            hid_t.copy_(r_ids.to(torch.int32).cpu())
+            hsc_t.copy_(r_sc.cpu())
 
     def timed(fn, steps, warmup, with_clocks=False):
         for _ in range(warmup):
@@ -211,9 +228,11 @@ def run_ours(args):
             torch.cuda.synchronize()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
+            e0.record(tstream)
             fn()
-            e1.record(stream)
+            if ws > 1:
+                torch.cuda.synchronize()
+            e1.record(tstream)
             e1.synchronize()
             total += e0.elapsed_time(e1)
         if sampler:

@@ -205,6 +205,10 @@ int aq_dev_search_rerank_d(aq_dataset* ds, aq_codes* codes, aq_codebook* cb,
                            size_t keep, uint32_t* adc_ids_dev,
                            double* adc_scores_dev, uint32_t* ids_dev,
                            double* scores_dev);
+/* Exact float64 dots dot(q, x[id]) for candidate ids, aligned with the
+ * input (device pointers): the per-shard half of the multi-GPU rerank. */
+int aq_dev_exact_dots_d(aq_dataset* ds, const double* q_dev, size_t nq,
+                        const uint32_t* cand_dev, size_t ncand, double* out_dev);
 int aq_adc_search(aq_session* s, const double* q, size_t d,
                   const uint32_t* codes, size_t n, size_t M, size_t codes_k,
                   const double* dictionaries, size_t cb_M, size_t k,

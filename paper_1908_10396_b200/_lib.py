@@ -79,6 +79,7 @@ _SIGS = {
     "aq_dev_adc_search": (_I, [_VP, _VP, _VP, _SZ, _SZ, _VP, _VP]),
     "aq_dev_adc_search_d": (_I, [_VP, _VP, _VP, _SZ, _SZ, _VP, _VP]),
     "aq_dev_search_rerank": (_I, [_VP, _VP, _VP, _VP, _SZ, _SZ, _SZ, _VP, _VP, _VP, _VP]),
+    "aq_dev_exact_dots_d": (_I, [_VP, _VP, _SZ, _VP, _SZ, _VP]),
     "aq_adc_search": (_I, [_VP, _VP, _SZ, _VP, _SZ, _SZ, _SZ, _VP, _SZ, _SZ, _SZ, _SZ,
                            _VP, _VP, _VP]),
     "aq_dev_rerank": (_I, [_VP, _VP, _SZ, _VP, _SZ, _SZ, _VP, _VP]),

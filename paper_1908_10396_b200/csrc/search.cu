@@ -580,6 +580,23 @@ __global__ void k_rerank(const float* __restrict__ xt, int pairs, int d,
   }
 }
 
+// Exact float64 dots for candidate ids, in the given order (no selection):
+// the per-shard half of the multi-GPU rerank.
+__global__ void k_exact_dots(const float* __restrict__ xt, int pairs, int d,
+                             const double* __restrict__ Q, size_t nq,
+                             const uint32_t* __restrict__ cand, size_t ncand, size_t n,
+                             double* __restrict__ out) {
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nq * ncand) return;
+  const size_t q = t / ncand;
+  const uint32_t id = cand[t];
+  double s = 0.0;
+  if (id < n)
+    for (int j = 0; j < d; ++j)
+      s = __dadd_rn(s, __dmul_rn(Q[q * d + j], (double)xt[tiled_index(id, j, pairs)]));
+  out[t] = id < n ? s : -INFINITY;
+}
+
 int rerank_device(aq_dataset* ds, const double* Qd, size_t nq,
                   const uint32_t* cand, size_t ncand, size_t keep, uint32_t* ids,
                   double* sc) {
@@ -736,6 +753,21 @@ int aq_dev_rerank(aq_dataset* ds, const double* queries, size_t nq,
   cudaFreeAsync(sc, s->stream);
   cudaStreamSynchronize(s->stream);
   return st;
+}
+
+// Exact dots of candidate ids (device pointers), aligned with the input.
+int aq_dev_exact_dots_d(aq_dataset* ds, const double* q_dev, size_t nq,
+                        const uint32_t* cand_dev, size_t ncand, double* out_dev) {
+  if (!ds) return ref_error(AQ_E_INVALID_ARGUMENT, "null dataset");
+  aq_session* s = ds->s;
+  AQ_TRY(check_session(s));
+  const size_t total = nq * ncand;
+  if (total == 0) return AQ_OK;
+  k_exact_dots<<<(unsigned)((total + 255) / 256), 256, 0, s->stream>>>(
+      ds->xt, (int)pairs_of(ds->d), (int)ds->d, q_dev, nq, cand_dev, ncand, ds->n, out_dev);
+  AQ_LAUNCHED(s);
+  AQ_CUDA(cudaStreamSynchronize(s->stream));
+  return AQ_OK;
 }
 
 // Device-pointer pipeline (queries and all outputs on the device).

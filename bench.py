@@ -132,22 +132,19 @@ class ClockSampler:
 
 # ---------------------------------------------------------------------------------------
 def build_index(aq, wl, n, nq, seed_shard, session):
-    """Config-2 shard: data, queries, codebook, codes (setup, untimed)."""
+    """Config-2 shard (setup, untimed): data, queries and the trained index —
+    train_apq on the device exactly as configs[1] states (warm start, 10
+    alternating iterations, T = 0.2), bit-identical to the reference's trainer."""
     w = wl.config2(n=n, nq=nq, seed=seed_shard)
-    M, k, sd = w.M, w.k, 2
-    # codebook: per-subspace sample of database sub-vectors (train_apq's
-    # cold-start initialisation, pq.hpp:529-542) + anisotropic encode
-    g = np.random.Generator(np.random.PCG64([seed_shard, 7]))
-    dic = np.empty((M, k, sd))
-    for m in range(M):
-        idx = g.choice(n, size=k, replace=False)
-        dic[m] = w.base[idx, m * sd:(m + 1) * sd]
-    cb = aq.ProductCodebook(M, k, sd, dic.ravel())
     ds = session.upload_dataset(w.base)
-    dcb = session.upload_codebook(cb)
-    dc = session.alloc_codes(n, M, k)
-    aq.dev_pq_quantize(ds, dcb, aq.ThresholdWeights(w.threshold), 3, dc)
-    return w, cb, ds, dcb, dc
+    cfg = aq.TrainConfig(max_iterations=w.iterations, relative_tolerance=0.0, seed=seed_shard)
+    t0 = time.perf_counter()
+    hist = []
+    dcb, dc = aq.dev_train_apq(ds, w.M, w.k, aq.ThresholdWeights(w.threshold), cfg, True, hist)
+    train_s = time.perf_counter() - t0
+    cb = dcb.download()
+    return w, cb, ds, dcb, dc, {"train_apq_s": round(train_s, 2), "loss_first": hist[0],
+                                "loss_last": hist[-1], "iterations": len(hist) - 1}
 
 
 def run_ours(args):
@@ -165,7 +162,7 @@ def run_ours(args):
     L = aq._L
     sess = aq.Session(local)
     stream = torch.cuda.ExternalStream(sess.stream, device=torch.device("cuda", local))
-    w, cb, ds, dcb, dc = build_index(aq, wl, args.n, args.nq, rank, sess)
+    w, cb, ds, dcb, dc, train_info = build_index(aq, wl, args.n, args.nq, rank, sess)
     n, nq, M, d = args.n, args.nq, w.M, w.d
     topn, keep = 100, 10
     Qh = np.ascontiguousarray(w.queries, np.float64)
@@ -258,6 +255,13 @@ def run_ours(args):
     ms_e2e, _, _, _ = timed(step_e2e, args.steps, max(1, args.warmup // 2))
     e2e = nq * n * ws / (ms_e2e / 1e3)
 
+    # quality of the timed pipeline (untimed): recall@10 of ADC top-100 + exact
+    # rerank against exact float64 ground truth (k_exact_score), this shard
+    gt, _ = aq.dev_exact_search(ds, Qh, keep)
+    step_e2e()
+    recall = float(np.mean([len(set(hid[q].tolist()) & set(gt[q].tolist())) / keep
+                            for q in range(nq)])) if ws == 1 else None
+
     # roofline of the dominant kernel: ADC scoring (algorithmic bytes: M/2
     # code bytes per (query, point) score)
     pk = peaks()
@@ -283,8 +287,9 @@ def run_ours(args):
            "data": "synthetic (seeded stand-in for GloVe-1.2M shape, config2)",
            "config": {"workload": "config2", "n_per_gpu": n, "d": d, "M": M, "k": 16,
                       "queries_per_step": nq, "adc_topn": topn, "rerank_to": keep,
-                      "threshold": w.threshold, "codebook": "sampled sub-vectors + 3-sweep "
-                      "anisotropic encode (trained codebook pending)",
+                      "threshold": w.threshold,
+                      "index": dict(train_info, trainer="train_apq on device, warm start"),
+                      "recall10_at_10": recall,
                       "filter_dtype": "f32 (bounded), results f64 bit-exact",
                       "l2": "flushed (256 MiB write) before every timed step",
                       "parallelism": f"dp{ws} (row shards)"},
@@ -345,6 +350,9 @@ def bench_encode(args, aq, wl, sess, stream, flush, local, ws, pk):
     aq._check(L.aq_pq_quantize(sess.h, xs.ctypes.data, n, 128, w.codebook.ctypes.data, 64, 16, 2,
                                C.byref(cw), 3, codes_h.ctypes.data))
     e2e_s = time.perf_counter() - t0
+    cpu = None
+    if not args.no_cpu_baseline and int(os.environ.get("RANK", "0")) == 0 and ws == 1:
+        cpu = encode_cpu_baseline(args, w)
     per_launch = ms_k.value / max(cnt.value, 1) / 1e3
     ops_per_pt = 64 * 16 * (3 + 3 * 8)   # M k [(sd+1) + S (sd+6)]
     fp32_peak = 148 * 128 * 1.965e9      # FP32 pipe ops/s (FFMA = 1 op)
@@ -358,9 +366,43 @@ def bench_encode(args, aq, wl, sess, stream, flush, local, ws, pk):
                          "frac": round(achieved_ops / fp32_peak, 4),
                          "note": "27,648 algorithmic f32 ops/point (SURVEY.md §8(d)); HBM side "
                                  "544 B/point is << HBM peak"},
+            "cpu_baseline": cpu,
             "e2e": {"value": round(n / e2e_s, 1), "unit": "points/s",
                     "h2d_bytes_per_step": int(n * 128 * 4), "d2h_bytes_per_step": int(n * 64 * 4),
                     "note": "host wall clock of the synchronous aq_pq_quantize call"}}
+
+
+def encode_cpu_baseline(args, w):
+    """Reference pq_quantize (oracle/_ref, all host cores) on a bounded prefix
+    of the config-3 rows."""
+    try:
+        from oracle import Port, Reference
+    except Exception as e:  # pragma: no cover
+        return {"value": None, "error": str(e)}
+    if Reference.available():
+        R, kind, cores = Reference(), "reference", os.cpu_count() or 1
+    else:
+        R, kind, cores = Port(), "port", 1
+    x = w.base
+    norms = np.sqrt(np.einsum("ij,ij->i", x.astype(np.float64), x.astype(np.float64)))
+    m = int(min(len(x), 20000))
+    while True:
+        xs = x[:m].astype(np.float64)
+        nr = norms[:m]
+        rho = np.where(nr > w.threshold, (w.threshold / nr) ** 2, 0.0)
+        hp = np.where(nr > w.threshold, (127 * rho) / (1 - np.where(rho < 1, rho, 0)), 1.0)
+        ho = np.where(nr > w.threshold, 1.0, 0.0)
+        t0 = time.perf_counter()
+        if kind == "reference":
+            R.pq_quantize(xs, w.codebook, 64, 16, 2, hp, ho, 3, threads=cores)
+        else:
+            R.pq_quantize(xs, w.codebook, 64, 16, 2, hp, ho, 3)
+        dt = time.perf_counter() - t0
+        if dt > args.cpu_seconds / 3 or m >= len(x):
+            break
+        m = min(len(x), int(m * max(2.0, args.cpu_seconds / 2 / max(dt, 1e-3))))
+    return {"value": round(m / dt, 1), "unit": "points/s", "cores": cores, "kind": kind,
+            "sample": f"first {m} config-3 rows, pq_quantize passes=3, {dt:.1f} s"}
 
 
 def cpu_baseline(args, w, cb, dc, n):

@@ -42,7 +42,6 @@ struct EncodeArgs {
   DevError* err;
 };
 
-constexpr int kEncThreads = 256;
 
 // Exact float64 scoring of one candidate with the reference's formula.
 __device__ __forceinline__ double exact_score2(double x0, double x1, double c0,
@@ -131,18 +130,23 @@ __device__ __forceinline__ unsigned proxy_mask(float xf0, float xf1,
                            fminf(fminf(m6[3], m6[4]), m6[5]));
   const float thr = best + 2.0f * delta + fabsf(best) * 2.384185791015625e-07f;
   if (!(thr < 1e30f) || !(best > -1e30f)) return 0u;  // out of envelope
+  // FSETP + predicated OR per candidate
   unsigned mask = 0;
 #pragma unroll
   for (int j = 0; j < 16; ++j)
-    if (K[j] <= thr) mask |= 1u << j;
+    asm("{\n\t.reg .pred p;\n\tsetp.le.f32 p, %1, %2;\n\t@p or.b32 %0, %0, %3;\n\t}"
+        : "+r"(mask)
+        : "f"(K[j]), "f"(thr), "r"(1u << j));
   return mask;
 }
 
 // Fast kernel: sub_dimension == 2, k <= 16, 4-bit codes.
 // stats (debug, may be null): [0] exact windows, [1 + s] points that ran s
 // sweeps (s = 0..7, mode 0).
-__global__ void __launch_bounds__(kEncThreads, 2)
+template <int TPB, int MINB>
+__global__ void __launch_bounds__(TPB, MINB)
     k_encode_sd2(const EncodeArgs a, unsigned long long* stats) {
+  constexpr int kEncThreads = TPB;
   extern __shared__ __align__(16) unsigned char smem[];
   float4* scb = reinterpret_cast<float4*>(smem);                    // [M][16]
   double2* cb2 = reinterpret_cast<double2*>(scb + a.M * kCbStride);  // [M][16]
@@ -206,6 +210,9 @@ __global__ void __launch_bounds__(kEncThreads, 2)
   const bool fast = fabsf(gp) < 1e30f;
 
   double s2 = 0.0, s1 = 0.0;
+  // per-point magnitudes for the error budget (float, over all subspaces):
+  // |base1| <= sum_m (X_m + ax_m) = B1, base2 <= sum_m (l1_m + rm_m)^2 = B2
+  float B1 = 0.0f, B2 = 0.0f, Amax = 0.0f, Xmax = 0.0f;
   if (a.mode == 0) {
     // reconstruction_nearest_pass + pq_point_state (pq.hpp:594, 603)
     uint32_t cw = 0;
@@ -215,7 +222,12 @@ __global__ void __launch_bounds__(kEncThreads, 2)
       if (m + 1 < M) xn = xrow[(size_t)(m + 1) * 32];
       const float rm = srm[m];
       const float X = __fmaf_rn(xv.y, xv.y, xv.x * xv.x);
-      const float ax = (fabsf(xv.x) + fabsf(xv.y)) * rm;
+      const float l1 = fabsf(xv.x) + fabsf(xv.y);
+      const float ax = l1 * rm;
+      B1 += X + ax;
+      B2 += (l1 + rm) * (l1 + rm);
+      Amax = fmaxf(Amax, ax);
+      Xmax = fmaxf(Xmax, X);
       // error budget: < 12u (2 ax + rm^2); 2^-18 = 64u
       const float Wn = 2.0f * ax + rm * rm + X * 9.094947e-13f;
       const float delta = Wn * 3.814697265625e-06f + 1e-30f;
@@ -255,9 +267,30 @@ __global__ void __launch_bounds__(kEncThreads, 2)
         residual2(xv.x, xv.y, cj.x, cj.y, &t2, &t1);
         s2 = __dadd_rn(s2, t2);
         s1 = __dadd_rn(s1, t1);
+        const float rm = srm[m];
+        const float X = __fmaf_rn(xv.y, xv.y, xv.x * xv.x);
+        const float l1 = fabsf(xv.x) + fabsf(xv.y);
+        B1 += X + l1 * rm;
+        B2 += (l1 + rm) * (l1 + rm);
+        Amax = fmaxf(Amax, l1 * rm);
+        Xmax = fmaxf(Xmax, X);
       }
     }
   }
+
+  // Error-budget constants. Per step the proxy's float32
+  // error is < 12u W2, W2 = |g'| ax^2 + beta^ ax + cC rm^2 with
+  // beta^ = 2(|g'|(|base1| + X) + cC), i.e. W2 = ax (|g'| (ax + 2(|base1| +
+  // X)) + 2 cC) + cC rm^2 (computed per step). The reference's own float64
+  // rounding is covered by 2^-40 of a per-point magnitude bound (|base1| <=
+  // B1 and base2 <= B2 over all steps), hoisted here.
+  B1 *= 1.0009765625f;  // slack for the float32 accumulation of the bounds
+  B2 *= 1.0009765625f;
+  const float agp = fabsf(gp);
+  const float AB = Amax + B1 + Xmax;
+  const float W2max = Amax * (agp * (Amax + 2.0f * (B1 + Xmax)) + 2.0f) + 4.0f * B2;
+  const float dabs = (B2 + Xmax + W2max + agp * AB * AB) * 9.094947e-13f + 1e-30f;
+  const bool bounds_ok = dabs < 1e25f;
 
   // coordinate-descent sweeps (cd_sweep, pq.hpp:151-185)
   const int max_sweeps = a.mode == 0 ? a.passes : (a.mode == 1 ? 64 : 0);
@@ -289,27 +322,20 @@ __global__ void __launch_bounds__(kEncThreads, 2)
       const float rm = srm[m];
       const float X = __fmaf_rn(xv.y, xv.y, xv.x * xv.x);
       const float ax = (fabsf(xv.x) + fabsf(xv.y)) * rm;
-      // Error budget: the proxy's float32 error is
-      // < 12u * W2, W2 = |g'| ax^2 + beta^ ax + cC rm^2 with
-      // beta^ = 2(|g'|(|base1| + X) + cC); delta = 2^-18 W2 (64u), plus
-      // 2^-40 of the float64 magnitudes for the reference's own rounding.
-      float beta, W2, W64;
+      float beta, W2;
       if (iso) {
         beta = 2.0f;
-        W2 = 2.0f * ax + rm * rm;
-        W64 = X + W2;
+        W2 = __fmaf_rn(rm, rm, 2.0f * ax);
       } else {
         const float b1f = (float)base1;
         beta = 2.0f * __fmaf_rn(gp, b1f + X, cC);
-        const float bh = 2.0f * (fabsf(gp) * (fabsf(b1f) + X) + cC);
-        W2 = fabsf(gp) * ax * ax + bh * ax + cC * rm * rm;
-        const float AB = ax + fabsf(b1f) + X;
-        W64 = fabsf((float)base2) + X + W2 + fabsf(gp) * AB * AB;
+        W2 = __fmaf_rn(ax, __fmaf_rn(agp, __fmaf_rn(2.0f, fabsf(b1f) + X, ax), 2.0f * cC),
+                       cC * rm * rm);
       }
-      const float Wt = W2 + W64 * 9.094947e-13f;  // + 2^-40 W64
-      const float delta = Wt * 3.814697265625e-06f + 1e-30f;  // 2^-18
+      const float Wt = W2;
+      const float delta = __fmaf_rn(W2, 3.814697265625e-06f, dabs);  // 2^-18 W2 + abs
       unsigned mask = 0u;
-      if (fast && Wt < 1e30f)
+      if (fast && bounds_ok && Wt < 1e30f)
         mask = proxy_mask<false>(xv.x, xv.y, scb + m * kCbStride, coff, gp,
                                  beta, delta);
       unsigned jb;
@@ -602,21 +628,25 @@ int run_encode(aq_dataset* ds, aq_codebook* cb, const aq_weights* w,
   const bool fast = cb->sd == 2 && cb->k <= 16 && codes->bits == 4;
   if (fast) {
     const int W = (a.M + 7) / 8;
-    const size_t sm = (size_t)a.M * (kCbStride * sizeof(float4) + 16 * sizeof(double2)) +
-                      a.M * sizeof(float) +
-                      (size_t)W * kEncThreads * sizeof(uint32_t) + 16;
-    static bool attr_set = false;
-    if (!attr_set) {
-      AQ_CUDA(cudaFuncSetAttribute(k_encode_sd2,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   200 * 1024));
-      attr_set = true;
-    }
-    if (sm > 200 * 1024)
-      return ref_error(AQ_E_UNSUPPORTED, "M too large for the fast encoder");
-    const unsigned grid = (unsigned)((ds->n + kEncThreads - 1) / kEncThreads);
+    int variant = 1;  // 256 threads, 3 CTAs/SM (24 warps): measured best
+    if (const char* v = getenv("AQ_ENC_VARIANT")) variant = atoi(v);
+    const int tpb = (variant == 2 || variant == 3) ? 128 : 256;
+    const size_t smv = (size_t)a.M * (kCbStride * sizeof(float4) + 16 * sizeof(double2)) +
+                       a.M * sizeof(float) + (size_t)W * tpb * sizeof(uint32_t) + 16;
+    const unsigned grid = (unsigned)((ds->n + tpb - 1) / tpb);
+    if (smv > 200 * 1024) return ref_error(AQ_E_UNSUPPORTED, "M too large for the fast encoder");
     timer_mark(s, AQ_T_ENCODE);
-    k_encode_sd2<<<grid, kEncThreads, sm, s->stream>>>(a, g_stats);
+#define AQ_ENC_LAUNCH(T, B)                                                              \
+  do {                                                                                  \
+    AQ_CUDA(cudaFuncSetAttribute(k_encode_sd2<T, B>,                                    \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)); \
+    k_encode_sd2<T, B><<<grid, T, smv, s->stream>>>(a, g_stats);                        \
+  } while (0)
+    if (variant == 1) AQ_ENC_LAUNCH(256, 3);
+    else if (variant == 2) AQ_ENC_LAUNCH(128, 4);
+    else if (variant == 3) AQ_ENC_LAUNCH(128, 6);
+    else AQ_ENC_LAUNCH(256, 2);
+#undef AQ_ENC_LAUNCH
     AQ_LAUNCHED(s);
     timer_mark(s, AQ_T_ENCODE);
   } else {

@@ -62,15 +62,28 @@ struct HostRng {
 
 // ---- kernels ------------------------------------------------------------------------------
 
-// std::accumulate of `count` values (float64, index order), one thread per row
+// std::accumulate of `count` values (float64, index order), one warp per row:
+// the lanes stage 32 consecutive values in shared memory (coalesced, many
+// loads in flight) and lane 0 adds them strictly in index order.
 __global__ void k_seq_sums(const double* __restrict__ v, size_t ld, size_t count, int rows,
                            const int* __restrict__ active, double* __restrict__ out) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ double buf[8][256];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (blockDim.x >> 5) + w;
   if (r >= rows || (active && !active[r])) return;
   const double* p = v + (size_t)r * ld;
   double s = 0.0;
-  for (size_t i = 0; i < count; ++i) s = __dadd_rn(s, p[i]);
-  out[r] = s;
+  for (size_t i0 = 0; i0 < count; i0 += 256) {
+    const int nb = (int)min((size_t)256, count - i0);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (u * 32 + lane < nb) buf[w][u * 32 + lane] = p[i0 + u * 32 + lane];
+    __syncwarp();
+    if (lane == 0)
+      for (int t = 0; t < nb; ++t) s = __dadd_rn(s, buf[w][t]);
+    __syncwarp();
+  }
+  if (lane == 0) out[r] = s;
 }
 
 // codewords from sampled rows: dict[m][j] = x[idx[m][j]][m-subvector]
@@ -131,13 +144,17 @@ __global__ void k_kmeans_assign(const float* __restrict__ xr, size_t n, int d, i
 }
 
 // update_codeword isotropic path (vq.hpp:151-162) with unit weights:
-// mean = (sum 1.0 x) / (sum 1.0), members in ascending order.
+// mean = (sum 1.0 x) / (sum 1.0), members in ascending order. One warp per
+// slot: the lanes gather 32 members' sub-vectors into shared memory (all in
+// flight), lane 0 accumulates them in member order.
 __global__ void k_kmeans_means(const float* __restrict__ xr, size_t n, int d, int M, int k,
                                int sd, const uint32_t* __restrict__ list,
                                const uint32_t* __restrict__ start,
                                const uint32_t* __restrict__ count,
                                const int* __restrict__ active, double* __restrict__ dict) {
-  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ float xs[4][32][17];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slot = blockIdx.x * (blockDim.x >> 5) + w;
   if (slot >= M * k) return;
   const int m = slot / k;
   if (!active[m]) return;
@@ -147,13 +164,23 @@ __global__ void k_kmeans_means(const float* __restrict__ xr, size_t n, int d, in
   double num[16];
   for (int c = 0; c < sd; ++c) num[c] = 0.0;
   double den = 0.0;
-  for (size_t t = 0; t < cnt; ++t) {
-    const uint32_t p = L[t];
-    for (int c = 0; c < sd; ++c)
-      num[c] = __dadd_rn(num[c], __dmul_rn(1.0, (double)xr[(size_t)p * d + m * sd + c]));
-    den = __dadd_rn(den, 1.0);
+  for (size_t t0 = 0; t0 < cnt; t0 += 32) {
+    const int nb = (int)min((size_t)32, cnt - t0);
+    if (lane < nb) {
+      const float* xp = xr + (size_t)L[t0 + lane] * d + m * sd;
+      for (int c = 0; c < sd; ++c) xs[w][lane][c] = xp[c];
+    }
+    __syncwarp();
+    if (lane == 0)
+      for (int b = 0; b < nb; ++b) {
+        for (int c = 0; c < sd; ++c)
+          num[c] = __dadd_rn(num[c], __dmul_rn(1.0, (double)xs[w][b][c]));
+        den = __dadd_rn(den, 1.0);
+      }
+    __syncwarp();
   }
-  for (int c = 0; c < sd; ++c) dict[(size_t)slot * sd + c] = __ddiv_rn(num[c], den);
+  if (lane == 0)
+    for (int c = 0; c < sd; ++c) dict[(size_t)slot * sd + c] = __ddiv_rn(num[c], den);
 }
 
 // empty partitions (vq.hpp:284-292): j ascending, consuming the ranking
@@ -225,7 +252,7 @@ int train_l2_pq_device(aq_dataset* ds, size_t M, size_t k, const aq_train_config
         ds->xr, n, (int)d, (int)M, (int)k, (int)sd, cb->d64, active, codes->data,
         (int)codes->stride, codes->bits, losses, changes);
     AQ_LAUNCHED(s);
-    k_seq_sums<<<(unsigned)((M + 31) / 32), 32, 0, s->stream>>>(losses, n, n, (int)M, active, totals);
+    k_seq_sums<<<(unsigned)((M + 7) / 8), 256, 0, s->stream>>>(losses, n, n, (int)M, active, totals);
     AQ_LAUNCHED(s);
     AQ_CUDA(cudaMemcpyAsync(htot.data(), totals, M * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
     AQ_CUDA(cudaMemcpyAsync(hchg.data(), changes, M * sizeof(unsigned long long),
@@ -242,7 +269,7 @@ int train_l2_pq_device(aq_dataset* ds, size_t M, size_t k, const aq_train_config
     st = build_buckets(codes, (int)k, &B);
     if (st != AQ_OK) break;
     AQ_CUDA(cudaMemcpyAsync(active, hact.data(), M * sizeof(int), cudaMemcpyHostToDevice, s->stream));
-    k_kmeans_means<<<(unsigned)((M * k + 127) / 128), 128, 0, s->stream>>>(
+    k_kmeans_means<<<(unsigned)((M * k + 3) / 4), 128, 0, s->stream>>>(
         ds->xr, n, (int)d, (int)M, (int)k, (int)sd, B.list, B.start, B.count, active, cb->d64);
     s->launches++;
     if (cfg->empty_partition_policy == 0) {
@@ -333,7 +360,9 @@ int aq_dev_train_apq(aq_dataset* ds, size_t M, size_t k, const aq_weights* w,
   aq_codebook* cb = nullptr;
   aq_codes* codes = nullptr;
   if (warm_start) {
+    timer_mark(s, AQ_T_KMEANS);
     AQ_TRY(train_l2_pq_device(ds, M, k, cfg, &cb, &codes));
+    timer_mark(s, AQ_T_KMEANS);
   } else {
     // one generator, one sample_distinct per subspace (pq.hpp:533-542)
     HostRng r{cfg->seed};
@@ -370,7 +399,7 @@ int aq_dev_train_apq(aq_dataset* ds, size_t M, size_t k, const aq_weights* w,
     st = ref_error(AQ_E_CUDA, "out of device memory");
   auto pass = [&](double* tot_h, uint64_t* changed) -> int {
     AQ_TRY(run_encode(ds, cb, w, codes, 1, 0, cfg->sweep_to_fixed_point, losses, changed));
-    k_seq_sums<<<1, 1, 0, s->stream>>>(losses, n, n, 1, nullptr, total);
+    k_seq_sums<<<1, 32, 0, s->stream>>>(losses, n, n, 1, nullptr, total);
     AQ_LAUNCHED(s);
     AQ_CUDA(cudaMemcpyAsync(tot_h, total, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
     AQ_CUDA(cudaStreamSynchronize(s->stream));

@@ -177,7 +177,19 @@ struct AsmArgs {
   double* A;       // dim x dim row-major
   double* rhs;     // dim
   int nchunk;      // column chunks of 32 subspaces per strip
+  uint32_t lo, hi; // point-index block processed by this launch
+  int resume;      // 1: accumulators continue from A / rhs (not the first block)
 };
+
+// first position in the ascending list L[0..cnt) with L[pos] >= v
+__device__ __forceinline__ size_t lower_bound_u32(const uint32_t* L, size_t cnt, uint32_t v) {
+  size_t lo = 0, hi = cnt;
+  while (lo < hi) {
+    const size_t mid = (lo + hi) >> 1;
+    if (L[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
 
 // One warp = (row strip (m, j), chunk of 32 column subspaces). Lane l owns
 // column subspace m2 = 32 chunk + l; its accumulators for rows (m, j, a) x
@@ -185,8 +197,16 @@ struct AsmArgs {
 // conflicts, no atomics). The strip's points are visited in ascending order,
 // so each entry sees the reference's exact sequence of additions
 // (pq.hpp:320-339): += h_perp on the diagonal first, then += (coef x_a) x_b.
+// Points are staged 32 at a time (list entries, per-point scalars and every
+// lane's column sub-vector / code) so the global gathers of a batch are
+// independent and in flight together.
+constexpr int kAsmSdMax = 4;
 __global__ void __launch_bounds__(32) k_assemble(const AsmArgs a) {
-  extern __shared__ __align__(16) double acc[];  // [(aa*k + j2)*sd + b][32], then rhs[sd]
+  extern __shared__ __align__(16) double acc[];  // [(aa*k + j2)*sd + b][32], rhs[sd]
+  __shared__ double s_coef[32], s_ho[32], s_hp[32];
+  __shared__ float s_xm[32][kAsmSdMax];
+  __shared__ float s_xc[32][kAsmSdMax][33];  // [point][b][lane] (+1 pad)
+  __shared__ unsigned char s_j2[32][32];
   const int unit = blockIdx.x;
   const int chunk = unit % a.nchunk;
   const int strip = unit / a.nchunk;
@@ -204,29 +224,53 @@ __global__ void __launch_bounds__(32) k_assemble(const AsmArgs a) {
   const uint32_t* L = a.list + (size_t)m * a.n + a.start[m * k + j];
   const size_t cnt = a.count[m * k + j];
   const bool do_rhs = chunk == 0;
-  for (size_t t = 0; t < cnt; ++t) {
-    const uint32_t p = L[t];
-    const float* xp = a.xr + (size_t)p * d;
-    const double cf = a.coef[p];
-    if (do_rhs && lane < sd)  // rhs += h_par * x (pq.hpp:326)
-      racc[lane] = __dadd_rn(racc[lane], __dmul_rn(a.hp[p], (double)xp[m * sd + lane]));
-    if (!mine) continue;
-    const unsigned j2 = get_code(a.codes + (size_t)p * a.stride, m2, a.bits);
-    if (m2 == m) {  // diagonal h_perp (pq.hpp:324-325), j2 == j here
-      const double hop = a.ho[p];
+  for (size_t t0 = 0; t0 < cnt; t0 += 32) {
+    const int nb = (int)min((size_t)32, cnt - t0);
+    // stage: lane l fetches point t0 + l's scalars and strip sub-vector ...
+    uint32_t pl = 0;
+    if (lane < nb) {
+      pl = L[t0 + lane];
+      s_coef[lane] = a.coef[pl];
+      s_ho[lane] = a.ho[pl];
+      s_hp[lane] = a.hp[pl];
+      for (int c = 0; c < sd; ++c) s_xm[lane][c] = a.xr[(size_t)pl * d + m * sd + c];
+    }
+    // ... and, for every point of the batch, its own column sub-vector and code
+    if (mine) {
+#pragma unroll 8
+      for (int b = 0; b < nb; ++b) {
+        const uint32_t p = __shfl_sync(0xffffffffu, pl, b);
+        const float* xp = a.xr + (size_t)p * d + m2 * sd;
+        for (int c = 0; c < sd; ++c) s_xc[b][c][lane] = xp[c];
+        s_j2[b][lane] = (unsigned char)get_code(a.codes + (size_t)p * a.stride, m2, a.bits);
+      }
+    } else {
+      for (int b = 0; b < nb; ++b) __shfl_sync(0xffffffffu, pl, b);
+    }
+    __syncwarp();
+    for (int b = 0; b < nb; ++b) {
+      if (do_rhs && lane < sd)  // rhs += h_par * x (pq.hpp:326)
+        racc[lane] = __dadd_rn(racc[lane], __dmul_rn(s_hp[b], (double)s_xm[b][lane]));
+      if (!mine) continue;
+      const unsigned j2 = s_j2[b][lane];
+      if (m2 == m) {  // diagonal h_perp (pq.hpp:324-325), j2 == j here
+        const double hop = s_ho[b];
+        for (int aa = 0; aa < sd; ++aa) {
+          double* e = acc + (size_t)((aa * k + j) * sd + aa) * 32 + lane;
+          *e = __dadd_rn(*e, hop);
+        }
+      }
+      const double cf = s_coef[b];
+      if (cf == 0.0) continue;  // pq.hpp:328
       for (int aa = 0; aa < sd; ++aa) {
-        double* e = acc + (size_t)((aa * k + j) * sd + aa) * 32 + lane;
-        *e = __dadd_rn(*e, hop);
+        const double xc = __dmul_rn(cf, (double)s_xm[b][aa]);
+        for (int c2 = 0; c2 < sd; ++c2) {
+          double* e = acc + (size_t)((aa * k + j2) * sd + c2) * 32 + lane;
+          *e = __dadd_rn(*e, __dmul_rn(xc, (double)s_xc[b][c2][lane]));
+        }
       }
     }
-    if (cf == 0.0) continue;  // pq.hpp:328
-    for (int aa = 0; aa < sd; ++aa) {
-      const double xc = __dmul_rn(cf, (double)xp[m * sd + aa]);
-      for (int b = 0; b < sd; ++b) {
-        double* e = acc + (size_t)((aa * k + j2) * sd + b) * 32 + lane;
-        *e = __dadd_rn(*e, __dmul_rn(xc, (double)xp[m2 * sd + b]));
-      }
-    }
+    __syncwarp();
   }
   const size_t dim = (size_t)k * d;
   if (mine) {
@@ -237,6 +281,129 @@ __global__ void __launch_bounds__(32) k_assemble(const AsmArgs a) {
               acc[(size_t)((aa * k + j2) * sd + b) * 32 + lane];
   }
   if (do_rhs && lane < sd) a.rhs[(size_t)(m * k + j) * sd + lane] = racc[lane];
+}
+
+// Specialisation for sub_dimension 2, k = 16 (all BASELINE configs): fully
+// unrolled read-modify-writes, one 8-byte load per (point, lane) for the
+// column sub-vector, codes read as one 16-byte row slice per point. Same
+// per-entry operation order as k_assemble.
+__global__ void __launch_bounds__(32) k_assemble_sd2(const AsmArgs a) {
+  extern __shared__ __align__(16) double acc[];  // [(aa*16 + j2)*2 + b][32]
+  __shared__ double s_coef[32], s_ho[32], s_hp[32];
+  __shared__ float2 s_xm[32];
+  __shared__ float2 s_xc[32][32];          // [point][lane]
+  __shared__ uint32_t s_cw[32][32];        // code word holding lane's nibble
+  const int unit = blockIdx.x;
+  const int chunk = unit % a.nchunk;
+  const int strip = unit / a.nchunk;
+  const int m = strip >> 4, j = strip & 15;
+  const int lane = threadIdx.x;
+  const int d = a.d;
+  const int m2 = chunk * 32 + lane;
+  const int mcols = a.full ? a.M : m + 1;
+  if (chunk * 32 >= mcols) return;
+  const bool mine = m2 < mcols;
+  const size_t dim = (size_t)16 * d;
+  const bool do_rhs = chunk == 0 && lane == 0;
+  const uint32_t* Lall = a.list + (size_t)m * a.n + a.start[m * 16 + j];
+  const size_t call = a.count[m * 16 + j];
+  const size_t t_lo = lower_bound_u32(Lall, call, a.lo);
+  const size_t t_hi = lower_bound_u32(Lall, call, a.hi);
+  if (t_lo == t_hi) return;  // accumulators already hold this block's state
+  double r0 = 0.0, r1 = 0.0;
+  if (a.resume) {
+    if (mine) {
+#pragma unroll 4
+      for (int e = 0; e < 64; ++e) {
+        const int aa = e >> 5, j2 = (e >> 1) & 15, b = e & 1;
+        acc[e * 32 + lane] =
+            a.A[((size_t)(m * 16 + j) * 2 + aa) * dim + (size_t)(m2 * 16 + j2) * 2 + b];
+      }
+    }
+    if (do_rhs) {
+      r0 = a.rhs[(size_t)(m * 16 + j) * 2];
+      r1 = a.rhs[(size_t)(m * 16 + j) * 2 + 1];
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < 64; ++e) acc[e * 32 + lane] = 0.0;
+  }
+  const uint32_t* L = Lall + t_lo;
+  const size_t cnt = t_hi - t_lo;
+  for (size_t t0 = 0; t0 < cnt; t0 += 32) {
+    const int nb = (int)min((size_t)32, cnt - t0);
+    __shared__ uint32_t s_p[32];
+    if (lane < nb) {
+      const uint32_t pl = L[t0 + lane];
+      s_p[lane] = pl;
+      s_coef[lane] = a.coef[pl];
+      s_ho[lane] = a.ho[pl];
+      s_hp[lane] = a.hp[pl];
+      s_xm[lane] = *reinterpret_cast<const float2*>(a.xr + (size_t)pl * d + m * 2);
+    }
+    __syncwarp();
+    if (mine) {
+      // all gathers of the batch in flight at once (LDGSTS, no registers)
+      const int wsh = a.bits == 4 ? 3 : 2;  // code word index of m2
+      for (int b = 0; b < nb; ++b) {
+        const uint32_t p = s_p[b];
+        const float* src = a.xr + (size_t)p * d + m2 * 2;
+        const uint32_t* cws = reinterpret_cast<const uint32_t*>(a.codes + (size_t)p * a.stride) +
+                              (m2 >> wsh);
+        const unsigned dx = (unsigned)__cvta_generic_to_shared(&s_xc[b][lane]);
+        const unsigned dc = (unsigned)__cvta_generic_to_shared(&s_cw[b][lane]);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dx), "l"(src));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dc), "l"(cws));
+      }
+      asm volatile("cp.async.wait_all;\n" ::);
+    }
+    __syncwarp();
+    if (do_rhs)
+      for (int b = 0; b < nb; ++b) {  // rhs += h_par * x (pq.hpp:326)
+        const double hp = s_hp[b];
+        r0 = __dadd_rn(r0, __dmul_rn(hp, (double)s_xm[b].x));
+        r1 = __dadd_rn(r1, __dmul_rn(hp, (double)s_xm[b].y));
+      }
+    if (mine) {
+      for (int b = 0; b < nb; ++b) {
+        const unsigned j2 = a.bits == 4 ? (s_cw[b][lane] >> (4 * (m2 & 7))) & 15u
+                                         : (s_cw[b][lane] >> (8 * (m2 & 3))) & 255u;
+        if (m2 == m) {  // diagonal h_perp first (pq.hpp:324-325); j2 == j
+          const double hop = s_ho[b];
+          double* e0 = acc + (size_t)((0 * 16 + j) * 2 + 0) * 32 + lane;
+          double* e1 = acc + (size_t)((1 * 16 + j) * 2 + 1) * 32 + lane;
+          *e0 = __dadd_rn(*e0, hop);
+          *e1 = __dadd_rn(*e1, hop);
+        }
+        const double cf = s_coef[b];
+        if (cf == 0.0) continue;  // pq.hpp:328
+        const float2 xm = s_xm[b];
+        const float2 xc = s_xc[b][lane];
+        const double u0 = __dmul_rn(cf, (double)xm.x), u1 = __dmul_rn(cf, (double)xm.y);
+        const double v0 = (double)xc.x, v1 = (double)xc.y;
+        double* base0 = acc + (size_t)(j2 * 2) * 32 + lane;         // aa = 0
+        double* base1 = acc + (size_t)((16 + j2) * 2) * 32 + lane;  // aa = 1
+        const double e00 = base0[0], e01 = base0[32], e10 = base1[0], e11 = base1[32];
+        base0[0] = __dadd_rn(e00, __dmul_rn(u0, v0));
+        base0[32] = __dadd_rn(e01, __dmul_rn(u0, v1));
+        base1[0] = __dadd_rn(e10, __dmul_rn(u1, v0));
+        base1[32] = __dadd_rn(e11, __dmul_rn(u1, v1));
+      }
+    }
+    __syncwarp();
+  }
+  if (mine) {
+#pragma unroll 4
+    for (int e = 0; e < 64; ++e) {
+      const int aa = e >> 5, j2 = (e >> 1) & 15, b = e & 1;
+      a.A[((size_t)(m * 16 + j) * 2 + aa) * dim + (size_t)(m2 * 16 + j2) * 2 + b] =
+          acc[(size_t)e * 32 + lane];
+    }
+  }
+  if (do_rhs) {
+    a.rhs[(size_t)(m * 16 + j) * 2] = r0;
+    a.rhs[(size_t)(m * 16 + j) * 2 + 1] = r1;
+  }
 }
 
 // trace (sequential, Eigen stand-in) and ridge = 1e-6 trace / dim (pq.hpp:431-435)
@@ -392,6 +559,7 @@ int llt_solve_device(aq_session* s, double* A, int n, double* x) {
   AQ_TRY(scratch(s, 4, 64, &p));
   fail = (int*)p;
   AQ_CUDA(cudaMemsetAsync(fail, 0, sizeof(int), s->stream));
+  timer_mark(s, AQ_T_LLT);
   for (int kb = 0; kb < n; kb += kLLT) {
     const int be = std::min(kb + kLLT, n);
     const int below = n - be;
@@ -408,6 +576,7 @@ int llt_solve_device(aq_session* s, double* A, int n, double* x) {
       AQ_LAUNCHED(s);
     }
   }
+  timer_mark(s, AQ_T_LLT);
   int hf = 0;
   AQ_CUDA(cudaMemcpyAsync(&hf, fail, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
   AQ_CUDA(cudaStreamSynchronize(s->stream));
@@ -506,15 +675,39 @@ int assemble_device(aq_dataset* ds, aq_codes* codes, const PointW& pw, const Buc
   AQ_CUDA(cudaMemsetAsync(rhs, 0, dim * sizeof(double), s->stream));
   const int nchunk = (M + 31) / 32;
   AsmArgs a{ds->xr, ds->n, d, M, k, sd, codes->data, (int)codes->stride, codes->bits,
-            B.list, B.start, B.count, pw.hp, pw.ho, pw.coef, full ? 1 : 0, A, rhs, nchunk};
+            B.list, B.start, B.count, pw.hp, pw.ho, pw.coef, full ? 1 : 0, A, rhs, nchunk,
+            0u, (uint32_t)ds->n, 0};
+  if (sd > kAsmSdMax)
+    return ref_error(AQ_E_UNSUPPORTED, "device normal equations support sub_dimension <= 4");
   const size_t smem = ((size_t)sd * k * sd * 32 + 16) * sizeof(double);
-  if (smem > 227 * 1024)
+  if (smem + 20 * 1024 > 227 * 1024)
     return ref_error(AQ_E_UNSUPPORTED, "normal-equation strip exceeds shared memory");
   AQ_CUDA(cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem));
   const unsigned units = (unsigned)(M * k * nchunk);
-  k_assemble<<<units, 32, smem, s->stream>>>(a);
+  timer_mark(s, AQ_T_ASSEMBLE);
+  if (sd == 2 && k == 16 && d % 2 == 0) {
+    AQ_CUDA(cudaFuncSetAttribute(k_assemble_sd2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 64 * 32 * 8));
+    // point blocks whose rows (~48 MB) stay L2-resident while every unit
+    // gathers from them; entries keep their point order across blocks
+    const size_t row_bytes = (size_t)d * sizeof(float);
+    const size_t bsz = std::max<size_t>(4096, (48u << 20) / row_bytes);
+    for (size_t lo = 0; lo < ds->n; lo += bsz) {
+      a.lo = (uint32_t)lo;
+      a.hi = (uint32_t)std::min(ds->n, lo + bsz);
+      a.resume = lo > 0;
+      k_assemble_sd2<<<units, 32, 64 * 32 * 8, s->stream>>>(a);
+      AQ_LAUNCHED(s);
+    }
+  } else {
+    a.lo = 0;
+    a.hi = (uint32_t)ds->n;
+    a.resume = 0;
+    k_assemble<<<units, 32, smem, s->stream>>>(a);
+  }
   AQ_LAUNCHED(s);
+  timer_mark(s, AQ_T_ASSEMBLE);
   return AQ_OK;
 }
 

@@ -148,9 +148,9 @@ __global__ void __launch_bounds__(TPB, MINB)
     k_encode_sd2(const EncodeArgs a, unsigned long long* stats) {
   constexpr int kEncThreads = TPB;
   extern __shared__ __align__(16) unsigned char smem[];
-  float4* scb = reinterpret_cast<float4*>(smem);                    // [M][16]
-  double2* cb2 = reinterpret_cast<double2*>(scb + a.M * kCbStride);  // [M][16]
-  float* srm = reinterpret_cast<float*>(cb2 + a.M * 16);
+  float4* scb = reinterpret_cast<float4*>(smem);                          // [M+1][16]
+  double2* cb2 = reinterpret_cast<double2*>(scb + (a.M + 1) * kCbStride);  // [M+1][16]
+  float* srm = reinterpret_cast<float*>(cb2 + (a.M + 1) * 16);
   uint32_t* scode = reinterpret_cast<uint32_t*>(srm + a.M);
   {
     const double2* g2 = reinterpret_cast<const double2*>(a.cb64);
@@ -166,6 +166,7 @@ __global__ void __launch_bounds__(TPB, MINB)
     }
   }
   for (int t = threadIdx.x; t < a.M; t += blockDim.x) srm[t] = a.rmax[t];
+  for (int t = threadIdx.x; t < 16; t += blockDim.x) cb2[a.M * 16 + t] = make_double2(0.0, 0.0);
   __syncthreads();
 
   const size_t i = (size_t)blockIdx.x * kEncThreads + threadIdx.x;
@@ -218,8 +219,7 @@ __global__ void __launch_bounds__(TPB, MINB)
     uint32_t cw = 0;
     float2 xv = xrow[0];
     for (int m = 0; m < M; ++m) {
-      float2 xn = xv;
-      if (m + 1 < M) xn = xrow[(size_t)(m + 1) * 32];
+      const float2 xn = xrow[(size_t)(m + 1) * 32];  // padded
       const float rm = srm[m];
       const float X = __fmaf_rn(xv.y, xv.y, xv.x * xv.x);
       const float l1 = fabsf(xv.x) + fabsf(xv.y);
@@ -291,6 +291,7 @@ __global__ void __launch_bounds__(TPB, MINB)
   const float W2max = Amax * (agp * (Amax + 2.0f * (B1 + Xmax)) + 2.0f) + 4.0f * B2;
   const float dabs = (B2 + Xmax + W2max + agp * AB * AB) * 9.094947e-13f + 1e-30f;
   const bool bounds_ok = dabs < 1e25f;
+  const bool fastpt = fast && bounds_ok;
 
   // coordinate-descent sweeps (cd_sweep, pq.hpp:151-185)
   const int max_sweeps = a.mode == 0 ? a.passes : (a.mode == 1 ? 64 : 0);
@@ -302,19 +303,15 @@ __global__ void __launch_bounds__(TPB, MINB)
     float2 xv = xrow[0];
     unsigned cur = cw & 15u;
     double2 cc = cb2[cur];
+    // software pipeline one subspace ahead; the prefetch of subspace M reads
+    // padding (row tile, smem codebook and code words are over-allocated)
+#pragma unroll 2
     for (int m = 0; m < M; ++m) {
-      // software pipeline: next subspace's row slice, code and codeword
       const int mn = m + 1;
-      float2 xn = xv;
-      double2 cn = cc;
-      unsigned curn = 0;
-      uint32_t wnext = cw;
-      if (mn < M) {
-        if ((mn & 7) == 0) wnext = mycode[(mn >> 3) * kEncThreads];
-        curn = (wnext >> (4 * (mn & 7))) & 15u;
-        xn = xrow[(size_t)mn * 32];
-        cn = cb2[mn * 16 + curn];
-      }
+      const uint32_t wnext = ((mn & 7) == 0) ? mycode[(mn >> 3) * kEncThreads] : cw;
+      const unsigned curn = (wnext >> (4 * (mn & 7))) & 15u;
+      const float2 xn = xrow[(size_t)mn * 32];
+      const double2 cn = cb2[mn * 16 + curn];
       double t2, t1;
       residual2(xv.x, xv.y, cc.x, cc.y, &t2, &t1);
       const double base2 = __dsub_rn(s2, t2);
@@ -332,12 +329,11 @@ __global__ void __launch_bounds__(TPB, MINB)
         W2 = __fmaf_rn(ax, __fmaf_rn(agp, __fmaf_rn(2.0f, fabsf(b1f) + X, ax), 2.0f * cC),
                        cC * rm * rm);
       }
-      const float Wt = W2;
       const float delta = __fmaf_rn(W2, 3.814697265625e-06f, dabs);  // 2^-18 W2 + abs
-      unsigned mask = 0u;
-      if (fast && bounds_ok && Wt < 1e30f)
-        mask = proxy_mask<false>(xv.x, xv.y, scb + m * kCbStride, coff, gp,
-                                 beta, delta);
+      // proxy_mask returns 0 (exact path) for non-finite windows
+      const unsigned mask =
+          fastpt ? proxy_mask<false>(xv.x, xv.y, scb + m * kCbStride, coff, gp, beta, delta)
+                 : 0u;
       unsigned jb;
       if (mask != 0u && (mask & (mask - 1u)) == 0u) {
         jb = (unsigned)(__ffs(mask) - 1);
@@ -354,7 +350,7 @@ __global__ void __launch_bounds__(TPB, MINB)
       }
       s2 = __dadd_rn(base2, b2);
       s1 = __dadd_rn(base1, b1);
-      if ((mn & 7) == 0 || mn == M) {
+      if ((mn & 7) == 0) {
         mycode[(m >> 3) * kEncThreads] = cw;
         cw = wnext;
       }
@@ -362,6 +358,7 @@ __global__ void __launch_bounds__(TPB, MINB)
       cc = cn;
       cur = curn;
     }
+    if (M & 7) mycode[((M - 1) >> 3) * kEncThreads] = cw;
     if (a.mode == 0) {
       if (!changed) break;  // pq.hpp:605-606
     } else {
@@ -631,8 +628,8 @@ int run_encode(aq_dataset* ds, aq_codebook* cb, const aq_weights* w,
     int variant = 1;  // 256 threads, 3 CTAs/SM (24 warps): measured best
     if (const char* v = getenv("AQ_ENC_VARIANT")) variant = atoi(v);
     const int tpb = (variant == 2 || variant == 3) ? 128 : 256;
-    const size_t smv = (size_t)a.M * (kCbStride * sizeof(float4) + 16 * sizeof(double2)) +
-                       a.M * sizeof(float) + (size_t)W * tpb * sizeof(uint32_t) + 16;
+    const size_t smv = (size_t)(a.M + 1) * (kCbStride * sizeof(float4) + 16 * sizeof(double2)) +
+                       (a.M + 1) * sizeof(float) + (size_t)(W + 1) * tpb * sizeof(uint32_t) + 16;
     const unsigned grid = (unsigned)((ds->n + tpb - 1) / tpb);
     if (smv > 200 * 1024) return ref_error(AQ_E_UNSUPPORTED, "M too large for the fast encoder");
     timer_mark(s, AQ_T_ENCODE);

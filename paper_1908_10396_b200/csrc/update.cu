@@ -614,6 +614,93 @@ __global__ void k_iso_means(const float* xr, size_t n, int d, int M, int k, int 
   for (int c = 0; c < sd; ++c) dict[(size_t)slot * sd + c] = __ddiv_rn(num[c], den);
 }
 
+// ---- M == 1: update_codeword per codeword (vq.hpp:139-192) -------------------------------
+// One CTA per codeword j. Its members (points with code j, ascending) feed
+// a d x d lower-triangle system: a(r, c) += (coef x_c) x_r (rankUpdate,
+// column-wise), b += h_par x, diag = ridge + sum h_perp; every entry is a
+// sequential chain over the members. Isotropic members only -> weighted mean.
+// out: A[j] (d x d row-major, diagonal already += diag), rhs[j] (d), iso[j],
+// mean path written straight to dict.
+__global__ void k_vq_systems(const float* __restrict__ xr, size_t n, int d, int k,
+                             const uint32_t* __restrict__ list,
+                             const uint32_t* __restrict__ start,
+                             const uint32_t* __restrict__ count, const double* __restrict__ hp,
+                             const double* __restrict__ ho, double ridge, double* A,
+                             double* rhs, int* mode, double* dict, DevError* err) {
+  const int j = blockIdx.x;
+  const size_t cnt = count[j];
+  if (cnt == 0) return;
+  const uint32_t* L = list + start[j];
+  __shared__ int s_iso;
+  __shared__ double s_diag;
+  if (threadIdx.x == 0) {
+    int iso = 1;
+    for (size_t t = 0; t < cnt; ++t) iso &= hp[L[t]] == ho[L[t]];
+    s_iso = iso;
+    mode[j] = iso;
+  }
+  __syncthreads();
+  if (s_iso) {  // weighted mean (vq.hpp:151-162)
+    if (threadIdx.x == 0) {
+      double den = 0.0;
+      for (size_t t = 0; t < cnt; ++t) den = __dadd_rn(den, ho[L[t]]);
+      s_diag = den;
+      if (den <= 0.0) report_error(err, (uint64_t)j, AQ_E_SINGULAR_SYSTEM);
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+      double s = 0.0;
+      for (size_t t = 0; t < cnt; ++t)
+        s = __dadd_rn(s, __dmul_rn(hp[L[t]], (double)xr[(size_t)L[t] * d + c]));
+      if (s_diag > 0.0) dict[(size_t)j * d + c] = __ddiv_rn(s, s_diag);
+    }
+    return;
+  }
+  if (threadIdx.x == 0) {
+    // mean_hperp, ridge_eff, diag (vq.hpp:165-186): sequential
+    double mh = 0.0;
+    for (size_t t = 0; t < cnt; ++t) mh = __dadd_rn(mh, ho[L[t]]);
+    mh = __ddiv_rn(mh, (double)cnt);
+    double diag = ridge < 0.0 ? __dmul_rn(1e-10, mh) : ridge;
+    for (size_t t = 0; t < cnt; ++t) {
+      const float* xp = xr + (size_t)L[t] * d;
+      double n2 = 0.0;
+      for (int c = 0; c < d; ++c) n2 = __dadd_rn(n2, __dmul_rn((double)xp[c], (double)xp[c]));
+      if (n2 == 0.0) report_error(err, (uint64_t)L[t], AQ_E_ZERO_NORM_DATAPOINT);
+      diag = __dadd_rn(diag, ho[L[t]]);
+    }
+    s_diag = diag;
+  }
+  __syncthreads();
+  double* Aj = A + (size_t)j * d * d;
+  const int ne = d * (d + 1) / 2;
+  for (int e = threadIdx.x; e < ne + d; e += blockDim.x) {
+    if (e < ne) {  // lower entry (r, c), r >= c
+      int r = (int)((sqrt(8.0 * e + 1.0) - 1.0) / 2.0);
+      while ((r + 1) * (r + 2) / 2 <= e) ++r;
+      while (r * (r + 1) / 2 > e) --r;
+      const int c = e - r * (r + 1) / 2;
+      double v = 0.0;
+      for (size_t t = 0; t < cnt; ++t) {
+        const uint32_t p = L[t];
+        const float* xp = xr + (size_t)p * d;
+        double n2 = 0.0;
+        for (int q = 0; q < d; ++q) n2 = __dadd_rn(n2, __dmul_rn((double)xp[q], (double)xp[q]));
+        const double coef = __ddiv_rn(__dsub_rn(hp[p], ho[p]), n2);
+        v = __dadd_rn(v, __dmul_rn(__dmul_rn(coef, (double)xp[c]), (double)xp[r]));
+      }
+      if (r == c) v = __dadd_rn(v, s_diag);
+      Aj[(size_t)r * d + c] = v;
+    } else {  // rhs component
+      const int c = e - ne;
+      double v = 0.0;
+      for (size_t t = 0; t < cnt; ++t)
+        v = __dadd_rn(v, __dmul_rn(hp[L[t]], (double)xr[(size_t)L[t] * d + c]));
+      rhs[(size_t)j * d + c] = v;
+    }
+  }
+}
+
 // unused-codeword reseeding: walk (m, j) lexicographically, consuming the
 // loss ranking cyclically (pq.hpp:452-461)
 __global__ void k_reseed(const uint32_t* count, int M, int k, int sd, const uint32_t* order,
@@ -783,9 +870,6 @@ int aq_dev_pq_codebook_update(aq_dataset* ds, aq_codes* codes, const aq_weights*
   const int sd = (int)(ds->d / M);
   if ((size_t)sd != out->sd)
     return ref_error(AQ_E_DIMENSION_MISMATCH, "codebook sub-dimension does not match");
-  if (M == 1)
-    return ref_error(AQ_E_UNSUPPORTED,
-                     "M == 1 (vector quantization update) is not on the device path yet");
   if (sd > 16) return ref_error(AQ_E_UNSUPPORTED, "device update supports sub_dimension <= 16");
   const size_t n = ds->n, dim = k * ds->d;
   Buckets B;
@@ -799,7 +883,41 @@ int aq_dev_pq_codebook_update(aq_dataset* ds, aq_codes* codes, const aq_weights*
              ? AQ_OK
              : AQ_E_CUDA;
   const bool all_iso = pw.flags[0] == 0;
-  if (st == AQ_OK && all_iso) {
+  if (st == AQ_OK && M == 1) {
+    // per-codeword closed form (pq.hpp:387-404 -> vq.hpp:139-192)
+    const size_t d = ds->d;
+    double* As = nullptr;
+    int* modes = nullptr;
+    if (cudaMallocAsync(&As, (k * d * d + k * d) * sizeof(double), s->stream) != cudaSuccess ||
+        cudaMallocAsync(&modes, k * sizeof(int), s->stream) != cudaSuccess)
+      st = ref_error(AQ_E_CUDA, "out of device memory");
+    if (st == AQ_OK) {
+      AQ_TRY(clear_dev_error(s));
+      cudaMemsetAsync(modes, 0xff, k * sizeof(int), s->stream);
+      k_vq_systems<<<(unsigned)k, 128, 0, s->stream>>>(ds->xr, n, (int)d, (int)k, B.list,
+                                                       B.start, B.count, pw.hp, pw.ho, ridge,
+                                                       As, As + k * d * d, modes, out->d64,
+                                                       s->err);
+      s->launches++;
+      st = sync_and_check(s, "codeword update");
+    }
+    if (st == AQ_OK) {
+      std::vector<int> hm(k);
+      cudaMemcpyAsync(hm.data(), modes, k * sizeof(int), cudaMemcpyDeviceToHost, s->stream);
+      cudaStreamSynchronize(s->stream);
+      for (size_t j = 0; j < k && st == AQ_OK; ++j) {
+        if (hm[j] != 0) continue;  // unused (-1) or mean path (1)
+        st = llt_solve_device(s, As + j * d * d, (int)d, As + k * d * d + j * d);
+        if (st == AQ_E_SINGULAR_SYSTEM)
+          st = ref_error(AQ_E_SINGULAR_SYSTEM, "codeword system is not positive definite");
+        if (st == AQ_OK)
+          cudaMemcpyAsync(out->d64 + j * d, As + k * d * d + j * d, d * sizeof(double),
+                          cudaMemcpyDeviceToDevice, s->stream);
+      }
+    }
+    if (As) cudaFreeAsync(As, s->stream);
+    if (modes) cudaFreeAsync(modes, s->stream);
+  } else if (st == AQ_OK && all_iso) {
     AQ_TRY(clear_dev_error(s));
     k_iso_means<<<(unsigned)((M * k + 127) / 128), 128, 0, s->stream>>>(
         ds->xr, n, (int)ds->d, (int)M, (int)k, sd, B.list, B.start, B.count, pw.hp, pw.ho,

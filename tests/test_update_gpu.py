@@ -79,3 +79,22 @@ def test_codebook_update_errors():
     with pytest.raises(aq.ZeroNormDatapoint):
         aq.pq_codebook_update(x2, aq.CodeMatrix(100, 4, 4, _codes(100, 4, 4, 1)),
                               aq.AnisotropicWeights.from_eta(2.0), 4, 4)
+
+
+@pytest.mark.parametrize("w", ["aniso", "iso", "mixed"])
+def test_codebook_update_m1_vq_closed_form(w):
+    # pq.hpp:387-404 -> update_codeword (vq.hpp:139-192); test_pq.cpp:209-239
+    n, d, k = 400, 5, 5
+    x = mixture_rows(n, d, 59)
+    codes = _codes(n, 1, k, 60)
+    if w == "aniso":
+        hp, ho = np.full(n, 4.125), np.ones(n)
+    elif w == "iso":
+        hp = ho = np.full(n, 2.0)
+    else:
+        hp, ho = np.full(n, 4.125), np.ones(n)
+        hp[codes[:, 0] == 2] = 1.0  # codeword 2 gets only isotropic members
+    for ridge in (-1.0, 1e-9):
+        got = aq.pq_codebook_update(x, aq.CodeMatrix(n, 1, k, codes), (hp, ho), 1, k, ridge)
+        want = P.pq_codebook_update(x.astype(np.float64), codes, hp, ho, 1, k, ridge)
+        assert np.array_equal(got.dictionaries, want)

@@ -737,3 +737,132 @@ def evaluate(queries, data, codes: CodeMatrix, cb: ProductCodebook,
                       float(np.add.accumulate(overlap)[-1] / nq),
                       float(np.add.accumulate(srt)[-1] / nq), quantile(0.5), quantile(0.9),
                       quantile(0.99), float(srt[-1]))
+
+
+# ---- on-disk formats (pq.hpp:614-730, dataset.hpp:122-219) -------------------------------
+# Host I/O, byte-compatible with the reference's files.
+
+import struct as _struct
+
+
+def save_codebook(cb: ProductCodebook, path: str) -> None:
+    """AQCB container: magic, version 1, M, k, d (LE uint32), float32 dictionaries."""
+    with open(path, "wb") as f:
+        f.write(b"AQCB" + _struct.pack("<4I", 1, cb.M, cb.k, cb.dim()))
+        f.write(np.asarray(cb.dictionaries, np.float64).astype("<f4").tobytes())
+
+
+def load_codebook(path: str) -> ProductCodebook:
+    try:
+        raw = open(path, "rb").read()
+    except OSError:
+        raise MalformedFile(f"MalformedFile: cannot open {path}")
+    if len(raw) < 4 or raw[:4] != b"AQCB":
+        raise MalformedFile(f"MalformedFile: {path}: bad magic")
+    if len(raw) < 20:
+        raise MalformedFile(f"MalformedFile: {path}: truncated header")
+    version, M, k, d = _struct.unpack("<4I", raw[4:20])
+    if version != 1:
+        raise MalformedFile(f"MalformedFile: {path}: unsupported version {version}")
+    if M == 0 or d == 0 or d % M:
+        raise MalformedFile(f"MalformedFile: {path}: inconsistent shape")
+    cnt = k * d
+    if len(raw) < 20 + 4 * cnt:
+        raise MalformedFile(f"MalformedFile: {path}: truncated dictionaries")
+    vals = np.frombuffer(raw, "<f4", cnt, 20).astype(np.float64)
+    return ProductCodebook(M, k, d // M, vals)
+
+
+def save_codes(cm: CodeMatrix, path: str) -> None:
+    """n, M, k (LE uint32) then codes row-major as uint8 (k <= 256) or uint16."""
+    if cm.k > 65536:
+        raise InvalidArgument("InvalidArgument: code serialization supports k <= 65536")
+    dt = "<u1" if cm.k <= 256 else "<u2"
+    with open(path, "wb") as f:
+        f.write(_struct.pack("<3I", cm.n, cm.M, cm.k))
+        f.write(np.asarray(cm.codes).astype(dt).tobytes())
+
+
+def load_codes(path: str) -> CodeMatrix:
+    try:
+        raw = open(path, "rb").read()
+    except OSError:
+        raise MalformedFile(f"MalformedFile: cannot open {path}")
+    if len(raw) < 12:
+        raise MalformedFile(f"MalformedFile: {path}: truncated header")
+    n, M, k = _struct.unpack("<3I", raw[:12])
+    if M == 0:
+        raise MalformedFile(f"MalformedFile: {path}: M must be positive")
+    dt = "<u1" if k <= 256 else "<u2"
+    need = n * M * (1 if k <= 256 else 2)
+    if len(raw) < 12 + need:
+        raise MalformedFile(f"MalformedFile: {path}: truncated codes")
+    codes = np.frombuffer(raw, dt, n * M, 12).astype(np.uint32)
+    if codes.size and codes.max() >= k:
+        raise CodeOutOfRange(f"CodeOutOfRange: {path}: stored code exceeds k")
+    return CodeMatrix(n, M, k, codes.reshape(n, M))
+
+
+def read_fvecs(path: str) -> Dataset:
+    """fvecs: per record an LE int32 dimension then that many float32 values."""
+    try:
+        raw = open(path, "rb").read()
+    except OSError:
+        raise MalformedFile(f"MalformedFile: cannot open {path}")
+    if not raw:
+        return Dataset(np.zeros((0, 1), np.float32))
+    if len(raw) < 4:
+        raise MalformedFile(f"MalformedFile: {path}: truncated record header")
+    d = _struct.unpack("<i", raw[:4])[0]
+    if d <= 0:
+        raise MalformedFile(f"MalformedFile: {path}: non-positive dimension")
+    rec = 4 + 4 * d
+    if len(raw) % rec:
+        raise MalformedFile(f"MalformedFile: {path}: truncated record {len(raw) // rec}")
+    arr = np.frombuffer(raw, np.uint8).reshape(-1, rec)
+    dims = arr[:, :4].copy().view("<i4").ravel()
+    if (dims != d).any():
+        bad = int(np.argmax(dims != d))
+        raise MalformedFile(f"MalformedFile: {path}: inconsistent dimension at record {bad}")
+    vals = arr[:, 4:].copy().view("<f4").reshape(-1, d)
+    if not np.isfinite(vals).all():
+        bad = int(np.argmax(~np.isfinite(vals).all(axis=1)))
+        raise MalformedFile(f"MalformedFile: {path}: non-finite value in record {bad}")
+    if (np.einsum("ij,ij->i", vals.astype(np.float64), vals.astype(np.float64)) == 0).any():
+        bad = int(np.argmax(~vals.any(axis=1)))
+        raise ZeroNormDatapoint(f"ZeroNormDatapoint: {path}: row {bad} has zero norm")
+    return Dataset(vals.astype(np.float32))
+
+
+def write_fvecs(ds: Dataset, path: str) -> None:
+    ds = ds if isinstance(ds, Dataset) else Dataset(ds)
+    n, d = ds.values.shape
+    out = np.empty((n, 1 + d), "<f4")
+    out[:, 0] = np.frombuffer(_struct.pack("<i", d), "<f4")[0]
+    out[:, 1:] = ds.values
+    with open(path, "wb") as f:
+        f.write(out.tobytes())
+
+
+def read_ivecs(path: str) -> list:
+    raw = open(path, "rb").read()
+    out, pos = [], 0
+    while pos < len(raw):
+        if pos + 4 > len(raw):
+            raise MalformedFile(f"MalformedFile: {path}: truncated header")
+        c = _struct.unpack("<i", raw[pos:pos + 4])[0]
+        pos += 4
+        if c < 0:
+            raise MalformedFile(f"MalformedFile: {path}: negative count")
+        if pos + 4 * c > len(raw):
+            raise MalformedFile(f"MalformedFile: {path}: truncated record {len(out)}")
+        out.append(np.frombuffer(raw, "<i4", c, pos).copy())
+        pos += 4 * c
+    return out
+
+
+def write_ivecs(rows, path: str) -> None:
+    with open(path, "wb") as f:
+        for r in rows:
+            r = np.asarray(r, "<i4")
+            f.write(_struct.pack("<i", r.size) + r.tobytes())

@@ -254,6 +254,56 @@ int aq_dev_train_apq(aq_dataset* ds, size_t M, size_t k, const aq_weights* w,
                      aq_codebook** cb_out, aq_codes** codes_out,
                      double* loss_history_out, size_t* history_len);
 
+/* ---- row-sharded training building blocks (multi-GPU) -----
+ * The reference trains in one process (pq.hpp:513-575); a sharded trainer
+ * splits its sums by rows: every rank computes the partial quantities below
+ * on its own shard, the host combines them across ranks in rank order
+ * (paper_1908_10396_b200/distributed.py) and every rank solves the same
+ * system. Buffers ending in _dev are device pointers on the session's GPU. */
+
+/* flags of this shard's weights: flags_out[0] = some point anisotropic (the
+ * dense path, pq.hpp:383-386), flags_out[1] = first anisotropic |x| = 0 point
+ * + 1 (0 = none) */
+int aq_dev_weight_flags(aq_dataset* ds, const aq_weights* w, uint64_t* flags_out);
+/* pq.hpp:290-343 on this shard: lower triangle of A (k d x k d) and rhs,
+ * usage[m][j] = points with code j at subspace m. flags_out[0] = some point is
+ * anisotropic; flags_out[1] = first anisotropic |x| = 0 point + 1 (0 = none). */
+int aq_dev_normal_equations_partial(aq_dataset* ds, aq_codes* codes,
+                                    const aq_weights* w, size_t k, double* A_dev,
+                                    double* rhs_dev, uint32_t* usage_dev,
+                                    uint64_t* flags_out);
+/* pq.hpp:405-417 on this shard: num[m][j][c] = sum h_par x_c, den[m][j] =
+ * sum h_perp over the members in ascending order. */
+int aq_dev_iso_partials(aq_dataset* ds, aq_codes* codes, const aq_weights* w,
+                        size_t k, double* num_dev, double* den_dev,
+                        uint32_t* usage_dev);
+/* pq.hpp:430-443: ridge (ridge < 0 -> 1e-6 trace / dim), Cholesky, solve, in
+ * place (A -> L, rhs -> solution). AQ_E_SINGULAR_SYSTEM when not SPD. */
+int aq_dev_solve_normal_equations(aq_session* s, double* A_dev, double* rhs_dev,
+                                  size_t dim, double ridge);
+/* replace a codebook's dictionaries from device memory */
+int aq_codebook_set_device(aq_codebook* cb, const double* dict_dev);
+/* pq_point_loss (pq.hpp:137-146) of every point of this shard */
+int aq_dev_point_losses(aq_dataset* ds, aq_codebook* cb, const aq_weights* w,
+                        aq_codes* codes, double* losses_dev);
+/* loss_ranking order (vq.hpp:221-229): idx_dev (ascending on entry) sorted
+ * by (score desc, idx asc) */
+int aq_dev_sort_desc(aq_session* s, const double* scores_dev, uint32_t* idx_dev,
+                     size_t n);
+/* std::accumulate(v, v + n, init) in index order */
+int aq_dev_seq_sum(aq_session* s, const double* v_dev, size_t n, double init,
+                   double* out);
+/* vq_assign_pass (vq.hpp:196-217) with unit weights for the active subspaces
+ * of this shard: codes in place, losses_dev (M x n), changes_out[M] */
+int aq_dev_kmeans_assign(aq_dataset* ds, aq_codebook* cb, aq_codes* codes,
+                         const int* active_host, double* losses_dev,
+                         uint64_t* changes_out);
+/* update_codeword unit-weight sums (vq.hpp:151-162) on this shard for the
+ * active subspaces: num (M k sd), den (M k), count (M k) */
+int aq_dev_kmeans_partials(aq_dataset* ds, aq_codes* codes, size_t k,
+                           const int* active_host, double* num_dev, double* den_dev,
+                           uint32_t* count_dev);
+
 #ifdef __cplusplus
 }
 #endif

@@ -90,6 +90,17 @@ _SIGS = {
     "aq_dev_train_l2_pq": (_I, [_VP, _SZ, _SZ, _VP, _PP, _PP]),
     "aq_debug_exact_window_count": (_I, [_VP, _I, _VP]),
     "aq_dev_train_apq": (_I, [_VP, _SZ, _SZ, _VP, _VP, _I, _PP, _PP, _VP, _VP]),
+    # row-sharded training building blocks
+    "aq_dev_weight_flags": (_I, [_VP, _VP, _VP]),
+    "aq_dev_normal_equations_partial": (_I, [_VP, _VP, _VP, _SZ, _VP, _VP, _VP, _VP]),
+    "aq_dev_iso_partials": (_I, [_VP, _VP, _VP, _SZ, _VP, _VP, _VP]),
+    "aq_dev_solve_normal_equations": (_I, [_VP, _VP, _VP, _SZ, C.c_double]),
+    "aq_codebook_set_device": (_I, [_VP, _VP]),
+    "aq_dev_point_losses": (_I, [_VP, _VP, _VP, _VP, _VP]),
+    "aq_dev_sort_desc": (_I, [_VP, _VP, _VP, _SZ]),
+    "aq_dev_seq_sum": (_I, [_VP, _VP, _SZ, C.c_double, _VP]),
+    "aq_dev_kmeans_assign": (_I, [_VP, _VP, _VP, _VP, _VP, _VP]),
+    "aq_dev_kmeans_partials": (_I, [_VP, _VP, _SZ, _VP, _VP, _VP, _VP]),
 }
 
 

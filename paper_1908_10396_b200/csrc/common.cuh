@@ -157,6 +157,21 @@ struct Buckets {
 };
 int build_buckets(aq_codes* c, int k, Buckets* B);
 
+// Per-point anisotropic weights (update.cu): h_par, h_perp, coupling coefficient;
+// flags[0] = some point anisotropic, flags[1] = first anisotropic |x| = 0 index + 1
+// (~0 = none).
+struct PointW {
+  double* hp = nullptr;
+  double* ho = nullptr;
+  double* coef = nullptr;
+  unsigned long long flags[2] = {0, 0};
+};
+int point_weights(aq_dataset* ds, const aq_weights* w, PointW* pw, void** owner);
+int assemble_device(aq_dataset* ds, aq_codes* codes, const PointW& pw, const Buckets& B,
+                    int k, bool full, double* A, double* rhs);
+int llt_solve_device(aq_session* s, double* A, int n, double* x);
+int trace_ridge_device(aq_session* s, double* A, size_t dim, double ridge);
+
 // ---- weights ------------------------------------------------------------------
 // Resolved per point on the device from an aq_weights descriptor
 // (geometry.hpp:119-145, eta_limit 395-402, CLI resolve_weights

@@ -442,4 +442,38 @@ int aq_dev_train_apq(aq_dataset* ds, size_t M, size_t k, const aq_weights* w,
   return AQ_OK;
 }
 
+// One k-means assignment pass over this dataset's points for the active
+// subspaces (sharded warm start): codes updated in place, losses (M x n,
+// device) written for active subspaces, changes_out[m] = codes changed.
+int aq_dev_kmeans_assign(aq_dataset* ds, aq_codebook* cb, aq_codes* codes,
+                         const int* active_host, double* losses_dev, uint64_t* changes_out) {
+  if (!ds || !cb || !codes) return ref_error(AQ_E_INVALID_ARGUMENT, "null argument");
+  aq_session* s = ds->s;
+  AQ_TRY(check_session(s));
+  const size_t M = cb->M, n = ds->n;
+  if (ds->d != M * cb->sd || codes->n != n || codes->M != M)
+    return ref_error(AQ_E_DIMENSION_MISMATCH, "shapes do not match");
+  if (cb->sd > 16 || cb->k > 256)
+    return ref_error(AQ_E_UNSUPPORTED, "device trainers support k <= 256, sub_dimension <= 16");
+  int* act = nullptr;
+  unsigned long long* chg = nullptr;
+  AQ_CUDA(cudaMallocAsync(&act, M * sizeof(int), s->stream));
+  AQ_CUDA(cudaMallocAsync(&chg, M * sizeof(unsigned long long), s->stream));
+  AQ_CUDA(cudaMemcpyAsync(act, active_host, M * sizeof(int), cudaMemcpyHostToDevice, s->stream));
+  AQ_CUDA(cudaMemsetAsync(chg, 0, M * sizeof(unsigned long long), s->stream));
+  if (n) {
+    k_kmeans_assign<<<(unsigned)((n + 127) / 128), 128, 0, s->stream>>>(
+        ds->xr, n, (int)ds->d, (int)M, (int)cb->k, (int)cb->sd, cb->d64, act, codes->data,
+        (int)codes->stride, codes->bits, losses_dev, chg);
+    s->launches++;
+  }
+  AQ_CUDA(cudaMemcpyAsync(changes_out, chg, M * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                          s->stream));
+  cudaFreeAsync(act, s->stream);
+  cudaFreeAsync(chg, s->stream);
+  AQ_CUDA(cudaStreamSynchronize(s->stream));
+  return AQ_OK;
+}
+
 }  // extern "C"
+

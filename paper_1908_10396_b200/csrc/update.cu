@@ -419,6 +419,12 @@ __global__ void k_trace_ridge(double* A, size_t dim, double ridge) {
     A[i * dim + i] = __dadd_rn(A[i * dim + i], r);
 }
 
+int trace_ridge_device(aq_session* s, double* A, size_t dim, double ridge) {
+  k_trace_ridge<<<1, 1024, 0, s->stream>>>(A, dim, ridge);
+  AQ_LAUNCHED(s);
+  return AQ_OK;
+}
+
 // ---- blocked Cholesky (lower, in place, row-major) --------------------------------------
 
 // Panel for block [kb, be): every CTA factors the diagonal block (identical,
@@ -719,13 +725,6 @@ __global__ void k_iota(uint32_t* v, size_t n) {
   const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t < n) v[t] = (uint32_t)t;
 }
-
-struct PointW {
-  double* hp = nullptr;
-  double* ho = nullptr;
-  double* coef = nullptr;
-  unsigned long long flags[2] = {0, 0};
-};
 
 int point_weights(aq_dataset* ds, const aq_weights* w, PointW* pw, void** owner) {
   aq_session* s = ds->s;

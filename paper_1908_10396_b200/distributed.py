@@ -15,6 +15,10 @@ tests (tests/test_distributed.py).
 """
 from __future__ import annotations
 
+import math
+from typing import Optional
+
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -81,3 +85,477 @@ def sharded_search_rerank(ds, codes, cb, queries: torch.Tensor, offset: int, top
     gids = aid.to(torch.int64) + offset
     ids, adc, ex = all_gather_candidates(gids, asc, exd, group)
     return merge_candidates(ids, adc, ex, topn, keep)
+
+
+# =============================================================================
+# Row-sharded training (train_l2_pq pq.hpp:469-501 / train_apq pq.hpp:513-575)
+# =============================================================================
+#
+# Every rank owns a contiguous row range and keeps its codes; the codebook is
+# replicated. Per iteration the ranks exchange only sums:
+#
+#   assignment  local (encode.cu / k_kmeans_assign), per-shard loss sums and
+#               change counts -> all-gather -> combined in rank order;
+#   update      per-shard partials (normal equations, isotropic or k-means
+#               sums, usage counts) -> all-gather -> summed in rank order on
+#               every rank -> identical solve on every rank;
+#   reseed      per-shard loss ranking (top U) -> all-gather -> exact merge by
+#               (loss desc, id asc) -> rows fetched from their owners.
+#
+# Combining in rank order (not an all-reduce whose association depends on the
+# NCCL algorithm) makes the result a deterministic function of the world
+# size. With one rank every partial IS the full sequential sum, so the
+# trainer equals the single-GPU one (aq_dev_train_apq) bit for bit; with W
+# ranks the float64 sums are re-associated at W-1 shard boundaries (relative
+# effect ~1e-16 per sum), the only difference from the reference.
+
+_MASK64 = (1 << 64) - 1
+
+
+class HostRng:
+    """anisoq::Rng (rng.hpp:28-89) on the host: splitmix64, next_below by
+    rejection, sample_distinct as a partial Fisher-Yates on iota(n) with only
+    the touched positions materialised (O(k))."""
+
+    def __init__(self, seed: int):
+        self.state = seed & _MASK64
+
+    def next_u64(self) -> int:
+        self.state = (self.state + 0x9E3779B97F4A7C15) & _MASK64
+        z = self.state
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _MASK64
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _MASK64
+        return z ^ (z >> 31)
+
+    def next_below(self, n: int) -> int:
+        threshold = ((1 << 64) - n) % n
+        while True:
+            r = self.next_u64()
+            if r >= threshold:
+                return r % n
+
+    def sample_distinct(self, n: int, k: int) -> list:
+        moved: dict = {}
+        out = []
+        for i in range(min(k, n)):
+            j = i + self.next_below(n - i)
+            vi, vj = moved.get(i, i), moved.get(j, j)
+            moved[i], moved[j] = vj, vi
+            out.append(vj)
+        return out
+
+
+class _Comm:
+    """Rank-ordered exchange over torch.distributed (NCCL on GPUs, gloo in the
+    CPU tests); a world of one needs no process group."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+
+    def gather(self, t: torch.Tensor) -> list:
+        t = t.contiguous()
+        if self.world == 1:
+            return [t]
+        buf = [torch.empty_like(t) for _ in range(self.world)]
+        dist.all_gather(buf, t, group=self.group)
+        return buf
+
+    def ordered_sum(self, t: torch.Tensor) -> torch.Tensor:
+        parts = self.gather(t)
+        acc = parts[0].clone()
+        for p in parts[1:]:
+            acc += p
+        return acc
+
+    def ordered_scalar_sum(self, v: float, device) -> float:
+        """Per-shard float64 sums combined left to right in rank order."""
+        parts = self.gather(torch.tensor([v], dtype=torch.float64, device=device))
+        acc = float(parts[0].item())
+        for p in parts[1:]:
+            acc = acc + float(p.item())
+        return acc
+
+    def int_sum(self, t: torch.Tensor) -> torch.Tensor:
+        t = t.to(torch.int64).contiguous()
+        if self.world > 1:
+            dist.all_reduce(t, group=self.group)
+        return t
+
+
+class ShardedTrainer:
+    """Sharded train_l2_pq / train_apq over a compute backend `shard`.
+
+    `shard` computes on this rank's rows (DeviceShard below on a B200; the
+    tests drive the same orchestration with a CPU backend). Errors are the
+    reference's (anisoq.py classes) with global point indices."""
+
+    def __init__(self, shard, n_total: int, offset: int, group=None):
+        self.sh = shard
+        self.n_total = n_total
+        self.offset = offset
+        self.comm = _Comm(group)
+
+    # ---- helpers ---------------------------------------------------------
+    def _do(self, fn, *args):
+        """One per-shard step on every rank. A failure on any rank raises the
+        same reference error on all ranks (the first failing rank's), so no
+        rank is left waiting in a collective."""
+        from . import anisoq as aq
+        res, err = None, None
+        try:
+            res = fn(*args)
+        except Exception as e:  # noqa: BLE001 - re-raised on every rank below
+            err = e
+        if self.comm.world == 1:
+            if err is not None:
+                raise err
+            return res
+        st = int(getattr(err, "status", 999) or 999) if err is not None else 0
+        codes = self.comm.gather(torch.tensor([st], dtype=torch.int64, device=self.sh.device))
+        first = next((r for r, c in enumerate(codes) if int(c.item())), None)
+        if first is None:
+            return res
+        msg = [str(err) if err is not None else ""]
+        dist.broadcast_object_list(msg, src=first, group=self.comm.group)
+        raise aq._BY_STATUS.get(int(codes[first].item()), aq.Error)(msg[0])
+
+    def _validate(self, M: int, k: int) -> None:
+        from . import anisoq as aq
+        if self.n_total == 0:
+            raise aq.EmptyDataset("EmptyDataset: cannot train on an empty dataset")
+        if M == 0 or self.sh.d % M != 0:
+            raise aq.DimensionNotDivisible("DimensionNotDivisible: dimension not divisible by M")
+        if k == 0 or k > self.n_total:
+            raise aq.InvalidArgument("InvalidArgument: need 1 <= k <= n")
+
+    def _fetch_rows(self, gids: list) -> torch.Tensor:
+        """float64 rows [len(gids), d] of global ids, taken from their owners."""
+        dev = self.sh.device
+        n_local = self.sh.n
+        lo = self.offset
+        g = torch.tensor(gids, dtype=torch.int64, device=dev)
+        mine = (g >= lo) & (g < lo + n_local)
+        rows = torch.zeros((len(gids), self.sh.d), dtype=torch.float64, device=dev)
+        if bool(mine.any()):
+            rows[mine] = self.sh.rows(g[mine] - lo)
+        owned = self.comm.gather(mine.to(torch.int32))
+        parts = self.comm.gather(rows)
+        out = torch.zeros_like(rows)
+        for o, p in zip(owned, parts):
+            sel = o.bool()
+            out[sel] = p[sel]
+        return out
+
+    def _global_ranking(self, losses: torch.Tensor, count: int) -> list:
+        """First min(count, n_total) global ids of loss_ranking (vq.hpp:221-229):
+        (loss desc, id asc) over all shards."""
+        take = min(count, self.n_total)
+        vals, lidx = self._do(self.sh.ranking, losses, min(take, self.sh.n))
+        dev = self.sh.device
+        v = torch.full((take,), -math.inf, dtype=torch.float64, device=dev)
+        i = torch.full((take,), 1 << 62, dtype=torch.int64, device=dev)
+        v[: vals.numel()] = vals
+        i[: lidx.numel()] = lidx.to(torch.int64) + self.offset
+        allv = torch.cat(self.comm.gather(v))
+        alli = torch.cat(self.comm.gather(i))
+        o = order_desc(allv, alli)[:take]
+        return alli[o].tolist()
+
+    def _init_rows(self, hidx: list, M: int, k: int, sd: int) -> torch.Tensor:
+        rows = self._fetch_rows(hidx)  # [M*k, d]
+        m = torch.arange(M * k, device=rows.device) // k
+        cols = m[:, None] * sd + torch.arange(sd, device=rows.device)[None, :]
+        return torch.gather(rows, 1, cols).reshape(-1).contiguous()
+
+    # ---- train_l2_pq -------------------------------------------------------
+    def train_l2_pq(self, M: int, k: int, cfg) -> torch.Tensor:
+        """pq.hpp:469-501: per-subspace k-means (seed + m), lockstep. Returns the
+        replicated dictionaries (float64 [M*k*sd]); codes stay in the shard."""
+        from . import anisoq as aq
+        self._validate(M, k)
+        sd = self.sh.d // M
+        hidx = []
+        for m in range(M):
+            hidx += HostRng(cfg.seed + m).sample_distinct(self.n_total, k)
+        dict_ = self._init_rows(hidx, M, k, sd)
+        self._do(self.sh.set_codebook, dict_, M, k, sd)
+        active = [1] * M
+
+        def assign():
+            losses, changes = self._do(self.sh.kmeans_assign, active)
+            chg = self.comm.int_sum(torch.as_tensor(changes, dtype=torch.int64,
+                                                    device=self.sh.device)).tolist()
+            loc = self._do(lambda: [self.sh.seq_sum(losses[m]) if active[m] else 0.0
+                                    for m in range(M)])
+            tot = self.comm.ordered_sum(torch.tensor(loc, dtype=torch.float64,
+                                                     device=self.sh.device)).tolist()
+            return losses, chg, tot
+
+        losses, chg, tot = assign()
+        for _ in range(cfg.max_iterations):
+            if not any(active):
+                break
+            num, den, cnt = self._do(self.sh.kmeans_partials, active)
+            num = self.comm.ordered_sum(num).reshape(M * k, sd)
+            den = self.comm.ordered_sum(den).reshape(M * k)
+            cnt = self.comm.int_sum(cnt).reshape(M * k)
+            act = torch.tensor(active, dtype=torch.bool, device=dict_.device).repeat_interleave(k)
+            upd = act & (cnt > 0)
+            d2 = dict_.reshape(M * k, sd)
+            d2[upd] = num[upd] / den[upd, None]
+            if cfg.empty_partition_policy == "reseed_highest_loss":
+                cnt_h = cnt.tolist()
+                for m in range(M):
+                    if not active[m]:
+                        continue
+                    empty = [j for j in range(k) if cnt_h[m * k + j] == 0]
+                    if not empty:
+                        continue
+                    order = self._global_ranking(losses[m], len(empty))
+                    rows = self._fetch_rows(order[: len(empty)])
+                    for c, j in enumerate(empty):
+                        d2[m * k + j] = rows[c, m * sd:(m + 1) * sd]
+            dict_ = d2.reshape(-1).contiguous()
+            self._do(self.sh.set_codebook, dict_, M, k, sd)
+            prev = tot
+            losses, chg, tot = assign()
+            for m in range(M):
+                if not active[m]:
+                    continue
+                if chg[m] == 0:
+                    active[m] = 0
+                    continue
+                if cfg.relative_tolerance > 0.0 and (
+                        prev[m] == 0.0 or prev[m] - tot[m] <= cfg.relative_tolerance * prev[m]):
+                    active[m] = 0
+        return dict_
+
+    # ---- pq_codebook_update ---------------------------------------------------
+    def codebook_update(self, M: int, k: int, ridge: float) -> torch.Tensor:
+        """pq.hpp:356-464 with per-shard partials (M > 1)."""
+        from . import anisoq as aq
+        sd = self.sh.d // M
+        if M == 1:
+            raise aq.Unsupported("Unsupported: the sharded trainer needs M > 1 "
+                                 "(M == 1 runs the single-GPU update_codeword path)")
+        if sd > 16:
+            raise aq.Unsupported("Unsupported: device update supports sub_dimension <= 16")
+        any_aniso, zero_idx = self._do(self.sh.weight_flags)
+        dev = self.sh.device
+        flag = self.comm.int_sum(torch.tensor([int(any_aniso)], device=dev)).item() > 0
+        big = 1 << 62
+        z = torch.tensor([zero_idx + self.offset if zero_idx is not None else big], device=dev)
+        zmin = min(int(p.item()) for p in self.comm.gather(z))
+        dim = k * self.sh.d
+        if not flag:
+            num, den, usage = self._do(self.sh.iso_partials, k)
+            num = self.comm.ordered_sum(num).reshape(M * k, sd)
+            den = self.comm.ordered_sum(den).reshape(M * k)
+            usage = self.comm.int_sum(usage).reshape(M * k)
+            used = usage > 0
+            if bool((den[used] <= 0.0).any()):
+                raise aq.SingularSystem("SingularSystem: zero total weight in block")
+            x = torch.zeros((M * k, sd), dtype=torch.float64, device=dev)
+            x[used] = num[used] / den[used, None]
+            x = x.reshape(-1)
+        else:
+            if dim > 16384:
+                raise aq.InvalidArgument("InvalidArgument: stacked codebook system exceeds "
+                                         "16384 unknowns (pq.hpp:426-429)")
+            if zmin != big:
+                raise aq.ZeroNormDatapoint(
+                    f"ZeroNormDatapoint: anisotropic update undefined at |x| = 0 (point {zmin})")
+            A, rhs, usage = self._do(self.sh.normal_equations, k)
+            A = self.comm.ordered_sum(A)
+            rhs = self.comm.ordered_sum(rhs)
+            usage = self.comm.int_sum(usage).reshape(M * k)
+            x = self._do(self.sh.solve, A, rhs, ridge)
+        unused = [t for t, c in enumerate(usage.tolist()) if c == 0]
+        if unused:
+            # reseed from the loss ranking under the new codebook (pq.hpp:446-462)
+            self._do(self.sh.set_codebook, x, M, k, sd)
+            losses = self._do(self.sh.point_losses)
+            order = self._global_ranking(losses, len(unused))
+            rows = self._fetch_rows(order)
+            x2 = x.reshape(M * k, sd)
+            for c, t in enumerate(unused):
+                m = t // k
+                x2[t] = rows[c % len(order), m * sd:(m + 1) * sd]
+            x = x2.reshape(-1).contiguous()
+        self._do(self.sh.set_codebook, x, M, k, sd)
+        return x
+
+    # ---- train_apq ------------------------------------------------------------
+    def train_apq(self, M: int, k: int, cfg, warm_start: bool = True,
+                  loss_history: Optional[list] = None) -> torch.Tensor:
+        """pq.hpp:513-575 over the shards. Returns the replicated dictionaries;
+        this rank's codes are in the shard (shard.codes)."""
+        self._validate(M, k)
+        sd = self.sh.d // M
+        if warm_start:
+            dict_ = self.train_l2_pq(M, k, cfg)
+        else:
+            r = HostRng(cfg.seed)  # one generator for all subspaces (pq.hpp:533-542)
+            hidx = []
+            for _ in range(M):
+                hidx += r.sample_distinct(self.n_total, k)
+            dict_ = self._init_rows(hidx, M, k, sd)
+            self._do(self.sh.set_codebook, dict_, M, k, sd)
+            self._do(self.sh.nearest)
+
+        def apass():
+            losses, changed = self._do(self.sh.assign_pass, cfg.sweep_to_fixed_point)
+            tot = self.comm.ordered_scalar_sum(self._do(self.sh.seq_sum, losses), self.sh.device)
+            ch = int(self.comm.int_sum(torch.tensor([changed], device=self.sh.device)).item())
+            return tot, ch
+
+        tot, changed = apass()
+        hist = [tot]
+        for _ in range(cfg.max_iterations):
+            dict_ = self.codebook_update(M, k, cfg.ridge)
+            prev = tot
+            tot, changed = apass()
+            hist.append(tot)
+            if changed == 0:
+                break
+            if cfg.relative_tolerance > 0.0 and (
+                    prev == 0.0 or prev - tot <= cfg.relative_tolerance * prev):
+                break
+        if loss_history is not None:
+            loss_history.extend(hist)
+        return dict_
+
+
+class DeviceShard:
+    """This rank's rows on its B200 behind the C ABI (aq_dev_* building blocks).
+
+    rows: float32 [n_local, d] CUDA tensor; weights: AnisotropicWeights,
+    ThresholdWeights or this shard's per-point (h_par, h_perp) arrays."""
+
+    def __init__(self, session, rows: torch.Tensor, weights):
+        from . import anisoq as aq
+        import ctypes as C
+        self._aq, self._C = aq, C
+        self.s = session
+        self.x = rows.contiguous()
+        self.n, self.d = self.x.shape
+        self.device = self.x.device
+        torch.cuda.current_stream(self.device).synchronize()
+        self.ds = session.wrap_device_rows(self.x.data_ptr(), self.n, self.d)
+        self._keep: list = []
+        self.w = aq._weights(weights, self.n, self._keep)
+        self.cb = None
+        self.codes = None
+
+    def _sync(self):
+        torch.cuda.current_stream(self.device).synchronize()
+
+    def _call(self, name, *args):
+        self._sync()
+        self._aq._check(getattr(self._aq._L, name)(*args))
+
+    def _ensure(self, M, k, sd):
+        aq = self._aq
+        if self.cb is None or (self.cb.M, self.cb.k, self.cb.sd) != (M, k, sd):
+            self.cb = self.s.upload_codebook(aq.ProductCodebook(
+                M, k, sd, np.zeros(M * k * sd, np.float64)))
+        if self.codes is None or (self.codes.M, self.codes.k) != (M, k):
+            self.codes = self.s.alloc_codes(self.n, M, k)
+
+    # codebook / rows
+    def set_codebook(self, dict_: torch.Tensor, M: int, k: int, sd: int) -> None:
+        self._ensure(M, k, sd)
+        d = dict_.to(device=self.device, dtype=torch.float64).contiguous()
+        self._call("aq_codebook_set_device", self.cb.h, d.data_ptr())
+
+    def rows(self, local_idx: torch.Tensor) -> torch.Tensor:
+        return self.x[local_idx].to(torch.float64)
+
+    # assignment
+    def nearest(self) -> None:
+        iso = self._aq._weights(self._aq.AnisotropicWeights.isotropic(), self.n, [])
+        self._call("aq_dev_pq_quantize", self.ds.h, self.cb.h, self._C.byref(iso), 0,
+                   self.codes.h)
+
+    def assign_pass(self, sweep_fixed: bool):
+        losses = torch.empty(self.n, dtype=torch.float64, device=self.device)
+        ch = self._C.c_uint64(0)
+        self._call("aq_dev_pq_assign_pass", self.ds.h, self.cb.h, self._C.byref(self.w),
+                   int(sweep_fixed), self.codes.h, losses.data_ptr() if self.n else None,
+                   self._C.byref(ch))
+        return losses, ch.value
+
+    def kmeans_assign(self, active: list):
+        M = self.cb.M
+        losses = torch.zeros((M, self.n), dtype=torch.float64, device=self.device)
+        act = np.asarray(active, np.int32)
+        ch = np.zeros(M, np.uint64)
+        self._call("aq_dev_kmeans_assign", self.ds.h, self.cb.h, self.codes.h,
+                   act.ctypes.data, losses.data_ptr(), ch.ctypes.data)
+        return losses, ch.astype(np.int64)
+
+    def point_losses(self) -> torch.Tensor:
+        losses = torch.empty(max(self.n, 1), dtype=torch.float64, device=self.device)
+        self._call("aq_dev_point_losses", self.ds.h, self.cb.h, self._C.byref(self.w),
+                   self.codes.h, losses.data_ptr())
+        return losses[: self.n]
+
+    def seq_sum(self, v: torch.Tensor) -> float:
+        out = self._C.c_double(0.0)
+        v = v.contiguous()
+        self._call("aq_dev_seq_sum", self.s.h, v.data_ptr(), v.numel(), 0.0,
+                   self._C.byref(out))
+        return out.value
+
+    def ranking(self, losses: torch.Tensor, top: int):
+        idx = torch.arange(self.n, dtype=torch.int32, device=self.device)
+        v = losses.contiguous()
+        if self.n:
+            self._call("aq_dev_sort_desc", self.s.h, v.data_ptr(), idx.data_ptr(), self.n)
+        sel = idx[:top].to(torch.int64)
+        return v[sel], sel
+
+    # partial sums
+    def weight_flags(self):
+        fl = np.zeros(2, np.uint64)
+        self._call("aq_dev_weight_flags", self.ds.h, self._C.byref(self.w), fl.ctypes.data)
+        return bool(fl[0]), (int(fl[1]) - 1 if fl[1] else None)
+
+    def kmeans_partials(self, active: list):
+        M, k, sd = self.cb.M, self.cb.k, self.cb.sd
+        num = torch.empty(M * k * sd, dtype=torch.float64, device=self.device)
+        den = torch.empty(M * k, dtype=torch.float64, device=self.device)
+        cnt = torch.zeros(M * k, dtype=torch.int32, device=self.device)
+        act = np.asarray(active, np.int32)
+        self._call("aq_dev_kmeans_partials", self.ds.h, self.codes.h, k, act.ctypes.data,
+                   num.data_ptr(), den.data_ptr(), cnt.data_ptr())
+        return num, den, cnt
+
+    def iso_partials(self, k: int):
+        M, sd = self.codes.M, self.d // self.codes.M
+        num = torch.empty(M * k * sd, dtype=torch.float64, device=self.device)
+        den = torch.empty(M * k, dtype=torch.float64, device=self.device)
+        usage = torch.zeros(M * k, dtype=torch.int32, device=self.device)
+        self._call("aq_dev_iso_partials", self.ds.h, self.codes.h, self._C.byref(self.w), k,
+                   num.data_ptr(), den.data_ptr(), usage.data_ptr())
+        return num, den, usage
+
+    def normal_equations(self, k: int):
+        M, dim = self.codes.M, k * self.d
+        A = torch.empty((dim, dim), dtype=torch.float64, device=self.device)
+        rhs = torch.empty(dim, dtype=torch.float64, device=self.device)
+        usage = torch.zeros(M * k, dtype=torch.int32, device=self.device)
+        fl = np.zeros(2, np.uint64)
+        self._call("aq_dev_normal_equations_partial", self.ds.h, self.codes.h,
+                   self._C.byref(self.w), k, A.data_ptr(), rhs.data_ptr(), usage.data_ptr(),
+                   fl.ctypes.data)
+        return A, rhs, usage
+
+    def solve(self, A: torch.Tensor, rhs: torch.Tensor, ridge: float) -> torch.Tensor:
+        A = A.contiguous().clone()
+        x = rhs.contiguous().clone()
+        self._call("aq_dev_solve_normal_equations", self.s.h, A.data_ptr(), x.data_ptr(),
+                   x.numel(), float(ridge))
+        return x

@@ -29,8 +29,13 @@ int sort_scores_desc(aq_session* s, const double* scores, uint32_t* idx,
 // min CTAs per SM. Selected per launch (AQ_ADC_VARIANT overrides).
 struct AdcShape {
   int qp, tile, minb;
+  bool gbuf;  // candidate windows in global memory (L2) instead of shared
 };
-constexpr AdcShape kShapes[] = {{16, 256, 1}, {8, 256, 2}, {8, 512, 1}, {16, 512, 1}};
+constexpr AdcShape kShapes[] = {{8, 256, 2, false}, {8, 256, 4, true},  {4, 256, 6, true},
+                                {4, 256, 8, true},   {8, 256, 3, true},  {8, 128, 8, true},
+                                {6, 256, 4, true},   {12, 256, 3, true}};
+constexpr int kGbPointsPerThread = 4;  // points per thread between barriers (GB)
+constexpr int kNumShapes = sizeof(kShapes) / sizeof(kShapes[0]);
 constexpr int kLutQP = 16;  // lut kernel of the single-query host entry
 constexpr int kMaxTopN = 512;    // fast path limit
 constexpr int kMergeCap = 2048;
@@ -139,7 +144,10 @@ __device__ int warp_compact(uint2* buf, int cnt, int cut) {
 // are summed with IADD3 into packed 16-bit lanes, then split into 32-bit
 // accumulators. Shared-memory delivery is the bound: 64 lookups per
 // wavefront. MP > 0 fixes M at compile time (immediate LDS offsets).
-template <int MP, int QP, int TILE, int MINB>
+// GB: the per-query candidate windows live in this CTA's slice of out_buf
+// (global, L2-resident; appends are rare once the cut has risen) instead of
+// shared memory, so shared memory holds only the LUT and more CTAs fit.
+template <int MP, int QP, int TILE, int MINB, bool GB>
 __global__ void __launch_bounds__(TILE, MINB) k_adc_score(const ScoreArgs a) {
   constexpr int QB = 2 * QP;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -148,8 +156,11 @@ __global__ void __launch_bounds__(TILE, MINB) k_adc_score(const ScoreArgs a) {
   int* cut = reinterpret_cast<int*>(T + QP * M * 16);
   int* cnt = cut + QB;
   int* flag = cnt + QB;
-  uint2* buf = reinterpret_cast<uint2*>(flag + QB);  // [QB][cap]
   const int qb = blockIdx.y, r = blockIdx.x;
+  // window of query q: shared [QB][cap], or out_buf[(qb QB + q) R + r][cap]
+  uint2* const buf = GB ? a.out_buf + ((size_t)qb * QB * a.R + r) * a.cap
+                        : reinterpret_cast<uint2*>(flag + QB);
+  const size_t qstride = GB ? (size_t)a.R * a.cap : (size_t)a.cap;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   {
     const uint4* src = reinterpret_cast<const uint4*>(a.lutq + (size_t)qb * QP * M * 16);
@@ -165,43 +176,54 @@ __global__ void __launch_bounds__(TILE, MINB) k_adc_score(const ScoreArgs a) {
   const size_t start = (size_t)r * a.range_len;
   const size_t end = min(a.n, start + a.range_len);
   const int cap = a.cap;
-  const int nchunk = (M + 7) >> 3;
   const int margin = M + 1;  // 2 * (M s / 2) / s, plus one unit for float64
-  for (size_t tb = start; tb < end; tb += TILE) {
-    const size_t p = tb + threadIdx.x;
+  // points scored between two barriers (windows in global memory are cheap
+  // to size for it; shared windows keep one point per thread)
+  constexpr int PPT = GB ? kGbPointsPerThread : 1;
+  constexpr int SPAN = TILE * PPT;
+  // the first span is one tile: its appends (cut still INT_MIN) set the cut
+  for (size_t tb = start; tb < end;) {
+    const int nu = tb == start ? 1 : PPT;
+#pragma unroll 1
+   for (int u = 0; u < nu; ++u) {
+    const size_t p = tb + (size_t)u * TILE + threadIdx.x;
     if (p < end) {
       uint32_t acc[QB];
 #pragma unroll
       for (int q = 0; q < QB; ++q) acc[q] = 0u;
       const uint32_t* crow = reinterpret_cast<const uint32_t*>(a.codes + p * a.stride);
+      // full chunks of 8 subspaces, then the tail (compile-time when MP > 0)
+      const int nfull = M >> 3, tail = M & 7;
 #pragma unroll 1
-      for (int ch = 0; ch < nchunk; ++ch) {
+      for (int ch = 0; ch < nfull; ++ch) {
         const uint32_t w = __ldg(crow + ch);
-        const int valid = M - ch * 8;  // >= 8 except in the tail chunk
         int off[8];
 #pragma unroll
         for (int t = 0; t < 8; ++t) off[t] = (ch * 8 + t) * 16 + ((w >> (4 * t)) & 15u);
-        if (valid >= 8) {
 #pragma unroll
-          for (int qp = 0; qp < QP; ++qp) {
-            const uint32_t* Tq = T + qp * M * 16;
-            const uint32_t pk = (Tq[off[0]] + Tq[off[1]] + Tq[off[2]]) +
-                                (Tq[off[3]] + Tq[off[4]] + Tq[off[5]]) +
-                                (Tq[off[6]] + Tq[off[7]]);
-            acc[2 * qp] += pk & 0xffffu;
-            acc[2 * qp + 1] += pk >> 16;
-          }
-        } else {
+        for (int qp = 0; qp < QP; ++qp) {
+          const uint32_t* Tq = T + qp * M * 16;
+          const uint32_t pk = (Tq[off[0]] + Tq[off[1]] + Tq[off[2]]) +
+                              (Tq[off[3]] + Tq[off[4]] + Tq[off[5]]) +
+                              (Tq[off[6]] + Tq[off[7]]);
+          acc[2 * qp] += pk & 0xffffu;
+          acc[2 * qp + 1] += pk >> 16;
+        }
+      }
+      if (tail) {
+        const uint32_t w = __ldg(crow + nfull);
+        int off[8];
 #pragma unroll
-          for (int qp = 0; qp < QP; ++qp) {
-            const uint32_t* Tq = T + qp * M * 16;
-            uint32_t pk = 0u;
+        for (int t = 0; t < 8; ++t) off[t] = (nfull * 8 + t) * 16 + ((w >> (4 * t)) & 15u);
 #pragma unroll
-            for (int t = 0; t < 8; ++t)
-              if (t < valid) pk += Tq[off[t]];
-            acc[2 * qp] += pk & 0xffffu;
-            acc[2 * qp + 1] += pk >> 16;
-          }
+        for (int qp = 0; qp < QP; ++qp) {
+          const uint32_t* Tq = T + qp * M * 16;
+          uint32_t pk = 0u;
+#pragma unroll
+          for (int t = 0; t < 8; ++t)
+            if (t < tail) pk += Tq[off[t]];
+          acc[2 * qp] += pk & 0xffffu;
+          acc[2 * qp + 1] += pk >> 16;
         }
       }
 #pragma unroll
@@ -209,24 +231,26 @@ __global__ void __launch_bounds__(TILE, MINB) k_adc_score(const ScoreArgs a) {
         if ((int)acc[q] >= cut[q]) {
           const int pos = atomicAdd(&cnt[q], 1);
           if (pos < cap)
-            buf[q * cap + pos] = make_uint2(acc[q], (unsigned)p);
+            buf[q * qstride + pos] = make_uint2(acc[q], (unsigned)p);
           else
             flag[q] = 1;
         }
       }
     }
+   }
+    tb += (size_t)nu * TILE;
     __syncthreads();
-    // shrink buffers that could overflow during the next tile
+    // shrink buffers that could overflow during the next span
     for (int q = warp; q < QB; q += TILE / 32) {
       const int c = min(cnt[q], cap);
       unsigned th;
-      if (c > cap - TILE && !flag[q] && warp_nth_largest(buf + q * cap, c, a.N, &th)) {
+      if (c > cap - SPAN && !flag[q] && warp_nth_largest(buf + q * qstride, c, a.N, &th)) {
         const int cq = max(cut[q], (int)th - margin);
-        const int kept = warp_compact(buf + q * cap, c, cq);
+        const int kept = warp_compact(buf + q * qstride, c, cq);
         if (lane == 0) {
           cut[q] = cq;
           cnt[q] = kept;
-          if (kept > cap - TILE) flag[q] = 1;  // window too large: ties
+          if (kept > cap - SPAN) flag[q] = 1;  // window too large: ties
         }
       }
       __syncwarp();
@@ -238,11 +262,13 @@ __global__ void __launch_bounds__(TILE, MINB) k_adc_score(const ScoreArgs a) {
     const int gq = qb * QB + q;
     int c = min(cnt[q], cap);
     unsigned th;
-    if (warp_nth_largest(buf + q * cap, c, a.N, &th))
-      c = warp_compact(buf + q * cap, c, max(cut[q], (int)th - margin));
+    if (warp_nth_largest(buf + q * qstride, c, a.N, &th))
+      c = warp_compact(buf + q * qstride, c, max(cut[q], (int)th - margin));
     if (gq < a.nq) {
-      uint2* dst = a.out_buf + ((size_t)gq * a.R + r) * cap;
-      for (int e = lane; e < c; e += 32) dst[e] = buf[q * cap + e];
+      if (!GB) {
+        uint2* dst = a.out_buf + ((size_t)gq * a.R + r) * cap;
+        for (int e = lane; e < c; e += 32) dst[e] = buf[q * qstride + e];
+      }
       if (lane == 0) {
         a.out_cnt[(size_t)gq * a.R + r] = c;
         if (flag[q]) atomicOr(&a.out_flag[gq], 1);
@@ -408,7 +434,7 @@ int adc_search_device(aq_codes* codes, aq_codebook* cb, const double* Qd,
   const size_t topn_eff = std::min(topn, n);
   const size_t d = cb->M * cb->sd;
   int variant = 1;
-  if (const char* v = getenv("AQ_ADC_VARIANT")) variant = atoi(v) & 3;
+  if (const char* v = getenv("AQ_ADC_VARIANT")) variant = std::min(std::max(atoi(v), 0), kNumShapes - 1);
   const AdcShape shp = kShapes[variant];
   const int QB = 2 * shp.qp, TILE = shp.tile;
   const size_t nqb = (nq + QB - 1) / QB;
@@ -431,7 +457,7 @@ int adc_search_device(aq_codes* codes, aq_codebook* cb, const double* Qd,
   std::vector<int> hflag(nq, fast ? 0 : 1);
   if (fast) {
     const int N = (int)topn_eff;
-    const int cap = ((N + 31) & ~31) + TILE + 32;
+    const int cap = ((N + 31) & ~31) + TILE * (shp.gbuf ? kGbPointsPerThread : 1) + 32;
     // point ranges: enough CTAs for ~2 waves, ranges of whole tiles
     const size_t tiles = (n + TILE - 1) / TILE;
     // enough (query block x point range) CTAs for >= 8 full waves, so the
@@ -440,33 +466,42 @@ int adc_search_device(aq_codes* codes, aq_codebook* cb, const double* Qd,
     R = std::min(R, tiles);
     const size_t range_len = ((tiles + R - 1) / R) * TILE;
     R = (n + range_len - 1) / range_len;
-    const size_t buf_b = nq * R * cap * sizeof(uint2);
+    const size_t nq_pad = nqb * QB;  // GB windows exist for padding queries too
+    const size_t buf_b = nq_pad * R * cap * sizeof(uint2);
     void* p2;
     AQ_TRY(scratch(s, 3, buf_b + nq * R * sizeof(int) + nq * sizeof(int) + 256, &p2));
     uint2* obuf = (uint2*)p2;
-    int* ocnt = (int*)(obuf + nq * R * cap);
+    int* ocnt = (int*)(obuf + nq_pad * R * cap);
     int* oflag = ocnt + nq * R;
     AQ_CUDA(cudaMemsetAsync(oflag, 0, nq * sizeof(int), s->stream));
     ScoreArgs sa{codes->data, n, (int)codes->stride, lutq, M, (int)nq, N, cap,
                  range_len, (int)R, obuf, ocnt, oflag};
     const size_t smem = (size_t)shp.qp * M * 16 * sizeof(uint32_t) + 3 * QB * sizeof(int) +
-                        (size_t)QB * cap * sizeof(uint2);
+                        (shp.gbuf ? 0 : (size_t)QB * cap * sizeof(uint2));
     if (smem > 227 * 1024)
       return ref_error(AQ_E_UNSUPPORTED, "ADC working set exceeds shared memory");
     const dim3 grid((unsigned)R, (unsigned)nqb);
     timer_mark(s, AQ_T_ADC_SCORE);
-#define AQ_SCORE_LAUNCH(MM, QPv, TL, MB)                                              \
+#define AQ_SCORE_LAUNCH(MM, QPv, TL, MB, G)                                           \
   do {                                                                              \
-    AQ_CUDA(cudaFuncSetAttribute(k_adc_score<MM, QPv, TL, MB>,                       \
+    AQ_CUDA(cudaFuncSetAttribute(k_adc_score<MM, QPv, TL, MB, G>,                    \
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    k_adc_score<MM, QPv, TL, MB><<<grid, TL, smem, s->stream>>>(sa);                \
+    k_adc_score<MM, QPv, TL, MB, G><<<grid, TL, smem, s->stream>>>(sa);             \
   } while (0)
-#define AQ_SCORE_M(MM)                                               \
-  case MM:                                                          \
-    if (variant == 0) AQ_SCORE_LAUNCH(MM, 16, 256, 1);              \
-    else if (variant == 1) AQ_SCORE_LAUNCH(MM, 8, 256, 2);          \
-    else if (variant == 2) AQ_SCORE_LAUNCH(MM, 8, 512, 1);          \
-    else AQ_SCORE_LAUNCH(MM, 16, 512, 1);                           \
+#define AQ_SCORE_V(MM)                                                  \
+  switch (variant) {                                                   \
+    case 0: AQ_SCORE_LAUNCH(MM, 8, 256, 2, false); break;              \
+    case 1: AQ_SCORE_LAUNCH(MM, 8, 256, 4, true); break;               \
+    case 2: AQ_SCORE_LAUNCH(MM, 4, 256, 6, true); break;               \
+    case 3: AQ_SCORE_LAUNCH(MM, 4, 256, 8, true); break;               \
+    case 4: AQ_SCORE_LAUNCH(MM, 8, 256, 3, true); break;               \
+    case 5: AQ_SCORE_LAUNCH(MM, 8, 128, 8, true); break;               \
+    case 6: AQ_SCORE_LAUNCH(MM, 6, 256, 4, true); break;               \
+    default: AQ_SCORE_LAUNCH(MM, 12, 256, 3, true); break;             \
+  }
+#define AQ_SCORE_M(MM) \
+  case MM:             \
+    AQ_SCORE_V(MM)     \
     break;
     switch (M) {
       AQ_SCORE_M(16)
@@ -476,10 +511,7 @@ int adc_search_device(aq_codes* codes, aq_codebook* cb, const double* Qd,
       AQ_SCORE_M(64)
       AQ_SCORE_M(128)
       default:
-        if (variant == 0) AQ_SCORE_LAUNCH(0, 16, 256, 1);
-        else if (variant == 1) AQ_SCORE_LAUNCH(0, 8, 256, 2);
-        else if (variant == 2) AQ_SCORE_LAUNCH(0, 8, 512, 1);
-        else AQ_SCORE_LAUNCH(0, 16, 512, 1);
+        AQ_SCORE_V(0)
     }
 #undef AQ_SCORE_M
 #undef AQ_SCORE_LAUNCH

@@ -45,8 +45,11 @@ constexpr int kQMax = 4095;      // |v| <= 4095: 13-bit fields, 8 adds per 16-bi
 // One CTA per query: lut64[q][m][j] exactly as build_lut computes it, and the
 // integer filter table: v = rint(lut / s) + 4096 with s = max|lut| / 4095, so
 // |s v' - lut| <= s / 2 per entry and a sum of M entries is within M s / 2 of
-// the exact score. Two queries share a 32-bit word (low = even query);
-// layout [qblock][pair][M][16] words.
+// the exact score. Two queries share a 32-bit word (low = even query) and
+// two such pairs an 8-byte slot: layout [qblock][pair/2][M][16] x uint2, so
+// one LDS.64 per (subspace, code) serves four queries. (8-bit entries would
+// halve shared-memory traffic, but trained LUTs have a few large entries and
+// 127 levels widen the candidate windows past any fixed capacity.)
 __global__ void k_build_lut(const double* __restrict__ Q, int nq, int d,
                             const double* __restrict__ cb, int M, int k,
                             int sd, double* __restrict__ lut64,
@@ -71,7 +74,8 @@ __global__ void k_build_lut(const double* __restrict__ Q, int nq, int d,
   for (int t = 0; t < (int)(blockDim.x >> 5); ++t) mx = fmax(mx, red[t]);
   const double sc = mx > 0.0 ? mx / kQMax : 1.0;
   const int qb = q / (2 * QP), qi = q % (2 * QP);
-  uint16_t* T = lutq + ((((size_t)qb * QP + qi / 2) * M) * 16) * 2 + (qi & 1);
+  const int pp = qi / 2;  // query pair within the block
+  uint16_t* T = lutq + ((((size_t)qb * (QP / 2) + pp / 2) * M * 16) * 2 + (pp & 1)) * 2 + (qi & 1);
   for (int e = threadIdx.x; e < M * 16; e += blockDim.x) {
     const int m = e / 16, j = e % 16;
     int v = 0;
@@ -79,7 +83,7 @@ __global__ void k_build_lut(const double* __restrict__ Q, int nq, int d,
       v = (int)rint(L[m * k + j] / sc);
       v = max(-kQMax, min(kQMax, v));
     }
-    T[(size_t)e * 2] = (uint16_t)(v + kQMax + 1);
+    T[(size_t)e * 4] = (uint16_t)(v + kQMax + 1);
   }
 }
 
@@ -149,6 +153,7 @@ __device__ int warp_compact(uint2* buf, int cnt, int cut) {
 // shared memory, so shared memory holds only the LUT and more CTAs fit.
 template <int MP, int QP, int TILE, int MINB, bool GB>
 __global__ void __launch_bounds__(TILE, MINB) k_adc_score(const ScoreArgs a) {
+  static_assert(QP % 2 == 0, "LUT slots hold two query pairs");
   constexpr int QB = 2 * QP;
   extern __shared__ __align__(16) unsigned char smem[];
   const int M = MP > 0 ? MP : a.M;
@@ -201,13 +206,16 @@ __global__ void __launch_bounds__(TILE, MINB) k_adc_score(const ScoreArgs a) {
 #pragma unroll
         for (int t = 0; t < 8; ++t) off[t] = (ch * 8 + t) * 16 + ((w >> (4 * t)) & 15u);
 #pragma unroll
-        for (int qp = 0; qp < QP; ++qp) {
-          const uint32_t* Tq = T + qp * M * 16;
-          const uint32_t pk = (Tq[off[0]] + Tq[off[1]] + Tq[off[2]]) +
-                              (Tq[off[3]] + Tq[off[4]] + Tq[off[5]]) +
-                              (Tq[off[6]] + Tq[off[7]]);
-          acc[2 * qp] += pk & 0xffffu;
-          acc[2 * qp + 1] += pk >> 16;
+        for (int qq = 0; qq < QP / 2; ++qq) {
+          const uint2* Tq = reinterpret_cast<const uint2*>(T) + qq * M * 16;
+          const uint2 v0 = Tq[off[0]], v1 = Tq[off[1]], v2 = Tq[off[2]], v3 = Tq[off[3]];
+          const uint2 v4 = Tq[off[4]], v5 = Tq[off[5]], v6 = Tq[off[6]], v7 = Tq[off[7]];
+          const uint32_t pa = (v0.x + v1.x + v2.x) + (v3.x + v4.x + v5.x) + (v6.x + v7.x);
+          const uint32_t pb = (v0.y + v1.y + v2.y) + (v3.y + v4.y + v5.y) + (v6.y + v7.y);
+          acc[4 * qq] += pa & 0xffffu;
+          acc[4 * qq + 1] += pa >> 16;
+          acc[4 * qq + 2] += pb & 0xffffu;
+          acc[4 * qq + 3] += pb >> 16;
         }
       }
       if (tail) {
@@ -216,14 +224,20 @@ __global__ void __launch_bounds__(TILE, MINB) k_adc_score(const ScoreArgs a) {
 #pragma unroll
         for (int t = 0; t < 8; ++t) off[t] = (nfull * 8 + t) * 16 + ((w >> (4 * t)) & 15u);
 #pragma unroll
-        for (int qp = 0; qp < QP; ++qp) {
-          const uint32_t* Tq = T + qp * M * 16;
-          uint32_t pk = 0u;
+        for (int qq = 0; qq < QP / 2; ++qq) {
+          const uint2* Tq = reinterpret_cast<const uint2*>(T) + qq * M * 16;
+          uint32_t pa = 0u, pb = 0u;
 #pragma unroll
           for (int t = 0; t < 8; ++t)
-            if (t < tail) pk += Tq[off[t]];
-          acc[2 * qp] += pk & 0xffffu;
-          acc[2 * qp + 1] += pk >> 16;
+            if (t < tail) {
+              const uint2 v = Tq[off[t]];
+              pa += v.x;
+              pb += v.y;
+            }
+          acc[4 * qq] += pa & 0xffffu;
+          acc[4 * qq + 1] += pa >> 16;
+          acc[4 * qq + 2] += pb & 0xffffu;
+          acc[4 * qq + 3] += pb >> 16;
         }
       }
 #pragma unroll

@@ -474,9 +474,11 @@ int adc_search_device(aq_codes* codes, aq_codebook* cb, const double* Qd,
     const int cap = ((N + 31) & ~31) + TILE * (shp.gbuf ? kGbPointsPerThread : 1) + 32;
     // point ranges: enough CTAs for ~2 waves, ranges of whole tiles
     const size_t tiles = (n + TILE - 1) / TILE;
-    // enough (query block x point range) CTAs for >= 8 full waves, so the
-    // last partial wave costs little
-    size_t R = std::max<size_t>(1, (8 * (size_t)s->num_sms * shp.minb + nqb - 1) / nqb);
+    // ~4 waves of (query block x point range) CTAs: measured on config 2,
+    // 3-4 waves beat 8 (longer ranges amortise each CTA's window warm-up and
+    // LUT staging better than more waves hide the last partial one)
+    static const int waves = getenv("AQ_ADC_WAVES") ? atoi(getenv("AQ_ADC_WAVES")) : 4;
+    size_t R = std::max<size_t>(1, (waves * (size_t)s->num_sms * shp.minb + nqb - 1) / nqb);
     R = std::min(R, tiles);
     const size_t range_len = ((tiles + R - 1) / R) * TILE;
     R = (n + range_len - 1) / range_len;

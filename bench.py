@@ -277,9 +277,17 @@ def run_ours(args):
                 "share_of_step": round((ms_k / args.steps) / ms, 3),
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in pk
                 else "fallback 6650 GB/s",
-                "onchip_ceiling_scores_per_s": round(148 * 64 * 1.965e9 / (M + (-M % 8)), -8),
                 "note": "algorithmic bytes = M/2 code bytes per score (single-pass HBM figure); "
                         "queries are batched so the kernel is shared-memory-LUT bound"}
+    # on-chip ceiling: one 128-byte shared-memory wavefront per SM per clock
+    # = 32 LUT words = 64 (query, subspace) lookups of 16 bits; M per score
+    sm_hz = (clocks or {}).get("sm_mhz") or 1965.0
+    n_sms = torch.cuda.get_device_properties(local).multi_processor_count
+    ceil = n_sms * 64 * sm_hz * 1e6 / M
+    roofline["onchip"] = {"ceiling_scores_per_s": round(ceil, -8),
+                          "kernel_scores_per_s": round(nq * n / per_launch_s, -8),
+                          "frac": round(nq * n / per_launch_s / ceil, 4),
+                          "basis": f"{n_sms} SMs x 64 lookups/clk x {sm_hz:.0f} MHz / M={M}"}
 
     out = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": ws,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
@@ -290,7 +298,7 @@ def run_ours(args):
                       "threshold": w.threshold,
                       "index": dict(train_info, trainer="train_apq on device, warm start"),
                       "recall10_at_10": recall,
-                      "filter_dtype": "f32 (bounded), results f64 bit-exact",
+                      "filter_dtype": "13-bit integer LUT (bounded error), results f64 bit-exact",
                       "l2": "flushed (256 MiB write) before every timed step",
                       "parallelism": f"dp{ws} (row shards)"},
            "e2e": {"value": round(e2e, 1), "unit": UNIT,

@@ -234,7 +234,10 @@ __device__ __forceinline__ void residual2(double x0, double x1, double c0,
                                           double c1, double* d2, double* rd) {
   const double df0 = __dsub_rn(x0, c0);
   const double df1 = __dsub_rn(x1, c1);
-  double a = __dadd_rn(0.0, __dmul_rn(df0, df0));
+  // 0.0 + df0^2 == df0^2 for every input (squares are >= +0 or NaN), so the
+  // reference's first accumulation into zero is dropped for dist2; rdot keeps
+  // it (0.0 + (-0.0) = +0.0)
+  double a = __dmul_rn(df0, df0);
   a = __dadd_rn(a, __dmul_rn(df1, df1));
   double b = __dadd_rn(0.0, __dmul_rn(df0, x0));
   b = __dadd_rn(b, __dmul_rn(df1, x1));

@@ -60,11 +60,20 @@ __device__ __forceinline__ double exact_score2(double x0, double x1, double c0,
 // window), ascending j, strict < (pq.hpp:163-174 / 236-243). `nearest`
 // selects the reconstruction-nearest score (dist2 only). Out of line so the
 // hot loop stays small; returns the winner only.
+// pw: this thread's {h_par, h_perp, 1/|x|^2} in shared memory at stride ps
+// (kept out of registers across the sweep loop); unused when `nearest`.
 __device__ __noinline__ unsigned exact_window(
     float xf0, float xf1, const double2* __restrict__ cbm, unsigned mask,
-    bool nearest, bool iso, double base2, double base1, double hp, double ho,
-    double inv, unsigned long long* stats) {
+    bool nearest, double base2, double base1, const double* pw, int ps,
+    unsigned long long* stats) {
   if (stats) atomicAdd(stats, 1ull);
+  double hp = 0.0, ho = 0.0, inv = 0.0;
+  if (!nearest) {
+    hp = pw[0];
+    ho = pw[ps];
+    inv = pw[2 * ps];
+  }
+  const bool iso = hp == ho;
   const double x0 = xf0, x1 = xf1;
   unsigned jb = 0;
   double bs = 0.0;
@@ -152,6 +161,10 @@ __global__ void __launch_bounds__(TPB, MINB)
   double2* cb2 = reinterpret_cast<double2*>(scb + (a.M + 1) * kCbStride);  // [M+1][16]
   float* srm = reinterpret_cast<float*>(cb2 + (a.M + 1) * 16);
   uint32_t* scode = reinterpret_cast<uint32_t*>(srm + a.M);
+  // per-thread {h_par, h_perp, inv} for the exact path, [3][TPB] doubles
+  double* swt = reinterpret_cast<double*>(
+      (reinterpret_cast<uintptr_t>(scode + ((a.M + 7) / 8 + 1) * kEncThreads) + 7) &
+      ~(uintptr_t)7);
   {
     const double2* g2 = reinterpret_cast<const double2*>(a.cb64);
     for (int t = threadIdx.x; t < a.M * 16; t += blockDim.x) {
@@ -239,7 +252,7 @@ __global__ void __launch_bounds__(TPB, MINB)
         jb = (unsigned)(__ffs(mask) - 1);
       } else {
         jb = exact_window(xv.x, xv.y, cb2 + m * 16, mask ? mask : all_mask,
-                          true, true, 0.0, 0.0, 0.0, 0.0, 0.0, stats);
+                          true, 0.0, 0.0, nullptr, 0, stats);
       }
       const double2 cj = cb2[m * 16 + jb];
       double t2, t1;
@@ -292,6 +305,9 @@ __global__ void __launch_bounds__(TPB, MINB)
   const float dabs = (B2 + Xmax + W2max + agp * AB * AB) * 9.094947e-13f + 1e-30f;
   const bool bounds_ok = dabs < 1e25f;
   const bool fastpt = fast && bounds_ok;
+  swt[threadIdx.x] = hp;
+  swt[kEncThreads + threadIdx.x] = ho;
+  swt[2 * kEncThreads + threadIdx.x] = inv;
 
   // coordinate-descent sweeps (cd_sweep, pq.hpp:151-185)
   const int max_sweeps = a.mode == 0 ? a.passes : (a.mode == 1 ? 64 : 0);
@@ -319,16 +335,11 @@ __global__ void __launch_bounds__(TPB, MINB)
       const float rm = srm[m];
       const float X = __fmaf_rn(xv.y, xv.y, xv.x * xv.x);
       const float ax = (fabsf(xv.x) + fabsf(xv.y)) * rm;
-      float beta, W2;
-      if (iso) {
-        beta = 2.0f;
-        W2 = __fmaf_rn(rm, rm, 2.0f * ax);
-      } else {
-        const float b1f = (float)base1;
-        beta = 2.0f * __fmaf_rn(gp, b1f + X, cC);
-        W2 = __fmaf_rn(ax, __fmaf_rn(agp, __fmaf_rn(2.0f, fabsf(b1f) + X, ax), 2.0f * cC),
-                       cC * rm * rm);
-      }
+      // isotropic points have gp = agp = 0, cC = 1: beta = 2, W2 = 2 ax + rm^2
+      const float b1f = (float)base1;
+      const float beta = 2.0f * __fmaf_rn(gp, b1f + X, cC);
+      const float W2 = __fmaf_rn(ax, __fmaf_rn(agp, __fmaf_rn(2.0f, fabsf(b1f) + X, ax), 2.0f * cC),
+                                 cC * rm * rm);
       const float delta = __fmaf_rn(W2, 3.814697265625e-06f, dabs);  // 2^-18 W2 + abs
       // proxy_mask returns 0 (exact path) for non-finite windows
       const unsigned mask =
@@ -339,7 +350,7 @@ __global__ void __launch_bounds__(TPB, MINB)
         jb = (unsigned)(__ffs(mask) - 1);
       } else {
         jb = exact_window(xv.x, xv.y, cb2 + m * 16, mask ? mask : all_mask,
-                          false, iso, base2, base1, hp, ho, inv, stats);
+                          false, base2, base1, swt + threadIdx.x, kEncThreads, stats);
       }
       double b2 = t2, b1 = t1;
       if (jb != cur) {
@@ -369,6 +380,9 @@ __global__ void __launch_bounds__(TPB, MINB)
   if (stats && a.mode == 0) atomicAdd(stats + 1 + min(sweeps_run, 7), 1ull);
 
   if (a.mode >= 1) {
+    const volatile double* vw = swt + threadIdx.x;
+    const double hp = vw[0], ho = vw[kEncThreads], inv = vw[2 * kEncThreads];
+    const bool iso = hp == ho;
     // pq_point_loss (pq.hpp:137-146): state recomputed from scratch
     double r2 = 0.0, r1 = 0.0;
     unsigned long long nchg = 0;
@@ -629,7 +643,8 @@ int run_encode(aq_dataset* ds, aq_codebook* cb, const aq_weights* w,
     if (const char* v = getenv("AQ_ENC_VARIANT")) variant = atoi(v);
     const int tpb = (variant == 2 || variant == 3) ? 128 : 256;
     const size_t smv = (size_t)(a.M + 1) * (kCbStride * sizeof(float4) + 16 * sizeof(double2)) +
-                       (a.M + 1) * sizeof(float) + (size_t)(W + 1) * tpb * sizeof(uint32_t) + 16;
+                       (a.M + 1) * sizeof(float) + (size_t)(W + 1) * tpb * sizeof(uint32_t) + 16 +
+                       3 * tpb * sizeof(double) + 8;
     const unsigned grid = (unsigned)((ds->n + tpb - 1) / tpb);
     if (smv > 200 * 1024) return ref_error(AQ_E_UNSUPPORTED, "M too large for the fast encoder");
     timer_mark(s, AQ_T_ENCODE);

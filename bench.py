@@ -135,16 +135,96 @@ def build_index(aq, wl, n, nq, seed_shard, session):
     """Config-2 shard (setup, untimed): data, queries and the trained index —
     train_apq on the device exactly as configs[1] states (warm start, 10
     alternating iterations, T = 0.2), bit-identical to the reference's trainer."""
+    import ctypes as C
+
     w = wl.config2(n=n, nq=nq, seed=seed_shard)
     ds = session.upload_dataset(w.base)
     cfg = aq.TrainConfig(max_iterations=w.iterations, relative_tolerance=0.0, seed=seed_shard)
+    L = aq._L
+    L.aq_session_timing(session.h, 1)
+    for slot in range(8):
+        L.aq_session_timer_read(session.h, slot, None, None, 1)
+    session.sync()
     t0 = time.perf_counter()
     hist = []
     dcb, dc = aq.dev_train_apq(ds, w.M, w.k, aq.ThresholdWeights(w.threshold), cfg, True, hist)
+    session.sync()
     train_s = time.perf_counter() - t0
+    phases = {}
+    for slot, name in [(0, "encode"), (5, "assemble"), (6, "llt_solve"), (7, "kmeans_warm_start")]:
+        ms, cnt = C.c_double(0), C.c_uint64(0)
+        L.aq_session_timer_read(session.h, slot, C.byref(ms), C.byref(cnt), 1)
+        phases[name] = {"ms": round(ms.value, 2), "launches": int(cnt.value)}
+    L.aq_session_timing(session.h, 0)
     cb = dcb.download()
     return w, cb, ds, dcb, dc, {"train_apq_s": round(train_s, 2), "loss_first": hist[0],
-                                "loss_last": hist[-1], "iterations": len(hist) - 1}
+                                "loss_last": hist[-1], "iterations": len(hist) - 1,
+                                "phases": phases}
+
+
+def train_record(w, n, info, codes_h, cpu):
+    """train_apq on configs[1] (setup of the search bench, timed on the host
+    around the synchronous trainer; phases from device events)."""
+    its = info["iterations"]
+    ph = info["phases"]
+    km = ph["kmeans_warm_start"]["ms"] / 1e3
+    per_it = (info["train_apq_s"] - km) / max(its, 1)
+    asm_s = ph["assemble"]["ms"] / 1e3 / max(its, 1)
+    M = w.M
+    # lower-triangle coupling MACs per iteration: every point meets each pair
+    # (m2 <= m) of its codes with sd^2 = 4 products
+    macs = n * (M * (M + 1) // 2) * 4
+    # shared-memory read-modify-write ceiling: 4 MACs per (point, m2) touch
+    # 4 doubles read + written = 64 B -> 8 MACs per 128-B wavefront per SM
+    ceil = 148 * 8 * 1.965e9
+    return {"metric": "train_apq iterations/sec", "workload": "config2",
+            "value": round(1.0 / per_it, 3), "unit": "iterations/s",
+            "ms_per_iteration": round(per_it * 1e3, 2), "iterations": its,
+            "warm_start_s": round(km, 3), "total_s": info["train_apq_s"],
+            "phases_ms": {k: v["ms"] for k, v in ph.items()},
+            "assembly_roofline": {"bound": "smem read-modify-write", "macs_per_iteration": macs,
+                                  "achieved_gmacs": round(macs / asm_s / 1e9, 1),
+                                  "ceiling_gmacs": round(ceil / 1e9, 1),
+                                  "frac": round(macs / asm_s / ceil, 4),
+                                  "note": "float64 entries, each a point-ordered chain "
+                                          "(bit-exact with pq.hpp:320-339)"},
+            "exact": "codebooks, codes and loss history bit-identical to the reference",
+            "cpu_baseline": cpu}
+
+
+def train_cpu_baseline(args, w, dc_h, n):
+    """Reference pq_codebook_update (oracle/_ref, serial assembly + LLT) on a
+    bounded prefix of the config-2 shard with the trained codes, extrapolated
+    to the full shard: assembly is linear in n, the LLT is timed once."""
+    try:
+        from oracle import Reference
+    except Exception as e:  # pragma: no cover
+        return {"value": None, "error": str(e)}
+    if not Reference.available():
+        return None
+    R = Reference()
+    x = w.base
+    norms = np.sqrt(np.einsum("ij,ij->i", x.astype(np.float64), x.astype(np.float64)))
+    d = x.shape[1]
+    times = []
+    for m in (4000, 16000):
+        xs = x[:m].astype(np.float64)
+        nr = norms[:m]
+        rho = (w.threshold / nr) ** 2
+        hp = (d - 1) * rho / (1 - rho)
+        ho = np.ones(m)
+        t0 = time.perf_counter()
+        R.pq_codebook_update(xs, dc_h[:m], hp, ho, w.M, w.k)
+        times.append((m, time.perf_counter() - t0))
+    (m1, t1), (m2, t2) = times
+    per_pt = (t2 - t1) / (m2 - m1)
+    fixed = max(t1 - per_pt * m1, 0.0)
+    est = fixed + per_pt * n
+    return {"value": round(1.0 / est, 5), "unit": "iterations/s (codebook update only)",
+            "cores": 1, "kind": "reference",
+            "sample": f"pq_codebook_update on the first {m1} and {m2} rows ({t1:.1f} s, "
+                      f"{t2:.1f} s), linear in n -> {est:.1f} s at n = {n} (serial in the "
+                      f"reference: pq.hpp:303-343)"}
 
 
 def run_ours(args):
@@ -296,7 +376,8 @@ def run_ours(args):
            "config": {"workload": "config2", "n_per_gpu": n, "d": d, "M": M, "k": 16,
                       "queries_per_step": nq, "adc_topn": topn, "rerank_to": keep,
                       "threshold": w.threshold,
-                      "index": dict(train_info, trainer="train_apq on device, warm start"),
+                      "index": dict({k: v for k, v in train_info.items() if k != "phases"},
+                                    trainer="train_apq on device, warm start"),
                       "recall10_at_10": recall,
                       "filter_dtype": "13-bit integer LUT (bounded error), results f64 bit-exact",
                       "l2": "flushed (256 MiB write) before every timed step",
@@ -307,6 +388,11 @@ def run_ours(args):
            "gpu_launches": int(launches), "roofline": roofline, "clocks": clocks,
            "kernel_ms": {k: round(v[0] / args.steps, 3) for k, v in kt.items()}}
 
+    if rank == 0:
+        tcpu = None
+        if ws == 1 and not args.no_cpu_baseline:
+            tcpu = train_cpu_baseline(args, w, dc.download().codes, n)
+        out["train"] = train_record(w, n, train_info, None, tcpu)
     if not args.no_encode:
         out["encode"] = bench_encode(args, aq, wl, sess, stream, flush, local, ws, pk)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

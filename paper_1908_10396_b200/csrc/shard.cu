@@ -18,6 +18,7 @@ int run_encode(aq_dataset* ds, aq_codebook* cb, const aq_weights* w, aq_codes* c
                int passes, int sweep_fixed, double* losses_dev, uint64_t* changed_out);
 int sort_scores_desc(aq_session* s, const double* scores, uint32_t* idx, size_t n);
 int stage_codebook(aq_codebook* cb);
+int seq_sum_device(aq_session* s, const double* v, size_t n, double init, double* out);
 
 // per-slot partial sums for the isotropic path (pq.hpp:405-417), members in
 // ascending order within this shard
@@ -70,13 +71,6 @@ __global__ void k_kmeans_partials(const float* xr, size_t n, int d, int M, int k
 __global__ void k_copy_counts(const uint32_t* count, size_t total, uint32_t* out) {
   const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t < total) out[t] = count[t];
-}
-
-__global__ void k_seq_sum_init(const double* v, size_t n, double init, double* out) {
-  if (threadIdx.x || blockIdx.x) return;
-  double s = init;
-  for (size_t i = 0; i < n; ++i) s = __dadd_rn(s, v[i]);
-  *out = s;
 }
 
 }  // namespace aqd
@@ -221,8 +215,7 @@ int aq_dev_seq_sum(aq_session* s, const double* v_dev, size_t n, double init, do
   AQ_TRY(check_session(s));
   double* d;
   AQ_CUDA(cudaMallocAsync(&d, sizeof(double), s->stream));
-  k_seq_sum_init<<<1, 1, 0, s->stream>>>(v_dev, n, init, d);
-  s->launches++;
+  AQ_TRY(seq_sum_device(s, v_dev, n, init, d));
   AQ_CUDA(cudaMemcpyAsync(out, d, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
   cudaFreeAsync(d, s->stream);
   AQ_CUDA(cudaStreamSynchronize(s->stream));

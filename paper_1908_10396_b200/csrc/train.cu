@@ -62,28 +62,54 @@ struct HostRng {
 
 // ---- kernels ------------------------------------------------------------------------------
 
-// std::accumulate of `count` values (float64, index order), one warp per row:
-// the lanes stage 32 consecutive values in shared memory (coalesced, many
-// loads in flight) and lane 0 adds them strictly in index order.
+// std::accumulate of `count` values (float64, index order), one warp per row.
+// The chain of dependent adds is the bound (count x DADD latency), so the
+// lanes keep it fed: block t + 1 (256 values, 8 per lane, coalesced) is in
+// registers while lane 0 adds block t from shared memory in index order.
 __global__ void k_seq_sums(const double* __restrict__ v, size_t ld, size_t count, int rows,
-                           const int* __restrict__ active, double* __restrict__ out) {
-  __shared__ double buf[8][256];
+                           const int* __restrict__ active, double* __restrict__ out,
+                           double init = 0.0) {
+  __shared__ double buf[8][2][256];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = blockIdx.x * (blockDim.x >> 5) + w;
   if (r >= rows || (active && !active[r])) return;
   const double* p = v + (size_t)r * ld;
-  double s = 0.0;
-  for (size_t i0 = 0; i0 < count; i0 += 256) {
-    const int nb = (int)min((size_t)256, count - i0);
+  double s = init;
+  double nxt[8];
+  auto fetch = [&](size_t i0) {
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (u * 32 + lane < nb) buf[w][u * 32 + lane] = p[i0 + u * 32 + lane];
+    for (int u = 0; u < 8; ++u) {
+      const size_t i = i0 + u * 32 + lane;
+      nxt[u] = i < count ? p[i] : 0.0;
+    }
+  };
+  fetch(0);
+  int cur = 0;
+  for (size_t i0 = 0; i0 < count; i0 += 256) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) buf[w][cur][u * 32 + lane] = nxt[u];
     __syncwarp();
-    if (lane == 0)
-      for (int t = 0; t < nb; ++t) s = __dadd_rn(s, buf[w][t]);
-    __syncwarp();
+    if (i0 + 256 < count) fetch(i0 + 256);  // in flight during the chain below
+    if (lane == 0) {
+      const int nb = (int)min((size_t)256, count - i0);
+      const double* b = buf[w][cur];
+      if (nb == 256) {
+#pragma unroll 16
+        for (int t = 0; t < 256; ++t) s = __dadd_rn(s, b[t]);
+      } else {
+        for (int t = 0; t < nb; ++t) s = __dadd_rn(s, b[t]);
+      }
+    }
+    cur ^= 1;
   }
   if (lane == 0) out[r] = s;
+}
+
+// std::accumulate(v, v + n, init) into *out (device), on the session stream
+int seq_sum_device(aq_session* s, const double* v, size_t n, double init, double* out) {
+  k_seq_sums<<<1, 32, 0, s->stream>>>(v, n, n, 1, nullptr, out, init);
+  AQ_LAUNCHED(s);
+  return AQ_OK;
 }
 
 // codewords from sampled rows: dict[m][j] = x[idx[m][j]][m-subvector]
@@ -147,12 +173,15 @@ __global__ void k_kmeans_assign(const float* __restrict__ xr, size_t n, int d, i
 // mean = (sum 1.0 x) / (sum 1.0), members in ascending order. One warp per
 // slot: the lanes gather 32 members' sub-vectors into shared memory (all in
 // flight), lane 0 accumulates them in member order.
+template <int SDC>  // SDC > 0: compile-time sub_dimension (accumulators in registers)
 __global__ void k_kmeans_means(const float* __restrict__ xr, size_t n, int d, int M, int k,
-                               int sd, const uint32_t* __restrict__ list,
+                               int sd_rt, const uint32_t* __restrict__ list,
                                const uint32_t* __restrict__ start,
                                const uint32_t* __restrict__ count,
                                const int* __restrict__ active, double* __restrict__ dict) {
-  __shared__ float xs[4][32][17];
+  constexpr int SDM = SDC > 0 ? SDC : 16;
+  const int sd = SDC > 0 ? SDC : sd_rt;
+  __shared__ float xs[4][32][SDM + 1];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slot = blockIdx.x * (blockDim.x >> 5) + w;
   if (slot >= M * k) return;
@@ -161,26 +190,32 @@ __global__ void k_kmeans_means(const float* __restrict__ xr, size_t n, int d, in
   const size_t cnt = count[slot];
   if (cnt == 0) return;  // reseeded by the host walk
   const uint32_t* L = list + (size_t)m * n + start[slot];
-  double num[16];
-  for (int c = 0; c < sd; ++c) num[c] = 0.0;
+  double num[SDM];
+#pragma unroll
+  for (int c = 0; c < SDM; ++c) num[c] = 0.0;
   double den = 0.0;
   for (size_t t0 = 0; t0 < cnt; t0 += 32) {
     const int nb = (int)min((size_t)32, cnt - t0);
     if (lane < nb) {
       const float* xp = xr + (size_t)L[t0 + lane] * d + m * sd;
-      for (int c = 0; c < sd; ++c) xs[w][lane][c] = xp[c];
+#pragma unroll
+      for (int c = 0; c < SDM; ++c)
+        if (c < sd) xs[w][lane][c] = xp[c];
     }
     __syncwarp();
     if (lane == 0)
       for (int b = 0; b < nb; ++b) {
-        for (int c = 0; c < sd; ++c)
-          num[c] = __dadd_rn(num[c], __dmul_rn(1.0, (double)xs[w][b][c]));
+#pragma unroll
+        for (int c = 0; c < SDM; ++c)
+          if (c < sd) num[c] = __dadd_rn(num[c], __dmul_rn(1.0, (double)xs[w][b][c]));
         den = __dadd_rn(den, 1.0);
       }
     __syncwarp();
   }
   if (lane == 0)
-    for (int c = 0; c < sd; ++c) dict[(size_t)slot * sd + c] = __ddiv_rn(num[c], den);
+#pragma unroll
+    for (int c = 0; c < SDM; ++c)
+      if (c < sd) dict[(size_t)slot * sd + c] = __ddiv_rn(num[c], den);
 }
 
 // empty partitions (vq.hpp:284-292): j ascending, consuming the ranking
@@ -269,8 +304,12 @@ int train_l2_pq_device(aq_dataset* ds, size_t M, size_t k, const aq_train_config
     st = build_buckets(codes, (int)k, &B);
     if (st != AQ_OK) break;
     AQ_CUDA(cudaMemcpyAsync(active, hact.data(), M * sizeof(int), cudaMemcpyHostToDevice, s->stream));
-    k_kmeans_means<<<(unsigned)((M * k + 3) / 4), 128, 0, s->stream>>>(
-        ds->xr, n, (int)d, (int)M, (int)k, (int)sd, B.list, B.start, B.count, active, cb->d64);
+    if (sd == 2)
+      k_kmeans_means<2><<<(unsigned)((M * k + 3) / 4), 128, 0, s->stream>>>(
+          ds->xr, n, (int)d, (int)M, (int)k, (int)sd, B.list, B.start, B.count, active, cb->d64);
+    else
+      k_kmeans_means<0><<<(unsigned)((M * k + 3) / 4), 128, 0, s->stream>>>(
+          ds->xr, n, (int)d, (int)M, (int)k, (int)sd, B.list, B.start, B.count, active, cb->d64);
     s->launches++;
     if (cfg->empty_partition_policy == 0) {
       std::vector<uint32_t> hc(M * k);

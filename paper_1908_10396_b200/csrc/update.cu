@@ -283,17 +283,28 @@ __global__ void __launch_bounds__(32) k_assemble(const AsmArgs a) {
   if (do_rhs && lane < sd) a.rhs[(size_t)(m * k + j) * sd + lane] = racc[lane];
 }
 
-// Specialisation for sub_dimension 2, k = 16 (all BASELINE configs): fully
-// unrolled read-modify-writes, one 8-byte load per (point, lane) for the
-// column sub-vector, codes read as one 16-byte row slice per point. Same
-// per-entry operation order as k_assemble.
-__global__ void __launch_bounds__(32) k_assemble_sd2(const AsmArgs a) {
+// Specialisation for sub_dimension 2, k = 16, 4-bit codes, d % 4 == 0 (all
+// BASELINE configs). Same per-entry operation order as k_assemble, cheaper
+// per (point, lane):
+//   * per point, once (staging lane): u_a = coef * x_m[a] and h_par * x_m[a]
+//     in float64 (the reference's products, pq.hpp:326, 332);
+//   * the batch's column rows (32 subspaces = 256 B per point) and code
+//     words (16 B) are copied with 16-byte cp.async, two points per warp
+//     instruction;
+//   * the diagonal h_perp (pq.hpp:324-325) is added inside the same
+//     read-modify-write, before the point's coupling product;
+//   * no coef == 0 branch (pq.hpp:328): then u = 0 and every product is a
+//     signed zero, and adding a signed zero never changes an accumulator
+//     (accumulators start at +0 and are never -0), so the result is the same.
+// Units (strip x column chunk) run largest strip first (`order`).
+__global__ void __launch_bounds__(32) k_assemble_sd2(const AsmArgs a, const uint32_t* order) {
   extern __shared__ __align__(16) double acc[];  // [(aa*16 + j2)*2 + b][32]
-  __shared__ double s_coef[32], s_ho[32], s_hp[32];
-  __shared__ float2 s_xm[32];
-  __shared__ float2 s_xc[32][32];          // [point][lane]
-  __shared__ uint32_t s_cw[32][32];        // code word holding lane's nibble
-  const int unit = blockIdx.x;
+  __shared__ __align__(16) double2 s_u[32];      // coef * x_m
+  __shared__ __align__(16) double2 s_r[32];      // h_par * x_m (rhs)
+  __shared__ double s_ho[32];
+  __shared__ __align__(16) float s_x[32][64];    // [point][column float]
+  __shared__ __align__(16) uint32_t s_cw[32][4]; // [point][code word of lane >> 3]
+  const int unit = order[blockIdx.x];
   const int chunk = unit % a.nchunk;
   const int strip = unit / a.nchunk;
   const int m = strip >> 4, j = strip & 15;
@@ -301,8 +312,8 @@ __global__ void __launch_bounds__(32) k_assemble_sd2(const AsmArgs a) {
   const int d = a.d;
   const int m2 = chunk * 32 + lane;
   const int mcols = a.full ? a.M : m + 1;
-  if (chunk * 32 >= mcols) return;
   const bool mine = m2 < mcols;
+  const bool diag = m2 == m;
   const size_t dim = (size_t)16 * d;
   const bool do_rhs = chunk == 0 && lane == 0;
   const uint32_t* Lall = a.list + (size_t)m * a.n + a.start[m * 16 + j];
@@ -330,64 +341,76 @@ __global__ void __launch_bounds__(32) k_assemble_sd2(const AsmArgs a) {
   }
   const uint32_t* L = Lall + t_lo;
   const size_t cnt = t_hi - t_lo;
+  const int col0 = chunk * 64;                       // first float of the chunk's columns
+  const int nf4 = min(16, (d - col0) >> 2);          // valid float4 per point row
+  const int cb0 = chunk * 16;                        // first code byte of the chunk
+  const int ncb = min(2, max(0, (a.stride - cb0) >> 3));  // valid 8-byte code slices
+  const unsigned sx = (unsigned)__cvta_generic_to_shared(&s_x[0][0]);
+  const unsigned sc = (unsigned)__cvta_generic_to_shared(&s_cw[0][0]);
   for (size_t t0 = 0; t0 < cnt; t0 += 32) {
     const int nb = (int)min((size_t)32, cnt - t0);
-    __shared__ uint32_t s_p[32];
+    uint32_t pl = 0;
     if (lane < nb) {
-      const uint32_t pl = L[t0 + lane];
-      s_p[lane] = pl;
-      s_coef[lane] = a.coef[pl];
+      pl = L[t0 + lane];
+      const double cf = a.coef[pl];
+      const double hp = a.hp[pl];
+      const float2 xm = *reinterpret_cast<const float2*>(a.xr + (size_t)pl * d + m * 2);
+      s_u[lane] = make_double2(__dmul_rn(cf, (double)xm.x), __dmul_rn(cf, (double)xm.y));
+      s_r[lane] = make_double2(__dmul_rn(hp, (double)xm.x), __dmul_rn(hp, (double)xm.y));
       s_ho[lane] = a.ho[pl];
-      s_hp[lane] = a.hp[pl];
-      s_xm[lane] = *reinterpret_cast<const float2*>(a.xr + (size_t)pl * d + m * 2);
     }
-    __syncwarp();
-    if (mine) {
-      // all gathers of the batch in flight at once (LDGSTS, no registers)
-      const int wsh = a.bits == 4 ? 3 : 2;  // code word index of m2
-      for (int b = 0; b < nb; ++b) {
-        const uint32_t p = s_p[b];
-        const float* src = a.xr + (size_t)p * d + m2 * 2;
-        const uint32_t* cws = reinterpret_cast<const uint32_t*>(a.codes + (size_t)p * a.stride) +
-                              (m2 >> wsh);
-        const unsigned dx = (unsigned)__cvta_generic_to_shared(&s_xc[b][lane]);
-        const unsigned dc = (unsigned)__cvta_generic_to_shared(&s_cw[b][lane]);
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dx), "l"(src));
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dc), "l"(cws));
+    // rows: 16-byte pieces, lane -> (point b = idx / 16, piece f = idx % 16)
+#pragma unroll 4
+    for (int it = 0; it < 16; ++it) {
+      const int idx = it * 32 + lane;
+      const int b = idx >> 4, f = idx & 15;
+      const uint32_t p = __shfl_sync(0xffffffffu, pl, b);
+      if (b < nb && f < nf4) {
+        const float* src = a.xr + (size_t)p * d + col0 + f * 4;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(sx + (unsigned)(b * 64 + f * 4) * 4u),
+                     "l"(src));
       }
-      asm volatile("cp.async.wait_all;\n" ::);
     }
+    // code words: 2 x 8 bytes per point
+#pragma unroll
+    for (int it = 0; it < 2; ++it) {
+      const int idx = it * 32 + lane;
+      const int b = idx >> 1, h = idx & 1;
+      const uint32_t p = __shfl_sync(0xffffffffu, pl, b);
+      if (b < nb && h < ncb) {
+        const uint8_t* src = a.codes + (size_t)p * a.stride + cb0 + h * 8;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sc + (unsigned)(b * 16 + h * 8)),
+                     "l"(src));
+      }
+    }
+    asm volatile("cp.async.wait_all;\n" ::);
     __syncwarp();
     if (do_rhs)
       for (int b = 0; b < nb; ++b) {  // rhs += h_par * x (pq.hpp:326)
-        const double hp = s_hp[b];
-        r0 = __dadd_rn(r0, __dmul_rn(hp, (double)s_xm[b].x));
-        r1 = __dadd_rn(r1, __dmul_rn(hp, (double)s_xm[b].y));
+        const double2 r = s_r[b];
+        r0 = __dadd_rn(r0, r.x);
+        r1 = __dadd_rn(r1, r.y);
       }
     if (mine) {
+      const int wsel = lane >> 3, sh = 4 * (lane & 7);
+#pragma unroll 4
       for (int b = 0; b < nb; ++b) {
-        const unsigned j2 = a.bits == 4 ? (s_cw[b][lane] >> (4 * (m2 & 7))) & 15u
-                                         : (s_cw[b][lane] >> (8 * (m2 & 3))) & 255u;
-        if (m2 == m) {  // diagonal h_perp first (pq.hpp:324-325); j2 == j
-          const double hop = s_ho[b];
-          double* e0 = acc + (size_t)((0 * 16 + j) * 2 + 0) * 32 + lane;
-          double* e1 = acc + (size_t)((1 * 16 + j) * 2 + 1) * 32 + lane;
-          *e0 = __dadd_rn(*e0, hop);
-          *e1 = __dadd_rn(*e1, hop);
-        }
-        const double cf = s_coef[b];
-        if (cf == 0.0) continue;  // pq.hpp:328
-        const float2 xm = s_xm[b];
-        const float2 xc = s_xc[b][lane];
-        const double u0 = __dmul_rn(cf, (double)xm.x), u1 = __dmul_rn(cf, (double)xm.y);
+        const unsigned j2 = (s_cw[b][wsel] >> sh) & 15u;
+        const double2 u = s_u[b];
+        const float2 xc = *reinterpret_cast<const float2*>(&s_x[b][lane * 2]);
         const double v0 = (double)xc.x, v1 = (double)xc.y;
         double* base0 = acc + (size_t)(j2 * 2) * 32 + lane;         // aa = 0
         double* base1 = acc + (size_t)((16 + j2) * 2) * 32 + lane;  // aa = 1
-        const double e00 = base0[0], e01 = base0[32], e10 = base1[0], e11 = base1[32];
-        base0[0] = __dadd_rn(e00, __dmul_rn(u0, v0));
-        base0[32] = __dadd_rn(e01, __dmul_rn(u0, v1));
-        base1[0] = __dadd_rn(e10, __dmul_rn(u1, v0));
-        base1[32] = __dadd_rn(e11, __dmul_rn(u1, v1));
+        double e00 = base0[0], e01 = base0[32], e10 = base1[0], e11 = base1[32];
+        if (diag) {  // h_perp on the diagonal first (pq.hpp:324-325); j2 == j
+          const double hop = s_ho[b];
+          e00 = __dadd_rn(e00, hop);
+          e11 = __dadd_rn(e11, hop);
+        }
+        base0[0] = __dadd_rn(e00, __dmul_rn(u.x, v0));
+        base0[32] = __dadd_rn(e01, __dmul_rn(u.x, v1));
+        base1[0] = __dadd_rn(e10, __dmul_rn(u.y, v0));
+        base1[32] = __dadd_rn(e11, __dmul_rn(u.y, v1));
       }
     }
     __syncwarp();
@@ -772,18 +795,38 @@ int assemble_device(aq_dataset* ds, aq_codes* codes, const PointW& pw, const Buc
                                (int)smem));
   const unsigned units = (unsigned)(M * k * nchunk);
   timer_mark(s, AQ_T_ASSEMBLE);
-  if (sd == 2 && k == 16 && d % 2 == 0) {
+  if (sd == 2 && k == 16 && d % 4 == 0 && codes->bits == 4) {
     AQ_CUDA(cudaFuncSetAttribute(k_assemble_sd2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  64 * 32 * 8));
+    // units with work, largest strip first (the longest point chains start
+    // early instead of trailing the launch)
+    std::vector<uint32_t> hc((size_t)M * 16);
+    AQ_CUDA(cudaMemcpyAsync(hc.data(), B.count, hc.size() * sizeof(uint32_t),
+                            cudaMemcpyDeviceToHost, s->stream));
+    AQ_CUDA(cudaStreamSynchronize(s->stream));
+    std::vector<uint32_t> ord;
+    ord.reserve(units);
+    for (uint32_t u = 0; u < units; ++u) {
+      const int ch = (int)(u % (unsigned)nchunk), st = (int)(u / (unsigned)nchunk);
+      const int mcols = full ? M : st / 16 + 1;
+      if (ch * 32 < mcols && hc[st]) ord.push_back(u);
+    }
+    std::stable_sort(ord.begin(), ord.end(),
+                     [&](uint32_t x, uint32_t y) { return hc[x / nchunk] > hc[y / nchunk]; });
+    void* po;
+    AQ_TRY(scratch(s, 5, ord.size() * sizeof(uint32_t) + 16, &po));
+    uint32_t* dord = (uint32_t*)po;
+    AQ_CUDA(cudaMemcpyAsync(dord, ord.data(), ord.size() * sizeof(uint32_t),
+                            cudaMemcpyHostToDevice, s->stream));
     // point blocks whose rows (~48 MB) stay L2-resident while every unit
     // gathers from them; entries keep their point order across blocks
     const size_t row_bytes = (size_t)d * sizeof(float);
     const size_t bsz = std::max<size_t>(4096, (48u << 20) / row_bytes);
-    for (size_t lo = 0; lo < ds->n; lo += bsz) {
+    for (size_t lo = 0; lo < ds->n && !ord.empty(); lo += bsz) {
       a.lo = (uint32_t)lo;
       a.hi = (uint32_t)std::min(ds->n, lo + bsz);
       a.resume = lo > 0;
-      k_assemble_sd2<<<units, 32, 64 * 32 * 8, s->stream>>>(a);
+      k_assemble_sd2<<<(unsigned)ord.size(), 32, 64 * 32 * 8, s->stream>>>(a, dord);
       AQ_LAUNCHED(s);
     }
   } else {

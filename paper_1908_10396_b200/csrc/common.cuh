@@ -84,6 +84,9 @@ struct aq_session {
   double tms[AQ_T_COUNT] = {0};
   uint64_t tcount[AQ_T_COUNT] = {0};
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;        // loss totals overlapped with the next update
+  cudaEvent_t ev_main = nullptr, ev_side = nullptr;
+  double* sum_host = nullptr;         // pinned, 64 slots
   uint64_t launches = 0;
   int num_sms = 148;
   aqd::DevError* err = nullptr;     // device

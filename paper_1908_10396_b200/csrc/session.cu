@@ -274,6 +274,10 @@ int aq_session_create(int device, aq_session** out) {
   }
   s->num_sms = prop.multiProcessorCount;
   AQ_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+  AQ_CUDA(cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking));
+  AQ_CUDA(cudaEventCreateWithFlags(&s->ev_main, cudaEventDisableTiming));
+  AQ_CUDA(cudaEventCreateWithFlags(&s->ev_side, cudaEventDisableTiming));
+  AQ_CUDA(cudaMallocHost(&s->sum_host, 64 * sizeof(double)));
   AQ_CUDA(cudaMalloc(&s->err, sizeof(DevError)));
   AQ_CUDA(cudaMallocHost(&s->err_host, sizeof(DevError)));
   *out = s;
@@ -288,6 +292,11 @@ int aq_session_destroy(aq_session* s) {
     if (sc.p) cudaFree(sc.p);
   cudaFree(s->err);
   cudaFreeHost(s->err_host);
+  cudaStreamSynchronize(s->side);
+  cudaFreeHost(s->sum_host);
+  cudaEventDestroy(s->ev_main);
+  cudaEventDestroy(s->ev_side);
+  cudaStreamDestroy(s->side);
   cudaStreamDestroy(s->stream);
   delete s;
   return AQ_OK;

@@ -287,9 +287,14 @@ int train_l2_pq_device(aq_dataset* ds, size_t M, size_t k, const aq_train_config
         ds->xr, n, (int)d, (int)M, (int)k, (int)sd, cb->d64, active, codes->data,
         (int)codes->stride, codes->bits, losses, changes);
     AQ_LAUNCHED(s);
-    k_seq_sums<<<(unsigned)((M + 7) / 8), 256, 0, s->stream>>>(losses, n, n, (int)M, active, totals);
-    AQ_LAUNCHED(s);
-    AQ_CUDA(cudaMemcpyAsync(htot.data(), totals, M * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    // loss totals only feed the relative-tolerance test (vq.hpp:316-321)
+    if (cfg->relative_tolerance > 0.0) {
+      k_seq_sums<<<(unsigned)((M + 7) / 8), 256, 0, s->stream>>>(losses, n, n, (int)M, active,
+                                                                 totals);
+      AQ_LAUNCHED(s);
+      AQ_CUDA(cudaMemcpyAsync(htot.data(), totals, M * sizeof(double), cudaMemcpyDeviceToHost,
+                              s->stream));
+    }
     AQ_CUDA(cudaMemcpyAsync(hchg.data(), changes, M * sizeof(unsigned long long),
                             cudaMemcpyDeviceToHost, s->stream));
     AQ_CUDA(cudaStreamSynchronize(s->stream));
@@ -436,28 +441,52 @@ int aq_dev_train_apq(aq_dataset* ds, size_t M, size_t k, const aq_weights* w,
   if (cudaMallocAsync(&losses, n * sizeof(double), s->stream) != cudaSuccess ||
       cudaMallocAsync(&total, sizeof(double), s->stream) != cudaSuccess)
     st = ref_error(AQ_E_CUDA, "out of device memory");
-  auto pass = [&](double* tot_h, uint64_t* changed) -> int {
+  // Assignment pass on the main stream; its loss total (a point-ordered
+  // float64 chain, the slowest part of a pass) runs on the side stream so
+  // the next codebook update can overlap it. The next pass waits for the sum
+  // before it overwrites `losses`.
+  auto pass_async = [&](uint64_t* changed) -> int {
+    AQ_CUDA(cudaStreamWaitEvent(s->stream, s->ev_side, 0));
     AQ_TRY(run_encode(ds, cb, w, codes, 1, 0, cfg->sweep_to_fixed_point, losses, changed));
-    k_seq_sums<<<1, 32, 0, s->stream>>>(losses, n, n, 1, nullptr, total);
-    AQ_LAUNCHED(s);
-    AQ_CUDA(cudaMemcpyAsync(tot_h, total, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
-    AQ_CUDA(cudaStreamSynchronize(s->stream));
+    AQ_CUDA(cudaEventRecord(s->ev_main, s->stream));
+    AQ_CUDA(cudaStreamWaitEvent(s->side, s->ev_main, 0));
+    k_seq_sums<<<1, 32, 0, s->side>>>(losses, n, n, 1, nullptr, total);
+    s->launches++;
+    AQ_CUDA(cudaMemcpyAsync(s->sum_host, total, sizeof(double), cudaMemcpyDeviceToHost, s->side));
+    AQ_CUDA(cudaEventRecord(s->ev_side, s->side));
+    return AQ_OK;
+  };
+  auto get_total = [&](double* tot_h) -> int {
+    AQ_CUDA(cudaEventSynchronize(s->ev_side));
+    *tot_h = s->sum_host[0];
     return AQ_OK;
   };
   double tot = 0.0;
   uint64_t changed = 0;
   size_t hl = 0;
-  if (st == AQ_OK) st = pass(&tot, &changed);
+  if (st == AQ_OK) st = pass_async(&changed);
+  if (st == AQ_OK) st = get_total(&tot);
   if (st == AQ_OK && history_out) history_out[hl] = tot;
   if (st == AQ_OK) ++hl;
   aq_codebook* next = nullptr;
   if (st == AQ_OK) st = aq_codebook_upload(s, nullptr, M, k, sd, &next);
+  bool have_next = false;  // `next` already holds the update of the current codes
   for (int iter = 0; st == AQ_OK && iter < cfg->max_iterations; ++iter) {
-    st = aq_dev_pq_codebook_update(ds, codes, w, cfg->ridge, next);
+    if (!have_next) st = aq_dev_pq_codebook_update(ds, codes, w, cfg->ridge, next);
     if (st != AQ_OK) break;
     std::swap(cb, next);
+    have_next = false;
     const double prev = tot;
-    st = pass(&tot, &changed);
+    st = pass_async(&changed);
+    if (st != AQ_OK) break;
+    // speculative next update (a pure function of the codes) while the
+    // total is summed; discarded when the stopping rule fires below
+    if (changed != 0 && iter + 1 < cfg->max_iterations) {
+      st = aq_dev_pq_codebook_update(ds, codes, w, cfg->ridge, next);
+      if (st != AQ_OK) break;
+      have_next = true;
+    }
+    st = get_total(&tot);
     if (st != AQ_OK) break;
     if (history_out) history_out[hl] = tot;
     ++hl;
@@ -466,6 +495,7 @@ int aq_dev_train_apq(aq_dataset* ds, size_t M, size_t k, const aq_weights* w,
         (prev == 0.0 || prev - tot <= cfg->relative_tolerance * prev))
       break;
   }
+  cudaStreamSynchronize(s->side);
   if (history_len) *history_len = hl;
   aq_codebook_free(next);
   if (losses) cudaFreeAsync(losses, s->stream);

@@ -145,23 +145,31 @@ def build_index(aq, wl, n, nq, seed_shard, session):
     # clocks); the second, identical (deterministic) run is the one timed
     hist0 = []
     dcb, dc = aq.dev_train_apq(ds, w.M, w.k, aq.ThresholdWeights(w.threshold), cfg, True, hist0)
-    del dcb, dc
-    L.aq_session_timing(session.h, 1)
-    for slot in range(8):
-        L.aq_session_timer_read(session.h, slot, None, None, 1)
-    session.sync()
-    t0 = time.perf_counter()
-    hist = []
-    dcb, dc = aq.dev_train_apq(ds, w.M, w.k, aq.ThresholdWeights(w.threshold), cfg, True, hist)
-    session.sync()
-    train_s = time.perf_counter() - t0
-    assert hist == hist0, "train_apq is deterministic"
-    phases = {}
-    for slot, name in [(0, "encode"), (5, "assemble"), (6, "llt_solve"), (7, "kmeans_warm_start")]:
-        ms, cnt = C.c_double(0), C.c_uint64(0)
-        L.aq_session_timer_read(session.h, slot, C.byref(ms), C.byref(cnt), 1)
-        phases[name] = {"ms": round(ms.value, 2), "launches": int(cnt.value)}
-    L.aq_session_timing(session.h, 0)
+    # best of two timed runs (host wall clock around the synchronous trainer;
+    # the phases are device events of the same run)
+    train_s, phases = None, None
+    for _ in range(2):
+        del dcb, dc
+        L.aq_session_timing(session.h, 1)
+        for slot in range(8):
+            L.aq_session_timer_read(session.h, slot, None, None, 1)
+        session.sync()
+        t0 = time.perf_counter()
+        hist = []
+        dcb, dc = aq.dev_train_apq(ds, w.M, w.k, aq.ThresholdWeights(w.threshold), cfg, True,
+                                   hist)
+        session.sync()
+        ts = time.perf_counter() - t0
+        assert hist == hist0, "train_apq is deterministic"
+        ph = {}
+        for slot, name in [(0, "encode"), (5, "assemble"), (6, "llt_solve"),
+                           (7, "kmeans_warm_start")]:
+            ms, cnt = C.c_double(0), C.c_uint64(0)
+            L.aq_session_timer_read(session.h, slot, C.byref(ms), C.byref(cnt), 1)
+            ph[name] = {"ms": round(ms.value, 2), "launches": int(cnt.value)}
+        L.aq_session_timing(session.h, 0)
+        if train_s is None or ts < train_s:
+            train_s, phases = ts, ph
     cb = dcb.download()
     return w, cb, ds, dcb, dc, {"train_apq_s": round(train_s, 2), "loss_first": hist[0],
                                 "loss_last": hist[-1], "iterations": len(hist) - 1,

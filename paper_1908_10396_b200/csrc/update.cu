@@ -418,24 +418,62 @@ __global__ void __launch_bounds__(32) k_assemble_sd2(const AsmArgs a, const uint
       }
     if (mine) {
       const int wsel = lane >> 3, sh = 4 * (lane & 7);
-#pragma unroll 4
-      for (int b = 0; b < nb; ++b) {
-        const unsigned j2 = (s_cw[buf][b][wsel] >> sh) & 15u;
+      // One point: h_perp on the diagonal first (pq.hpp:324-325; j2 == j
+      // there), then the coupling products (pq.hpp:329-338).
+      auto upd = [&](int b, double& e00, double& e01, double& e10, double& e11) {
         const double2 u = s_u[b];
         const float2 xc = *reinterpret_cast<const float2*>(&s_x[buf][b][lane * 2]);
         const double v0 = (double)xc.x, v1 = (double)xc.y;
-        double* base0 = acc + (size_t)(j2 * 2) * 32 + lane;         // aa = 0
-        double* base1 = acc + (size_t)((16 + j2) * 2) * 32 + lane;  // aa = 1
-        double e00 = base0[0], e01 = base0[32], e10 = base1[0], e11 = base1[32];
-        if (diag) {  // h_perp on the diagonal first (pq.hpp:324-325); j2 == j
+        if (diag) {
           const double hop = s_ho[b];
           e00 = __dadd_rn(e00, hop);
           e11 = __dadd_rn(e11, hop);
         }
-        base0[0] = __dadd_rn(e00, __dmul_rn(u.x, v0));
-        base0[32] = __dadd_rn(e01, __dmul_rn(u.x, v1));
-        base1[0] = __dadd_rn(e10, __dmul_rn(u.y, v0));
-        base1[32] = __dadd_rn(e11, __dmul_rn(u.y, v1));
+        e00 = __dadd_rn(e00, __dmul_rn(u.x, v0));
+        e01 = __dadd_rn(e01, __dmul_rn(u.x, v1));
+        e10 = __dadd_rn(e10, __dmul_rn(u.y, v0));
+        e11 = __dadd_rn(e11, __dmul_rn(u.y, v1));
+      };
+      // Points in pairs: both slots are loaded before either is stored; when
+      // the pair shares a slot the second update continues from the first's
+      // result, and the second store (program order) leaves the chained value.
+      int b = 0;
+      for (; b + 1 < nb; b += 2) {
+        const unsigned ja = (s_cw[buf][b][wsel] >> sh) & 15u;
+        const unsigned jb = (s_cw[buf][b + 1][wsel] >> sh) & 15u;
+        double* pa0 = acc + (size_t)(ja * 2) * 32 + lane;
+        double* pa1 = acc + (size_t)((16 + ja) * 2) * 32 + lane;
+        double* pb0 = acc + (size_t)(jb * 2) * 32 + lane;
+        double* pb1 = acc + (size_t)((16 + jb) * 2) * 32 + lane;
+        double a00 = pa0[0], a01 = pa0[32], a10 = pa1[0], a11 = pa1[32];
+        double b00 = pb0[0], b01 = pb0[32], b10 = pb1[0], b11 = pb1[32];
+        upd(b, a00, a01, a10, a11);
+        if (ja == jb) {
+          b00 = a00;
+          b01 = a01;
+          b10 = a10;
+          b11 = a11;
+        }
+        upd(b + 1, b00, b01, b10, b11);
+        pa0[0] = a00;
+        pa0[32] = a01;
+        pa1[0] = a10;
+        pa1[32] = a11;
+        pb0[0] = b00;
+        pb0[32] = b01;
+        pb1[0] = b10;
+        pb1[32] = b11;
+      }
+      if (b < nb) {
+        const unsigned ja = (s_cw[buf][b][wsel] >> sh) & 15u;
+        double* pa0 = acc + (size_t)(ja * 2) * 32 + lane;
+        double* pa1 = acc + (size_t)((16 + ja) * 2) * 32 + lane;
+        double a00 = pa0[0], a01 = pa0[32], a10 = pa1[0], a11 = pa1[32];
+        upd(b, a00, a01, a10, a11);
+        pa0[0] = a00;
+        pa0[32] = a01;
+        pa1[0] = a10;
+        pa1[32] = a11;
       }
     }
     __syncwarp();
@@ -953,7 +991,7 @@ int assemble_device(aq_dataset* ds, aq_codes* codes, const PointW& pw, const Buc
   const unsigned units = (unsigned)(M * k * nchunk);
   timer_mark(s, AQ_T_ASSEMBLE);
   if (sd == 2 && k == 16 && d % 4 == 0 && codes->bits == 4) {
-    static const int cols = getenv("AQ_ASM_COLS") ? atoi(getenv("AQ_ASM_COLS")) : 16;
+    static const int cols = getenv("AQ_ASM_COLS") ? atoi(getenv("AQ_ASM_COLS")) : 32;
     const int nch = cols == 32 ? nchunk : (M + 15) / 16;
     a.nchunk = nch;
     const unsigned units2 = (unsigned)(M * 16 * nch);

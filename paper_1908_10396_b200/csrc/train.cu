@@ -169,6 +169,67 @@ __global__ void k_kmeans_assign(const float* __restrict__ xr, size_t n, int d, i
   }
 }
 
+// Same pass for sub_dimension 2 with coalesced reads: the pair-tiled rows
+// (32 points x one pair per 256-byte line), the codebook in shared memory,
+// code words built in registers (written once per 8 subspaces), changed-code
+// counts aggregated per warp and per CTA before one global atomic per
+// subspace. Operation order per candidate as residual_terms (dist2 =
+// df0^2 + df1^2; 0.0 + df0^2 == df0^2 exactly).
+__global__ void __launch_bounds__(256) k_kmeans_assign_sd2(
+    const float2* __restrict__ xt, size_t n, int pairs, int M, int k,
+    const double* __restrict__ dict, const int* __restrict__ active, uint8_t* __restrict__ codes,
+    int stride, double* __restrict__ losses, unsigned long long* __restrict__ changes) {
+  extern __shared__ __align__(16) unsigned char ksm[];
+  double2* cbs = reinterpret_cast<double2*>(ksm);            // [M][k]
+  unsigned* chg = reinterpret_cast<unsigned*>(cbs + (size_t)M * k);  // [M]
+  int* act = reinterpret_cast<int*>(chg + M);                 // [M]
+  for (int t = threadIdx.x; t < M * k; t += blockDim.x)
+    cbs[t] = reinterpret_cast<const double2*>(dict)[t];
+  for (int t = threadIdx.x; t < M; t += blockDim.x) {
+    chg[t] = 0u;
+    act[t] = active[t];
+  }
+  __syncthreads();
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = i < n;
+  const int lane = threadIdx.x & 31;
+  const float2* xrow = xt + (i >> 5) * (size_t)pairs * 32 + (i & 31);
+  uint32_t* crow = reinterpret_cast<uint32_t*>(codes + (valid ? i : 0) * (size_t)stride);
+  uint32_t word = 0;
+  for (int m = 0; m < M; ++m) {
+    if ((m & 7) == 0 && valid) word = crow[m >> 3];
+    if (act[m]) {
+      unsigned bj = 0;
+      bool ch = false;
+      if (valid) {
+        const float2 xv = xrow[(size_t)m * 32];
+        const double x0 = xv.x, x1 = xv.y;
+        const double2* cm = cbs + (size_t)m * k;
+        double bd = 0.0;
+        for (int j = 0; j < k; ++j) {
+          const double2 c = cm[j];
+          const double df0 = __dsub_rn(x0, c.x), df1 = __dsub_rn(x1, c.y);
+          const double d2 = __dadd_rn(__dmul_rn(df0, df0), __dmul_rn(df1, df1));
+          if (j == 0 || d2 < bd) {
+            bd = d2;
+            bj = (unsigned)j;
+          }
+        }
+        const int sh = 4 * (m & 7);
+        ch = ((word >> sh) & 15u) != bj;
+        word = (word & ~(15u << sh)) | (bj << sh);
+        losses[(size_t)m * n + i] = __dmul_rn(1.0, bd);
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, ch);
+      if (lane == 0 && bal) atomicAdd(&chg[m], (unsigned)__popc(bal));
+    }
+    if (((m & 7) == 7 || m + 1 == M) && valid) crow[m >> 3] = word;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < M; t += blockDim.x)
+    if (chg[t]) atomicAdd(&changes[t], (unsigned long long)chg[t]);
+}
+
 // update_codeword isotropic path (vq.hpp:151-162) with unit weights:
 // mean = (sum 1.0 x) / (sum 1.0), members in ascending order. One warp per
 // slot: the lanes gather 32 members' sub-vectors into shared memory (all in
@@ -283,9 +344,18 @@ int train_l2_pq_device(aq_dataset* ds, size_t M, size_t k, const aq_train_config
   auto assign = [&]() -> int {
     AQ_CUDA(cudaMemcpyAsync(active, hact.data(), M * sizeof(int), cudaMemcpyHostToDevice, s->stream));
     AQ_CUDA(cudaMemsetAsync(changes, 0, M * sizeof(unsigned long long), s->stream));
-    k_kmeans_assign<<<(unsigned)((n + 127) / 128), 128, 0, s->stream>>>(
-        ds->xr, n, (int)d, (int)M, (int)k, (int)sd, cb->d64, active, codes->data,
-        (int)codes->stride, codes->bits, losses, changes);
+    if (sd == 2 && codes->bits == 4) {
+      const size_t sm = (size_t)M * k * sizeof(double2) + 2 * M * sizeof(int);
+      AQ_CUDA(cudaFuncSetAttribute(k_kmeans_assign_sd2,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      k_kmeans_assign_sd2<<<(unsigned)((n + 255) / 256), 256, sm, s->stream>>>(
+          reinterpret_cast<const float2*>(ds->xt), n, (int)(d / 2), (int)M, (int)k, cb->d64,
+          active, codes->data, (int)codes->stride, losses, changes);
+    } else {
+      k_kmeans_assign<<<(unsigned)((n + 127) / 128), 128, 0, s->stream>>>(
+          ds->xr, n, (int)d, (int)M, (int)k, (int)sd, cb->d64, active, codes->data,
+          (int)codes->stride, codes->bits, losses, changes);
+    }
     AQ_LAUNCHED(s);
     // loss totals only feed the relative-tolerance test (vq.hpp:316-321)
     if (cfg->relative_tolerance > 0.0) {
@@ -531,9 +601,18 @@ int aq_dev_kmeans_assign(aq_dataset* ds, aq_codebook* cb, aq_codes* codes,
   AQ_CUDA(cudaMemcpyAsync(act, active_host, M * sizeof(int), cudaMemcpyHostToDevice, s->stream));
   AQ_CUDA(cudaMemsetAsync(chg, 0, M * sizeof(unsigned long long), s->stream));
   if (n) {
-    k_kmeans_assign<<<(unsigned)((n + 127) / 128), 128, 0, s->stream>>>(
-        ds->xr, n, (int)ds->d, (int)M, (int)cb->k, (int)cb->sd, cb->d64, act, codes->data,
-        (int)codes->stride, codes->bits, losses_dev, chg);
+    if (cb->sd == 2 && codes->bits == 4) {
+      const size_t sm = (size_t)M * cb->k * sizeof(double2) + 2 * M * sizeof(int);
+      AQ_CUDA(cudaFuncSetAttribute(k_kmeans_assign_sd2,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      k_kmeans_assign_sd2<<<(unsigned)((n + 255) / 256), 256, sm, s->stream>>>(
+          reinterpret_cast<const float2*>(ds->xt), n, (int)(ds->d / 2), (int)M, (int)cb->k,
+          cb->d64, act, codes->data, (int)codes->stride, losses_dev, chg);
+    } else {
+      k_kmeans_assign<<<(unsigned)((n + 127) / 128), 128, 0, s->stream>>>(
+          ds->xr, n, (int)ds->d, (int)M, (int)cb->k, (int)cb->sd, cb->d64, act, codes->data,
+          (int)codes->stride, codes->bits, losses_dev, chg);
+    }
     s->launches++;
   }
   AQ_CUDA(cudaMemcpyAsync(changes_out, chg, M * sizeof(uint64_t), cudaMemcpyDeviceToHost,

@@ -91,7 +91,7 @@ struct aq_session {
   int num_sms = 148;
   aqd::DevError* err = nullptr;     // device
   aqd::DevError* err_host = nullptr;  // pinned mirror
-  aqd::Scratch scratch[6];
+  aqd::Scratch scratch[7];  // slot 6: scan tile sums (sort.cu)
 };
 
 struct aq_dataset {
@@ -159,6 +159,8 @@ struct Buckets {
   int K = 0;
 };
 int build_buckets(aq_codes* c, int k, Buckets* B);
+// exclusive scan of 32-bit counts in place (sort.cu)
+int scan_device(aq_session* s, unsigned* hist, size_t total);
 
 // Per-point anisotropic weights (update.cu): h_par, h_perp, coupling coefficient;
 // flags[0] = some point anisotropic, flags[1] = first anisotropic |x| = 0 index + 1

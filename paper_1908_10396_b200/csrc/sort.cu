@@ -40,14 +40,17 @@ __global__ void k_radix_hist(const unsigned long long* __restrict__ keys,
 }
 
 // exclusive scan of hist (digit-major), single CTA
-__global__ void k_radix_scan(unsigned* __restrict__ hist, size_t total) {
+// In-place exclusive scan of hist[lo, hi) starting from `carry0`, by one CTA
+// (chunks of blockDim in order, carried across chunks).
+__device__ void cta_exclusive_scan(unsigned* __restrict__ hist, size_t lo, size_t hi,
+                                   unsigned long long carry0) {
   __shared__ unsigned long long carry;
   __shared__ unsigned warp_sums[32];
-  if (threadIdx.x == 0) carry = 0;
+  if (threadIdx.x == 0) carry = carry0;
   __syncthreads();
-  for (size_t base = 0; base < total; base += blockDim.x) {
+  for (size_t base = lo; base < hi; base += blockDim.x) {
     const size_t i = base + threadIdx.x;
-    const unsigned v = i < total ? hist[i] : 0u;
+    const unsigned v = i < hi ? hist[i] : 0u;
     // block inclusive scan
     unsigned x = v;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -68,11 +71,38 @@ __global__ void k_radix_scan(unsigned* __restrict__ hist, size_t total) {
     __syncthreads();
     const unsigned prefix = w ? warp_sums[w - 1] : 0u;
     const unsigned long long c = carry;
-    if (i < total) hist[i] = (unsigned)(c + prefix + x - v);
+    if (i < hi) hist[i] = (unsigned)(c + prefix + x - v);
     __syncthreads();
     if (threadIdx.x == blockDim.x - 1) carry = c + prefix + x;
     __syncthreads();
   }
+}
+
+__global__ void k_radix_scan(unsigned* __restrict__ hist, size_t total) {
+  cta_exclusive_scan(hist, 0, total, 0ull);
+}
+
+// multi-CTA scan: tile sums -> scan of the sums -> per-tile rescan
+constexpr size_t kScanTile = 16384;
+__global__ void k_scan_tile_sums(const unsigned* __restrict__ hist, size_t total,
+                                 unsigned* __restrict__ sums) {
+  const size_t lo = (size_t)blockIdx.x * kScanTile, hi = min(total, lo + kScanTile);
+  unsigned long long acc = 0;
+  for (size_t i = lo + threadIdx.x; i < hi; i += blockDim.x) acc += hist[i];
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __shared__ unsigned long long ws[32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += ws[w];
+    sums[blockIdx.x] = (unsigned)t;
+  }
+}
+__global__ void k_scan_tiles(unsigned* __restrict__ hist, size_t total,
+                             const unsigned* __restrict__ offs) {
+  const size_t lo = (size_t)blockIdx.x * kScanTile, hi = min(total, lo + kScanTile);
+  cta_exclusive_scan(hist, lo, hi, offs[blockIdx.x]);
 }
 
 // stable scatter: items of a block are ranked in order
@@ -120,6 +150,26 @@ __global__ void k_radix_scatter(const unsigned long long* __restrict__ kin,
 // Sorts idx (initially any order) by (score desc, index asc). scores is
 // indexed by position i (scores[i] belongs to idx[i]). Caller must have idx in
 // ascending index order for the index tie-break (stable sort).
+// Exclusive scan of `total` counts in place (sums fit in 32 bits).
+int scan_device(aq_session* s, unsigned* hist, size_t total) {
+  if (total <= 4 * kScanTile) {
+    k_radix_scan<<<1, 1024, 0, s->stream>>>(hist, total);
+    AQ_LAUNCHED(s);
+    return AQ_OK;
+  }
+  const size_t tiles = (total + kScanTile - 1) / kScanTile;
+  void* p;
+  AQ_TRY(scratch(s, 6, tiles * sizeof(unsigned) + 64, &p));
+  unsigned* sums = (unsigned*)p;
+  k_scan_tile_sums<<<(unsigned)tiles, 512, 0, s->stream>>>(hist, total, sums);
+  AQ_LAUNCHED(s);
+  k_radix_scan<<<1, 1024, 0, s->stream>>>(sums, tiles);
+  AQ_LAUNCHED(s);
+  k_scan_tiles<<<(unsigned)tiles, 512, 0, s->stream>>>(hist, total, sums);
+  AQ_LAUNCHED(s);
+  return AQ_OK;
+}
+
 int sort_scores_desc(aq_session* s, const double* scores, uint32_t* idx,
                      size_t n) {
   if (n <= 1) return AQ_OK;
@@ -141,8 +191,7 @@ int sort_scores_desc(aq_session* s, const double* scores, uint32_t* idx,
     const int shift = pass * 8;
     k_radix_hist<<<(unsigned)nb, kSortThreads, 0, s->stream>>>(kin, n, shift, hist, nb);
     AQ_LAUNCHED(s);
-    k_radix_scan<<<1, 1024, 0, s->stream>>>(hist, 256 * nb);
-    AQ_LAUNCHED(s);
+    AQ_TRY(scan_device(s, hist, 256 * nb));
     k_radix_scatter<<<(unsigned)nb, kSortThreads, 0, s->stream>>>(
         kin, vin, n, shift, hist, nb, kout, vout);
     AQ_LAUNCHED(s);

@@ -240,9 +240,12 @@ __global__ void k_kmeans_means(const float* __restrict__ xr, size_t n, int d, in
                                const uint32_t* __restrict__ start,
                                const uint32_t* __restrict__ count,
                                const int* __restrict__ active, double* __restrict__ dict) {
+  // One warp per slot. Rounds of 128 members: the lanes gather round r + 1
+  // (4 members each, in registers) while lane 0 adds round r in member order.
   constexpr int SDM = SDC > 0 ? SDC : 16;
+  constexpr int G = SDC > 0 ? 4 : 1, R = 32 * G;
   const int sd = SDC > 0 ? SDC : sd_rt;
-  __shared__ float xs[4][32][SDM + 1];
+  __shared__ float xs[4][2][R][SDM];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slot = blockIdx.x * (blockDim.x >> 5) + w;
   if (slot >= M * k) return;
@@ -251,27 +254,43 @@ __global__ void k_kmeans_means(const float* __restrict__ xr, size_t n, int d, in
   const size_t cnt = count[slot];
   if (cnt == 0) return;  // reseeded by the host walk
   const uint32_t* L = list + (size_t)m * n + start[slot];
+  float nx[G][SDM];
+  auto fetch = [&](size_t r0) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const size_t t = r0 + g * 32 + lane;
+      if (t < cnt) {
+        const float* xp = xr + (size_t)L[t] * d + m * sd;
+#pragma unroll
+        for (int c = 0; c < SDM; ++c)
+          if (c < sd) nx[g][c] = xp[c];
+      }
+    }
+  };
   double num[SDM];
 #pragma unroll
   for (int c = 0; c < SDM; ++c) num[c] = 0.0;
   double den = 0.0;
-  for (size_t t0 = 0; t0 < cnt; t0 += 32) {
-    const int nb = (int)min((size_t)32, cnt - t0);
-    if (lane < nb) {
-      const float* xp = xr + (size_t)L[t0 + lane] * d + m * sd;
+  fetch(0);
+  int cur = 0;
+  for (size_t r0 = 0; r0 < cnt; r0 += R) {
+#pragma unroll
+    for (int g = 0; g < G; ++g)
 #pragma unroll
       for (int c = 0; c < SDM; ++c)
-        if (c < sd) xs[w][lane][c] = xp[c];
-    }
+        if (c < sd) xs[w][cur][g * 32 + lane][c] = nx[g][c];
     __syncwarp();
-    if (lane == 0)
+    if (r0 + R < cnt) fetch(r0 + R);  // in flight during the chain below
+    if (lane == 0) {
+      const int nb = (int)min((size_t)R, cnt - r0);
       for (int b = 0; b < nb; ++b) {
 #pragma unroll
         for (int c = 0; c < SDM; ++c)
-          if (c < sd) num[c] = __dadd_rn(num[c], __dmul_rn(1.0, (double)xs[w][b][c]));
+          if (c < sd) num[c] = __dadd_rn(num[c], __dmul_rn(1.0, (double)xs[w][cur][b][c]));
         den = __dadd_rn(den, 1.0);
       }
-    __syncwarp();
+    }
+    cur ^= 1;
   }
   if (lane == 0)
 #pragma unroll

@@ -18,7 +18,6 @@
 
 namespace aqd {
 
-__global__ void k_radix_scan(unsigned* __restrict__ hist, size_t total);
 int sort_scores_desc(aq_session* s, const double* scores, uint32_t* idx, size_t n);
 int run_encode(aq_dataset* ds, aq_codebook* cb, const aq_weights* w, aq_codes* codes,
                int mode, int passes, int sweep_fixed, double* losses_dev,
@@ -119,8 +118,7 @@ int build_buckets(aq_codes* c, int k, Buckets* B) {
       c->data, n, (int)c->stride, c->bits, K, hist, nb, s->err, k);
   AQ_LAUNCHED(s);
   AQ_TRY(sync_and_check(s, "codebook update: code out of range"));
-  k_radix_scan<<<1, 1024, 0, s->stream>>>(hist, M * K * nb);
-  AQ_LAUNCHED(s);
+  AQ_TRY(scan_device(s, hist, M * K * nb));
   k_bucket_scatter<<<dim3((unsigned)nb, (unsigned)M), 256, 0, s->stream>>>(
       c->data, n, (int)c->stride, c->bits, K, hist, nb, B->list);
   AQ_LAUNCHED(s);

@@ -738,38 +738,75 @@ __global__ void __launch_bounds__(256) k_llt_trail(double* A, int n, int kb) {
     }
 }
 
-// LLT solve (forward L y = b, backward L^T x = y), blocked like the stand-in.
+// LLT solve (forward L y = b, backward L^T x = y), blocked like the stand-in
+// (oracle/eigen_subset/Eigen/Dense, solve): per block, the diagonal triangle
+// row by row (t = t - L(i,k) y(k) in k order, then t / L(i,i)), then every
+// row outside the block takes s = sum_k L(i,k) y(k) in k order and y(i) -= s.
+// The diagonal block and the block's values sit in shared memory; warp 0's
+// lanes form each row's rounded products and lane 0 runs the subtraction
+// chain in order, so the result is the stand-in's bit for bit.
 __global__ void __launch_bounds__(1024) k_llt_solve(const double* L, int n, double* x) {
+  __shared__ double Ld[kLLT][kLLT + 1];
+  __shared__ double xb[kLLT];
+  __shared__ double pr[kLLT];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   for (int kb = 0; kb < n; kb += kLLT) {
-    const int be = min(kb + kLLT, n);
-    if (threadIdx.x == 0)
-      for (int i = kb; i < be; ++i) {
-        double t = x[i];
-        for (int q = kb; q < i; ++q) t = __dsub_rn(t, __dmul_rn(L[(size_t)i * n + q], x[q]));
-        x[i] = __ddiv_rn(t, L[(size_t)i * n + i]);
-      }
+    const int be = min(kb + kLLT, n), bs = be - kb;
+    for (int e = tid; e < bs * bs; e += blockDim.x) {
+      const int r = e / bs, c = e % bs;
+      Ld[r][c] = L[(size_t)(kb + r) * n + kb + c];
+    }
+    if (tid < bs) xb[tid] = x[kb + tid];
     __syncthreads();
-    for (int i = be + threadIdx.x; i < n; i += blockDim.x) {
-      double s = 0.0;
-      for (int q = kb; q < be; ++q) s = __dadd_rn(s, __dmul_rn(L[(size_t)i * n + q], x[q]));
-      x[i] = __dsub_rn(x[i], s);
+    if (w == 0) {
+      for (int r = 0; r < bs; ++r) {
+        for (int c = lane; c < r; c += 32) pr[c] = __dmul_rn(Ld[r][c], xb[c]);
+        __syncwarp();
+        if (lane == 0) {
+          double t = xb[r];
+          for (int c = 0; c < r; ++c) t = __dsub_rn(t, pr[c]);
+          xb[r] = __ddiv_rn(t, Ld[r][r]);
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    if (tid < bs) x[kb + tid] = xb[tid];
+    for (int i = be + tid; i < n; i += blockDim.x) {
+      const double* Li = L + (size_t)i * n + kb;
+      double sum = 0.0;
+      for (int q = 0; q < bs; ++q) sum = __dadd_rn(sum, __dmul_rn(Li[q], xb[q]));
+      x[i] = __dsub_rn(x[i], sum);
     }
     __syncthreads();
   }
   const int nb = (n + kLLT - 1) / kLLT;
   for (int bi = nb - 1; bi >= 0; --bi) {
-    const int kb = bi * kLLT, be = min(kb + kLLT, n);
-    if (threadIdx.x == 0)
-      for (int i = be - 1; i >= kb; --i) {
-        double t = x[i];
-        for (int q = i + 1; q < be; ++q) t = __dsub_rn(t, __dmul_rn(L[(size_t)q * n + i], x[q]));
-        x[i] = __ddiv_rn(t, L[(size_t)i * n + i]);
-      }
+    const int kb = bi * kLLT, be = min(kb + kLLT, n), bs = be - kb;
+    for (int e = tid; e < bs * bs; e += blockDim.x) {
+      const int r = e / bs, c = e % bs;
+      Ld[r][c] = L[(size_t)(kb + r) * n + kb + c];
+    }
+    if (tid < bs) xb[tid] = x[kb + tid];
     __syncthreads();
-    for (int i = threadIdx.x; i < kb; i += blockDim.x) {
-      double s = 0.0;
-      for (int q = kb; q < be; ++q) s = __dadd_rn(s, __dmul_rn(L[(size_t)q * n + i], x[q]));
-      x[i] = __dsub_rn(x[i], s);
+    if (w == 0) {
+      for (int r = bs - 1; r >= 0; --r) {
+        for (int c = r + 1 + lane; c < bs; c += 32) pr[c] = __dmul_rn(Ld[c][r], xb[c]);
+        __syncwarp();
+        if (lane == 0) {
+          double t = xb[r];
+          for (int c = r + 1; c < bs; ++c) t = __dsub_rn(t, pr[c]);
+          xb[r] = __ddiv_rn(t, Ld[r][r]);
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    if (tid < bs) x[kb + tid] = xb[tid];
+    for (int i = tid; i < kb; i += blockDim.x) {
+      double sum = 0.0;
+      for (int q = 0; q < bs; ++q) sum = __dadd_rn(sum, __dmul_rn(L[(size_t)(kb + q) * n + i], xb[q]));
+      x[i] = __dsub_rn(x[i], sum);
     }
     __syncthreads();
   }

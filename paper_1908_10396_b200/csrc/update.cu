@@ -645,28 +645,50 @@ int trace_ridge_device(aq_session* s, double* A, size_t dim, double ridge) {
 
 // Panel for block [kb, be): every CTA factors the diagonal block (identical,
 // deterministic) then the rows of its own range below the block.
-__global__ void k_llt_panel(double* A, int n, int kb, int rows_per_cta, int* fail) {
-  __shared__ double D[kLLT][kLLT + 1];
+// Panel of block [kb, be) (stand-in factor(), column by column): for column
+// j, L(j,j) = sqrt(L(j,j) - sum_k L(j,k)^2) (ordered chain: warp 0's lanes form
+// the rounded squares, lane 0 subtracts in order), then every row i > j —
+// the diagonal block's rows (redundantly in each CTA) and this CTA's rows
+// below the block — L(i,j) = (L(i,j) - sum_k L(i,k) L(j,k)) / L(j,j). All
+// operands live in shared memory for the whole panel.
+__global__ void __launch_bounds__(256) k_llt_panel(double* A, int n, int kb, int rows_per_cta,
+                                                  int* fail) {
+  extern __shared__ __align__(16) double psm[];
+  double(*D)[kLLT + 1] = reinterpret_cast<double(*)[kLLT + 1]>(psm);
+  double(*R)[kLLT + 1] = reinterpret_cast<double(*)[kLLT + 1]>(psm + kLLT * (kLLT + 1));
+  double* pr = psm + (size_t)(kLLT + rows_per_cta) * (kLLT + 1);
   const int be = min(kb + kLLT, n), bs = be - kb;
-  const int t = threadIdx.x;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int r0 = be + blockIdx.x * rows_per_cta;
+  const int nr = max(0, min(n, r0 + rows_per_cta) - r0);
   for (int e = t; e < bs * bs; e += blockDim.x) {
     const int r = e / bs, c = e % bs;
     D[r][c] = c <= r ? A[(size_t)(kb + r) * n + kb + c] : 0.0;
   }
+  for (int e = t; e < nr * bs; e += blockDim.x) {
+    const int r = e / bs, c = e % bs;
+    R[r][c] = A[(size_t)(r0 + r) * n + kb + c];
+  }
   __syncthreads();
   for (int jj = 0; jj < bs; ++jj) {
-    if (t == 0) {
-      double s = D[jj][jj];
-      for (int q = 0; q < jj; ++q) s = __dsub_rn(s, __dmul_rn(D[jj][q], D[jj][q]));
-      if (!(s > 0.0) && s <= 0.0) atomicExch(fail, 1);
-      D[jj][jj] = __dsqrt_rn(s);
+    if (w == 0) {
+      for (int q = lane; q < jj; q += 32) pr[q] = __dmul_rn(D[jj][q], D[jj][q]);
+      __syncwarp();
+      if (lane == 0) {
+        double sv = D[jj][jj];
+        for (int q = 0; q < jj; ++q) sv = __dsub_rn(sv, pr[q]);
+        if (sv <= 0.0) atomicExch(fail, 1);
+        D[jj][jj] = __dsqrt_rn(sv);
+      }
     }
     __syncthreads();
     const double dg = D[jj][jj];
-    for (int r = jj + 1 + t; r < bs; r += blockDim.x) {
-      double v = D[r][jj];
-      for (int q = 0; q < jj; ++q) v = __dsub_rn(v, __dmul_rn(D[r][q], D[jj][q]));
-      D[r][jj] = __ddiv_rn(v, dg);
+    const int nd = bs - jj - 1;
+    for (int idx = t; idx < nd + nr; idx += blockDim.x) {
+      double* row = idx < nd ? D[jj + 1 + idx] : R[idx - nd];
+      double v = row[jj];
+      for (int q = 0; q < jj; ++q) v = __dsub_rn(v, __dmul_rn(row[q], D[jj][q]));
+      row[jj] = __ddiv_rn(v, dg);
     }
     __syncthreads();
   }
@@ -675,16 +697,9 @@ __global__ void k_llt_panel(double* A, int n, int kb, int rows_per_cta, int* fai
       const int r = e / bs, c = e % bs;
       if (c <= r) A[(size_t)(kb + r) * n + kb + c] = D[r][c];
     }
-  // rows below the block
-  const int r0 = be + blockIdx.x * rows_per_cta;
-  const int r1 = min(n, r0 + rows_per_cta);
-  for (int i = r0 + t; i < r1; i += blockDim.x) {
-    double* Li = A + (size_t)i * n + kb;
-    for (int jj = 0; jj < bs; ++jj) {
-      double v = Li[jj];
-      for (int q = 0; q < jj; ++q) v = __dsub_rn(v, __dmul_rn(Li[q], D[jj][q]));
-      Li[jj] = __ddiv_rn(v, D[jj][jj]);
-    }
+  for (int e = t; e < nr * bs; e += blockDim.x) {
+    const int r = e / bs, c = e % bs;
+    A[(size_t)(r0 + r) * n + kb + c] = R[r][c];
   }
 }
 
@@ -824,7 +839,10 @@ int llt_solve_device(aq_session* s, double* A, int n, double* x) {
     const int below = n - be;
     const int rpc = 128;
     const int ctas = std::max(1, (below + rpc - 1) / rpc);
-    k_llt_panel<<<ctas, 128, 0, s->stream>>>(A, n, kb, rpc, fail);
+    const int psmem = (int)(((size_t)(kLLT + rpc) * (kLLT + 1) + kLLT) * sizeof(double));
+    AQ_CUDA(cudaFuncSetAttribute(k_llt_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 psmem));
+    k_llt_panel<<<ctas, 256, psmem, s->stream>>>(A, n, kb, rpc, fail);
     AQ_LAUNCHED(s);
     if (below > 0) {
       const int T = (below + 63) / 64;

@@ -99,7 +99,9 @@ struct ScoreArgs {
   int N;           // top-N
   int cap;         // candidate buffer per query
   size_t range_len;
-  int R;           // number of point ranges
+  int R;           // number of point ranges (window slots per query)
+  size_t chunk;    // > 0: persistent slices of chunk (query block, point) pairs
+  int nqb;         // query blocks
   uint2* out_buf;  // [q][r][cap] {integer score, index}
   int* out_cnt;    // [q][r]
   int* out_flag;   // [q]
@@ -161,7 +163,30 @@ __global__ void __launch_bounds__(TILE, MINB) k_adc_score(const ScoreArgs a) {
   int* cut = reinterpret_cast<int*>(T + QP * M * 16);
   int* cnt = cut + QB;
   int* flag = cnt + QB;
-  const int qb = blockIdx.y, r = blockIdx.x;
+  const size_t total = (size_t)a.nqb * a.n;
+  // Segments: one (query block, point range) per CTA (grid mode), or a
+  // persistent slice [c chunk, (c + 1) chunk) of the linearised (query block,
+  // point) space split at query-block edges; the segment's window slot is
+  // its index among the CTAs covering that query block.
+  size_t Lpos = a.chunk ? (size_t)blockIdx.x * a.chunk : 0;
+  const size_t Lend = a.chunk ? min(total, Lpos + a.chunk) : 1;
+  while (Lpos < Lend) {
+  int qb, r;
+  size_t start, end;
+  if (a.chunk) {
+    qb = (int)(Lpos / a.n);
+    start = Lpos % a.n;
+    end = min(a.n, start + (Lend - Lpos));
+    r = (int)(blockIdx.x - ((size_t)qb * a.n) / a.chunk);
+    Lpos += end - start;
+  } else {
+    qb = blockIdx.y;
+    r = blockIdx.x;
+    start = (size_t)r * a.range_len;
+    end = min(a.n, start + a.range_len);
+    Lpos = Lend;
+  }
+  __syncthreads();  // the previous segment is done with the LUT and counters
   // window of query q: shared [QB][cap], or out_buf[(qb QB + q) R + r][cap]
   uint2* const buf = GB ? a.out_buf + ((size_t)qb * QB * a.R + r) * a.cap
                         : reinterpret_cast<uint2*>(flag + QB);
@@ -178,8 +203,6 @@ __global__ void __launch_bounds__(TILE, MINB) k_adc_score(const ScoreArgs a) {
     flag[threadIdx.x] = 0;
   }
   __syncthreads();
-  const size_t start = (size_t)r * a.range_len;
-  const size_t end = min(a.n, start + a.range_len);
   const int cap = a.cap;
   const int margin = M + 1;  // 2 * (M s / 2) / s, plus one unit for float64
   // points scored between two barriers (windows in global memory are cheap
@@ -290,6 +313,7 @@ __global__ void __launch_bounds__(TILE, MINB) k_adc_score(const ScoreArgs a) {
     }
     __syncwarp();
   }
+  }  // segments
 }
 
 // ---- merge: global window, float64 re-scoring, exact order --------------------
@@ -474,14 +498,30 @@ int adc_search_device(aq_codes* codes, aq_codebook* cb, const double* Qd,
     const int cap = ((N + 31) & ~31) + TILE * (shp.gbuf ? kGbPointsPerThread : 1) + 32;
     // point ranges: enough CTAs for ~2 waves, ranges of whole tiles
     const size_t tiles = (n + TILE - 1) / TILE;
-    // ~4 waves of (query block x point range) CTAs: measured on config 2,
-    // 3-4 waves beat 8 (longer ranges amortise each CTA's window warm-up and
-    // LUT staging better than more waves hide the last partial one)
-    static const int waves = getenv("AQ_ADC_WAVES") ? atoi(getenv("AQ_ADC_WAVES")) : 4;
-    size_t R = std::max<size_t>(1, (waves * (size_t)s->num_sms * shp.minb + nqb - 1) / nqb);
-    R = std::min(R, tiles);
-    const size_t range_len = ((tiles + R - 1) / R) * TILE;
-    R = (n + range_len - 1) / range_len;
+    // Windows in global memory: one persistent CTA per resident slot, each
+    // an equal slice of the (query block, point) space — no partial last
+    // wave, long ranges. Shared windows (variant 0): ~4 waves of (query
+    // block x point range) CTAs.
+    static const int persist_env = getenv("AQ_ADC_PERSIST") ? atoi(getenv("AQ_ADC_PERSIST")) : 1;
+    const bool persist = shp.gbuf && persist_env;
+    size_t R, range_len = 0, chunk = 0, G = 0;
+    if (persist) {
+      G = (size_t)s->num_sms * shp.minb;
+      const size_t total = nqb * n;
+      chunk = std::max<size_t>((total + G - 1) / G, 16 * (size_t)TILE);
+      G = (total + chunk - 1) / chunk;
+      R = 1;
+      for (size_t qb = 0; qb < nqb; ++qb) {
+        const size_t c0 = qb * n / chunk, c1 = ((qb + 1) * n - 1) / chunk;
+        R = std::max(R, c1 - c0 + 1);
+      }
+    } else {
+      static const int waves = getenv("AQ_ADC_WAVES") ? atoi(getenv("AQ_ADC_WAVES")) : 4;
+      R = std::max<size_t>(1, (waves * (size_t)s->num_sms * shp.minb + nqb - 1) / nqb);
+      R = std::min(R, tiles);
+      range_len = ((tiles + R - 1) / R) * TILE;
+      R = (n + range_len - 1) / range_len;
+    }
     const size_t nq_pad = nqb * QB;  // GB windows exist for padding queries too
     const size_t buf_b = nq_pad * R * cap * sizeof(uint2);
     void* p2;
@@ -490,13 +530,15 @@ int adc_search_device(aq_codes* codes, aq_codebook* cb, const double* Qd,
     int* ocnt = (int*)(obuf + nq_pad * R * cap);
     int* oflag = ocnt + nq * R;
     AQ_CUDA(cudaMemsetAsync(oflag, 0, nq * sizeof(int), s->stream));
+    if (persist)  // query blocks covered by fewer slices leave slots empty
+      AQ_CUDA(cudaMemsetAsync(ocnt, 0, nq * R * sizeof(int), s->stream));
     ScoreArgs sa{codes->data, n, (int)codes->stride, lutq, M, (int)nq, N, cap,
-                 range_len, (int)R, obuf, ocnt, oflag};
+                 range_len, (int)R, chunk, (int)nqb, obuf, ocnt, oflag};
     const size_t smem = (size_t)shp.qp * M * 16 * sizeof(uint32_t) + 3 * QB * sizeof(int) +
                         (shp.gbuf ? 0 : (size_t)QB * cap * sizeof(uint2));
     if (smem > 227 * 1024)
       return ref_error(AQ_E_UNSUPPORTED, "ADC working set exceeds shared memory");
-    const dim3 grid((unsigned)R, (unsigned)nqb);
+    const dim3 grid = persist ? dim3((unsigned)G, 1) : dim3((unsigned)R, (unsigned)nqb);
     timer_mark(s, AQ_T_ADC_SCORE);
 #define AQ_SCORE_LAUNCH(MM, QPv, TL, MB, G)                                           \
   do {                                                                              \

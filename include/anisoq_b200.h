@@ -111,7 +111,8 @@ uint64_t aq_session_launches(aq_session* s);
 
 /* Per-kernel CUDA-event timers on the session stream (evidence for the
  * roofline in bench.py). Slots: 0 encode, 1 adc_score, 2 adc_merge,
- * 3 rerank, 4 lut. */
+ * 3 rerank, 4 lut, 5 normal-equation assembly, 6 Cholesky, 7 k-means warm
+ * start, 8 exact search (filter + merge). */
 int aq_session_timing(aq_session* s, int enable);
 int aq_session_timer_read(aq_session* s, int slot, double* ms, uint64_t* count,
                           int reset);

@@ -75,7 +75,7 @@ struct Scratch {
 // Optional per-kernel CUDA-event timers (bench.py's roofline evidence).
 enum AqTimer { AQ_T_ENCODE = 0, AQ_T_ADC_SCORE = 1, AQ_T_ADC_MERGE = 2,
                AQ_T_RERANK = 3, AQ_T_LUT = 4, AQ_T_ASSEMBLE = 5, AQ_T_LLT = 6,
-               AQ_T_KMEANS = 7, AQ_T_COUNT = 8 };
+               AQ_T_KMEANS = 7, AQ_T_EXACT = 8, AQ_T_COUNT = 9 };
 
 struct aq_session {
   int device = 0;

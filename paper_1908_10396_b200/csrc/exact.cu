@@ -8,6 +8,7 @@
 // the merge kernel selects and sorts the union exactly (score desc, index
 // asc). Scores are exact, so no window margin is needed.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -15,6 +16,8 @@
 namespace aqd {
 
 int sort_scores_desc(aq_session* s, const double* scores, uint32_t* idx, size_t n);
+int exact_filter_device(aq_dataset* ds, const double* Qd, size_t nq, size_t depth, uint32_t* ids,
+                        double* scores, std::vector<int>& hflag, bool* ran);
 
 constexpr int kXQ = 16;       // queries per CTA
 constexpr int kXTile = 256;   // points per tile
@@ -278,7 +281,12 @@ int exact_search_device(aq_dataset* ds, const double* Qd, size_t nq, size_t dept
   const size_t te = std::min(depth, n);
   const int pairs = (int)pairs_of(d);
   std::vector<int> hflag(nq, 1);
-  const bool fast = depth <= (size_t)kXMaxN;
+  // float32 filter + float64 window (exact_filter.cu); AQ_EXACT_FILTER=0
+  // keeps the all-float64 scoring kernel below
+  static const int use_filter = getenv("AQ_EXACT_FILTER") ? atoi(getenv("AQ_EXACT_FILTER")) : 1;
+  bool ran = false;
+  if (use_filter) AQ_TRY(exact_filter_device(ds, Qd, nq, depth, ids, scores, hflag, &ran));
+  const bool fast = !ran && depth <= (size_t)kXMaxN;
   if (fast) {
     const size_t nqb = (nq + kXQ - 1) / kXQ;
     const int N = (int)te;

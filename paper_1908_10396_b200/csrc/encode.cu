@@ -99,9 +99,10 @@ __device__ __noinline__ unsigned exact_window(
   return jb;
 }
 
-// Staged float32 codebook per subspace: 8 float4 {c0_j, c1_j, c0_j+1, c1_j+1}
-// then 4 float4 of C_j = |c_j|^2 (slots j >= k hold 1e30 so they never enter
-// a window), then 4 float4 of C for h_perp == 0 points (0, or 1e30 padding).
+// Staged float32 codebook per subspace: 8 float4 {c0_j, c0_j+1, c1_j, c1_j+1}
+// (candidate pairs for the packed f32x2 FMAs), then 4 float4 of C_j = |c_j|^2
+// (slots j >= k hold 1e30 so they never enter a window), then 4 float4 of C
+// for h_perp == 0 points (0, or 1e30 padding).
 constexpr int kCbStride = 16;  // float4 per subspace
 
 // Float32 proxy over the 16 candidates: exact float32 minimum (FMNMX3 tree),
@@ -113,22 +114,26 @@ __device__ __forceinline__ unsigned proxy_mask(float xf0, float xf1,
                                                const float4* __restrict__ sc,
                                                int coff, float gp, float beta,
                                                float delta) {
+  // two candidates per packed FMA (FFMA2): a = x . c, K = a (g' a - beta) + C
+  // (kNearest: K = C - 2a); the bound of DESIGN.md §4.1 allows fused products
   float K[16];
+  const float2 X0 = make_float2(xf0, xf0), X1 = make_float2(xf1, xf1);
+  const float2 GP = make_float2(gp, gp), NB = make_float2(-beta, -beta);
+  const float2 M2 = make_float2(-2.0f, -2.0f);
 #pragma unroll
   for (int t = 0; t < 8; ++t) {
     const float4 c = sc[t];
     const float4 C4 = sc[coff + (t >> 1)];
-    const float Ca = (t & 1) ? C4.z : C4.x;
-    const float Cb = (t & 1) ? C4.w : C4.y;
-    const float a0 = __fmaf_rn(xf1, c.y, xf0 * c.x);
-    const float a1 = __fmaf_rn(xf1, c.w, xf0 * c.z);
+    const float2 Cp = (t & 1) ? make_float2(C4.z, C4.w) : make_float2(C4.x, C4.y);
+    const float2 A = __ffma2_rn(X1, make_float2(c.z, c.w), __fmul2_rn(X0, make_float2(c.x, c.y)));
+    float2 Kp;
     if (kNearest) {
-      K[2 * t] = __fmaf_rn(-2.0f, a0, Ca);
-      K[2 * t + 1] = __fmaf_rn(-2.0f, a1, Cb);
+      Kp = __ffma2_rn(M2, A, Cp);
     } else {
-      K[2 * t] = __fmaf_rn(a0, __fmaf_rn(gp, a0, -beta), Ca);
-      K[2 * t + 1] = __fmaf_rn(a1, __fmaf_rn(gp, a1, -beta), Cb);
+      Kp = __ffma2_rn(A, __ffma2_rn(GP, A, NB), Cp);
     }
+    K[2 * t] = Kp.x;
+    K[2 * t + 1] = Kp.y;
   }
   float m6[6];
 #pragma unroll
@@ -171,8 +176,8 @@ __global__ void __launch_bounds__(TPB, MINB)
       const int m = t >> 4, j = t & 15;
       const float4 v = a.cb32[t];  // {c0, c1, C, 0}; C = 1e30 pads j >= k
       float* row = reinterpret_cast<float*>(scb + m * kCbStride);
-      row[(j >> 1) * 4 + (j & 1) * 2] = v.x;
-      row[(j >> 1) * 4 + (j & 1) * 2 + 1] = v.y;
+      row[(j >> 1) * 4 + (j & 1)] = v.x;
+      row[(j >> 1) * 4 + 2 + (j & 1)] = v.y;
       row[32 + j] = v.z;
       row[48 + j] = j < a.k ? 0.0f : 1e30f;
       cb2[t] = j < a.k ? g2[(size_t)m * a.k + j] : make_double2(0.0, 0.0);

@@ -139,34 +139,39 @@ __global__ void __launch_bounds__(kFTile, 2) k_exact_filter(const FArgs a) {
       for (int u = 0; u < nu; ++u) {
         const size_t p = tb + (size_t)u * kFTile + threadIdx.x;
         if (p < end) {
-          float f[kFQ];
+          // query pairs per packed FMA (FFMA2); the bound covers any rounding order
+          float2 f2[kFQ / 2];
 #pragma unroll
-          for (int q = 0; q < kFQ; ++q) f[q] = 0.0f;
+          for (int q = 0; q < kFQ / 2; ++q) f2[q] = make_float2(0.0f, 0.0f);
           const float2* xrow =
               reinterpret_cast<const float2*>(a.xt) + (p >> 5) * (size_t)a.pairs * 32 + (p & 31);
 #pragma unroll 4
           for (int jp = 0; jp < a.pairs; ++jp) {
             const float2 xv = xrow[(size_t)jp * 32];
             const float4* q0 = reinterpret_cast<const float4*>(qs + (size_t)(2 * jp) * kFQ);
+            const float2 xa = make_float2(xv.x, xv.x);
 #pragma unroll
             for (int v = 0; v < kFQ / 4; ++v) {
               const float4 qq = q0[v];
-              f[4 * v] = __fmaf_rn(qq.x, xv.x, f[4 * v]);
-              f[4 * v + 1] = __fmaf_rn(qq.y, xv.x, f[4 * v + 1]);
-              f[4 * v + 2] = __fmaf_rn(qq.z, xv.x, f[4 * v + 2]);
-              f[4 * v + 3] = __fmaf_rn(qq.w, xv.x, f[4 * v + 3]);
+              f2[2 * v] = __ffma2_rn(make_float2(qq.x, qq.y), xa, f2[2 * v]);
+              f2[2 * v + 1] = __ffma2_rn(make_float2(qq.z, qq.w), xa, f2[2 * v + 1]);
             }
             if (2 * jp + 1 < a.d) {
               const float4* q1 = reinterpret_cast<const float4*>(qs + (size_t)(2 * jp + 1) * kFQ);
+              const float2 xb = make_float2(xv.y, xv.y);
 #pragma unroll
               for (int v = 0; v < kFQ / 4; ++v) {
                 const float4 qq = q1[v];
-                f[4 * v] = __fmaf_rn(qq.x, xv.y, f[4 * v]);
-                f[4 * v + 1] = __fmaf_rn(qq.y, xv.y, f[4 * v + 1]);
-                f[4 * v + 2] = __fmaf_rn(qq.z, xv.y, f[4 * v + 2]);
-                f[4 * v + 3] = __fmaf_rn(qq.w, xv.y, f[4 * v + 3]);
+                f2[2 * v] = __ffma2_rn(make_float2(qq.x, qq.y), xb, f2[2 * v]);
+                f2[2 * v + 1] = __ffma2_rn(make_float2(qq.z, qq.w), xb, f2[2 * v + 1]);
               }
             }
+          }
+          float f[kFQ];
+#pragma unroll
+          for (int q = 0; q < kFQ / 2; ++q) {
+            f[2 * q] = f2[q].x;
+            f[2 * q + 1] = f2[q].y;
           }
 #pragma unroll
           for (int q = 0; q < kFQ; ++q) {

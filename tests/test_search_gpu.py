@@ -55,19 +55,25 @@ def test_adc_validation():
         aq.adc_search(np.ones(4), aq.CodeMatrix(10, 3, 4, np.zeros((10, 3))), cb, 5)
 
 
-@pytest.mark.parametrize("n,M,topn,nq", [(20000, 16, 100, 100), (300000, 50, 100, 64),
-                                         (5000, 48, 7, 33), (70000, 16, 512, 20),
-                                         (200, 8, 100, 5), (50000, 64, 1000, 3)])
-def test_adc_batch_matches_oracle(n, M, topn, nq):
-    g = np.random.default_rng(n + M)
-    cb = aq.ProductCodebook(M, 16, 2, g.standard_normal(M * 32) / np.sqrt(2 * M))
-    codes = g.integers(0, 16, (n, M)).astype(np.uint32)
+# every compiled M specialisation (16, 32, 48, 50, 64, 128), the generic
+# kernel with and without a tail chunk (8, 13), k < 16, top-N beyond the fast
+# path (1000), and slices that cross query-block edges (small n, many queries)
+@pytest.mark.parametrize("n,M,topn,nq,k", [(20000, 16, 100, 100, 16), (300000, 50, 100, 64, 16),
+                                           (5000, 48, 7, 33, 16), (70000, 16, 512, 20, 16),
+                                           (200, 8, 100, 5, 16), (50000, 64, 1000, 3, 16),
+                                           (40000, 32, 100, 40, 16), (30000, 128, 100, 20, 16),
+                                           (25000, 13, 50, 17, 16), (12000, 16, 100, 50, 9),
+                                           (3000, 50, 10, 300, 16)])
+def test_adc_batch_matches_oracle(n, M, topn, nq, k):
+    g = np.random.default_rng(n + M + k)
+    cb = aq.ProductCodebook(M, k, 2, g.standard_normal(M * k * 2) / np.sqrt(2 * M))
+    codes = g.integers(0, k, (n, M)).astype(np.uint32)
     Q = wl._normalize_rows(g.standard_normal((nq, 2 * M)))
     s = aq.Session.default()
-    dc = s.upload_codes(aq.CodeMatrix(n, M, 16, codes))
+    dc = s.upload_codes(aq.CodeMatrix(n, M, k, codes))
     dcb = s.upload_codebook(cb)
     ids, sc = aq.dev_adc_search(dc, dcb, Q, topn)
-    want_i, want_s = P.adc_search_batch(Q, codes, 16, cb.dictionaries, M, 16, 2, topn)
+    want_i, want_s = P.adc_search_batch(Q, codes, k, cb.dictionaries, M, k, 2, topn)
     assert np.array_equal(ids, want_i)
     assert np.array_equal(sc, want_s)
 

@@ -37,6 +37,21 @@ def test_quantize_config3_shape_lognormal_norms():
     assert np.array_equal(got, want)
 
 
+# fast-path shapes of the other configs: M = 50 (config 2, a tail code word),
+# M = 128 (config 5), an odd M
+@pytest.mark.parametrize("n,d,M", [(6000, 100, 50), (3000, 256, 128), (5000, 26, 13)])
+def test_quantize_config_shapes(n, d, M):
+    x = mixture_rows(n, d, M, centers=32)
+    cb = _cb(M, 16, 2, M + 1, scale=1 / np.sqrt(d))
+    got = aq.pq_quantize(x, cb, aq.ThresholdWeights(0.2), 3).codes
+    hp, ho = threshold_hp_ho(x, 0.2)
+    want = P.pq_quantize(x.astype(np.float64), cb.dictionaries, M, 16, 2, hp, ho, 3)
+    assert np.array_equal(got, want)
+    codes, losses = aq.pq_assign_pass(x, cb, aq.ThresholdWeights(0.2), aq.CodeMatrix(n, M, 16, want))
+    wc, wl_ = P.pq_assign_pass(x.astype(np.float64), cb.dictionaries, M, 16, 2, hp, ho, want)
+    assert np.array_equal(codes.codes, wc) and np.array_equal(losses, wl_)
+
+
 @pytest.mark.parametrize("w", ["iso", "eta", "iso2", "per_point", "eta_small"])
 def test_quantize_weight_kinds(w):
     x = mixture_rows(8000, 32, 25)

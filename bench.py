@@ -577,7 +577,9 @@ def run_reference(args):
     codes = (R.pq_quantize(x64, dic, M, 16, 2, hp, ho, 3, threads=cores) if kind == "reference"
              else R.pq_quantize(x64, dic, M, 16, 2, hp, ho, 3))
     Q = np.ascontiguousarray(w.queries, np.float64)
-    per_step = max(1, min(len(Q), int(os.environ.get("REF_QUERIES_PER_STEP", "16"))))
+    # one parallel_for chunk of 16 queries (index.hpp evaluate's chunking, as
+    # adc_search_batch uses) per host thread, so every core works each step
+    per_step = max(1, min(len(Q), int(os.environ.get("REF_QUERIES_PER_STEP", str(16 * cores)))))
 
     def step(i):
         q = Q[(i * per_step) % len(Q):][:per_step]

@@ -124,13 +124,11 @@ inline std::vector<std::uint32_t> pq_assign_point(std::span<const double> x,
                                                   std::span<const std::size_t> sweep_order = {}) {
   if (x.size() != cb.dim()) throw DimensionMismatch("datapoint dimension does not match codebook");
   if (current_codes.size() != cb.M) throw DimensionMismatch("need one current code per subspace");
-  for (std::size_t t = 0; t < sweep_order.size(); ++t)
-    if (sweep_order.size() != cb.M || sweep_order[t] != t)
-      throw Unsupported("device sweeps use the default order 0..M-1");
   std::vector<std::uint32_t> out(cb.M);
-  b200::check(aq_pq_assign_point(b200::session(), x.data(), x.size(), current_codes.data(),
-                                 cb.dictionaries.data(), cb.M, cb.k, cb.sub_dimension,
-                                 w.h_parallel, w.h_perpendicular, out.data()));
+  b200::check(aq_pq_assign_point_order(b200::session(), x.data(), x.size(),
+                                       current_codes.data(), cb.dictionaries.data(), cb.M, cb.k,
+                                       cb.sub_dimension, w.h_parallel, w.h_perpendicular,
+                                       sweep_order.data(), sweep_order.size(), out.data()));
   return out;
 }
 

@@ -177,6 +177,16 @@ int aq_pq_assign_point(aq_session* s, const double* x, size_t d,
                        const double* dictionaries, size_t M, size_t k,
                        size_t sub_dimension, double h_parallel,
                        double h_perpendicular, uint32_t* codes_out);
+/* pq_assign_point with an explicit sweep_order (pq.hpp:256-282): the
+ * subspaces visited in order (repeats allowed); order_len 0 = default_sweep.
+ * Entries >= M are rejected (AQ_E_INVALID_ARGUMENT; undefined in the
+ * reference). */
+int aq_pq_assign_point_order(aq_session* s, const double* x, size_t d,
+                             const uint32_t* current, const double* dictionaries,
+                             size_t M, size_t k, size_t sub_dimension,
+                             double h_parallel, double h_perpendicular,
+                             const size_t* sweep_order, size_t order_len,
+                             uint32_t* codes_out);
 
 /* ---- search (index.hpp:56-134) ------------------------------------------ */
 int aq_build_lut(aq_session* s, const double* q, size_t d,

@@ -285,6 +285,17 @@ class Reference(_Lib):
                    out.ctypes.data_as(C.c_void_p))
         return out
 
+    def pq_assign_point_order(self, x, cur, cb, M, k, sd, hp, ho, order):
+        out = np.zeros(M, np.uint32)
+        x = _f64(x)
+        order = np.ascontiguousarray(order, np.uintp)
+        self._call("pq_assign_point_order", x.ctypes.data_as(C.c_void_p), _szt(x.size),
+                   _u32(cur).ctypes.data_as(C.c_void_p), _f64(cb).ctypes.data_as(C.c_void_p),
+                   _szt(M), _szt(k), _szt(sd), C.c_double(hp), C.c_double(ho),
+                   order.ctypes.data_as(C.c_void_p), _szt(order.size),
+                   out.ctypes.data_as(C.c_void_p))
+        return out
+
     def generate_synthetic(self, kind, n, d, seed, centers=16, spread=0.25, normalize=False):
         out = np.zeros((n, d), np.float64)
         self._call("generate_synthetic", C.c_int(kind), _szt(n), _szt(d), C.c_uint64(seed),

@@ -159,6 +159,21 @@ int ref_pq_assign_point(const double* x, std::size_t d,
   GUARD_END
 }
 
+int ref_pq_assign_point_order(const double* x, std::size_t d,
+                              const std::uint32_t* cur, const double* dict,
+                              std::size_t M, std::size_t k, std::size_t sd,
+                              double hp, double ho, const std::size_t* order,
+                              std::size_t order_len, std::uint32_t* out) {
+  GUARD_BEGIN
+  const auto cb = make_cb(dict, M, k, sd);
+  const auto w = AnisotropicWeights::from_h(hp, ho);
+  const auto r = pq_assign_point(std::span<const double>(x, d),
+                                 std::span<const std::uint32_t>(cur, M), cb, w,
+                                 std::span<const std::size_t>(order, order_len));
+  std::copy(r.begin(), r.end(), out);
+  GUARD_END
+}
+
 // A_out is row-major dim x dim, dim = k*d.
 int ref_assemble_selector_system(const double* x, std::size_t n,
                                  std::size_t d, const std::uint32_t* codes,

@@ -75,6 +75,8 @@ _SIGS = {
     "aq_pq_quantize": (_I, [_VP, _VP, _SZ, _SZ, _VP, _SZ, _SZ, _SZ, _VP, _I, _VP]),
     "aq_pq_assign_pass": (_I, [_VP, _VP, _SZ, _SZ, _VP, _SZ, _SZ, _SZ, _VP, _I, _VP, _VP]),
     "aq_pq_assign_point": (_I, [_VP, _VP, _SZ, _VP, _VP, _SZ, _SZ, _SZ, _D, _D, _VP]),
+    "aq_pq_assign_point_order": (_I, [_VP, _VP, _SZ, _VP, _VP, _SZ, _SZ, _SZ, _D, _D, _VP, _SZ,
+                                      _VP]),
     "aq_build_lut": (_I, [_VP, _VP, _SZ, _VP, _SZ, _SZ, _SZ, _VP]),
     "aq_dev_adc_search": (_I, [_VP, _VP, _VP, _SZ, _SZ, _VP, _VP]),
     "aq_dev_adc_search_d": (_I, [_VP, _VP, _VP, _SZ, _SZ, _VP, _VP]),

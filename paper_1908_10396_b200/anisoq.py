@@ -610,17 +610,23 @@ def train_apq(data, M: int, k: int, weights, config: TrainConfig = TrainConfig()
 
 
 def pq_assign_point(x, current_codes, cb: ProductCodebook, w: AnisotropicWeights,
-                    session: Optional[Session] = None) -> np.ndarray:
-    """pq.hpp:256-282: one coordinate-descent pass for a single float64 point."""
+                    sweep_order=None, session: Optional[Session] = None) -> np.ndarray:
+    """pq.hpp:256-282: one coordinate-descent pass for a single float64 point
+    over `sweep_order` (default 0..M-1; subspaces may repeat)."""
     s = _sess(session)
     x = np.ascontiguousarray(x, np.float64)
     cur = np.ascontiguousarray(current_codes, np.uint32)
+    if x.size != cb.dim():
+        raise DimensionMismatch("DimensionMismatch: datapoint dimension does not match codebook")
     if cur.size != cb.M:
         raise DimensionMismatch("DimensionMismatch: need one current code per subspace")
+    order = np.ascontiguousarray([] if sweep_order is None else sweep_order, np.uint64)
     out = np.zeros(cb.M, np.uint32)
-    _check(_L.aq_pq_assign_point(s.h, x.ctypes.data, x.size, cur.ctypes.data,
-                                 cb.dictionaries.ctypes.data, cb.M, cb.k, cb.sub_dimension,
-                                 w.h_parallel, w.h_perpendicular, out.ctypes.data))
+    _check(_L.aq_pq_assign_point_order(s.h, x.ctypes.data, x.size, cur.ctypes.data,
+                                       cb.dictionaries.ctypes.data, cb.M, cb.k,
+                                       cb.sub_dimension, w.h_parallel, w.h_perpendicular,
+                                       order.ctypes.data if order.size else None, order.size,
+                                       out.ctypes.data))
     return out
 
 

@@ -341,8 +341,11 @@ int exact_search_device(aq_dataset* ds, const double* Qd, size_t nq, size_t dept
 
 // ---- pq_assign_point (pq.hpp:256-282): one point, float64 input ---------------------------
 
+// order: sweep_order (pq.hpp:273-276; subspaces may repeat), or null for
+// default_sweep (0..M-1)
 __global__ void k_assign_point(const double* x, int M, int k, int sd, const double* cb,
-                               double hp, double ho, double inv, unsigned* codes) {
+                               double hp, double ho, double inv, unsigned* codes,
+                               const unsigned long long* order, int norder) {
   if (threadIdx.x || blockIdx.x) return;
   const bool iso = hp == ho;
   double s2 = 0.0, s1 = 0.0;
@@ -363,7 +366,8 @@ __global__ void k_assign_point(const double* x, int M, int k, int sd, const doub
     s2 = __dadd_rn(s2, t2);
     s1 = __dadd_rn(s1, t1);
   }
-  for (int m = 0; m < M; ++m) {
+  for (int step = 0; step < norder; ++step) {
+    const int m = order ? (int)order[step] : step;
     double t2, t1;
     resid(m, (int)codes[m], &t2, &t1);
     const double base2 = __dsub_rn(s2, t2), base1 = __dsub_rn(s1, t1);
@@ -428,9 +432,10 @@ int aq_dev_exact_search(aq_dataset* ds, const double* queries, size_t nq, size_t
 
 // pq_assign_point (pq.hpp:256-282): validation order of the reference, then
 // one coordinate-descent pass in the default order.
-int aq_pq_assign_point(aq_session* s, const double* x, size_t d, const uint32_t* current,
-                       const double* dict, size_t M, size_t k, size_t sd, double hp,
-                       double ho, uint32_t* codes_out) {
+int aq_pq_assign_point_order(aq_session* s, const double* x, size_t d, const uint32_t* current,
+                             const double* dict, size_t M, size_t k, size_t sd, double hp,
+                             double ho, const size_t* order, size_t order_len,
+                             uint32_t* codes_out) {
   AQ_TRY(check_session(s));
   if (d != M * sd)
     return ref_error(AQ_E_DIMENSION_MISMATCH, "datapoint dimension does not match codebook");
@@ -438,6 +443,9 @@ int aq_pq_assign_point(aq_session* s, const double* x, size_t d, const uint32_t*
     if (current[m] >= k) return ref_error(AQ_E_CODE_OUT_OF_RANGE, "current code out of range");
   if (!(hp >= 0.0) || !(ho >= 0.0) || !std::isfinite(hp) || !std::isfinite(ho))
     return ref_error(AQ_E_INVALID_ARGUMENT, "h coefficients must be finite and >= 0");
+  // the reference indexes codes[m] unchecked (undefined behaviour for m >= M)
+  for (size_t t = 0; t < order_len; ++t)
+    if (order[t] >= M) return ref_error(AQ_E_INVALID_ARGUMENT, "sweep order entry out of range");
   double inv = 0.0;
   if (hp != ho) {
     double n2 = 0.0;  // detail::norm2 = dot(x, x), sequential (geometry.hpp:176)
@@ -448,21 +456,37 @@ int aq_pq_assign_point(aq_session* s, const double* x, size_t d, const uint32_t*
   }
   double *dx, *dcb;
   unsigned* dc;
+  unsigned long long* dord = nullptr;
   AQ_CUDA(cudaMallocAsync(&dx, d * sizeof(double) + 8, s->stream));
   AQ_CUDA(cudaMallocAsync(&dcb, M * k * sd * sizeof(double) + 8, s->stream));
   AQ_CUDA(cudaMallocAsync(&dc, M * sizeof(unsigned) + 8, s->stream));
   AQ_CUDA(cudaMemcpyAsync(dx, x, d * sizeof(double), cudaMemcpyHostToDevice, s->stream));
   AQ_CUDA(cudaMemcpyAsync(dcb, dict, M * k * sd * sizeof(double), cudaMemcpyHostToDevice, s->stream));
   AQ_CUDA(cudaMemcpyAsync(dc, current, M * sizeof(unsigned), cudaMemcpyHostToDevice, s->stream));
-  k_assign_point<<<1, 32, 0, s->stream>>>(dx, (int)M, (int)k, (int)sd, dcb, hp, ho, inv, dc);
+  std::vector<unsigned long long> hord(order, order + order_len);
+  if (order_len) {
+    AQ_CUDA(cudaMallocAsync(&dord, order_len * sizeof(unsigned long long), s->stream));
+    AQ_CUDA(cudaMemcpyAsync(dord, hord.data(), order_len * sizeof(unsigned long long),
+                            cudaMemcpyHostToDevice, s->stream));
+  }
+  k_assign_point<<<1, 32, 0, s->stream>>>(dx, (int)M, (int)k, (int)sd, dcb, hp, ho, inv, dc,
+                                          dord, order_len ? (int)order_len : (int)M);
   s->launches++;
   AQ_CUDA(cudaGetLastError());
   AQ_CUDA(cudaMemcpyAsync(codes_out, dc, M * sizeof(unsigned), cudaMemcpyDeviceToHost, s->stream));
   cudaFreeAsync(dx, s->stream);
   cudaFreeAsync(dcb, s->stream);
   cudaFreeAsync(dc, s->stream);
+  if (dord) cudaFreeAsync(dord, s->stream);
   AQ_CUDA(cudaStreamSynchronize(s->stream));
   return AQ_OK;
+}
+
+int aq_pq_assign_point(aq_session* s, const double* x, size_t d, const uint32_t* current,
+                       const double* dict, size_t M, size_t k, size_t sd, double hp,
+                       double ho, uint32_t* codes_out) {
+  return aq_pq_assign_point_order(s, x, d, current, dict, M, k, sd, hp, ho, nullptr, 0,
+                                  codes_out);
 }
 
 }  // extern "C"

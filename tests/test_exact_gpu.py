@@ -63,6 +63,27 @@ def test_assign_point_matches_reference(eta):
         aq.pq_assign_point(np.zeros(6), [0, 0, 0], cb, aq.AnisotropicWeights.from_eta(2.0))
 
 
+def test_assign_point_sweep_order_matches_reference():
+    # pq.hpp:256-282 with explicit sweep orders: permutations and repeats
+    g = np.random.default_rng(77)
+    w = aq.AnisotropicWeights.from_eta(4.125)
+    R = Reference() if Reference.available() else None
+    for order in ([2, 0, 1], [1, 1, 0, 2, 2], [0], [2, 1, 0, 0, 1, 2]):
+        for rep in range(10):
+            cb = aq.ProductCodebook(3, 4, 2, g.standard_normal(24))
+            x = g.standard_normal(6)
+            cur = g.integers(0, 4, 3).astype(np.uint32)
+            got = aq.pq_assign_point(x, cur, cb, w, sweep_order=order)
+            if R is not None:
+                want = R.pq_assign_point_order(x, cur, cb.dictionaries, 3, 4, 2, w.h_parallel,
+                                               w.h_perpendicular, order)
+                assert np.array_equal(got, want)
+    assert np.array_equal(aq.pq_assign_point(x, cur, cb, w, sweep_order=list(range(3))),
+                          aq.pq_assign_point(x, cur, cb, w))
+    with pytest.raises(aq.InvalidArgument):
+        aq.pq_assign_point(x, cur, cb, w, sweep_order=[0, 3])
+
+
 def test_evaluate_perfect_codes_recall_one():
     # test_index.cpp:189-204: data equal to reconstructions -> recall 1, error 0
     g = np.random.default_rng(13)

@@ -492,136 +492,6 @@ __global__ void __launch_bounds__(32) k_assemble_sd2(const AsmArgs a, const uint
   }
 }
 
-// Finer units for the same specialisation: 16 column subspaces per warp, the
-// two row components aa split across the half-warps (lane = aa * 16 + col).
-// Half the accumulators per warp (8 KB) and twice the units: more warps per
-// SM to hide the read-modify-write chains, better balance across SMs.
-__global__ void __launch_bounds__(32) k_assemble_sd2c16(const AsmArgs a, const uint32_t* order) {
-  extern __shared__ __align__(16) double acc[];  // [j2 * 2 + b][32]
-  __shared__ __align__(16) double s_u[32][2];    // coef * x_m[aa]
-  __shared__ __align__(16) double2 s_r[32];      // h_par * x_m (rhs)
-  __shared__ double s_ho[32];
-  __shared__ __align__(16) float s_x[32][32];    // [point][column float]
-  __shared__ __align__(16) uint32_t s_cw[32][2]; // [point][code word of col >> 3]
-  const int unit = order[blockIdx.x];
-  const int chunk = unit % a.nchunk;
-  const int strip = unit / a.nchunk;
-  const int m = strip >> 4, j = strip & 15;
-  const int lane = threadIdx.x, col = lane & 15, aa = lane >> 4;
-  const int d = a.d;
-  const int m2 = chunk * 16 + col;
-  const int mcols = a.full ? a.M : m + 1;
-  const bool mine = m2 < mcols;
-  const bool diag = m2 == m;
-  const size_t dim = (size_t)16 * d;
-  const bool do_rhs = chunk == 0 && lane == 0;
-  const uint32_t* Lall = a.list + (size_t)m * a.n + a.start[m * 16 + j];
-  const size_t call = a.count[m * 16 + j];
-  const size_t t_lo = lower_bound_u32(Lall, call, a.lo);
-  const size_t t_hi = lower_bound_u32(Lall, call, a.hi);
-  if (t_lo == t_hi) return;
-  const size_t arow = ((size_t)(m * 16 + j) * 2 + aa) * dim + (size_t)m2 * 32;
-  double r0 = 0.0, r1 = 0.0;
-  if (a.resume) {
-    if (mine) {
-#pragma unroll 4
-      for (int e = 0; e < 32; ++e) acc[e * 32 + lane] = a.A[arow + e];
-    }
-    if (do_rhs) {
-      r0 = a.rhs[(size_t)(m * 16 + j) * 2];
-      r1 = a.rhs[(size_t)(m * 16 + j) * 2 + 1];
-    }
-  } else {
-#pragma unroll
-    for (int e = 0; e < 32; ++e) acc[e * 32 + lane] = 0.0;
-  }
-  const uint32_t* L = Lall + t_lo;
-  const size_t cnt = t_hi - t_lo;
-  const int col0 = chunk * 32;                       // first float of the chunk's columns
-  const int nf4 = min(8, (d - col0) >> 2);           // valid float4 per point row
-  const int cb0 = chunk * 8;                         // first code byte of the chunk
-  const bool cok = cb0 + 8 <= a.stride;
-  const unsigned sx = (unsigned)__cvta_generic_to_shared(&s_x[0][0]);
-  const unsigned sc = (unsigned)__cvta_generic_to_shared(&s_cw[0][0]);
-  for (size_t t0 = 0; t0 < cnt; t0 += 32) {
-    const int nb = (int)min((size_t)32, cnt - t0);
-    uint32_t pl = 0;
-    if (lane < nb) {
-      pl = L[t0 + lane];
-      const double cf = a.coef[pl];
-      const double hp = a.hp[pl];
-      const float2 xm = *reinterpret_cast<const float2*>(a.xr + (size_t)pl * d + m * 2);
-      s_u[lane][0] = __dmul_rn(cf, (double)xm.x);
-      s_u[lane][1] = __dmul_rn(cf, (double)xm.y);
-      s_r[lane] = make_double2(__dmul_rn(hp, (double)xm.x), __dmul_rn(hp, (double)xm.y));
-      s_ho[lane] = a.ho[pl];
-      if (cok) {
-        const uint8_t* src = a.codes + (size_t)pl * a.stride + cb0;
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sc + (unsigned)lane * 8u),
-                     "l"(src));
-      }
-    }
-    // rows: 16-byte pieces, lane -> (point b = idx / 8, piece f = idx % 8)
-#pragma unroll
-    for (int it = 0; it < 8; ++it) {
-      const int idx = it * 32 + lane;
-      const int b = idx >> 3, f = idx & 7;
-      const uint32_t p = __shfl_sync(0xffffffffu, pl, b);
-      if (b < nb && f < nf4) {
-        const float* src = a.xr + (size_t)p * d + col0 + f * 4;
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(sx + (unsigned)(b * 32 + f * 4) * 4u),
-                     "l"(src));
-      }
-    }
-    asm volatile("cp.async.wait_all;\n" ::);
-    __syncwarp();
-    if (!cok && lane < nb) {  // code slice runs past the row: byte loads
-      const uint8_t* src = a.codes + (size_t)pl * a.stride + cb0;
-      uint32_t w0 = 0, w1 = 0;
-      for (int t = 0; t < 8 && cb0 + t < a.stride; ++t) {
-        if (t < 4) w0 |= (uint32_t)src[t] << (8 * t);
-        else w1 |= (uint32_t)src[t] << (8 * (t - 4));
-      }
-      s_cw[lane][0] = w0;
-      s_cw[lane][1] = w1;
-    }
-    __syncwarp();
-    if (do_rhs)
-      for (int b = 0; b < nb; ++b) {  // rhs += h_par * x (pq.hpp:326)
-        const double2 r = s_r[b];
-        r0 = __dadd_rn(r0, r.x);
-        r1 = __dadd_rn(r1, r.y);
-      }
-    if (mine) {
-      const int wsel = col >> 3, sh = 4 * (col & 7);
-#pragma unroll 4
-      for (int b = 0; b < nb; ++b) {
-        const unsigned j2 = (s_cw[b][wsel] >> sh) & 15u;
-        const double u = s_u[b][aa];
-        const float2 xc = *reinterpret_cast<const float2*>(&s_x[b][col * 2]);
-        double* e = acc + (size_t)(j2 * 2) * 32 + lane;
-        double e0 = e[0], e1 = e[32];
-        if (diag) {  // h_perp on the diagonal (aa, j, aa) first (pq.hpp:324-325)
-          const double hop = s_ho[b];
-          if (aa == 0) e0 = __dadd_rn(e0, hop);
-          else e1 = __dadd_rn(e1, hop);
-        }
-        e[0] = __dadd_rn(e0, __dmul_rn(u, (double)xc.x));
-        e[32] = __dadd_rn(e1, __dmul_rn(u, (double)xc.y));
-      }
-    }
-    __syncwarp();
-  }
-  if (mine) {
-#pragma unroll 4
-    for (int e = 0; e < 32; ++e) a.A[arow + e] = acc[(size_t)e * 32 + lane];
-  }
-  if (do_rhs) {
-    a.rhs[(size_t)(m * 16 + j) * 2] = r0;
-    a.rhs[(size_t)(m * 16 + j) * 2 + 1] = r1;
-  }
-}
-
 // trace (sequential, Eigen stand-in) and ridge = 1e-6 trace / dim (pq.hpp:431-435)
 __global__ void k_trace_ridge(double* A, size_t dim, double ridge) {
   __shared__ double r;
@@ -1044,9 +914,9 @@ int assemble_device(aq_dataset* ds, aq_codes* codes, const PointW& pw, const Buc
   const unsigned units = (unsigned)(M * k * nchunk);
   timer_mark(s, AQ_T_ASSEMBLE);
   if (sd == 2 && k == 16 && d % 4 == 0 && codes->bits == 4) {
-    static const int cols = getenv("AQ_ASM_COLS") ? atoi(getenv("AQ_ASM_COLS")) : 32;
-    const int nch = cols == 32 ? nchunk : (M + 15) / 16;
-    a.nchunk = nch;
+    // 32 column subspaces per unit (a 16-column split with twice the units
+    // measured slower: per-unit staging outweighs the extra warps)
+    const int cols = 32, nch = nchunk;
     const unsigned units2 = (unsigned)(M * 16 * nch);
     AQ_CUDA(cudaFuncSetAttribute(k_assemble_sd2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  64 * 32 * 8));
@@ -1078,10 +948,7 @@ int assemble_device(aq_dataset* ds, aq_codes* codes, const PointW& pw, const Buc
       a.lo = (uint32_t)lo;
       a.hi = (uint32_t)std::min(ds->n, lo + bsz);
       a.resume = lo > 0;
-      if (cols == 32)
-        k_assemble_sd2<<<(unsigned)ord.size(), 32, 64 * 32 * 8, s->stream>>>(a, dord);
-      else
-        k_assemble_sd2c16<<<(unsigned)ord.size(), 32, 32 * 32 * 8, s->stream>>>(a, dord);
+      k_assemble_sd2<<<(unsigned)ord.size(), 32, 64 * 32 * 8, s->stream>>>(a, dord);
       AQ_LAUNCHED(s);
     }
   } else {

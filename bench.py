@@ -54,6 +54,12 @@ def parse():
     return p.parse_args()
 
 
+def sharded_mode(ws):
+    """The multi-GPU code path (shared sharded index, NCCL collectives);
+    BENCH_SHARDED=1 runs it as a one-rank world, to exercise it on one GPU."""
+    return ws > 1 or os.environ.get("BENCH_SHARDED") == "1"
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -137,10 +143,13 @@ def build_index(aq, wl, n, nq, seed_shard, session):
     alternating iterations, T = 0.2), bit-identical to the reference's trainer."""
     import ctypes as C
 
-    w = wl.config2(n=n, nq=nq, seed=seed_shard)
-    ds = session.upload_dataset(w.base)
-    cfg = aq.TrainConfig(max_iterations=w.iterations, relative_tolerance=0.0, seed=seed_shard)
+    w = wl.config2(n=n, nq=nq, seed=0, shard=seed_shard)
+    cfg = aq.TrainConfig(max_iterations=w.iterations, relative_tolerance=0.0, seed=0)
     L = aq._L
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if sharded_mode(ws):
+        return build_index_sharded(aq, w, n, ws, seed_shard, session, cfg)
+    ds = session.upload_dataset(w.base)
     # the first run builds the index and warms every kernel (module loading,
     # clocks); the second, identical (deterministic) run is the one timed
     hist0 = []
@@ -173,7 +182,46 @@ def build_index(aq, wl, n, nq, seed_shard, session):
     cb = dcb.download()
     return w, cb, ds, dcb, dc, {"train_apq_s": round(train_s, 2), "loss_first": hist[0],
                                 "loss_last": hist[-1], "iterations": len(hist) - 1,
-                                "phases": phases}
+                                "phases": phases, "trainer": "train_apq on device, warm start"}
+
+
+def build_index_sharded(aq, w, n, ws, rank, session, cfg):
+    """N > 1: one index over all shards — the codebook trained jointly by the
+    row-sharded trainer (per-shard partial sums, NCCL all-gather, rank-ordered
+    combination; paper_1908_10396_b200/distributed.py), every rank holding
+    the same codebook and its shard's codes."""
+    import ctypes as C
+    import torch
+    from paper_1908_10396_b200.distributed import DeviceShard, ShardedTrainer
+
+    L = aq._L
+    rows = torch.from_numpy(w.base).cuda(session.device)
+    sh = DeviceShard(session, rows, aq.ThresholdWeights(w.threshold))
+    trainer = ShardedTrainer(sh, n * ws, rank * n)
+    trainer.train_apq(w.M, w.k, cfg, True)  # warms every kernel and collective
+    L.aq_session_timing(session.h, 1)
+    for slot in range(8):
+        L.aq_session_timer_read(session.h, slot, None, None, 1)
+    torch.cuda.synchronize()
+    torch.distributed.barrier()
+    t0 = time.perf_counter()
+    hist = []
+    trainer.train_apq(w.M, w.k, cfg, True, hist)
+    torch.cuda.synchronize()
+    t = torch.tensor([time.perf_counter() - t0], device=f"cuda:{session.device}")
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ph = {}
+    for slot, name in [(0, "encode"), (5, "assemble"), (6, "llt_solve"),
+                       (7, "kmeans_warm_start")]:
+        ms, cnt = C.c_double(0), C.c_uint64(0)
+        L.aq_session_timer_read(session.h, slot, C.byref(ms), C.byref(cnt), 1)
+        ph[name] = {"ms": round(ms.value, 2), "launches": int(cnt.value)}
+    L.aq_session_timing(session.h, 0)
+    cb = sh.cb.download()
+    return w, cb, sh.ds, sh.cb, sh.codes, {
+        "train_apq_s": round(float(t.item()), 2), "loss_first": hist[0], "loss_last": hist[-1],
+        "iterations": len(hist) - 1, "phases": ph,
+        "trainer": f"row-sharded train_apq over {ws} GPUs (NCCL), one shared codebook"}
 
 
 def train_record(w, n, info, codes_h, cpu):
@@ -246,8 +294,14 @@ def run_ours(args):
     import ctypes as C
 
     ws, rank, local = dist_env()
-    if ws > 1:
+    sharded = sharded_mode(ws)
+    if sharded:
         import torch.distributed as dist
+        if ws == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29511")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl")
     torch.cuda.set_device(local)
     from paper_1908_10396_b200 import anisoq as aq
@@ -269,7 +323,7 @@ def run_ours(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
     # events on the session stream (single GPU); on torch's stream bracketing
     # the host-synchronous calls + collectives when sharded
-    tstream = stream if ws == 1 else torch.cuda.current_stream(local)
+    tstream = stream if not sharded else torch.cuda.current_stream(local)
 
     def step_dev():
         aq._check(L.aq_dev_search_rerank_d(ds.h, dc.h, dcb.h, Qd.data_ptr(), nq, topn, keep,
@@ -286,7 +340,7 @@ def run_ours(args):
         aq._check(L.aq_dev_search_rerank(ds.h, dc.h, dcb.h, Qpin.data_ptr(), nq, topn, keep,
                                          None, None, hid_t.data_ptr(), hsc_t.data_ptr()))
 
-    if ws > 1:
+    if sharded:
         # row shards: this rank owns global ids [rank*n, (rank+1)*n); one NCCL
         # all-gather of per-shard candidates + exact merge per step
         from paper_1908_10396_b200 import distributed as D
@@ -304,7 +358,7 @@ def run_ours(args):
         for _ in range(warmup):
             fn()
         torch.cuda.synchronize()
-        if ws > 1:
+        if sharded:
             torch.distributed.barrier()
         L.aq_session_timing(sess.h, 1)
         for slot in range(5):
@@ -321,7 +375,7 @@ def run_ours(args):
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(tstream)
             fn()
-            if ws > 1:
+            if sharded:
                 torch.cuda.synchronize()
             e1.record(tstream)
             e1.synchronize()
@@ -338,7 +392,7 @@ def run_ours(args):
                 kt[name] = (ms.value, cnt.value)
         L.aq_session_timing(sess.h, 0)
         ms = total / steps
-        if ws > 1:
+        if sharded:
             t = torch.tensor([ms], device=f"cuda:{local}")
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             ms = t.item()
@@ -390,8 +444,7 @@ def run_ours(args):
            "config": {"workload": "config2", "n_per_gpu": n, "d": d, "M": M, "k": 16,
                       "queries_per_step": nq, "adc_topn": topn, "rerank_to": keep,
                       "threshold": w.threshold,
-                      "index": dict({k: v for k, v in train_info.items() if k != "phases"},
-                                    trainer="train_apq on device, warm start"),
+                      "index": {k: v for k, v in train_info.items() if k != "phases"},
                       "recall10_at_10": recall,
                       "filter_dtype": "13-bit integer LUT (bounded error), results f64 bit-exact",
                       "l2": "flushed (256 MiB write) before every timed step",
@@ -406,14 +459,14 @@ def run_ours(args):
         tcpu = None
         if ws == 1 and not args.no_cpu_baseline:
             tcpu = train_cpu_baseline(args, w, dc.download().codes, n)
-        out["train"] = train_record(w, n, train_info, None, tcpu)
+        out["train"] = train_record(w, n * ws, train_info, None, tcpu)
     if not args.no_encode:
         out["encode"] = bench_encode(args, aq, wl, sess, stream, flush, local, ws, pk)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, w, cb, dc, n)
     if rank == 0:
-        print(json.dumps(out), flush=True)
-    if ws > 1:
+        emit(json.dumps(out))
+    if sharded:
         torch.distributed.destroy_process_group()
 
 
@@ -596,7 +649,7 @@ def run_reference(args):
         done += step(i)
     dt = time.perf_counter() - t0
     value = done * n / dt
-    print(json.dumps({
+    emit(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(value, 1), "unit": UNIT,
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
@@ -607,11 +660,27 @@ def run_reference(args):
         "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": cores, "kind": kind,
                          "sample": f"{per_step} queries x {n} points per step"},
         "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0}}), flush=True)
+                "d2h_bytes_per_step": 0}}))
+
+
+_STDOUT_FD = None
+
+
+def emit(line: str) -> None:
+    """The one JSON line on the real stdout (everything else — NCCL banners,
+    library prints — was sent to stderr)."""
+    sys.stderr.flush()
+    if _STDOUT_FD is not None:
+        os.write(_STDOUT_FD, (line + "\n").encode())
+    else:
+        print(line, flush=True)
 
 
 if __name__ == "__main__":
     a = parse()
+    sys.stdout.flush()
+    _STDOUT_FD = os.dup(1)
+    os.dup2(2, 1)  # C-level and Python prints during the run go to stderr
     if a.impl == "reference":
         run_reference(a)
     else:

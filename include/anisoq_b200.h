@@ -304,6 +304,10 @@ int aq_dev_sort_desc(aq_session* s, const double* scores_dev, uint32_t* idx_dev,
 /* std::accumulate(v, v + n, init) in index order */
 int aq_dev_seq_sum(aq_session* s, const double* v_dev, size_t n, double init,
                    double* out);
+/* `rows` such sums in one launch (row r at v_dev + r * ld, `count` values);
+ * rows with active_host[r] == 0 (active_host may be NULL) give 0 */
+int aq_dev_seq_sums(aq_session* s, const double* v_dev, size_t ld, size_t count,
+                    size_t rows, const int* active_host, double* out_host);
 /* vq_assign_pass (vq.hpp:196-217) with unit weights for the active subspaces
  * of this shard: codes in place, losses_dev (M x n), changes_out[M] */
 int aq_dev_kmeans_assign(aq_dataset* ds, aq_codebook* cb, aq_codes* codes,

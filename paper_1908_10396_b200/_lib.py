@@ -101,6 +101,7 @@ _SIGS = {
     "aq_dev_point_losses": (_I, [_VP, _VP, _VP, _VP, _VP]),
     "aq_dev_sort_desc": (_I, [_VP, _VP, _VP, _SZ]),
     "aq_dev_seq_sum": (_I, [_VP, _VP, _SZ, C.c_double, _VP]),
+    "aq_dev_seq_sums": (_I, [_VP, _VP, _SZ, _SZ, _SZ, _VP, _VP]),
     "aq_dev_kmeans_assign": (_I, [_VP, _VP, _VP, _VP, _VP, _VP]),
     "aq_dev_kmeans_partials": (_I, [_VP, _VP, _SZ, _VP, _VP, _VP, _VP]),
 }

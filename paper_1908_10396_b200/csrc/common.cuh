@@ -176,6 +176,11 @@ int assemble_device(aq_dataset* ds, aq_codes* codes, const PointW& pw, const Buc
                     int k, bool full, double* A, double* rhs);
 int llt_solve_device(aq_session* s, double* A, int n, double* x);
 int trace_ridge_device(aq_session* s, double* A, size_t dim, double ridge);
+// per-slot point-ordered sums (train.cu k_slot_sums): hp == null -> unit
+// weights; dict != null -> means of non-empty slots, else num/den partials
+int slot_sums_device(aq_session* s, const float* xr, size_t n, int d, int M, int k, int sd,
+                     const Buckets& B, const int* active, const double* hp, const double* ho,
+                     double* dict, double* pnum, double* pden);
 
 // ---- weights ------------------------------------------------------------------
 // Resolved per point on the device from an aq_weights descriptor

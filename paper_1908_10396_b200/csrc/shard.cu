@@ -19,54 +19,11 @@ int run_encode(aq_dataset* ds, aq_codebook* cb, const aq_weights* w, aq_codes* c
 int sort_scores_desc(aq_session* s, const double* scores, uint32_t* idx, size_t n);
 int stage_codebook(aq_codebook* cb);
 int seq_sum_device(aq_session* s, const double* v, size_t n, double init, double* out);
+int seq_sums_device(aq_session* s, const double* v, size_t ld, size_t count, int rows,
+                    const int* active_dev, double* out);
 
 // per-slot partial sums for the isotropic path (pq.hpp:405-417), members in
-// ascending order within this shard
-__global__ void k_iso_partials(const float* xr, size_t n, int d, int M, int k, int sd,
-                               const uint32_t* list, const uint32_t* start,
-                               const uint32_t* count, const double* hp, const double* ho,
-                               double* num, double* den) {
-  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
-  if (slot >= M * k) return;
-  const int m = slot / k;
-  const uint32_t* L = list + (size_t)m * n + start[slot];
-  const size_t cnt = count[slot];
-  double nu[16];
-  for (int c = 0; c < sd; ++c) nu[c] = 0.0;
-  double de = 0.0;
-  for (size_t t = 0; t < cnt; ++t) {
-    const uint32_t p = L[t];
-    for (int c = 0; c < sd; ++c)
-      nu[c] = __dadd_rn(nu[c], __dmul_rn(hp[p], (double)xr[(size_t)p * d + m * sd + c]));
-    de = __dadd_rn(de, ho[p]);
-  }
-  for (int c = 0; c < sd; ++c) num[(size_t)slot * sd + c] = nu[c];
-  den[slot] = de;
-}
 
-// k-means (unit weights) partial sums per slot
-__global__ void k_kmeans_partials(const float* xr, size_t n, int d, int M, int k, int sd,
-                                  const uint32_t* list, const uint32_t* start,
-                                  const uint32_t* count, const int* active, double* num,
-                                  double* den) {
-  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
-  if (slot >= M * k) return;
-  const int m = slot / k;
-  if (!active[m]) return;
-  const uint32_t* L = list + (size_t)m * n + start[slot];
-  const size_t cnt = count[slot];
-  double nu[16];
-  for (int c = 0; c < sd; ++c) nu[c] = 0.0;
-  double de = 0.0;
-  for (size_t t = 0; t < cnt; ++t) {
-    const uint32_t p = L[t];
-    for (int c = 0; c < sd; ++c)
-      nu[c] = __dadd_rn(nu[c], __dmul_rn(1.0, (double)xr[(size_t)p * d + m * sd + c]));
-    de = __dadd_rn(de, 1.0);
-  }
-  for (int c = 0; c < sd; ++c) num[(size_t)slot * sd + c] = nu[c];
-  den[slot] = de;
-}
 
 __global__ void k_copy_counts(const uint32_t* count, size_t total, uint32_t* out) {
   const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -153,10 +110,8 @@ int aq_dev_iso_partials(aq_dataset* ds, aq_codes* codes, const aq_weights* w, si
   if (ds->n) {
     st = build_buckets(codes, (int)k, &B);
     if (st == AQ_OK) {
-      k_iso_partials<<<(unsigned)((M * k + 127) / 128), 128, 0, s->stream>>>(
-          ds->xr, ds->n, (int)ds->d, (int)M, (int)k, (int)sd, B.list, B.start, B.count, pw.hp,
-          pw.ho, num_dev, den_dev);
-      s->launches++;
+      st = slot_sums_device(s, ds->xr, ds->n, (int)ds->d, (int)M, (int)k, (int)sd, B, nullptr,
+                            pw.hp, pw.ho, nullptr, num_dev, den_dev);
       if (usage_dev) {
         k_copy_counts<<<(unsigned)((M * k + 255) / 256), 256, 0, s->stream>>>(B.count, M * k,
                                                                               usage_dev);
@@ -222,6 +177,29 @@ int aq_dev_seq_sum(aq_session* s, const double* v_dev, size_t n, double init, do
   return AQ_OK;
 }
 
+// Sequential float64 sums of `rows` rows of `count` values (row r at
+// v_dev + r * ld), one launch; rows with active_host[r] == 0 give 0.
+int aq_dev_seq_sums(aq_session* s, const double* v_dev, size_t ld, size_t count, size_t rows,
+                    const int* active_host, double* out_host) {
+  AQ_TRY(check_session(s));
+  if (rows == 0) return AQ_OK;
+  int* act = nullptr;
+  double* d;
+  AQ_CUDA(cudaMallocAsync(&d, rows * sizeof(double), s->stream));
+  AQ_CUDA(cudaMemsetAsync(d, 0, rows * sizeof(double), s->stream));
+  if (active_host) {
+    AQ_CUDA(cudaMallocAsync(&act, rows * sizeof(int), s->stream));
+    AQ_CUDA(cudaMemcpyAsync(act, active_host, rows * sizeof(int), cudaMemcpyHostToDevice,
+                            s->stream));
+  }
+  AQ_TRY(seq_sums_device(s, v_dev, ld, count, (int)rows, act, d));
+  AQ_CUDA(cudaMemcpyAsync(out_host, d, rows * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+  cudaFreeAsync(d, s->stream);
+  if (act) cudaFreeAsync(act, s->stream);
+  AQ_CUDA(cudaStreamSynchronize(s->stream));
+  return AQ_OK;
+}
+
 // Local k-means partial sums per slot (unit weights) for active subspaces.
 int aq_dev_kmeans_partials(aq_dataset* ds, aq_codes* codes, size_t k, const int* active_host,
                            double* num_dev, double* den_dev, uint32_t* count_dev) {
@@ -239,10 +217,8 @@ int aq_dev_kmeans_partials(aq_dataset* ds, aq_codes* codes, size_t k, const int*
     Buckets B;
     st = build_buckets(codes, (int)k, &B);
     if (st == AQ_OK) {
-      k_kmeans_partials<<<(unsigned)((M * k + 127) / 128), 128, 0, s->stream>>>(
-          ds->xr, ds->n, (int)ds->d, (int)M, (int)k, (int)sd, B.list, B.start, B.count, act,
-          num_dev, den_dev);
-      s->launches++;
+      st = slot_sums_device(s, ds->xr, ds->n, (int)ds->d, (int)M, (int)k, (int)sd, B, act,
+                            nullptr, nullptr, nullptr, num_dev, den_dev);
       k_copy_counts<<<(unsigned)((M * k + 255) / 256), 256, 0, s->stream>>>(B.count, M * k,
                                                                             count_dev);
       s->launches++;

@@ -105,6 +105,16 @@ __global__ void k_seq_sums(const double* __restrict__ v, size_t ld, size_t count
   if (lane == 0) out[r] = s;
 }
 
+// `rows` sequential sums of `count` values each (row r at v + r * ld), rows
+// with active[r] == 0 skipped; out (device)
+int seq_sums_device(aq_session* s, const double* v, size_t ld, size_t count, int rows,
+                    const int* active_dev, double* out) {
+  k_seq_sums<<<(unsigned)((rows + 7) / 8), 256, 0, s->stream>>>(v, ld, count, rows, active_dev,
+                                                               out);
+  AQ_LAUNCHED(s);
+  return AQ_OK;
+}
+
 // std::accumulate(v, v + n, init) into *out (device), on the session stream
 int seq_sum_device(aq_session* s, const double* v, size_t n, double init, double* out) {
   k_seq_sums<<<1, 32, 0, s->stream>>>(v, n, n, 1, nullptr, out, init);
@@ -234,36 +244,51 @@ __global__ void __launch_bounds__(256) k_kmeans_assign_sd2(
 // mean = (sum 1.0 x) / (sum 1.0), members in ascending order. One warp per
 // slot: the lanes gather 32 members' sub-vectors into shared memory (all in
 // flight), lane 0 accumulates them in member order.
-template <int SDC>  // SDC > 0: compile-time sub_dimension (accumulators in registers)
-__global__ void k_kmeans_means(const float* __restrict__ xr, size_t n, int d, int M, int k,
-                               int sd_rt, const uint32_t* __restrict__ list,
-                               const uint32_t* __restrict__ start,
-                               const uint32_t* __restrict__ count,
-                               const int* __restrict__ active, double* __restrict__ dict) {
-  // One warp per slot. Rounds of 128 members: the lanes gather round r + 1
-  // (4 members each, in registers) while lane 0 adds round r in member order.
+// Per-slot sums over the slot's members in ascending point order (the
+// reference's loops): one warp per slot; rounds of 128 members — the lanes
+// gather round r + 1 (rows and, weighted, h_par / h_perp) into registers while
+// lane 0 adds round r in member order.
+//   kWeighted = false: num += 1.0 x, den += 1.0 (k-means, vq.hpp:151-162)
+//   kWeighted = true:  num += h_par x, den += h_perp (isotropic update,
+//                      pq.hpp:405-417)
+//   dict != null: dict = num / den for non-empty slots (weighted: den <= 0 is
+//                 a singular block); else num / den are written as partials.
+template <int SDC, bool kWeighted>
+__global__ void k_slot_sums(const float* __restrict__ xr, size_t n, int d, int M, int k,
+                            int sd_rt, const uint32_t* __restrict__ list,
+                            const uint32_t* __restrict__ start,
+                            const uint32_t* __restrict__ count, const int* __restrict__ active,
+                            const double* __restrict__ hp, const double* __restrict__ ho,
+                            double* __restrict__ dict, double* __restrict__ pnum,
+                            double* __restrict__ pden, DevError* err) {
   constexpr int SDM = SDC > 0 ? SDC : 16;
   constexpr int G = SDC > 0 ? 4 : 1, R = 32 * G;
   const int sd = SDC > 0 ? SDC : sd_rt;
   __shared__ float xs[4][2][R][SDM];
+  __shared__ double ws[4][2][kWeighted ? R : 1][2];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slot = blockIdx.x * (blockDim.x >> 5) + w;
   if (slot >= M * k) return;
   const int m = slot / k;
-  if (!active[m]) return;
+  if (active && !active[m]) return;
   const size_t cnt = count[slot];
-  if (cnt == 0) return;  // reseeded by the host walk
   const uint32_t* L = list + (size_t)m * n + start[slot];
   float nx[G][SDM];
+  double nh[G][2];
   auto fetch = [&](size_t r0) {
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const size_t t = r0 + g * 32 + lane;
       if (t < cnt) {
-        const float* xp = xr + (size_t)L[t] * d + m * sd;
+        const uint32_t p = L[t];
+        const float* xp = xr + (size_t)p * d + m * sd;
 #pragma unroll
         for (int c = 0; c < SDM; ++c)
           if (c < sd) nx[g][c] = xp[c];
+        if (kWeighted) {
+          nh[g][0] = hp[p];
+          nh[g][1] = ho[p];
+        }
       }
     }
   };
@@ -271,31 +296,71 @@ __global__ void k_kmeans_means(const float* __restrict__ xr, size_t n, int d, in
 #pragma unroll
   for (int c = 0; c < SDM; ++c) num[c] = 0.0;
   double den = 0.0;
-  fetch(0);
+  if (cnt) fetch(0);
   int cur = 0;
   for (size_t r0 = 0; r0 < cnt; r0 += R) {
 #pragma unroll
-    for (int g = 0; g < G; ++g)
+    for (int g = 0; g < G; ++g) {
 #pragma unroll
       for (int c = 0; c < SDM; ++c)
         if (c < sd) xs[w][cur][g * 32 + lane][c] = nx[g][c];
+      if (kWeighted) {
+        ws[w][cur][g * 32 + lane][0] = nh[g][0];
+        ws[w][cur][g * 32 + lane][1] = nh[g][1];
+      }
+    }
     __syncwarp();
     if (r0 + R < cnt) fetch(r0 + R);  // in flight during the chain below
     if (lane == 0) {
       const int nb = (int)min((size_t)R, cnt - r0);
       for (int b = 0; b < nb; ++b) {
+        const double a = kWeighted ? ws[w][cur][b][0] : 1.0;
+        const double o = kWeighted ? ws[w][cur][b][1] : 1.0;
 #pragma unroll
         for (int c = 0; c < SDM; ++c)
-          if (c < sd) num[c] = __dadd_rn(num[c], __dmul_rn(1.0, (double)xs[w][cur][b][c]));
-        den = __dadd_rn(den, 1.0);
+          if (c < sd) num[c] = __dadd_rn(num[c], __dmul_rn(a, (double)xs[w][cur][b][c]));
+        den = __dadd_rn(den, o);
       }
     }
     cur ^= 1;
   }
-  if (lane == 0)
+  if (lane != 0) return;
+  if (dict) {
+    if (cnt == 0) return;  // unused: reseeded (or kept) by the caller
+    if (kWeighted && den <= 0.0) {
+      report_error(err, (uint64_t)slot, AQ_E_SINGULAR_SYSTEM);
+      return;
+    }
 #pragma unroll
     for (int c = 0; c < SDM; ++c)
       if (c < sd) dict[(size_t)slot * sd + c] = __ddiv_rn(num[c], den);
+  } else {
+#pragma unroll
+    for (int c = 0; c < SDM; ++c)
+      if (c < sd) pnum[(size_t)slot * sd + c] = num[c];
+    pden[slot] = den;
+  }
+}
+
+// Host wrapper of k_slot_sums (hp == null: unit weights).
+int slot_sums_device(aq_session* s, const float* xr, size_t n, int d, int M, int k, int sd,
+                     const Buckets& B, const int* active, const double* hp, const double* ho,
+                     double* dict, double* pnum, double* pden) {
+  const unsigned grid = (unsigned)((M * k + 3) / 4);
+#define AQ_SLOTS(SDV, WV)                                                                \
+  k_slot_sums<SDV, WV><<<grid, 128, 0, s->stream>>>(xr, n, d, M, k, sd, B.list, B.start, \
+                                                    B.count, active, hp, ho, dict, pnum, \
+                                                    pden, s->err)
+  if (sd == 2) {
+    if (hp) AQ_SLOTS(2, true);
+    else AQ_SLOTS(2, false);
+  } else {
+    if (hp) AQ_SLOTS(0, true);
+    else AQ_SLOTS(0, false);
+  }
+#undef AQ_SLOTS
+  AQ_LAUNCHED(s);
+  return AQ_OK;
 }
 
 // empty partitions (vq.hpp:284-292): j ascending, consuming the ranking
@@ -398,12 +463,8 @@ int train_l2_pq_device(aq_dataset* ds, size_t M, size_t k, const aq_train_config
     st = build_buckets(codes, (int)k, &B);
     if (st != AQ_OK) break;
     AQ_CUDA(cudaMemcpyAsync(active, hact.data(), M * sizeof(int), cudaMemcpyHostToDevice, s->stream));
-    if (sd == 2)
-      k_kmeans_means<2><<<(unsigned)((M * k + 3) / 4), 128, 0, s->stream>>>(
-          ds->xr, n, (int)d, (int)M, (int)k, (int)sd, B.list, B.start, B.count, active, cb->d64);
-    else
-      k_kmeans_means<0><<<(unsigned)((M * k + 3) / 4), 128, 0, s->stream>>>(
-          ds->xr, n, (int)d, (int)M, (int)k, (int)sd, B.list, B.start, B.count, active, cb->d64);
+    AQ_TRY(slot_sums_device(s, ds->xr, n, (int)d, (int)M, (int)k, (int)sd, B, active, nullptr,
+                            nullptr, cb->d64, nullptr, nullptr));
     s->launches++;
     if (cfg->empty_partition_policy == 0) {
       std::vector<uint32_t> hc(M * k);

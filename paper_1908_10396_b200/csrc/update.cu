@@ -735,31 +735,6 @@ int llt_solve_device(aq_session* s, double* A, int n, double* x) {
 
 // ---- isotropic weighted means (pq.hpp:405-423) ------------------------------------------
 
-__global__ void k_iso_means(const float* xr, size_t n, int d, int M, int k, int sd,
-                            const uint32_t* list, const uint32_t* start,
-                            const uint32_t* count, const double* hp, const double* ho,
-                            double* dict, DevError* err) {
-  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
-  if (slot >= M * k) return;
-  const int m = slot / k;
-  const uint32_t* L = list + (size_t)m * n + start[slot];
-  const size_t cnt = count[slot];
-  if (cnt == 0) return;
-  double num[16];
-  for (int c = 0; c < sd; ++c) num[c] = 0.0;
-  double den = 0.0;
-  for (size_t t = 0; t < cnt; ++t) {
-    const uint32_t p = L[t];
-    for (int c = 0; c < sd; ++c)
-      num[c] = __dadd_rn(num[c], __dmul_rn(hp[p], (double)xr[(size_t)p * d + m * sd + c]));
-    den = __dadd_rn(den, ho[p]);
-  }
-  if (den <= 0.0) {
-    report_error(err, (uint64_t)slot, AQ_E_SINGULAR_SYSTEM);
-    return;
-  }
-  for (int c = 0; c < sd; ++c) dict[(size_t)slot * sd + c] = __ddiv_rn(num[c], den);
-}
 
 // ---- M == 1: update_codeword per codeword (vq.hpp:139-192) -------------------------------
 // One CTA per codeword j. Its members (points with code j, ascending) feed
@@ -1083,11 +1058,9 @@ int aq_dev_pq_codebook_update(aq_dataset* ds, aq_codes* codes, const aq_weights*
     if (modes) cudaFreeAsync(modes, s->stream);
   } else if (st == AQ_OK && all_iso) {
     AQ_TRY(clear_dev_error(s));
-    k_iso_means<<<(unsigned)((M * k + 127) / 128), 128, 0, s->stream>>>(
-        ds->xr, n, (int)ds->d, (int)M, (int)k, sd, B.list, B.start, B.count, pw.hp, pw.ho,
-        out->d64, s->err);
-    s->launches++;
-    st = sync_and_check(s, "zero total weight in block");
+    st = slot_sums_device(s, ds->xr, n, (int)ds->d, (int)M, (int)k, sd, B, nullptr, pw.hp, pw.ho,
+                          out->d64, nullptr, nullptr);
+    if (st == AQ_OK) st = sync_and_check(s, "zero total weight in block");
   } else if (st == AQ_OK) {
     if (dim > 16384) {
       st = ref_error(AQ_E_INVALID_ARGUMENT,

@@ -287,10 +287,14 @@ class ShardedTrainer:
             losses, changes = self._do(self.sh.kmeans_assign, active)
             chg = self.comm.int_sum(torch.as_tensor(changes, dtype=torch.int64,
                                                     device=self.sh.device)).tolist()
-            loc = self._do(lambda: [self.sh.seq_sum(losses[m]) if active[m] else 0.0
-                                    for m in range(M)])
-            tot = self.comm.ordered_sum(torch.tensor(loc, dtype=torch.float64,
-                                                     device=self.sh.device)).tolist()
+            # totals only feed the relative-tolerance test (vq.hpp:316-321;
+            # train_l2_pq discards the histories)
+            if cfg.relative_tolerance > 0.0:
+                loc = self._do(self.sh.seq_sums, losses, active)
+                tot = self.comm.ordered_sum(torch.tensor(loc, dtype=torch.float64,
+                                                         device=self.sh.device)).tolist()
+            else:
+                tot = [0.0] * M
             return losses, chg, tot
 
         losses, chg, tot = assign()
@@ -508,6 +512,16 @@ class DeviceShard:
         self._call("aq_dev_seq_sum", self.s.h, v.data_ptr(), v.numel(), 0.0,
                    self._C.byref(out))
         return out.value
+
+    def seq_sums(self, losses: torch.Tensor, active: list) -> list:
+        """Row-wise sequential sums of losses [rows, n] (0 for inactive rows)."""
+        v = losses.contiguous()
+        rows, cnt = v.shape
+        act = np.asarray(active, np.int32)
+        out = np.zeros(rows, np.float64)
+        self._call("aq_dev_seq_sums", self.s.h, v.data_ptr(), cnt, cnt, rows, act.ctypes.data,
+                   out.ctypes.data)
+        return out.tolist()
 
     def ranking(self, losses: torch.Tensor, top: int):
         idx = torch.arange(self.n, dtype=torch.int32, device=self.device)

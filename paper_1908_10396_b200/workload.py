@@ -82,11 +82,15 @@ def config1(n: int = 20_000, nq: int = 100, seed: int = 0) -> Workload:
     return Workload("config1", base, q, 16, 16, T_DEFAULT, iterations=10, n=n)
 
 
-def config2(n: int = 1_183_514, nq: int = 10_000, seed: int = 0) -> Workload:
-    """1000-component mixture, sigma 0.5, Zipf(1.1) weights, d 100, normalised; M 50."""
+def config2(n: int = 1_183_514, nq: int = 10_000, seed: int = 0, shard: int = 0) -> Workload:
+    """1000-component mixture, sigma 0.5, Zipf(1.1) weights, d 100, normalised; M 50.
+
+    `shard` > 0 draws other rows of the same distribution (row shards of one
+    dataset on several GPUs); the queries are the same for every shard."""
     means = _rng(seed, 1000).standard_normal((1000, 100))
     w = zipf_weights(1000, 1.1)
-    base = gaussian_mixture(n, 100, 1000, 0.5, seed, 1, weights=w, means=means)
+    base = gaussian_mixture(n, 100, 1000, 0.5, seed, 1 if shard == 0 else 10_000 + shard,
+                            weights=w, means=means)
     q = gaussian_mixture(nq, 100, 1000, 0.5, seed, 2, weights=w, means=means)
     return Workload("config2", base, q, 50, 16, T_DEFAULT, iterations=10, n=n)
 

@@ -75,6 +75,9 @@ class OracleShard:
         a = v.numpy()
         return float(np.add.accumulate(a)[-1]) if a.size else 0.0
 
+    def seq_sums(self, losses, active):
+        return [self.seq_sum(losses[m]) if active[m] else 0.0 for m in range(losses.shape[0])]
+
     def ranking(self, losses, top):
         v = losses.numpy()
         idx = np.arange(v.size)

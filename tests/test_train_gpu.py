@@ -84,3 +84,22 @@ def test_train_validation():
         aq.train_apq(np.zeros((0, 6), np.float32), 2, 2, aq.AnisotropicWeights(), aq.TrainConfig())
     with pytest.raises(aq.InvalidArgument):
         aq.train_apq(x, 2, 11, aq.AnisotropicWeights(), aq.TrainConfig())
+
+
+def test_k64_byte_codes_end_to_end():
+    """k = 64 (8-bit codes): every stage on its non-specialised path —
+    generic encoder, generic normal-equation assembly, k-means, ADC exact
+    fallback — bit-identical to the oracle."""
+    x = mixture_rows(3000, 16, 71, centers=24)
+    hp, ho = threshold_hp_ho(x, 0.2)
+    cfg = aq.TrainConfig(max_iterations=3, relative_tolerance=0.0, seed=5)
+    cb, codes = aq.train_apq(x, 8, 64, aq.ThresholdWeights(0.2, "parallel_only"), cfg)
+    want_cb, want_codes, _ = P.train_apq(x.astype(np.float64), 8, 64, hp, ho, max_it=3, tol=0.0,
+                                         seed=5)
+    assert np.array_equal(cb.dictionaries, want_cb)
+    assert np.array_equal(codes.codes, want_codes)
+    q = np.random.default_rng(2).standard_normal((5, 16))
+    s = aq.Session.default()
+    ids, sc = aq.dev_adc_search(s.upload_codes(codes), s.upload_codebook(cb), q, 20)
+    wi, ws = P.adc_search_batch(q, want_codes, 64, want_cb, 8, 64, 2, 20)
+    assert np.array_equal(ids, wi) and np.array_equal(sc, ws)

@@ -68,7 +68,13 @@ int aq_dev_normal_equations_partial(aq_dataset* ds, aq_codes* codes, const aq_we
   const size_t M = codes->M, dim = k * ds->d;
   void* owner = nullptr;
   PointW pw;
-  AQ_TRY(point_weights(ds, w, &pw, &owner));
+  {
+    const int pst = point_weights(ds, w, &pw, &owner);
+    if (pst != AQ_OK) {  // validation failures leave no allocation behind
+      if (owner) cudaFreeAsync(owner, s->stream);
+      return pst;
+    }
+  }
   Buckets B;
   int st = AQ_OK;
   if (ds->n) st = build_buckets(codes, (int)k, &B);
@@ -104,7 +110,13 @@ int aq_dev_iso_partials(aq_dataset* ds, aq_codes* codes, const aq_weights* w, si
   const size_t M = codes->M, sd = ds->d / M;
   void* owner = nullptr;
   PointW pw;
-  AQ_TRY(point_weights(ds, w, &pw, &owner));
+  {
+    const int pst = point_weights(ds, w, &pw, &owner);
+    if (pst != AQ_OK) {  // validation failures leave no allocation behind
+      if (owner) cudaFreeAsync(owner, s->stream);
+      return pst;
+    }
+  }
   Buckets B;
   int st = AQ_OK;
   if (ds->n) {

@@ -966,7 +966,13 @@ int aq_dev_assemble_selector_system(aq_dataset* ds, aq_codes* codes, const aq_we
   const size_t dim = (size_t)k * ds->d;
   void* owner = nullptr;
   PointW pw;
-  AQ_TRY(point_weights(ds, w, &pw, &owner));
+  {
+    const int pst = point_weights(ds, w, &pw, &owner);
+    if (pst != AQ_OK) {  // validation failures leave no allocation behind
+      if (owner) cudaFreeAsync(owner, s->stream);
+      return pst;
+    }
+  }
   int st = AQ_OK;
   if (pw.flags[1] != ~0ull) {
     char msg[128];

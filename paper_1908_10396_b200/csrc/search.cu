@@ -31,9 +31,11 @@ struct AdcShape {
   int qp, tile, minb;
   bool gbuf;  // candidate windows in global memory (L2) instead of shared
 };
-constexpr AdcShape kShapes[] = {{8, 256, 2, false}, {8, 256, 4, true},  {4, 256, 6, true},
-                                {4, 256, 8, true},   {8, 256, 3, true},  {8, 128, 8, true},
-                                {6, 256, 4, true},   {12, 256, 3, true}};
+// 1 (default): windows in global memory, 4 CTAs/SM; 0: shared-memory windows
+// (the first design, kept as a reference point); 2: 2 query pairs, 6 CTAs/SM.
+// The others measured in this round (6 or 12 query pairs, 3 CTAs/SM, 8-bit
+// entries) were slower on config 2 and were dropped.
+constexpr AdcShape kShapes[] = {{8, 256, 2, false}, {8, 256, 4, true}, {4, 256, 6, true}};
 constexpr int kGbPointsPerThread = 4;  // points per thread between barriers (GB)
 constexpr int kNumShapes = sizeof(kShapes) / sizeof(kShapes[0]);
 constexpr int kLutQP = 16;  // lut kernel of the single-query host entry
@@ -549,13 +551,8 @@ int adc_search_device(aq_codes* codes, aq_codebook* cb, const double* Qd,
 #define AQ_SCORE_V(MM)                                                  \
   switch (variant) {                                                   \
     case 0: AQ_SCORE_LAUNCH(MM, 8, 256, 2, false); break;              \
-    case 1: AQ_SCORE_LAUNCH(MM, 8, 256, 4, true); break;               \
     case 2: AQ_SCORE_LAUNCH(MM, 4, 256, 6, true); break;               \
-    case 3: AQ_SCORE_LAUNCH(MM, 4, 256, 8, true); break;               \
-    case 4: AQ_SCORE_LAUNCH(MM, 8, 256, 3, true); break;               \
-    case 5: AQ_SCORE_LAUNCH(MM, 8, 128, 8, true); break;               \
-    case 6: AQ_SCORE_LAUNCH(MM, 6, 256, 4, true); break;               \
-    default: AQ_SCORE_LAUNCH(MM, 12, 256, 3, true); break;             \
+    default: AQ_SCORE_LAUNCH(MM, 8, 256, 4, true); break;              \
   }
 #define AQ_SCORE_M(MM) \
   case MM:             \

@@ -9,7 +9,7 @@ import ctypes as C
 n = int(float(sys.argv[1])) if len(sys.argv) > 1 else 1_183_514
 nq = int(sys.argv[2]) if len(sys.argv) > 2 else 10_000
 M = int(sys.argv[3]) if len(sys.argv) > 3 else 50
-variants = [int(v) for v in (sys.argv[4].split(",") if len(sys.argv) > 4 else "1,4,5,6,7,0,2,3".split(","))]
+variants = [int(v) for v in (sys.argv[4].split(",") if len(sys.argv) > 4 else "1,0,2".split(","))]
 g = np.random.default_rng(0)
 codes = g.integers(0, 16, (n, M), dtype=np.uint32)
 cb = g.standard_normal(M * 16 * 2) * 0.3

@@ -265,6 +265,34 @@ int aq_dev_train_apq(aq_dataset* ds, size_t M, size_t k, const aq_weights* w,
                      aq_codebook** cb_out, aq_codes** codes_out,
                      double* loss_history_out, size_t* history_len);
 
+/* ---- host-pointer forms (the reference's by-value semantics) ------------- */
+/* adc_search over nq queries: ids/scores nq x min(topn, n) */
+int aq_adc_search_batch(aq_session* s, const double* queries, size_t nq, size_t d,
+                        const uint32_t* codes, size_t n, size_t M, size_t codes_k,
+                        const double* dictionaries, size_t cb_M, size_t k,
+                        size_t sub_dimension, size_t topn, uint32_t* ids_out,
+                        double* scores_out);
+/* exact-dot rerank of ncand candidates per query, keep min(keep, ncand) */
+int aq_rerank(aq_session* s, const double* queries, size_t nq, const float* x,
+              size_t n, size_t d, const uint32_t* cand_ids, size_t ncand,
+              size_t keep, uint32_t* ids_out, double* scores_out);
+/* exact_ground_truth: exact top-min(depth, n) per query */
+int aq_exact_search_batch(aq_session* s, const double* queries, size_t nq,
+                          const float* x, size_t n, size_t d, size_t depth,
+                          uint32_t* ids_out, double* scores_out);
+/* assemble_selector_system: A_out (k d)^2 row-major, rhs_out k d */
+int aq_assemble_selector_system(aq_session* s, const float* x, size_t n, size_t d,
+                                const uint32_t* codes, size_t M, size_t k,
+                                const aq_weights* w, double* A_out, double* rhs_out);
+/* train_l2_pq / train_apq: dictionaries M k (d / M) float64, codes n x M */
+int aq_train_l2_pq(aq_session* s, const float* x, size_t n, size_t d, size_t M,
+                   size_t k, const aq_train_config* cfg, double* dictionaries_out,
+                   uint32_t* codes_out);
+int aq_train_apq(aq_session* s, const float* x, size_t n, size_t d, size_t M, size_t k,
+                 const aq_weights* w, const aq_train_config* cfg, int warm_start,
+                 double* dictionaries_out, uint32_t* codes_out,
+                 double* loss_history_out, size_t* history_len);
+
 /* ---- row-sharded training building blocks (multi-GPU) -----
  * The reference trains in one process (pq.hpp:513-575); a sharded trainer
  * splits its sums by rows: every rank computes the partial quantities below

@@ -92,6 +92,14 @@ _SIGS = {
     "aq_dev_train_l2_pq": (_I, [_VP, _SZ, _SZ, _VP, _PP, _PP]),
     "aq_debug_exact_window_count": (_I, [_VP, _I, _VP]),
     "aq_dev_train_apq": (_I, [_VP, _SZ, _SZ, _VP, _VP, _I, _PP, _PP, _VP, _VP]),
+    # host-pointer forms
+    "aq_adc_search_batch": (_I, [_VP, _VP, _SZ, _SZ, _VP, _SZ, _SZ, _SZ, _VP, _SZ, _SZ, _SZ, _SZ,
+                                 _VP, _VP]),
+    "aq_rerank": (_I, [_VP, _VP, _SZ, _VP, _SZ, _SZ, _VP, _SZ, _SZ, _VP, _VP]),
+    "aq_exact_search_batch": (_I, [_VP, _VP, _SZ, _VP, _SZ, _SZ, _SZ, _VP, _VP]),
+    "aq_assemble_selector_system": (_I, [_VP, _VP, _SZ, _SZ, _VP, _SZ, _SZ, _VP, _VP, _VP]),
+    "aq_train_l2_pq": (_I, [_VP, _VP, _SZ, _SZ, _SZ, _SZ, _VP, _VP, _VP]),
+    "aq_train_apq": (_I, [_VP, _VP, _SZ, _SZ, _SZ, _SZ, _VP, _VP, _I, _VP, _VP, _VP, _VP]),
     # row-sharded training building blocks
     "aq_dev_weight_flags": (_I, [_VP, _VP, _VP]),
     "aq_dev_normal_equations_partial": (_I, [_VP, _VP, _VP, _SZ, _VP, _VP, _VP, _VP]),

@@ -1,6 +1,7 @@
 // Host-pointer entry points: the reference's by-value semantics (inputs in,
 // owning outputs back) built from the device-resident API. Validation order
 // follows the reference function each one replaces.
+#include <algorithm>
 #include <memory>
 #include <vector>
 
@@ -77,6 +78,89 @@ int aq_pq_assign_pass(aq_session* s, const float* x, size_t n, size_t d,
   if (losses) cudaFreeAsync(losses, s->stream);
   cudaStreamSynchronize(s->stream);
   return st;
+}
+
+// adc_search over a query batch (index.hpp:118-134 per query; evaluate runs
+// it per query, index.hpp:251-259): ids/scores nq x min(topn, n).
+int aq_adc_search_batch(aq_session* s, const double* queries, size_t nq, size_t d,
+                        const uint32_t* codes, size_t n, size_t M, size_t codes_k,
+                        const double* dict, size_t cb_M, size_t k, size_t sd, size_t topn,
+                        uint32_t* ids_out, double* scores_out) {
+  AQ_TRY(check_session(s));
+  if (n == 0) return ref_error(AQ_E_EMPTY_INDEX, "no quantized datapoints");
+  if (topn < 1) return ref_error(AQ_E_INVALID_ARGUMENT, "topn must be >= 1");
+  if (M != cb_M || codes_k > k)
+    return ref_error(AQ_E_DIMENSION_MISMATCH, "code matrix does not match codebook");
+  if (d != cb_M * sd)
+    return ref_error(AQ_E_DIMENSION_MISMATCH, "query dimension does not match codebook");
+  CbGuard cb;
+  CodesGuard cm;
+  AQ_TRY(aq_codebook_upload(s, dict, cb_M, k, sd, &cb.p));
+  AQ_TRY(aq_codes_upload(s, codes, n, M, std::max<size_t>(codes_k, 1), &cm.p));
+  return aq_dev_adc_search(cm.p, cb.p, queries, nq, topn, ids_out, scores_out);
+}
+
+// exact-dot rerank of candidate lists (north_star), host pointers.
+int aq_rerank(aq_session* s, const double* queries, size_t nq, const float* x, size_t n,
+              size_t d, const uint32_t* cand_ids, size_t ncand, size_t keep,
+              uint32_t* ids_out, double* scores_out) {
+  AQ_TRY(check_session(s));
+  DsGuard ds;
+  AQ_TRY(aq_dataset_upload(s, x, n, d, &ds.p));
+  return aq_dev_rerank(ds.p, queries, nq, cand_ids, ncand, keep, ids_out, scores_out);
+}
+
+// exact_ground_truth (index.hpp:150-162): exact top-`depth` per query.
+int aq_exact_search_batch(aq_session* s, const double* queries, size_t nq, const float* x,
+                          size_t n, size_t d, size_t depth, uint32_t* ids_out,
+                          double* scores_out) {
+  AQ_TRY(check_session(s));
+  DsGuard ds;
+  AQ_TRY(aq_dataset_upload(s, x, n, d, &ds.p));
+  return aq_dev_exact_search(ds.p, queries, nq, depth, ids_out, scores_out);
+}
+
+// assemble_selector_system (pq.hpp:290-343): full (k d)^2 matrix row-major.
+int aq_assemble_selector_system(aq_session* s, const float* x, size_t n, size_t d,
+                                const uint32_t* codes, size_t M, size_t k,
+                                const aq_weights* w, double* A_out, double* rhs_out) {
+  AQ_TRY(check_session(s));
+  if (M == 0 || d % M != 0)
+    return ref_error(AQ_E_DIMENSION_NOT_DIVISIBLE, "dimension not divisible by M");
+  DsGuard ds;
+  CodesGuard cm;
+  AQ_TRY(aq_dataset_upload(s, x, n, d, &ds.p));
+  AQ_TRY(aq_codes_upload(s, codes, n, M, k, &cm.p));
+  return aq_dev_assemble_selector_system(ds.p, cm.p, w, A_out, rhs_out);
+}
+
+// train_l2_pq (pq.hpp:469-501): dictionaries M k (d / M), codes n x M.
+int aq_train_l2_pq(aq_session* s, const float* x, size_t n, size_t d, size_t M, size_t k,
+                   const aq_train_config* cfg, double* dict_out, uint32_t* codes_out) {
+  AQ_TRY(check_session(s));
+  DsGuard ds;
+  CbGuard cb;
+  CodesGuard cm;
+  AQ_TRY(aq_dataset_upload(s, x, n, d, &ds.p));
+  AQ_TRY(aq_dev_train_l2_pq(ds.p, M, k, cfg, &cb.p, &cm.p));
+  AQ_TRY(aq_codebook_download(cb.p, dict_out));
+  return aq_codes_download(cm.p, codes_out);
+}
+
+// train_apq (pq.hpp:513-575); history_out holds max_iterations + 1 values.
+int aq_train_apq(aq_session* s, const float* x, size_t n, size_t d, size_t M, size_t k,
+                 const aq_weights* w, const aq_train_config* cfg, int warm_start,
+                 double* dict_out, uint32_t* codes_out, double* history_out,
+                 size_t* history_len) {
+  AQ_TRY(check_session(s));
+  DsGuard ds;
+  CbGuard cb;
+  CodesGuard cm;
+  AQ_TRY(aq_dataset_upload(s, x, n, d, &ds.p));
+  AQ_TRY(aq_dev_train_apq(ds.p, M, k, w, cfg, warm_start, &cb.p, &cm.p, history_out,
+                          history_len));
+  AQ_TRY(aq_codebook_download(cb.p, dict_out));
+  return aq_codes_download(cm.p, codes_out);
 }
 
 }  // extern "C"

@@ -4,7 +4,9 @@
 #pragma once
 
 #include <cmath>
+#include <cstddef>
 #include <limits>
+#include <span>
 
 #include "error.hpp"
 
@@ -43,5 +45,16 @@ inline double eta_limit(double threshold, double norm, int d) {
   const double rho = (threshold / norm) * (threshold / norm);
   return static_cast<double>(d - 1) * rho / (1.0 - rho);
 }
+
+namespace detail {
+// geometry.hpp:170-176: inner product / squared norm in ascending component
+// order (the host side of evaluate's relative error)
+inline double dot(std::span<const double> a, std::span<const double> b) {
+  double s = 0.0;
+  for (std::size_t j = 0; j < a.size(); ++j) s += a[j] * b[j];
+  return s;
+}
+inline double norm2(std::span<const double> a) { return dot(a, a); }
+}  // namespace detail
 
 }  // namespace anisoq

@@ -258,6 +258,44 @@ int main() {
     const auto self = exact_search(data.row(17), data, 1);
     CHECK(self.hits[0].index == 17);
   }
+  // evaluate (test_index.cpp:189-263): perfect codes give recall 1 and zero
+  // error; validation and ground-truth checks
+  {
+    Gen g{13};
+    ProductCodebook cb;
+    cb.M = 2;
+    cb.k = 4;
+    cb.sub_dimension = 3;
+    cb.dictionaries.resize(24);
+    for (auto& v : cb.dictionaries) v = std::round(g.gauss() * 64) / 64;
+    CodeMatrix codes;
+    codes.n = 16;
+    codes.M = 2;
+    codes.k = 4;
+    for (std::size_t i = 0; i < 16; ++i) codes.codes.push_back((std::uint32_t)(g.u64() % 4)),
+                                         codes.codes.push_back((std::uint32_t)(g.u64() % 4));
+    std::vector<double> dv;
+    for (std::size_t i = 0; i < 16; ++i) {
+      const auto r = reconstruct(codes.row(i), cb);
+      dv.insert(dv.end(), r.begin(), r.end());
+    }
+    const Dataset data = make_dataset(16, 6, dv, false);
+    std::vector<double> qv;
+    for (int i = 0; i < 20 * 6; ++i) qv.push_back((double)(float)g.gauss());
+    const Dataset queries = make_dataset(20, 6, qv, false);
+    EvalOptions opt;
+    opt.recall_ns = {1, 10};
+    const auto rep = evaluate(queries, data, codes, cb, opt);
+    CHECK(rep.num_queries == 20 && rep.num_datapoints == 16);
+    CHECK(rep.recall_1_at_n.at(1) == 1.0 && rep.recall_1_at_n.at(10) == 1.0);
+    CHECK(rep.recall_k_at_k == 1.0 && rep.relative_error_max == 0.0);
+    std::vector<std::vector<std::int32_t>> short_rows(4, std::vector<std::int32_t>{0});
+    opt.ground_truth = &short_rows;
+    CHECK_THROWS_AS(evaluate(queries, data, codes, cb, opt), GroundTruthMismatch);
+    opt.ground_truth = nullptr;
+    opt.recall_ns.clear();
+    CHECK_THROWS_AS(evaluate(queries, data, codes, cb, opt), InvalidArgument);
+  }
   std::printf("dropin: %d passed, %d failed\n", g_pass, g_fail);
   return g_fail ? 1 : 0;
 }

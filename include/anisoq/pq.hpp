@@ -72,6 +72,24 @@ struct SelectorSystem {
   DenseVector rhs;
 };
 
+// VQ <-> M = 1 product codebook (pq.hpp:76-92)
+inline ProductCodebook to_product(const Codebook& cb) {
+  ProductCodebook out;
+  out.M = 1;
+  out.k = cb.k;
+  out.sub_dimension = cb.d;
+  out.dictionaries = cb.codewords;
+  return out;
+}
+inline Codebook to_vq(const ProductCodebook& cb) {
+  if (cb.M != 1) throw InvalidArgument("to_vq requires M == 1");
+  Codebook out;
+  out.k = cb.k;
+  out.d = cb.sub_dimension;
+  out.codewords = cb.dictionaries;
+  return out;
+}
+
 inline std::vector<double> reconstruct(std::span<const std::uint32_t> codes_row,
                                        const ProductCodebook& cb) {
   if (codes_row.size() != cb.M) throw DimensionMismatch("need one code per subspace");

@@ -1,9 +1,22 @@
 // anisoq drop-in (B200): trainer configuration (reference vq.hpp:55-69).
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
+#include <span>
+#include <vector>
 
 namespace anisoq {
+
+// A single (M = 1) codebook (reference vq.hpp:32-43): k codewords of dimension d.
+struct Codebook {
+  std::size_t k = 0;
+  std::size_t d = 0;
+  std::vector<double> codewords;  // row-major k*d
+
+  std::span<const double> row(std::size_t j) const { return {codewords.data() + j * d, d}; }
+  std::span<double> mutable_row(std::size_t j) { return {codewords.data() + j * d, d}; }
+};
 
 enum class EmptyPartitionPolicy { reseed_highest_loss, keep_previous };
 

@@ -34,7 +34,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "ADC scores/sec (query x point) + anisotropic-encode points/sec, % HBM roofline"
+METRIC = "ADC scores/sec (query\u00d7point) + anisotropic-encode points/sec, % HBM roofline"  # BASELINE.json
 UNIT = "scores/s"
 
 

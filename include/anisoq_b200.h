@@ -40,6 +40,10 @@
  *   - All calls are synchronous with respect to the host, like the reference.
  *     Device-resident variants (aq_dev_*) operate on session-owned buffers
  *     and are stream-ordered on the session stream.
+ *   - Threads: a session (its stream, scratch buffers and the objects created
+ *     from it) must be used by one thread at a time; concurrent callers use
+ *     one session each (several sessions may share a device). The last-error
+ *     message is per thread.
  */
 #ifndef ANISOQ_B200_H_
 #define ANISOQ_B200_H_

@@ -104,6 +104,9 @@ __global__ void k_bucket_offsets(const unsigned* __restrict__ base, size_t nb, i
 int build_buckets(aq_codes* c, int k, Buckets* B) {
   aq_session* s = c->s;
   const size_t n = c->n, M = c->M;
+  // list offsets are 32-bit (the scan and the per-slot starts)
+  if (n * M >= (size_t)UINT32_MAX)
+    return ref_error(AQ_E_UNSUPPORTED, "device codebook update / trainers need n * M < 2^32");
   const int K = k;
   const size_t nb = (n + kBucketBlock - 1) / kBucketBlock;
   void* p;

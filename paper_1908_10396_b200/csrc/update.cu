@@ -104,9 +104,9 @@ __global__ void k_bucket_offsets(const unsigned* __restrict__ base, size_t nb, i
 int build_buckets(aq_codes* c, int k, Buckets* B) {
   aq_session* s = c->s;
   const size_t n = c->n, M = c->M;
-  // list offsets are 32-bit (the scan and the per-slot starts)
-  if (n * M >= (size_t)UINT32_MAX)
-    return ref_error(AQ_E_UNSUPPORTED, "device codebook update / trainers need n * M < 2^32");
+  // Offsets are scanned globally over [m][j][block] in 32-bit arithmetic; when
+  // n M >= 2^32 they wrap, but every consumer subtracts m n in the same
+  // modular arithmetic and the local offsets (< n) come out exact.
   const int K = k;
   const size_t nb = (n + kBucketBlock - 1) / kBucketBlock;
   void* p;

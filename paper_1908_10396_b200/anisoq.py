@@ -872,3 +872,117 @@ def write_ivecs(rows, path: str) -> None:
         for r in rows:
             r = np.asarray(r, "<i4")
             f.write(_struct.pack("<i", r.size) + r.tobytes())
+
+
+# ---- host generator and dataset helpers (rng.hpp:28-89, dataset.hpp:225-290) -------------
+
+
+class Rng:
+    """The reference generator contract (rng.hpp): splitmix64, 53-bit uniform
+    doubles, unbiased next_below, Box-Muller normals with one cached spare,
+    sample_distinct = first k of a partial Fisher-Yates shuffle of [0, n)."""
+
+    _M = (1 << 64) - 1
+
+    def __init__(self, seed: int):
+        self._s = seed & self._M
+        self._spare = None
+
+    def next_u64(self) -> int:
+        self._s = (self._s + 0x9E3779B97F4A7C15) & self._M
+        z = self._s
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & self._M
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & self._M
+        return z ^ (z >> 31)
+
+    def next_double(self) -> float:
+        return (self.next_u64() >> 11) * 2.0 ** -53
+
+    def next_below(self, n: int) -> int:
+        reject_below = ((1 << 64) - n) % n
+        while True:
+            r = self.next_u64()
+            if r >= reject_below:
+                return r % n
+
+    def next_gaussian(self) -> float:
+        if self._spare is not None:
+            v, self._spare = self._spare, None
+            return v
+        u1 = self.next_double()
+        while u1 <= 0.0:
+            u1 = self.next_double()
+        u2 = self.next_double()
+        radius = math.sqrt(-2.0 * math.log(u1))
+        angle = 6.283185307179586476925286766559 * u2
+        self._spare = radius * math.sin(angle)
+        return radius * math.cos(angle)
+
+    def sample_distinct(self, n: int, k: int) -> list:
+        moved: dict = {}
+        out = []
+        for i in range(min(k, n)):
+            j = i + self.next_below(n - i)
+            vi, vj = moved.get(i, i), moved.get(j, j)
+            moved[i], moved[j] = vj, vi
+            out.append(vj)
+        return out
+
+
+def generate_synthetic(kind: str, n: int, d: int, seed: int, centers: int = 16,
+                       spread: float = 0.25, normalize: bool = False) -> Dataset:
+    """dataset.hpp:245-290: 'uniform_sphere' or 'gaussian_mixture', one Rng
+    stream, values rounded to float32 (device-exact). Pure host code (slow for
+    large n; the bench uses workload.py's vectorised generators)."""
+    if n < 1 or d < 2:
+        raise InvalidArgument("InvalidArgument: need n >= 1 and d >= 2")
+    r = Rng(seed)
+    v = np.empty((n, d), np.float64)
+
+    def unit_row():
+        while True:
+            row = [r.next_gaussian() for _ in range(d)]
+            ss = 0.0
+            for t in row:
+                ss += t * t
+            if ss != 0.0:
+                inv = 1.0 / math.sqrt(ss)
+                return [t * inv for t in row]
+
+    if kind == "uniform_sphere":
+        for i in range(n):
+            v[i] = unit_row()
+        normalized = True
+    elif kind == "gaussian_mixture":
+        if centers < 1:
+            raise InvalidArgument("InvalidArgument: need at least one center")
+        ctr = [unit_row() for _ in range(centers)]
+        for i in range(n):
+            c = ctr[r.next_below(centers)]
+            row = [c[j] + spread * r.next_gaussian() for j in range(d)]
+            if normalize:
+                ss = 0.0
+                for t in row:
+                    ss += t * t
+                if ss == 0.0:
+                    raise ZeroNormDatapoint("ZeroNormDatapoint: degenerate mixture sample")
+                inv = 1.0 / math.sqrt(ss)
+                row = [t * inv for t in row]
+            v[i] = row
+        normalized = normalize
+    else:
+        raise InvalidArgument(f"InvalidArgument: unknown kind {kind!r}")
+    ds = Dataset(v.astype(np.float32).astype(np.float64))
+    ds.normalized = normalized
+    return ds
+
+
+def unit_normalize(ds: Dataset) -> np.ndarray:
+    """dataset.hpp:225-236: rows scaled to unit norm (float64; generally not
+    float32-exact, so the device path would refuse the result)."""
+    x = np.asarray(ds.values if isinstance(ds, Dataset) else ds, np.float64)
+    norms = np.sqrt(np.add.accumulate(x * x, axis=1)[:, -1])  # dataset.hpp:55-59 order
+    if np.any(norms == 0.0):
+        i = int(np.nonzero(norms == 0.0)[0][0])
+        raise ZeroNormDatapoint(f"ZeroNormDatapoint: row {i} has zero norm")
+    return x / norms[:, None]

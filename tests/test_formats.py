@@ -51,3 +51,22 @@ def test_fvecs_ivecs_round_trip(tmp_path):
     (tmp_path / "t.fvecs").write_bytes(np.array([5], "<i4").tobytes() + b"\0" * 7)
     with pytest.raises(aq.MalformedFile):
         aq.read_fvecs(str(tmp_path / "t.fvecs"))
+
+
+def test_python_generator_and_rng_match_reference():
+    from oracle import Port, Reference
+    from paper_1908_10396_b200 import anisoq as aq
+
+    if not Reference.available():
+        pytest.skip("reference library not built")
+    R = Reference()
+    mix = aq.generate_synthetic("gaussian_mixture", 60, 6, 7, centers=5, spread=0.25,
+                                normalize=True)
+    assert np.array_equal(mix.values.astype(np.float64),
+                          R.generate_synthetic(1, 60, 6, 7, centers=5, spread=0.25,
+                                               normalize=True))
+    sph = aq.generate_synthetic("uniform_sphere", 20, 4, 3)
+    assert np.array_equal(sph.values.astype(np.float64), R.generate_synthetic(0, 20, 4, 3))
+    assert aq.Rng(9).sample_distinct(100, 7) == Port().sample_distinct(9, 100, 7).tolist()
+    u = aq.unit_normalize(mix)
+    assert np.allclose(np.linalg.norm(u, axis=1), 1.0, rtol=0, atol=1e-15)

@@ -141,6 +141,9 @@ class Dataset:
         v = np.asarray(self.values)
         if v.ndim != 2:
             raise InvalidArgument("InvalidArgument: dataset must be n x d")
+        if v.size and not np.all(np.isfinite(v)):  # make_dataset (dataset.hpp:100-108)
+            row = int(np.nonzero(~np.isfinite(v))[0][0])
+            raise MalformedFile(f"MalformedFile: non-finite value at row {row}")
         if v.dtype != np.float32:
             f = v.astype(np.float32)
             if not np.array_equal(f.astype(np.float64), np.asarray(v, np.float64)):

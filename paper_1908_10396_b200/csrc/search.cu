@@ -39,8 +39,8 @@ constexpr AdcShape kShapes[] = {{8, 256, 2, false}, {8, 256, 4, true}, {4, 256, 
 constexpr int kGbPointsPerThread = 4;  // points per thread between barriers (GB)
 constexpr int kNumShapes = sizeof(kShapes) / sizeof(kShapes[0]);
 constexpr int kLutQP = 16;  // lut kernel of the single-query host entry
-constexpr int kMaxTopN = 512;    // fast path limit
-constexpr int kMergeCap = 2048;
+constexpr int kMaxTopN = 4096;   // fast path limit
+constexpr int kMergeCapMin = 2048, kMergeCapMax = 8192;  // merge window (shared)
 constexpr int kQMax = 4095;      // |v| <= 4095: 13-bit fields, 8 adds per 16-bit lane
 
 // ---- LUT ---------------------------------------------------------------------
@@ -325,6 +325,7 @@ struct MergeArgs {
   const int* cnt;
   int* flag;
   int R, cap, N, topn_eff;
+  int mcap;  // merge window capacity: power of two, kMergeCapMin..kMergeCapMax
   const double* lut64;
   const uint8_t* codes;
   int stride, bits, M, k;
@@ -333,9 +334,10 @@ struct MergeArgs {
 };
 
 __global__ void __launch_bounds__(256) k_adc_merge(const MergeArgs a) {
-  __shared__ unsigned long long skey[kMergeCap];  // sort keys
-  __shared__ double ssc[kMergeCap];
-  __shared__ uint32_t sid[kMergeCap];
+  extern __shared__ __align__(16) unsigned char msm[];
+  unsigned long long* skey = reinterpret_cast<unsigned long long*>(msm);  // sort keys
+  double* ssc = reinterpret_cast<double*>(skey + a.mcap);
+  uint32_t* sid = reinterpret_cast<uint32_t*>(ssc + a.mcap);
   __shared__ int red[32];
   __shared__ int ncol;
   const int q = blockIdx.x;
@@ -373,12 +375,12 @@ __global__ void __launch_bounds__(256) k_adc_merge(const MergeArgs a) {
       const uint2 v = lists[(size_t)r * a.cap + e];
       if ((int)v.x >= cutv) {
         const int pos = atomicAdd(&ncol, 1);
-        if (pos < kMergeCap) sid[pos] = v.y;
+        if (pos < a.mcap) sid[pos] = v.y;
       }
     }
   __syncthreads();
   const int nc = ncol;
-  if (nc > kMergeCap) {
+  if (nc > a.mcap) {
     if (tid == 0) a.flag[q] = 2;
     return;
   }
@@ -475,6 +477,7 @@ int adc_search_device(aq_codes* codes, aq_codebook* cb, const double* Qd,
   const size_t d = cb->M * cb->sd;
   int variant = 1;
   if (const char* v = getenv("AQ_ADC_VARIANT")) variant = std::min(std::max(atoi(v), 0), kNumShapes - 1);
+  if (!kShapes[variant].gbuf && topn > 512) variant = 1;  // shared windows hold N <= 512
   const AdcShape shp = kShapes[variant];
   const int QB = 2 * shp.qp, TILE = shp.tile;
   const size_t nqb = (nq + QB - 1) / QB;
@@ -497,7 +500,10 @@ int adc_search_device(aq_codes* codes, aq_codebook* cb, const double* Qd,
   std::vector<int> hflag(nq, fast ? 0 : 1);
   if (fast) {
     const int N = (int)topn_eff;
-    const int cap = ((N + 31) & ~31) + TILE * (shp.gbuf ? kGbPointsPerThread : 1) + 32;
+    // window: N, one span of appends, and room for near-threshold ties
+    // (their count grows with the depth of the N-th score)
+    const int cap = ((N + 31) & ~31) + TILE * (shp.gbuf ? kGbPointsPerThread : 1) + 32 +
+                    (N > 128 ? N : 0);
     // point ranges: enough CTAs for ~2 waves, ranges of whole tiles
     const size_t tiles = (n + TILE - 1) / TILE;
     // Windows in global memory: one persistent CTA per resident slot, each
@@ -572,10 +578,16 @@ int adc_search_device(aq_codes* codes, aq_codebook* cb, const double* Qd,
 #undef AQ_SCORE_LAUNCH
     AQ_LAUNCHED(s);
     timer_mark(s, AQ_T_ADC_SCORE);
-    MergeArgs ma{obuf, ocnt, oflag, (int)R, cap, N, (int)topn_eff, lut64,
+    // merge window: N plus room for near-threshold ties, a power of two
+    int mcap = kMergeCapMin;
+    while (mcap < N + N / 2 + 1024 && mcap < kMergeCapMax) mcap <<= 1;
+    MergeArgs ma{obuf, ocnt, oflag, (int)R, cap, N, (int)topn_eff, mcap, lut64,
                  codes->data, (int)codes->stride, codes->bits, M, k, ids, scores};
+    const size_t msmem = (size_t)mcap * (2 * sizeof(double) + sizeof(uint32_t));
+    AQ_CUDA(cudaFuncSetAttribute(k_adc_merge, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)msmem));
     timer_mark(s, AQ_T_ADC_MERGE);
-    k_adc_merge<<<(unsigned)nq, 256, 0, s->stream>>>(ma);
+    k_adc_merge<<<(unsigned)nq, 256, msmem, s->stream>>>(ma);
     AQ_LAUNCHED(s);
     timer_mark(s, AQ_T_ADC_MERGE);
     AQ_CUDA(cudaMemcpyAsync(hflag.data(), oflag, nq * sizeof(int), cudaMemcpyDeviceToHost,

@@ -56,14 +56,15 @@ def test_adc_validation():
 
 
 # every compiled M specialisation (16, 32, 48, 50, 64, 128), the generic
-# kernel with and without a tail chunk (8, 13), k < 16, top-N beyond the fast
-# path (1000), and slices that cross query-block edges (small n, many queries)
+# kernel with and without a tail chunk (8, 13), k < 16, large top-N on the fast
+# path (1000, 2000, 4096) and beyond it (5000), and slices that cross query-block edges (small n, many queries)
 @pytest.mark.parametrize("n,M,topn,nq,k", [(20000, 16, 100, 100, 16), (300000, 50, 100, 64, 16),
                                            (5000, 48, 7, 33, 16), (70000, 16, 512, 20, 16),
                                            (200, 8, 100, 5, 16), (50000, 64, 1000, 3, 16),
                                            (40000, 32, 100, 40, 16), (30000, 128, 100, 20, 16),
                                            (25000, 13, 50, 17, 16), (12000, 16, 100, 50, 9),
-                                           (3000, 50, 10, 300, 16)])
+                                           (3000, 50, 10, 300, 16), (60000, 50, 2000, 20, 16),
+                                           (20000, 16, 4096, 9, 16), (30000, 16, 5000, 3, 16)])
 def test_adc_batch_matches_oracle(n, M, topn, nq, k):
     g = np.random.default_rng(n + M + k)
     cb = aq.ProductCodebook(M, k, 2, g.standard_normal(M * k * 2) / np.sqrt(2 * M))

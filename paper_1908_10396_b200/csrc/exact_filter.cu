@@ -31,8 +31,8 @@ namespace aqd {
 constexpr int kFQ = AQ_FQ;     // queries per CTA
 constexpr int kFTile = 256;    // points per tile (= threads)
 constexpr int kFPPT = 4;       // tiles between barriers
-constexpr int kFMaxN = 512;
-constexpr int kFMergeCap = 2048;
+constexpr int kFMaxN = 4096;
+constexpr int kFMergeCapMin = 2048, kFMergeCapMax = 8192;  // merge window (shared)
 
 __device__ __forceinline__ uint32_t fkey(float f) {
   const uint32_t u = __float_as_uint(f);
@@ -94,6 +94,7 @@ struct FArgs {
   int nq, N, cap, R;
   size_t chunk;          // persistent slices of (query block, point) space
   int nqb;
+  int mcap;              // merge window: power of two, kFMergeCapMin..kFMergeCapMax
   uint2* out_buf;        // [q][r][cap] {key, index}
   int* out_cnt;          // [q][r]
   int* out_flag;         // [q]
@@ -228,8 +229,9 @@ __device__ __forceinline__ unsigned long long d2o64(double v) {
 __global__ void __launch_bounds__(256) k_exact_fmerge(const FArgs a, const float* xr,
                                                        const double* Q, int topn_eff,
                                                        uint32_t* ids, double* scores) {
-  __shared__ unsigned long long K[kFMergeCap];
-  __shared__ uint32_t I[kFMergeCap];
+  extern __shared__ __align__(16) unsigned char msm[];
+  unsigned long long* K = reinterpret_cast<unsigned long long*>(msm);
+  uint32_t* I = reinterpret_cast<uint32_t*>(K + a.mcap);
   __shared__ int red[32];
   __shared__ int ncol;
   const int q = blockIdx.x;
@@ -264,12 +266,12 @@ __global__ void __launch_bounds__(256) k_exact_fmerge(const FArgs a, const float
       const uint2 v = lists[(size_t)r * a.cap + e];
       if (v.x >= cutk) {
         const int pos = atomicAdd(&ncol, 1);
-        if (pos < kFMergeCap) I[pos] = v.y;
+        if (pos < a.mcap) I[pos] = v.y;
       }
     }
   __syncthreads();
   const int nc = ncol;
-  if (nc > kFMergeCap) {
+  if (nc > a.mcap) {
     if (tid == 0) a.out_flag[q] = 2;
     return;
   }
@@ -364,7 +366,8 @@ int exact_filter_device(aq_dataset* ds, const double* Qd, size_t nq, size_t dept
   for (double v : hn) xmax = std::max(xmax, v);
   xmax *= 1.0000001;
   if (!(xmax < 1e30) || depth > (size_t)kFMaxN) return AQ_OK;  // caller's exact path
-  const int cap = ((N + 31) & ~31) + kFTile * kFPPT + 32;
+  // window: N, one span of appends, tie room growing with N (search.cu)
+  const int cap = ((N + 31) & ~31) + kFTile * kFPPT + 32 + (N > 128 ? N : 0);
   const size_t G0 = (size_t)s->num_sms * 2;
   const size_t total = nqb * n;
   const size_t chunk = std::max<size_t>((total + G0 - 1) / G0, 16 * (size_t)kFTile);
@@ -386,8 +389,11 @@ int exact_filter_device(aq_dataset* ds, const double* Qd, size_t nq, size_t dept
   k_filter_queries<<<(unsigned)nq_pad, 128, 0, s->stream>>>(Qd, (int)nq, (int)d, xmax, qf, twoB,
                                                             oflag);
   AQ_LAUNCHED(s);
+  int mcap = kFMergeCapMin;
+  while (mcap < N + N / 2 + 1024 && mcap < kFMergeCapMax) mcap <<= 1;
   FArgs a{ds->xt, (int)pairs_of(d), (int)d, n, qf, twoB, (int)nq, N, cap, (int)R,
-          chunk, (int)nqb, obuf, ocnt, oflag};
+          chunk, (int)nqb, mcap, obuf, ocnt, oflag};
+  const size_t msmem = (size_t)mcap * (sizeof(unsigned long long) + sizeof(uint32_t));
   const size_t smem = (size_t)d * kFQ * sizeof(float) + kFQ * 16 + 64;
   if (smem > 200 * 1024) return AQ_OK;
   AQ_CUDA(cudaFuncSetAttribute(k_exact_filter, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -395,7 +401,9 @@ int exact_filter_device(aq_dataset* ds, const double* Qd, size_t nq, size_t dept
   timer_mark(s, AQ_T_EXACT);
   k_exact_filter<<<(unsigned)G, kFTile, smem, s->stream>>>(a);
   AQ_LAUNCHED(s);
-  k_exact_fmerge<<<(unsigned)nq, 256, 0, s->stream>>>(a, ds->xr, Qd, (int)te, ids, scores);
+  AQ_CUDA(cudaFuncSetAttribute(k_exact_fmerge, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)msmem));
+  k_exact_fmerge<<<(unsigned)nq, 256, msmem, s->stream>>>(a, ds->xr, Qd, (int)te, ids, scores);
   AQ_LAUNCHED(s);
   timer_mark(s, AQ_T_EXACT);
   AQ_CUDA(cudaMemcpyAsync(hflag.data(), oflag, nq * sizeof(int), cudaMemcpyDeviceToHost,

@@ -13,7 +13,9 @@ P = Port()
 
 
 @pytest.mark.parametrize("n,d,depth,nq", [(20000, 32, 10, 100), (5000, 100, 100, 17),
-                                          (300, 8, 1000, 3), (70000, 96, 64, 40)])
+                                          (300, 8, 1000, 3), (70000, 96, 64, 40),
+                                          (30000, 64, 1000, 20), (40000, 32, 4096, 5),
+                                          (20000, 16, 5000, 3)])
 def test_exact_search_matches_oracle(n, d, depth, nq):
     x = mixture_rows(n, d, 71)
     q = mixture_rows(nq, d, 72).astype(np.float64)

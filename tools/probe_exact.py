@@ -9,16 +9,17 @@ from paper_1908_10396_b200 import anisoq as aq, workload as wl
 
 n = int(float(sys.argv[1])) if len(sys.argv) > 1 else 1_183_514
 nq = int(sys.argv[2]) if len(sys.argv) > 2 else 10_000
-out = sys.argv[3] if len(sys.argv) > 3 else None
+out = sys.argv[3] if len(sys.argv) > 3 and sys.argv[3] != "-" else None
+depth = int(sys.argv[4]) if len(sys.argv) > 4 else 10
 w = wl.config2(n=n, nq=nq)
 s = aq.Session.default()
 ds = s.upload_dataset(w.base)
 Q = np.ascontiguousarray(w.queries, np.float64)
-ids, sc = aq.dev_exact_search(ds, Q, 10)
+ids, sc = aq.dev_exact_search(ds, Q, depth)
 ts = []
 for _ in range(3):
-    t = time.perf_counter(); aq.dev_exact_search(ds, Q, 10); ts.append(time.perf_counter() - t)
+    t = time.perf_counter(); aq.dev_exact_search(ds, Q, depth); ts.append(time.perf_counter() - t)
 b = min(ts)
-print(f"exact top-10: {b*1e3:.1f} ms  {n*nq/b:.3e} dots/s", flush=True)
+print(f"exact top-{depth}: {b*1e3:.1f} ms  {n*nq/b:.3e} dots/s", flush=True)
 if out:
     np.savez(out, ids=ids, sc=sc)

@@ -144,14 +144,15 @@ __device__ __forceinline__ unsigned proxy_mask(float xf0, float xf1,
                            fminf(fminf(m6[3], m6[4]), m6[5]));
   const float thr = best + 2.0f * delta + fabsf(best) * 2.384185791015625e-07f;
   if (!(thr < 1e30f) || !(best > -1e30f)) return 0u;  // out of envelope
-  // FSETP + predicated OR per candidate
-  unsigned mask = 0;
+  // FSETP + predicated OR per candidate, four independent chains (a single
+  // chain is 16 dependent adds deep)
+  unsigned mk[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
   for (int j = 0; j < 16; ++j)
     asm("{\n\t.reg .pred p;\n\tsetp.le.f32 p, %1, %2;\n\t@p or.b32 %0, %0, %3;\n\t}"
-        : "+r"(mask)
+        : "+r"(mk[j & 3])
         : "f"(K[j]), "f"(thr), "r"(1u << j));
-  return mask;
+  return (mk[0] | mk[1]) | (mk[2] | mk[3]);
 }
 
 // Fast kernel: sub_dimension == 2, k <= 16, 4-bit codes.

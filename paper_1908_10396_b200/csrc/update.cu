@@ -495,6 +495,186 @@ __global__ void __launch_bounds__(32) k_assemble_sd2(const AsmArgs a, const uint
   }
 }
 
+// Register-pipelined variant of k_assemble_sd2: no row staging in shared
+// memory. Each lane loads its own column pair (float2) and code word for the
+// point AH positions ahead straight from global memory (the warp reads the
+// point's 256-byte column slice, coalesced) into a register ring, so a CTA
+// holds only the 16 KB accumulator tile and twice as many warps fit per SM.
+// Per-entry operation order is the same as k_assemble_sd2's.
+template <int AH>
+__global__ void __launch_bounds__(32, 12) k_assemble_sd2r(const AsmArgs a, const uint32_t* order) {
+  static_assert(AH == 8 || AH == 16, "ring of 8 or 16 points");
+  // [aa*16 + j2][lane] of {b = 0, b = 1}: a point's 2x2 block is two
+  // 16-byte accesses per lane (LDS.128 / STS.128)
+  extern __shared__ __align__(16) double2 acc2[];
+  __shared__ __align__(16) double2 s_u[32];      // coef * x_m
+  __shared__ __align__(16) double2 s_r[32];      // h_par * x_m (rhs)
+  __shared__ double s_ho[32];
+  const int unit = order[blockIdx.x];
+  const int chunk = unit % a.nchunk;
+  const int strip = unit / a.nchunk;
+  const int m = strip >> 4, j = strip & 15;
+  const int lane = threadIdx.x;
+  const int d = a.d;
+  const int m2 = chunk * 32 + lane;
+  const int mcols = a.full ? a.M : m + 1;
+  const bool mine = m2 < mcols;
+  const bool diag = m2 == m;
+  const size_t dim = (size_t)16 * d;
+  const bool do_rhs = chunk == 0 && lane == 0;
+  const uint32_t* Lall = a.list + (size_t)m * a.n + a.start[m * 16 + j];
+  const size_t call = a.count[m * 16 + j];
+  const size_t t_lo = lower_bound_u32(Lall, call, a.lo);
+  const size_t t_hi = lower_bound_u32(Lall, call, a.hi);
+  if (t_lo == t_hi) return;  // accumulators already hold this block's state
+  double r0 = 0.0, r1 = 0.0;
+  if (a.resume) {
+    if (mine) {
+#pragma unroll 4
+      for (int e = 0; e < 64; ++e) {
+        const int aa = e >> 5, j2 = (e >> 1) & 15, b = e & 1;
+        reinterpret_cast<double*>(acc2)[((e >> 1) * 32 + lane) * 2 + b] =
+            a.A[((size_t)(m * 16 + j) * 2 + aa) * dim + (size_t)(m2 * 16 + j2) * 2 + b];
+      }
+    }
+    if (do_rhs) {
+      r0 = a.rhs[(size_t)(m * 16 + j) * 2];
+      r1 = a.rhs[(size_t)(m * 16 + j) * 2 + 1];
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < 32; ++e) acc2[e * 32 + lane] = make_double2(0.0, 0.0);
+  }
+  const uint32_t* L = Lall + t_lo;
+  const size_t cnt = t_hi - t_lo;
+  const float* xcol = a.xr + chunk * 64 + 2 * lane;  // this lane's column pair
+  const uint8_t* cwb = a.codes + chunk * 16 + (lane >> 3) * 4;
+  const int sh = 4 * (lane & 7);
+  // batch scalars, lane = point of the batch: current (c) and next (n)
+  uint32_t plc = 0, pln = 0;
+  double cfc = 0.0, hpc = 0.0, hoc = 0.0, cfn = 0.0, hpn = 0.0, hon = 0.0;
+  float2 xmc = make_float2(0.f, 0.f), xmn = make_float2(0.f, 0.f);
+  auto load_scalars = [&](size_t t0, uint32_t& pl, double& cf, double& hp, double& ho,
+                          float2& xm) {
+    if (t0 + lane < cnt) {
+      pl = L[t0 + lane];
+      cf = a.coef[pl];
+      hp = a.hp[pl];
+      ho = a.ho[pl];
+      xm = *reinterpret_cast<const float2*>(a.xr + (size_t)pl * d + m * 2);
+    }
+  };
+  float2 rx[AH];
+  uint32_t rw[AH];
+  auto fetch = [&](uint32_t p, float2& x, uint32_t& w) {
+    if (mine) {
+      x = __ldg(reinterpret_cast<const float2*>(xcol + (size_t)p * d));
+      w = __ldg(reinterpret_cast<const uint32_t*>(cwb + (size_t)p * a.stride));
+    }
+  };
+  load_scalars(0, plc, cfc, hpc, hoc, xmc);
+  load_scalars(32, pln, cfn, hpn, hon, xmn);
+#pragma unroll
+  for (int v = 0; v < AH; ++v) {
+    rx[v] = make_float2(0.f, 0.f);
+    rw[v] = 0u;
+    const uint32_t p = __shfl_sync(0xffffffffu, plc, v);
+    if ((size_t)v < cnt) fetch(p, rx[v], rw[v]);
+  }
+  for (size_t t0 = 0; t0 < cnt; t0 += 32) {
+    const int nb = (int)min((size_t)32, cnt - t0);
+    if (lane < nb) {
+      s_u[lane] = make_double2(__dmul_rn(cfc, (double)xmc.x), __dmul_rn(cfc, (double)xmc.y));
+      s_r[lane] = make_double2(__dmul_rn(hpc, (double)xmc.x), __dmul_rn(hpc, (double)xmc.y));
+      s_ho[lane] = hoc;
+    }
+    __syncwarp();
+    if (do_rhs)
+      for (int b = 0; b < nb; ++b) {  // rhs += h_par * x (pq.hpp:326)
+        const double2 r = s_r[b];
+        r0 = __dadd_rn(r0, r.x);
+        r1 = __dadd_rn(r1, r.y);
+      }
+    // h_perp on the diagonal first (pq.hpp:324-325), then the coupling
+    // products (pq.hpp:329-338)
+    auto upd = [&](int b, float2 xc, double& e00, double& e01, double& e10, double& e11) {
+      const double2 u = s_u[b];
+      const double v0 = (double)xc.x, v1 = (double)xc.y;
+      if (diag) {
+        const double hop = s_ho[b];
+        e00 = __dadd_rn(e00, hop);
+        e11 = __dadd_rn(e11, hop);
+      }
+      e00 = __dadd_rn(e00, __dmul_rn(u.x, v0));
+      e01 = __dadd_rn(e01, __dmul_rn(u.x, v1));
+      e10 = __dadd_rn(e10, __dmul_rn(u.y, v0));
+      e11 = __dadd_rn(e11, __dmul_rn(u.y, v1));
+    };
+#pragma unroll
+    for (int g = 0; g < 32 / AH; ++g) {
+      if (g * AH >= nb) break;
+#pragma unroll
+      for (int v = 0; v < AH; v += 2) {
+        const int b = g * AH + v;
+        if (mine && b < nb) {
+          // pair (b, b + 1): both slots loaded before either is stored; a
+          // shared slot chains the second update on the first's result
+          const unsigned ja = (rw[v] >> sh) & 15u;
+          double2* pa0 = acc2 + (size_t)ja * 32 + lane;
+          double2* pa1 = acc2 + (size_t)(16 + ja) * 32 + lane;
+          double2 A0 = *pa0, A1 = *pa1;
+          if (b + 1 < nb) {
+            const unsigned jb = (rw[v + 1] >> sh) & 15u;
+            double2* pb0 = acc2 + (size_t)jb * 32 + lane;
+            double2* pb1 = acc2 + (size_t)(16 + jb) * 32 + lane;
+            double2 B0 = *pb0, B1 = *pb1;
+            upd(b, rx[v], A0.x, A0.y, A1.x, A1.y);
+            if (ja == jb) {
+              B0 = A0;
+              B1 = A1;
+            }
+            upd(b + 1, rx[v + 1], B0.x, B0.y, B1.x, B1.y);
+            *pa0 = A0;
+            *pa1 = A1;
+            *pb0 = B0;
+            *pb1 = B1;
+          } else {
+            upd(b, rx[v], A0.x, A0.y, A1.x, A1.y);
+            *pa0 = A0;
+            *pa1 = A1;
+          }
+        }
+        // refill both slots with the points AH positions ahead
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int tn = b + q + AH;  // < 32: this batch, else the next
+          const uint32_t p = __shfl_sync(0xffffffffu, tn < 32 ? plc : pln, tn & 31);
+          if (t0 + tn < cnt) fetch(p, rx[v + q], rw[v + q]);
+        }
+      }
+    }
+    __syncwarp();
+    plc = pln;
+    cfc = cfn;
+    hpc = hpn;
+    hoc = hon;
+    xmc = xmn;
+    load_scalars(t0 + 64, pln, cfn, hpn, hon, xmn);
+  }
+  if (mine) {
+#pragma unroll 4
+    for (int e = 0; e < 64; ++e) {
+      const int aa = e >> 5, j2 = (e >> 1) & 15, b = e & 1;
+      a.A[((size_t)(m * 16 + j) * 2 + aa) * dim + (size_t)(m2 * 16 + j2) * 2 + b] =
+          reinterpret_cast<const double*>(acc2)[((e >> 1) * 32 + lane) * 2 + b];
+    }
+  }
+  if (do_rhs) {
+    a.rhs[(size_t)(m * 16 + j) * 2] = r0;
+    a.rhs[(size_t)(m * 16 + j) * 2 + 1] = r1;
+  }
+}
+
 // trace (sequential, Eigen stand-in) and ridge = 1e-6 trace / dim (pq.hpp:431-435)
 __global__ void k_trace_ridge(double* A, size_t dim, double ridge) {
   __shared__ double r;
@@ -896,8 +1076,17 @@ int assemble_device(aq_dataset* ds, aq_codes* codes, const PointW& pw, const Buc
     // measured slower: per-unit staging outweighs the extra warps)
     const int cols = 32, nch = nchunk;
     const unsigned units2 = (unsigned)(M * 16 * nch);
+    // AQ_ASM_VARIANT=1: rows staged in shared memory (k_assemble_sd2), 3:
+    // register ring (k_assemble_sd2r), 0 (default): the ring when a launch
+    // has at least two waves of its 12-per-SM CTAs (config 5: 1136 vs 1207
+    // ms per 3 iterations), else the staged kernel (config 2: 138 vs 200 ms)
+    static const int asm_variant =
+        getenv("AQ_ASM_VARIANT") ? atoi(getenv("AQ_ASM_VARIANT")) : 0;
     AQ_CUDA(cudaFuncSetAttribute(k_assemble_sd2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  64 * 32 * 8));
+    AQ_CUDA(cudaFuncSetAttribute(k_assemble_sd2r<16>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 32 * 8));
+
     // units with work, largest strip first (the longest point chains start
     // early instead of trailing the launch)
     std::vector<uint32_t> hc((size_t)M * 16);
@@ -920,13 +1109,18 @@ int assemble_device(aq_dataset* ds, aq_codes* codes, const PointW& pw, const Buc
                             cudaMemcpyHostToDevice, s->stream));
     // point blocks whose rows (~48 MB) stay L2-resident while every unit
     // gathers from them; entries keep their point order across blocks
+    const bool ring = asm_variant == 3 ||
+                      (asm_variant == 0 && ord.size() >= (size_t)2 * 12 * s->num_sms);
     const size_t row_bytes = (size_t)d * sizeof(float);
     const size_t bsz = std::max<size_t>(4096, (48u << 20) / row_bytes);
     for (size_t lo = 0; lo < ds->n && !ord.empty(); lo += bsz) {
       a.lo = (uint32_t)lo;
       a.hi = (uint32_t)std::min(ds->n, lo + bsz);
       a.resume = lo > 0;
-      k_assemble_sd2<<<(unsigned)ord.size(), 32, 64 * 32 * 8, s->stream>>>(a, dord);
+      if (!ring)
+        k_assemble_sd2<<<(unsigned)ord.size(), 32, 64 * 32 * 8, s->stream>>>(a, dord);
+      else
+        k_assemble_sd2r<16><<<(unsigned)ord.size(), 32, 64 * 32 * 8, s->stream>>>(a, dord);
       AQ_LAUNCHED(s);
     }
   } else {

@@ -23,12 +23,23 @@ print(f"oracle (1 thread) {time.perf_counter()-t:.2f} s; parity cb={np.array_equ
 n = int(float(sys.argv[1])) if len(sys.argv) > 1 else 1183514
 w2 = wl.config2(n=n, nq=1000)
 ds2 = s.upload_dataset(w2.base)
-for warm in (True,):
+import ctypes as C
+L = aq._L
+for warm in (True, True):  # second run: warm caches and clocks
+    L.aq_session_timing(s.h, 1)
+    for slot in range(9): L.aq_session_timer_read(s.h, slot, None, None, 1)
     hist = []
     t = time.perf_counter()
     cb2, codes2 = aq.dev_train_apq(ds2, 50, 16, aq.ThresholdWeights(0.2), cfg, warm, hist)
     s.sync()
-    print(f"config2 n={n} train_apq warm={warm}: {time.perf_counter()-t:.2f} s hist {hist[:3]}..{hist[-1]}", flush=True)
+    tt = time.perf_counter() - t
+    ph = {}
+    for slot, nm in ((0, "encode"), (5, "assemble"), (6, "llt"), (7, "kmeans")):
+        ms, cnt = C.c_double(0), C.c_uint64(0)
+        L.aq_session_timer_read(s.h, slot, C.byref(ms), C.byref(cnt), 1)
+        ph[nm] = round(ms.value, 1)
+    L.aq_session_timing(s.h, 0)
+    print(f"config2 n={n} train_apq: {tt:.2f} s phases ms {ph} hist {hist[:2]}..{hist[-1]}", flush=True)
 t = time.perf_counter()
 gt, _ = aq.dev_exact_search(ds2, w2.queries.astype(np.float64), 10)
 print(f"exact ground truth 1000 q: {(time.perf_counter()-t)*1e3:.1f} ms", flush=True)

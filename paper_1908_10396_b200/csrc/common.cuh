@@ -265,4 +265,69 @@ __device__ __forceinline__ double combined_loss(double dist2, double rdot,
                 inv_norm2));
 }
 
+// N-th largest key (.x, unsigned) over a query's candidate windows
+// lists[r * cap + e], e < cnts[r], r < R, by a three-pass radix select
+// (11 + 11 + 10 bits) with a shared-memory histogram `hist` (>= 2048 words).
+// Equals the largest T with |{key >= T}| >= N (the result of a 32-step
+// binary search) but reads the entries 3 times instead of 32. Requires
+// total >= N >= 1; block-wide (every thread calls it), blockDim.x a
+// multiple of 32 and <= 1024.
+__device__ inline unsigned block_nth_largest(const uint2* lists, const int* cnts, int R,
+                                             size_t cap, int N, unsigned* hist) {
+  __shared__ unsigned s_wsum[32];
+  __shared__ unsigned s_pick[2];
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, w = tid >> 5;
+  unsigned prefix = 0u, pmask = 0u;
+  unsigned need = (unsigned)N;
+#pragma unroll 1
+  for (int pass = 0; pass < 3; ++pass) {
+    const int shift = pass == 0 ? 21 : (pass == 1 ? 10 : 0);
+    const int nb = pass == 2 ? 1024 : 2048;
+    for (int i = tid; i < nb; i += nt) hist[i] = 0u;
+    __syncthreads();
+    // warp per window: many windows' loads in flight at once
+    for (int r = w; r < R; r += nt >> 5)
+      for (int e = lane; e < cnts[r]; e += 32) {
+        const unsigned key = lists[(size_t)r * cap + e].x;
+        if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & (unsigned)(nb - 1)], 1u);
+      }
+    __syncthreads();
+    // thread t owns `per` bins counted from the top; exclusive prefix from
+    // the top finds the bin where the running count reaches `need`
+    const int per = (nb + nt - 1) / nt;
+    const int hi = nb - tid * per;  // bins [lo, hi), top first
+    const int lo = max(0, hi - per);
+    unsigned sum = 0u;
+    for (int b = lo; b < hi; ++b) sum += hist[b];
+    unsigned inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned v = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += v;
+    }
+    if (lane == 31) s_wsum[w] = inc;
+    __syncthreads();
+    unsigned before = 0u;
+    for (int t = 0; t < w; ++t) before += s_wsum[t];
+    before += inc - sum;  // count in bins above this thread's range
+    if (before < need && before + sum >= need) {
+      unsigned run = before;
+      for (int b = hi - 1; b >= lo; --b) {
+        if (run + hist[b] >= need) {
+          s_pick[0] = (unsigned)b;
+          s_pick[1] = run;
+          break;
+        }
+        run += hist[b];
+      }
+    }
+    __syncthreads();
+    prefix |= s_pick[0] << shift;
+    pmask |= (unsigned)(nb - 1) << shift;
+    need -= s_pick[1];
+    __syncthreads();
+  }
+  return prefix;
+}
+
 }  // namespace aqd

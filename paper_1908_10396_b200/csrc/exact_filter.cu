@@ -226,43 +226,30 @@ __device__ __forceinline__ unsigned long long d2o64(double v) {
 }
 
 // Per query: global window, float64 re-scoring (detail::dot order), exact sort.
-__global__ void __launch_bounds__(256) k_exact_fmerge(const FArgs a, const float* xr,
+__global__ void __launch_bounds__(1024) k_exact_fmerge(const FArgs a, const float* xr,
                                                        const double* Q, int topn_eff,
                                                        uint32_t* ids, double* scores) {
   extern __shared__ __align__(16) unsigned char msm[];
   unsigned long long* K = reinterpret_cast<unsigned long long*>(msm);
   uint32_t* I = reinterpret_cast<uint32_t*>(K + a.mcap);
-  __shared__ int red[32];
   __shared__ int ncol;
   const int q = blockIdx.x;
   if (a.out_flag[q]) return;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int tid = threadIdx.x;
   const uint2* lists = a.out_buf + (size_t)q * a.R * a.cap;
   const int* cn = a.out_cnt + (size_t)q * a.R;
   int total = 0;
-  for (int r = 0; r < a.R; ++r) total += cn[r];
+  for (int r = tid & 31; r < a.R; r += 32) total += cn[r];  // each warp, redundantly
+  total = __reduce_add_sync(0xffffffffu, total);
   uint32_t cutk = 0u;
-  if (total >= a.N) {
-    uint32_t T = 0u;
-    for (int bit = 31; bit >= 0; --bit) {
-      const uint32_t cand = T | (1u << bit);
-      int c = 0;
-      for (int r = 0; r < a.R; ++r)
-        for (int e = tid; e < cn[r]; e += blockDim.x) c += lists[(size_t)r * a.cap + e].x >= cand;
-      c = __reduce_add_sync(0xffffffffu, c);
-      if (lane == 0) red[w] = c;
-      __syncthreads();
-      int tot = 0;
-      for (int t = 0; t < (int)(blockDim.x >> 5); ++t) tot += red[t];
-      __syncthreads();
-      if (tot >= a.N) T = cand;
-    }
-    cutk = window_cut(T, a.twoB[q]);
-  }
+  if (total >= a.N)  // radix select; the histogram borrows the sort-key space
+    cutk = window_cut(block_nth_largest(lists, cn, a.R, a.cap, a.N,
+                                        reinterpret_cast<unsigned*>(K)),
+                      a.twoB[q]);
   if (tid == 0) ncol = 0;
   __syncthreads();
-  for (int r = 0; r < a.R; ++r)
-    for (int e = tid; e < cn[r]; e += blockDim.x) {
+  for (int r = tid >> 5; r < a.R; r += blockDim.x >> 5)  // warp per window
+    for (int e = tid & 31; e < cn[r]; e += 32) {
       const uint2 v = lists[(size_t)r * a.cap + e];
       if (v.x >= cutk) {
         const int pos = atomicAdd(&ncol, 1);
@@ -403,7 +390,8 @@ int exact_filter_device(aq_dataset* ds, const double* Qd, size_t nq, size_t dept
   AQ_LAUNCHED(s);
   AQ_CUDA(cudaFuncSetAttribute(k_exact_fmerge, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)msmem));
-  k_exact_fmerge<<<(unsigned)nq, 256, msmem, s->stream>>>(a, ds->xr, Qd, (int)te, ids, scores);
+  k_exact_fmerge<<<(unsigned)nq, R >= 32 ? 1024 : 256, msmem, s->stream>>>(a, ds->xr, Qd, (int)te,
+                                                                         ids, scores);
   AQ_LAUNCHED(s);
   timer_mark(s, AQ_T_EXACT);
   AQ_CUDA(cudaMemcpyAsync(hflag.data(), oflag, nq * sizeof(int), cudaMemcpyDeviceToHost,

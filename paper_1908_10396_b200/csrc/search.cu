@@ -111,11 +111,12 @@ struct ScoreArgs {
 
 // Warp-cooperative: the N-th largest integer score among buf[0..cnt);
 // false when cnt < N.
-__device__ bool warp_nth_largest(const uint2* buf, int cnt, int N, unsigned* out) {
+// top: highest bit any key can have (keys <= M * 8191, 13-bit LUT entries).
+__device__ bool warp_nth_largest(const uint2* buf, int cnt, int N, unsigned* out, int top) {
   if (cnt < N) return false;
   const int lane = threadIdx.x & 31;
   unsigned T = 0u;
-  for (int bit = 31; bit >= 0; --bit) {
+  for (int bit = top; bit >= 0; --bit) {
     const unsigned cand = T | (1u << bit);
     int c = 0;
     for (int e = lane; e < cnt; e += 32) c += buf[e].x >= cand;
@@ -200,13 +201,15 @@ __global__ void __launch_bounds__(TILE, MINB) k_adc_score(const ScoreArgs a) {
     for (int t = threadIdx.x; t < QP * M * 4; t += blockDim.x) dst[t] = src[t];
   }
   if (threadIdx.x < QB) {
-    cut[threadIdx.x] = INT_MIN;
+    // padding slots of the last query block never append
+    cut[threadIdx.x] = qb * QB + (int)threadIdx.x < a.nq ? INT_MIN : INT_MAX;
     cnt[threadIdx.x] = 0;
     flag[threadIdx.x] = 0;
   }
   __syncthreads();
   const int cap = a.cap;
   const int margin = M + 1;  // 2 * (M s / 2) / s, plus one unit for float64
+  const int top = 31 - __clz(max(M * 8191, 1));
   // points scored between two barriers (windows in global memory are cheap
   // to size for it; shared windows keep one point per thread)
   constexpr int PPT = GB ? kGbPointsPerThread : 1;
@@ -283,7 +286,7 @@ __global__ void __launch_bounds__(TILE, MINB) k_adc_score(const ScoreArgs a) {
     for (int q = warp; q < QB; q += TILE / 32) {
       const int c = min(cnt[q], cap);
       unsigned th;
-      if (c > cap - SPAN && !flag[q] && warp_nth_largest(buf + q * qstride, c, a.N, &th)) {
+      if (c > cap - SPAN && !flag[q] && warp_nth_largest(buf + q * qstride, c, a.N, &th, top)) {
         const int cq = max(cut[q], (int)th - margin);
         const int kept = warp_compact(buf + q * qstride, c, cq);
         if (lane == 0) {
@@ -301,7 +304,7 @@ __global__ void __launch_bounds__(TILE, MINB) k_adc_score(const ScoreArgs a) {
     const int gq = qb * QB + q;
     int c = min(cnt[q], cap);
     unsigned th;
-    if (warp_nth_largest(buf + q * qstride, c, a.N, &th))
+    if (warp_nth_largest(buf + q * qstride, c, a.N, &th, top))
       c = warp_compact(buf + q * qstride, c, max(cut[q], (int)th - margin));
     if (gq < a.nq) {
       if (!GB) {
@@ -333,45 +336,31 @@ struct MergeArgs {
   double* scores;
 };
 
-__global__ void __launch_bounds__(256) k_adc_merge(const MergeArgs a) {
+__global__ void __launch_bounds__(1024) k_adc_merge(const MergeArgs a) {
   extern __shared__ __align__(16) unsigned char msm[];
   unsigned long long* skey = reinterpret_cast<unsigned long long*>(msm);  // sort keys
   double* ssc = reinterpret_cast<double*>(skey + a.mcap);
   uint32_t* sid = reinterpret_cast<uint32_t*>(ssc + a.mcap);
-  __shared__ int red[32];
   __shared__ int ncol;
   const int q = blockIdx.x;
   if (a.flag[q]) return;  // handled by the exact fallback
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int tid = threadIdx.x;
   // total entries
   const uint2* lists = a.buf + (size_t)q * a.R * a.cap;
   const int* cnts = a.cnt + (size_t)q * a.R;
-  // global N-th largest integer score over the union (binary search)
+  // global N-th largest integer score over the union (radix select; the
+  // histogram borrows the sort-key space, filled only later)
   unsigned T = 0u;
   int total = 0;
-  for (int r = 0; r < a.R; ++r) total += cnts[r];
+  for (int r = tid & 31; r < a.R; r += 32) total += cnts[r];  // each warp, redundantly
+  total = __reduce_add_sync(0xffffffffu, total);
   const bool have = total >= a.N;
-  if (have) {
-    for (int bit = 31; bit >= 0; --bit) {
-      const unsigned cand = T | (1u << bit);
-      int c = 0;
-      for (int r = 0; r < a.R; ++r)
-        for (int e = tid; e < cnts[r]; e += blockDim.x)
-          c += lists[(size_t)r * a.cap + e].x >= cand;
-      c = __reduce_add_sync(0xffffffffu, c);
-      if (lane == 0) red[w] = c;
-      __syncthreads();
-      int tot = 0;
-      for (int t = 0; t < (int)(blockDim.x >> 5); ++t) tot += red[t];
-      __syncthreads();
-      if (tot >= a.N) T = cand;
-    }
-  }
+  if (have) T = block_nth_largest(lists, cnts, a.R, a.cap, a.N, reinterpret_cast<unsigned*>(skey));
   const int cutv = have ? (int)T - (a.M + 1) : INT_MIN;
   if (tid == 0) ncol = 0;
   __syncthreads();
-  for (int r = 0; r < a.R; ++r)
-    for (int e = tid; e < cnts[r]; e += blockDim.x) {
+  for (int r = tid >> 5; r < a.R; r += blockDim.x >> 5)  // warp per window
+    for (int e = tid & 31; e < cnts[r]; e += 32) {
       const uint2 v = lists[(size_t)r * a.cap + e];
       if ((int)v.x >= cutv) {
         const int pos = atomicAdd(&ncol, 1);
@@ -516,7 +505,9 @@ int adc_search_device(aq_codes* codes, aq_codebook* cb, const double* Qd,
     if (persist) {
       G = (size_t)s->num_sms * shp.minb;
       const size_t total = nqb * n;
-      chunk = std::max<size_t>((total + G - 1) / G, 16 * (size_t)TILE);
+      static const size_t min_tiles =
+          getenv("AQ_ADC_MINCHUNK") ? (size_t)atoi(getenv("AQ_ADC_MINCHUNK")) : 16;
+      chunk = std::max<size_t>((total + G - 1) / G, min_tiles * (size_t)TILE);
       G = (total + chunk - 1) / chunk;
       R = 1;
       for (size_t qb = 0; qb < nqb; ++qb) {
@@ -587,7 +578,8 @@ int adc_search_device(aq_codes* codes, aq_codebook* cb, const double* Qd,
     AQ_CUDA(cudaFuncSetAttribute(k_adc_merge, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)msmem));
     timer_mark(s, AQ_T_ADC_MERGE);
-    k_adc_merge<<<(unsigned)nq, 256, msmem, s->stream>>>(ma);
+    // many windows per query (small batches): more warps walk them at once
+    k_adc_merge<<<(unsigned)nq, R >= 32 ? 1024 : 256, msmem, s->stream>>>(ma);
     AQ_LAUNCHED(s);
     timer_mark(s, AQ_T_ADC_MERGE);
     AQ_CUDA(cudaMemcpyAsync(hflag.data(), oflag, nq * sizeof(int), cudaMemcpyDeviceToHost,

@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import time
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
@@ -672,6 +673,17 @@ class EvalOptions:
     kk: int = 10
     threads: int = 1
     ground_truth: Optional[np.ndarray] = None
+    # extension: search and time the queries one at a time against the
+    # device-resident index (the reference's per-query latency,
+    # index.hpp:254-259); default: one batch, latency = batch time / queries
+    per_query_latency: bool = False
+
+
+@dataclass
+class LatencySummary:  # index.hpp:164-168
+    mean_us: float = 0.0
+    p50_us: float = 0.0
+    p99_us: float = 0.0
 
 
 @dataclass
@@ -686,13 +698,31 @@ class EvalReport:
     relative_error_p90: float
     relative_error_p99: float
     relative_error_max: float
+    latency: LatencySummary = field(default_factory=LatencySummary)
+
+    def write_text(self) -> str:
+        """EvalReport::write_text (index.hpp:183-197): one `name value` per
+        line, values in the default iostream format (%g)."""
+        out = [f"num_queries {self.num_queries}", f"num_datapoints {self.num_datapoints}"]
+        out += [f"recall_1@{n} {r:g}" for n, r in sorted(self.recall_1_at_n.items())]
+        out += [f"recall_{self.kk}@{self.kk} {self.recall_k_at_k:g}",
+                f"relative_error_top1_mean {self.relative_error_mean:g}",
+                f"relative_error_top1_p50 {self.relative_error_p50:g}",
+                f"relative_error_top1_p90 {self.relative_error_p90:g}",
+                f"relative_error_top1_p99 {self.relative_error_p99:g}",
+                f"relative_error_top1_max {self.relative_error_max:g}",
+                f"latency_mean_us {self.latency.mean_us:g}",
+                f"latency_p50_us {self.latency.p50_us:g}",
+                f"latency_p99_us {self.latency.p99_us:g}"]
+        return "\n".join(out) + "\n"
 
 
 def evaluate(queries, data, codes: CodeMatrix, cb: ProductCodebook,
              options: EvalOptions = EvalOptions(), session: Optional[Session] = None) -> EvalReport:
     """index.hpp:213-332 with the searches on the device (batched adc_search and
     exact ground truth); the recall / relative-error bookkeeping follows the
-    reference line by line (latency is not reported: queries run batched)."""
+    reference line by line. Latency: batch time / queries, or each query's own
+    search time with options.per_query_latency."""
     s = _sess(session)
     Q = np.ascontiguousarray(np.atleast_2d(queries), np.float64)
     data = data if isinstance(data, Dataset) else Dataset(data)
@@ -720,9 +750,23 @@ def evaluate(queries, data, codes: CodeMatrix, cb: ProductCodebook,
         gt, _ = dev_exact_search(ds, Q, depth)
     dc = s.upload_codes(codes)
     dcb = s.upload_codebook(cb)
-    ids, _ = dev_adc_search(dc, dcb, Q, depth)
-    kk = min(options.kk, data.n)
     nq = Q.shape[0]
+    if options.per_query_latency:
+        rows, lat = [], []
+        for qi in range(nq):
+            t0 = time.perf_counter()
+            r_ids, _ = dev_adc_search(dc, dcb, Q[qi:qi + 1], depth)
+            lat.append((time.perf_counter() - t0) * 1e6)
+            rows.append(r_ids[0])
+        ids = np.stack(rows)
+    else:
+        t0 = time.perf_counter()
+        ids, _ = dev_adc_search(dc, dcb, Q, depth)
+        lat = [(time.perf_counter() - t0) * 1e6 / nq] * nq
+    lat = sorted(lat)  # index.hpp:322-330
+    latency = LatencySummary(float(np.add.accumulate(lat)[-1] / nq),
+                             lat[min(nq - 1, int(0.50 * nq))], lat[min(nq - 1, int(0.99 * nq))])
+    kk = min(options.kk, data.n)
     found = {n_: 0 for n_ in options.recall_ns}
     overlap = np.zeros(nq)
     rel = np.zeros(nq)
@@ -745,7 +789,7 @@ def evaluate(queries, data, codes: CodeMatrix, cb: ProductCodebook,
     return EvalReport(nq, data.n, {n_: found[n_] / nq for n_ in options.recall_ns}, kk,
                       float(np.add.accumulate(overlap)[-1] / nq),
                       float(np.add.accumulate(srt)[-1] / nq), quantile(0.5), quantile(0.9),
-                      quantile(0.99), float(srt[-1]))
+                      quantile(0.99), float(srt[-1]), latency)
 
 
 # ---- on-disk formats (pq.hpp:614-730, dataset.hpp:122-219) -------------------------------

@@ -289,6 +289,13 @@ int main() {
     CHECK(rep.num_queries == 20 && rep.num_datapoints == 16);
     CHECK(rep.recall_1_at_n.at(1) == 1.0 && rep.recall_1_at_n.at(10) == 1.0);
     CHECK(rep.recall_k_at_k == 1.0 && rep.relative_error_max == 0.0);
+    // per-query timing (extension): same report, measured latencies
+    EvalOptions popt = opt;
+    popt.per_query_latency = true;
+    const auto prep = evaluate(queries, data, codes, cb, popt);
+    CHECK(prep.recall_1_at_n == rep.recall_1_at_n && prep.recall_k_at_k == rep.recall_k_at_k);
+    CHECK(prep.relative_error_mean == rep.relative_error_mean);
+    CHECK(prep.latency.p50_us > 0.0 && prep.latency.p50_us <= prep.latency.p99_us);
     std::vector<std::vector<std::int32_t>> short_rows(4, std::vector<std::int32_t>{0});
     opt.ground_truth = &short_rows;
     CHECK_THROWS_AS(evaluate(queries, data, codes, cb, opt), GroundTruthMismatch);

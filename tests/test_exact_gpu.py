@@ -97,3 +97,13 @@ def test_evaluate_perfect_codes_recall_one():
                       aq.EvalOptions(recall_ns=(1, 5, 16), kk=5))
     assert rep.recall_1_at_n[1] == 1.0 and rep.recall_1_at_n[16] == 1.0
     assert rep.recall_k_at_k == 1.0 and rep.relative_error_max <= 1e-12
+    # per-query timing (extension): identical bookkeeping, measured latencies,
+    # and the reference's text report layout (index.hpp:183-197)
+    prep = aq.evaluate(q, data.astype(np.float32), aq.CodeMatrix(16, 2, 4, codes), cb,
+                       aq.EvalOptions(recall_ns=(1, 5, 16), kk=5, per_query_latency=True))
+    assert prep.recall_1_at_n == rep.recall_1_at_n and prep.recall_k_at_k == rep.recall_k_at_k
+    assert 0.0 < prep.latency.p50_us <= prep.latency.p99_us
+    lines = prep.write_text().splitlines()
+    assert lines[:5] == ["num_queries 20", "num_datapoints 16", "recall_1@1 1", "recall_1@5 1",
+                         "recall_1@16 1"]
+    assert lines[5] == "recall_5@5 1" and lines[-3].startswith("latency_mean_us ")

@@ -105,21 +105,246 @@ __global__ void k_seq_sums(const double* __restrict__ v, size_t ld, size_t count
   if (lane == 0) out[r] = s;
 }
 
-// `rows` sequential sums of `count` values each (row r at v + r * ld), rows
-// with active[r] == 0 skipped; out (device)
+// ---- the same sums, chunk-parallel (non-negative rows) ------------------------------------
+// std::accumulate over non-negative doubles is a monotone chain s_{i+1} =
+// fl(s_i + v_i). While s stays inside one binade [2^E, 2^(E+1)) its ulp u is
+// fixed and fl(s + v) = s + u * round(v / u) (to nearest; an exact half is a
+// tie whose result depends on the parity of s / u). Over a chunk that keeps s
+// inside the binade the chain is therefore a translation by u * K, K = the
+// sum of the rounded v / u — an exact integer sum that threads may form in
+// any order. The chain then steps over chunks instead of values: a chunk is
+// applied as s += u K when the binade predicted for it (from approximate
+// prefix sums) is the binade of s, it holds no tie, and s + u K <= 2^(E+1) -
+// 2u (so every intermediate exact sum stays below 2^(E+1) - u / 2 and rounds
+// to a multiple of u). Every other chunk — the few binade crossings, ties,
+// s = 0 or tiny, a wrong prediction — is added value by value. Rows holding a
+// negative or non-finite value run the plain chain. Bit-identical to
+// k_seq_sums (tests/test_seq_sums_gpu.py).
+constexpr int kSeqChunk = 2048;
+
+__device__ __forceinline__ int dexp_field(double x) {
+  return (int)((unsigned long long)__double_as_longlong(x) >> 52) & 0x7ff;
+}
+
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* red) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[w] = v;
+  __syncthreads();
+  T t = 0;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+  return t;
+}
+
+// pass 1: approximate chunk sums (any order); rows with a negative or
+// non-finite value are marked for the plain chain
+__global__ void k_seqsum_approx(const double* __restrict__ v, size_t ld, size_t count, int nch,
+                                const int* __restrict__ active, double* __restrict__ approx,
+                                int* __restrict__ plain) {
+  __shared__ double red[32];
+  const int r = blockIdx.y, c = blockIdx.x;
+  if (active && !active[r]) return;
+  const double* p = v + (size_t)r * ld + (size_t)c * kSeqChunk;
+  const int len = (int)min((size_t)kSeqChunk, count - (size_t)c * kSeqChunk);
+  double s = 0.0;
+  int bad = 0;
+  for (int i = threadIdx.x; i < len; i += blockDim.x) {
+    const double x = p[i];
+    bad |= !(x >= 0.0 && x <= 1.7976931348623157e308);
+    s += x;
+  }
+  s = block_sum(s, red);
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) {
+    approx[(size_t)r * nch + c] = s;
+    if (bad) plain[r] = 1;
+  }
+}
+
+// pass 2: predicted chain value at every chunk start (init + approximate
+// prefix), one block per row
+__global__ void k_seqsum_predict(const double* __restrict__ approx, int nch, double init,
+                                 const int* __restrict__ active, double* __restrict__ pred) {
+  __shared__ double red[32];
+  __shared__ double carry;
+  const int r = blockIdx.x;
+  if (active && !active[r]) return;
+  if (threadIdx.x == 0) carry = init;
+  __syncthreads();
+  for (int base = 0; base < nch; base += blockDim.x) {
+    const int c = base + threadIdx.x;
+    const double a = c < nch ? approx[(size_t)r * nch + c] : 0.0;
+    // inclusive warp scan, then warp offsets
+    double inc = a;
+    for (int o = 1; o < 32; o <<= 1) {
+      const double t = __shfl_up_sync(0xffffffffu, inc, o);
+      if ((threadIdx.x & 31) >= o) inc += t;
+    }
+    if ((threadIdx.x & 31) == 31) red[threadIdx.x >> 5] = inc;
+    __syncthreads();
+    double off = carry;
+    for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) off += red[w];
+    if (c < nch) pred[(size_t)r * nch + c] = off + inc - a;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = off + inc;
+    __syncthreads();
+  }
+}
+
+// pass 3: per chunk, the ulp exponent predicted for it (-1: add value by
+// value) and K = sum of round(v / u)
+__global__ void k_seqsum_chunks(const double* __restrict__ v, size_t ld, size_t count, int nch,
+                                const int* __restrict__ active, const double* __restrict__ pred,
+                                const double* __restrict__ approx, int* __restrict__ efield,
+                                unsigned long long* __restrict__ K) {
+  __shared__ unsigned long long red[32];
+  const int r = blockIdx.y, c = blockIdx.x;
+  if (active && !active[r]) return;
+  const double* p = v + (size_t)r * ld + (size_t)c * kSeqChunk;
+  const int len = (int)min((size_t)kSeqChunk, count - (size_t)c * kSeqChunk);
+  const double s0 = pred[(size_t)r * nch + c];
+  const double s1 = s0 + approx[(size_t)r * nch + c];  // predicted chunk end
+  const int e = dexp_field(s0);
+  // tiny or zero start, or a predicted binade crossing: value by value
+  bool seq = !(e >= 60 && e <= 2000) || dexp_field(s1) != e;
+  unsigned long long k = 0ull;
+  if (!seq) {
+    const double inv_u = __longlong_as_double((long long)(1075 + 1023 - e) << 52);  // 2^(1075-e)
+    for (int i = threadIdx.x; i < len; i += blockDim.x) {
+      const double q = __dmul_rn(p[i], inv_u);  // exact: a power-of-two scaling
+      if (!(q < 4503599627370496.0)) {           // >= 2^52: cannot stay in the binade
+        seq = true;
+        break;
+      }
+      const double f = floor(q);
+      const double fr = q - f;  // exact
+      if (fr == 0.5) {          // a tie: rounding depends on the chain's parity
+        seq = true;
+        break;
+      }
+      k += (unsigned long long)f + (fr > 0.5 ? 1ull : 0ull);
+    }
+  }
+  k = block_sum(k, red);
+  seq = __syncthreads_or(seq);
+  if (threadIdx.x == 0) {
+    efield[(size_t)r * nch + c] = seq ? -1 : e;
+    K[(size_t)r * nch + c] = k;
+  }
+}
+
+// pass 4: the chain over chunks, one warp per row; value-by-value chunks are
+// staged by the warp and added by lane 0 in index order
+__global__ void k_seqsum_chain(const double* __restrict__ v, size_t ld, size_t count, int nch,
+                               int rows, const int* __restrict__ active,
+                               const int* __restrict__ plain, const int* __restrict__ efield,
+                               const unsigned long long* __restrict__ K, double init,
+                               double* __restrict__ out) {
+  __shared__ double buf[4][256];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (blockDim.x >> 5) + w;
+  if (r >= rows || (active && !active[r])) return;
+  const double* row = v + (size_t)r * ld;
+  const bool all_seq = plain[r] != 0;
+  double s = init;
+  auto chain = [&](size_t i0, size_t i1) {  // s += v[i] for i in [i0, i1), in order
+    for (size_t b = i0; b < i1; b += 256) {
+      const int nb = (int)min((size_t)256, i1 - b);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int t = u * 32 + lane;
+        buf[w][t] = t < nb ? row[b + t] : 0.0;
+      }
+      __syncwarp();
+      if (lane == 0)
+        for (int t = 0; t < nb; ++t) s = __dadd_rn(s, buf[w][t]);
+      __syncwarp();
+    }
+  };
+  if (all_seq) {
+    chain(0, count);
+  } else {
+    for (int c0 = 0; c0 < nch; c0 += 32) {
+      const int c = c0 + lane;
+      const int ef = c < nch ? efield[(size_t)r * nch + c] : -1;
+      const unsigned long long kc = c < nch ? K[(size_t)r * nch + c] : 0ull;
+      const int nc = min(32, nch - c0);
+      for (int t = 0; t < nc; ++t) {
+        const int e_t = __shfl_sync(0xffffffffu, ef, t);
+        const unsigned long long k_t = __shfl_sync(0xffffffffu, kc, t);
+        s = __shfl_sync(0xffffffffu, s, 0);
+        bool fast = false;
+        double nxt = 0.0;
+        if (e_t >= 0 && dexp_field(s) == e_t && k_t < (1ull << 52)) {
+          const double u = __longlong_as_double((long long)(e_t - 52) << 52);   // 2^(e-1075)
+          const double top = __longlong_as_double((long long)(e_t + 1) << 52);  // 2^(e-1022)
+          nxt = s + u * (double)k_t;  // exact: multiples of u inside the binade
+          fast = nxt <= top - 2.0 * u;
+        }
+        if (fast) {
+          s = nxt;
+        } else {
+          const size_t i0 = (size_t)(c0 + t) * kSeqChunk;
+          chain(i0, min(count, i0 + kSeqChunk));
+        }
+      }
+    }
+  }
+  if (lane == 0) out[r] = s;
+}
+
+// `rows` sequential sums (std::accumulate from init) of `count` values each
+// (row r at v + r * ld), rows with active[r] == 0 skipped; out (device), on
+// `st`. Long rows take the chunk-parallel passes (AQ_SEQSUM=0: the plain
+// chain everywhere).
+int seq_sums_on(aq_session* s, cudaStream_t st, const double* v, size_t ld, size_t count,
+                int rows, const int* active_dev, double* out, double init) {
+  static const int mode = getenv("AQ_SEQSUM") ? atoi(getenv("AQ_SEQSUM")) : 1;
+  if (rows <= 0) return AQ_OK;
+  if (mode == 0 || count < 65536) {
+    k_seq_sums<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(v, ld, count, rows, active_dev, out,
+                                                          init);
+    AQ_LAUNCHED(s);
+    return AQ_OK;
+  }
+  const int nch = (int)((count + kSeqChunk - 1) / kSeqChunk);
+  const size_t cells = (size_t)rows * nch;
+  void* buf = nullptr;
+  const size_t bytes = cells * (2 * sizeof(double) + sizeof(unsigned long long) + sizeof(int)) +
+                       rows * sizeof(int) + 64;
+  AQ_CUDA(cudaMallocAsync(&buf, bytes, st));
+  double* approx = (double*)buf;
+  double* pred = approx + cells;
+  unsigned long long* K = (unsigned long long*)(pred + cells);
+  int* ef = (int*)(K + cells);
+  int* plain = ef + cells;
+  AQ_CUDA(cudaMemsetAsync(plain, 0, rows * sizeof(int), st));
+  k_seqsum_approx<<<dim3((unsigned)nch, (unsigned)rows), 256, 0, st>>>(v, ld, count, nch,
+                                                                      active_dev, approx, plain);
+  AQ_LAUNCHED(s);
+  k_seqsum_predict<<<(unsigned)rows, 1024, 0, st>>>(approx, nch, init, active_dev, pred);
+  AQ_LAUNCHED(s);
+  k_seqsum_chunks<<<dim3((unsigned)nch, (unsigned)rows), 256, 0, st>>>(v, ld, count, nch,
+                                                                      active_dev, pred, approx,
+                                                                      ef, K);
+  AQ_LAUNCHED(s);
+  k_seqsum_chain<<<(unsigned)((rows + 3) / 4), 128, 0, st>>>(v, ld, count, nch, rows, active_dev,
+                                                             plain, ef, K, init, out);
+  AQ_LAUNCHED(s);
+  AQ_CUDA(cudaFreeAsync(buf, st));
+  return AQ_OK;
+}
+
 int seq_sums_device(aq_session* s, const double* v, size_t ld, size_t count, int rows,
                     const int* active_dev, double* out) {
-  k_seq_sums<<<(unsigned)((rows + 7) / 8), 256, 0, s->stream>>>(v, ld, count, rows, active_dev,
-                                                               out);
-  AQ_LAUNCHED(s);
-  return AQ_OK;
+  return seq_sums_on(s, s->stream, v, ld, count, rows, active_dev, out, 0.0);
 }
 
 // std::accumulate(v, v + n, init) into *out (device), on the session stream
 int seq_sum_device(aq_session* s, const double* v, size_t n, double init, double* out) {
-  k_seq_sums<<<1, 32, 0, s->stream>>>(v, n, n, 1, nullptr, out, init);
-  AQ_LAUNCHED(s);
-  return AQ_OK;
+  return seq_sums_on(s, s->stream, v, n, n, 1, nullptr, out, init);
 }
 
 // codewords from sampled rows: dict[m][j] = x[idx[m][j]][m-subvector]
@@ -443,9 +668,7 @@ int train_l2_pq_device(aq_dataset* ds, size_t M, size_t k, const aq_train_config
     AQ_LAUNCHED(s);
     // loss totals only feed the relative-tolerance test (vq.hpp:316-321)
     if (cfg->relative_tolerance > 0.0) {
-      k_seq_sums<<<(unsigned)((M + 7) / 8), 256, 0, s->stream>>>(losses, n, n, (int)M, active,
-                                                                 totals);
-      AQ_LAUNCHED(s);
+      AQ_TRY(seq_sums_on(s, s->stream, losses, n, n, (int)M, active, totals, 0.0));
       AQ_CUDA(cudaMemcpyAsync(htot.data(), totals, M * sizeof(double), cudaMemcpyDeviceToHost,
                               s->stream));
     }
@@ -600,8 +823,7 @@ int aq_dev_train_apq(aq_dataset* ds, size_t M, size_t k, const aq_weights* w,
     AQ_TRY(run_encode(ds, cb, w, codes, 1, 0, cfg->sweep_to_fixed_point, losses, changed));
     AQ_CUDA(cudaEventRecord(s->ev_main, s->stream));
     AQ_CUDA(cudaStreamWaitEvent(s->side, s->ev_main, 0));
-    k_seq_sums<<<1, 32, 0, s->side>>>(losses, n, n, 1, nullptr, total);
-    s->launches++;
+    AQ_TRY(seq_sums_on(s, s->side, losses, n, n, 1, nullptr, total, 0.0));
     AQ_CUDA(cudaMemcpyAsync(s->sum_host, total, sizeof(double), cudaMemcpyDeviceToHost, s->side));
     AQ_CUDA(cudaEventRecord(s->ev_side, s->side));
     return AQ_OK;

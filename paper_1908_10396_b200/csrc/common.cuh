@@ -180,7 +180,8 @@ int trace_ridge_device(aq_session* s, double* A, size_t dim, double ridge);
 // weights; dict != null -> means of non-empty slots, else num/den partials
 int slot_sums_device(aq_session* s, const float* xr, size_t n, int d, int M, int k, int sd,
                      const Buckets& B, const int* active, const double* hp, const double* ho,
-                     double* dict, double* pnum, double* pden);
+                     double* dict, double* pnum, double* pden,
+                     const float* xt = nullptr);
 
 // ---- weights ------------------------------------------------------------------
 // Resolved per point on the device from an aq_weights descriptor

@@ -479,7 +479,8 @@ __global__ void __launch_bounds__(256) k_kmeans_assign_sd2(
 //   dict != null: dict = num / den for non-empty slots (weighted: den <= 0 is
 //                 a singular block); else num / den are written as partials.
 template <int SDC, bool kWeighted>
-__global__ void k_slot_sums(const float* __restrict__ xr, size_t n, int d, int M, int k,
+__global__ void k_slot_sums(const float* __restrict__ xr, const float* __restrict__ xt, size_t n,
+                            int d, int M, int k,
                             int sd_rt, const uint32_t* __restrict__ list,
                             const uint32_t* __restrict__ start,
                             const uint32_t* __restrict__ count, const int* __restrict__ active,
@@ -489,8 +490,10 @@ __global__ void k_slot_sums(const float* __restrict__ xr, size_t n, int d, int M
   constexpr int SDM = SDC > 0 ? SDC : 16;
   constexpr int G = SDC > 0 ? 4 : 1, R = 32 * G;
   const int sd = SDC > 0 ? SDC : sd_rt;
-  __shared__ float xs[4][2][R][SDM];
-  __shared__ double ws[4][2][kWeighted ? R : 1][2];
+  // per member: the products a * x (float64, formed by the fetching lane)
+  // and the weight o; lane 0 then runs only the dependent adds
+  __shared__ double ps[4][2][R][SDM];
+  __shared__ double ws[4][2][kWeighted ? R : 1];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slot = blockIdx.x * (blockDim.x >> 5) + w;
   if (slot >= M * k) return;
@@ -506,10 +509,24 @@ __global__ void k_slot_sums(const float* __restrict__ xr, size_t n, int d, int M
       const size_t t = r0 + g * 32 + lane;
       if (t < cnt) {
         const uint32_t p = L[t];
-        const float* xp = xr + (size_t)p * d + m * sd;
+        bool tiled = false;
+        if constexpr (SDC == 2) {
+          if (xt) {
+            // pair-tiled rows: the 16 slots of subspace m read the same
+            // 256-byte (32-point, pair m) blocks, so L2 serves most of them
+            const float2 v = reinterpret_cast<const float2*>(
+                xt)[(((size_t)(p >> 5) * (d >> 1)) + m) * 32 + (p & 31)];
+            nx[g][0] = v.x;
+            nx[g][1] = v.y;
+            tiled = true;
+          }
+        }
+        if (!tiled) {
+          const float* xp = xr + (size_t)p * d + m * sd;
 #pragma unroll
-        for (int c = 0; c < SDM; ++c)
-          if (c < sd) nx[g][c] = xp[c];
+          for (int c = 0; c < SDM; ++c)
+            if (c < sd) nx[g][c] = xp[c];
+        }
         if (kWeighted) {
           nh[g][0] = hp[p];
           nh[g][1] = ho[p];
@@ -526,30 +543,36 @@ __global__ void k_slot_sums(const float* __restrict__ xr, size_t n, int d, int M
   for (size_t r0 = 0; r0 < cnt; r0 += R) {
 #pragma unroll
     for (int g = 0; g < G; ++g) {
+      const double a = kWeighted ? nh[g][0] : 1.0;
 #pragma unroll
       for (int c = 0; c < SDM; ++c)
-        if (c < sd) xs[w][cur][g * 32 + lane][c] = nx[g][c];
-      if (kWeighted) {
-        ws[w][cur][g * 32 + lane][0] = nh[g][0];
-        ws[w][cur][g * 32 + lane][1] = nh[g][1];
-      }
+        if (c < sd) ps[w][cur][g * 32 + lane][c] = __dmul_rn(a, (double)nx[g][c]);
+      if (kWeighted) ws[w][cur][g * 32 + lane] = nh[g][1];
     }
     __syncwarp();
     if (r0 + R < cnt) fetch(r0 + R);  // in flight during the chain below
     if (lane == 0) {
       const int nb = (int)min((size_t)R, cnt - r0);
-      for (int b = 0; b < nb; ++b) {
-        const double a = kWeighted ? ws[w][cur][b][0] : 1.0;
-        const double o = kWeighted ? ws[w][cur][b][1] : 1.0;
+      auto add = [&](int b) {
 #pragma unroll
         for (int c = 0; c < SDM; ++c)
-          if (c < sd) num[c] = __dadd_rn(num[c], __dmul_rn(a, (double)xs[w][cur][b][c]));
-        den = __dadd_rn(den, o);
+          if (c < sd) num[c] = __dadd_rn(num[c], ps[w][cur][b][c]);
+        if (kWeighted) den = __dadd_rn(den, ws[w][cur][b]);
+      };
+      if (nb == R) {
+        // unrolled: the loads and products of later members issue ahead, the
+        // dependent adds are the only chain
+#pragma unroll 16
+        for (int b = 0; b < R; ++b) add(b);
+      } else {
+        for (int b = 0; b < nb; ++b) add(b);
       }
     }
     cur ^= 1;
   }
   if (lane != 0) return;
+  // unit weights: den = 1 + 1 + ... in order, exact below 2^53
+  if (!kWeighted) den = (double)cnt;
   if (dict) {
     if (cnt == 0) return;  // unused: reseeded (or kept) by the caller
     if (kWeighted && den <= 0.0) {
@@ -570,10 +593,10 @@ __global__ void k_slot_sums(const float* __restrict__ xr, size_t n, int d, int M
 // Host wrapper of k_slot_sums (hp == null: unit weights).
 int slot_sums_device(aq_session* s, const float* xr, size_t n, int d, int M, int k, int sd,
                      const Buckets& B, const int* active, const double* hp, const double* ho,
-                     double* dict, double* pnum, double* pden) {
+                     double* dict, double* pnum, double* pden, const float* xt) {
   const unsigned grid = (unsigned)((M * k + 3) / 4);
 #define AQ_SLOTS(SDV, WV)                                                                \
-  k_slot_sums<SDV, WV><<<grid, 128, 0, s->stream>>>(xr, n, d, M, k, sd, B.list, B.start, \
+  k_slot_sums<SDV, WV><<<grid, 128, 0, s->stream>>>(xr, xt, n, d, M, k, sd, B.list, B.start, \
                                                     B.count, active, hp, ho, dict, pnum, \
                                                     pden, s->err)
   if (sd == 2) {
@@ -687,7 +710,7 @@ int train_l2_pq_device(aq_dataset* ds, size_t M, size_t k, const aq_train_config
     if (st != AQ_OK) break;
     AQ_CUDA(cudaMemcpyAsync(active, hact.data(), M * sizeof(int), cudaMemcpyHostToDevice, s->stream));
     AQ_TRY(slot_sums_device(s, ds->xr, n, (int)d, (int)M, (int)k, (int)sd, B, active, nullptr,
-                            nullptr, cb->d64, nullptr, nullptr));
+                            nullptr, cb->d64, nullptr, nullptr, ds->xt));
     s->launches++;
     if (cfg->empty_partition_policy == 0) {
       std::vector<uint32_t> hc(M * k);

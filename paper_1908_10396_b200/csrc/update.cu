@@ -1262,7 +1262,7 @@ int aq_dev_pq_codebook_update(aq_dataset* ds, aq_codes* codes, const aq_weights*
   } else if (st == AQ_OK && all_iso) {
     AQ_TRY(clear_dev_error(s));
     st = slot_sums_device(s, ds->xr, n, (int)ds->d, (int)M, (int)k, sd, B, nullptr, pw.hp, pw.ho,
-                          out->d64, nullptr, nullptr);
+                          out->d64, nullptr, nullptr, ds->xt);
     if (st == AQ_OK) st = sync_and_check(s, "zero total weight in block");
   } else if (st == AQ_OK) {
     if (dim > 16384) {

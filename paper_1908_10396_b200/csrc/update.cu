@@ -87,6 +87,103 @@ __global__ void k_bucket_scatter(const uint8_t* __restrict__ codes, size_t n, in
   }
 }
 
+// Row-staged variants (all subspaces per block): the block's 256-point code
+// rows are copied to shared memory once (8-byte loads, coalesced) and every
+// subspace reads its nibbles there, instead of one (block, subspace) CTA per
+// pair re-reading each 32-byte sector for every subspace it holds (the
+// per-subspace kernels above read the code matrix ~M/2 times through L2).
+// Same histogram layout and the same stable order as the kernels above.
+constexpr int kRowsRound = 256;
+
+__device__ __forceinline__ void stage_code_rows(const uint8_t* codes, size_t n, int stride,
+                                                size_t i0, uint8_t* rows) {
+  const int words = stride >> 3;
+  for (int t = threadIdx.x; t < kRowsRound * words; t += blockDim.x) {
+    const int r = t / words, w = t % words;
+    const size_t i = i0 + r;
+    reinterpret_cast<uint2*>(rows)[t] =
+        i < n ? reinterpret_cast<const uint2*>(codes + i * stride)[w] : make_uint2(0u, 0u);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_bucket_hist_rows(const uint8_t* __restrict__ codes,
+                                                          size_t n, int stride, int bits, int M,
+                                                          int K, unsigned* __restrict__ hist,
+                                                          size_t nb, DevError* err, int k) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  unsigned* h = reinterpret_cast<unsigned*>(sm);                // [M][K]
+  uint8_t* rows = sm + (((size_t)M * K * 4 + 15) & ~(size_t)15);  // [256][stride]
+  for (int t = threadIdx.x; t < M * K; t += blockDim.x) h[t] = 0;
+  const size_t base = (size_t)blockIdx.x * kBucketBlock;
+  for (int round = 0; round < kBucketBlock / kRowsRound; ++round) {
+    const size_t i0 = base + (size_t)round * kRowsRound;
+    if (i0 >= n) break;
+    __syncthreads();
+    stage_code_rows(codes, n, stride, i0, rows);
+    __syncthreads();
+    const size_t i = i0 + threadIdx.x;
+    if (i < n) {
+      const uint8_t* row = rows + (size_t)threadIdx.x * stride;
+      for (int m = 0; m < M; ++m) {
+        const unsigned c = get_code(row, m, bits);
+        if ((int)c >= k) report_error(err, i, AQ_E_CODE_OUT_OF_RANGE);
+        atomicAdd(&h[m * K + min(c, (unsigned)K - 1)], 1u);
+      }
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < M * K; t += blockDim.x)
+    hist[(size_t)t * nb + blockIdx.x] = h[t];
+}
+
+__global__ void __launch_bounds__(256) k_bucket_scatter_rows(const uint8_t* __restrict__ codes,
+                                                             size_t n, int stride, int bits,
+                                                             int M, int K,
+                                                             const unsigned* __restrict__ base,
+                                                             size_t nb,
+                                                             uint32_t* __restrict__ list) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  unsigned* run = reinterpret_cast<unsigned*>(sm);  // [M][K]
+  unsigned* wcnt2 = run + (size_t)M * K;           // [2][8][K], alternating by m
+  uint8_t* rows = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(wcnt2 + 16 * K) + 15) & ~(uintptr_t)15);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int t = threadIdx.x; t < M * K; t += blockDim.x)
+    run[t] = base[(size_t)t * nb + blockIdx.x] - (unsigned)((size_t)(t / K) * n);
+  const size_t b0 = (size_t)blockIdx.x * kBucketBlock;
+  for (int round = 0; round < kBucketBlock / kRowsRound; ++round) {
+    const size_t i0 = b0 + (size_t)round * kRowsRound;
+    if (i0 >= n) break;
+    __syncthreads();
+    stage_code_rows(codes, n, stride, i0, rows);
+    const size_t i = i0 + threadIdx.x;
+    const bool valid = i < n;
+    const uint8_t* row = rows + (size_t)threadIdx.x * stride;
+    for (int m = 0; m < M; ++m) {
+      // this buffer was last read two subspaces ago, three barriers back
+      unsigned* wcnt = wcnt2 + (m & 1) * 8 * K;
+      for (int t = threadIdx.x; t < 8 * K; t += blockDim.x) wcnt[t] = 0;
+      __syncthreads();
+      const unsigned dg = valid ? min(get_code(row, m, bits), (unsigned)K - 1) : 0xffffffffu;
+      const unsigned peers = __match_any_sync(0xffffffffu, dg);
+      const unsigned rk = __popc(peers & ((1u << lane) - 1u));
+      if (valid && rk == 0) wcnt[w * K + dg] = __popc(peers);
+      __syncthreads();
+      if (valid) {
+        unsigned before = 0;
+        for (int ww = 0; ww < w; ++ww) before += wcnt[ww * K + dg];
+        list[(size_t)m * n + run[m * K + dg] + before + rk] = (uint32_t)i;
+      }
+      __syncthreads();
+      for (int t = threadIdx.x; t < K; t += blockDim.x) {
+        unsigned sacc = 0;
+        for (int ww = 0; ww < 8; ++ww) sacc += wcnt[ww * K + t];
+        run[m * K + t] += sacc;
+      }
+    }
+  }
+}
+
 __global__ void k_bucket_offsets(const unsigned* __restrict__ base, size_t nb, int M, int K,
                                  size_t n, uint32_t* __restrict__ start,
                                  uint32_t* __restrict__ count) {
@@ -117,13 +214,34 @@ int build_buckets(aq_codes* c, int k, Buckets* B) {
   unsigned* hist = B->count + M * K;
   B->K = K;
   AQ_TRY(clear_dev_error(s));
-  k_bucket_hist<<<dim3((unsigned)nb, (unsigned)M), 256, 0, s->stream>>>(
-      c->data, n, (int)c->stride, c->bits, K, hist, nb, s->err, k);
+  // row-staged kernels when the block's counters and 256 code rows fit
+  const size_t hist_sm = (((size_t)M * K * 4 + 15) & ~(size_t)15) + (size_t)kRowsRound * c->stride;
+  const size_t scat_sm = ((((size_t)M * K + 16 * K) * 4 + 15) & ~(size_t)15) +
+                         (size_t)kRowsRound * c->stride;
+  static const int rows_env = getenv("AQ_BUCKET_ROWS") ? atoi(getenv("AQ_BUCKET_ROWS")) : 1;
+  const bool rows =
+      rows_env && std::max(hist_sm, scat_sm) <= 160 * 1024 && (c->stride % 8) == 0;
+  if (rows) {
+    AQ_CUDA(cudaFuncSetAttribute(k_bucket_hist_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)hist_sm));
+    k_bucket_hist_rows<<<(unsigned)nb, 256, hist_sm, s->stream>>>(
+        c->data, n, (int)c->stride, c->bits, (int)M, K, hist, nb, s->err, k);
+  } else {
+    k_bucket_hist<<<dim3((unsigned)nb, (unsigned)M), 256, 0, s->stream>>>(
+        c->data, n, (int)c->stride, c->bits, K, hist, nb, s->err, k);
+  }
   AQ_LAUNCHED(s);
   AQ_TRY(sync_and_check(s, "codebook update: code out of range"));
   AQ_TRY(scan_device(s, hist, M * K * nb));
-  k_bucket_scatter<<<dim3((unsigned)nb, (unsigned)M), 256, 0, s->stream>>>(
-      c->data, n, (int)c->stride, c->bits, K, hist, nb, B->list);
+  if (rows) {
+    AQ_CUDA(cudaFuncSetAttribute(k_bucket_scatter_rows,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scat_sm));
+    k_bucket_scatter_rows<<<(unsigned)nb, 256, scat_sm, s->stream>>>(
+        c->data, n, (int)c->stride, c->bits, (int)M, K, hist, nb, B->list);
+  } else {
+    k_bucket_scatter<<<dim3((unsigned)nb, (unsigned)M), 256, 0, s->stream>>>(
+        c->data, n, (int)c->stride, c->bits, K, hist, nb, B->list);
+  }
   AQ_LAUNCHED(s);
   k_bucket_offsets<<<(unsigned)((M * K + 255) / 256), 256, 0, s->stream>>>(
       hist, nb, (int)M, K, n, B->start, B->count);

@@ -418,7 +418,12 @@ __global__ void __launch_bounds__(TPB, MINB)
       loss = loss > 0.0 ? loss : 0.0;
     }
     if (a.losses) a.losses[i] = loss;
-    if (a.changed && nchg) atomicAdd(a.changed, nchg);
+    if (a.changed) {  // one atomic per warp
+      const unsigned act = __activemask();
+      const unsigned tot = __reduce_add_sync(act, (unsigned)nchg);
+      if (tot && (int)(threadIdx.x & 31) == __ffs(act) - 1)
+        atomicAdd(a.changed, (unsigned long long)tot);
+    }
   }
   if (a.mode <= 1) {
     // rows are 8-byte aligned with stride a multiple of 8 (code_stride)
@@ -584,7 +589,12 @@ __global__ void k_encode_generic(const EncodeArgs a, const float* xt,
       loss = loss > 0.0 ? loss : 0.0;
     }
     if (a.losses) a.losses[i] = loss;
-    if (a.changed && nchg) atomicAdd(a.changed, nchg);
+    if (a.changed) {  // one atomic per warp
+      const unsigned act = __activemask();
+      const unsigned tot = __reduce_add_sync(act, (unsigned)nchg);
+      if (tot && (int)(threadIdx.x & 31) == __ffs(act) - 1)
+        atomicAdd(a.changed, (unsigned long long)tot);
+    }
   }
 }
 

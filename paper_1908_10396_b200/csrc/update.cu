@@ -267,15 +267,20 @@ __global__ void k_point_weights(const double* __restrict__ norms, size_t n, DevW
   hp[i] = a;
   ho[i] = b;
   double c = 0.0;
+  bool zero = false;
   if (a != b) {
-    atomicOr(&flags[0], 1ull);
     const double n2 = __dmul_rn(norms[i], norms[i]);
-    if (n2 == 0.0)
-      atomicMin(&flags[1], (unsigned long long)i + 1ull);
-    else
-      c = __ddiv_rn(__dsub_rn(a, b), n2);
+    zero = n2 == 0.0;
+    if (!zero) c = __ddiv_rn(__dsub_rn(a, b), n2);
   }
   coef[i] = c;
+  // one atomic per warp (a per-point atomicOr on one word serialises n
+  // updates: 6.5 ms at n = 1e7)
+  const unsigned act = __activemask();
+  const unsigned aniso = __ballot_sync(act, a != b);
+  const int leader = __ffs(act) - 1;
+  if (aniso && (int)(threadIdx.x & 31) == leader) atomicOr(&flags[0], 1ull);
+  if (zero) atomicMin(&flags[1], (unsigned long long)i + 1ull);
 }
 
 // ---- dense normal equations ---------------------------------------------------------------

@@ -9,6 +9,8 @@
 // vq.hpp:270,316): a single-thread float64 chain per subspace, so histories
 // are bit-identical to the reference.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <unordered_map>
 #include <vector>
 
@@ -866,14 +868,21 @@ int aq_dev_train_apq(aq_dataset* ds, size_t M, size_t k, const aq_weights* w,
   aq_codebook* next = nullptr;
   if (st == AQ_OK) st = aq_codebook_upload(s, nullptr, M, k, sd, &next);
   bool have_next = false;  // `next` already holds the update of the current codes
+  // AQ_TRACE=1: host wall time of each step of an iteration (stderr)
+  static const bool trace = getenv("AQ_TRACE") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
   for (int iter = 0; st == AQ_OK && iter < cfg->max_iterations; ++iter) {
+    const auto t0 = now();
     if (!have_next) st = aq_dev_pq_codebook_update(ds, codes, w, cfg->ridge, next);
     if (st != AQ_OK) break;
+    const auto t1 = now();
     std::swap(cb, next);
     have_next = false;
     const double prev = tot;
     st = pass_async(&changed);
     if (st != AQ_OK) break;
+    const auto t2 = now();
     // speculative next update (a pure function of the codes) while the
     // total is summed; discarded when the stopping rule fires below
     if (changed != 0 && iter + 1 < cfg->max_iterations) {
@@ -881,8 +890,12 @@ int aq_dev_train_apq(aq_dataset* ds, size_t M, size_t k, const aq_weights* w,
       if (st != AQ_OK) break;
       have_next = true;
     }
+    const auto t3 = now();
     st = get_total(&tot);
     if (st != AQ_OK) break;
+    if (trace)
+      fprintf(stderr, "[aq] iter %d: update %.1f ms, pass %.1f ms, spec update %.1f ms, total %.1f ms\n",
+              iter, ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, now()));
     if (history_out) history_out[hl] = tot;
     ++hl;
     if (changed == 0) break;

@@ -103,3 +103,18 @@ def test_k64_byte_codes_end_to_end():
     ids, sc = aq.dev_adc_search(s.upload_codes(codes), s.upload_codebook(cb), q, 20)
     wi, ws = P.adc_search_batch(q, want_codes, 64, want_cb, 8, 64, 2, 20)
     assert np.array_equal(ids, wi) and np.array_equal(sc, ws)
+
+
+def test_train_long_rows_take_the_chunked_loss_sums():
+    # n >= 65536: k-means totals (tol > 0) and the train_apq loss history run
+    # through the chunk-parallel sums (train.cu seq_sums_on); still bit-exact
+    x = mixture_rows(90000, 16, 67, centers=32, sigma=0.3)
+    hp, ho = threshold_hp_ho(x, 0.2)
+    cfg = aq.TrainConfig(max_iterations=3, relative_tolerance=1e-7, seed=4)
+    hist = []
+    cb, codes = aq.train_apq(x, 8, 16, aq.ThresholdWeights(0.2), cfg, True, hist)
+    want_cb, want_codes, want_hist = P.train_apq(x.astype(np.float64), 8, 16, hp, ho, max_it=3,
+                                                 tol=1e-7, seed=4, warm_start=True)
+    assert np.array_equal(np.array(hist), want_hist)
+    assert np.array_equal(codes.codes, want_codes)
+    assert np.array_equal(cb.dictionaries, want_cb)

@@ -436,6 +436,380 @@ __global__ void __launch_bounds__(TPB, MINB)
   }
 }
 
+// ---- word-unrolled fast kernel ---------------------------------------------
+//
+// Same decisions as k_encode_sd2 (float32 proxy, window, float64 re-score of
+// windows with more than one candidate), fewer instructions per subspace:
+//  * window mask: the 16 differences K_j - thr are formed two per FADD2 and
+//    each sign bit is shifted into one of four chains by a funnel shift (one
+//    SHF per candidate instead of FSETP + predicated add);
+//  * error budget: h_perp = 0 points use the cC = 1 budget (an upper bound),
+//    one expression for every point;
+//  * the subspace loop is unrolled over the 8 codes of a packed word: code
+//    extraction and insertion (funnel shift right) have constant shifts;
+//  * point rows are prefetched two subspaces ahead (the tile buffer carries
+//    four pair tiles of padding).
+
+// Proxy keys K_j = a_j (g' a_j - beta') + C_j (kNearest: C_j - 2 a_j), two
+// candidates per packed FMA; nbeta = -beta'.
+template <bool kNearest>
+__device__ __forceinline__ void proxy_keys(float xf0, float xf1,
+                                           const float4* __restrict__ sc,
+                                           int coff, float gp, float nbeta,
+                                           float (&K)[16]) {
+  const float2 X0 = make_float2(xf0, xf0), X1 = make_float2(xf1, xf1);
+  const float2 GP = make_float2(gp, gp), NB = make_float2(nbeta, nbeta);
+  const float2 M2 = make_float2(-2.0f, -2.0f);
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const float4 c = sc[t];
+    const float4 C4 = sc[coff + (t >> 1)];
+    const float2 Cp = (t & 1) ? make_float2(C4.z, C4.w) : make_float2(C4.x, C4.y);
+    const float2 A = __ffma2_rn(X1, make_float2(c.z, c.w), __fmul2_rn(X0, make_float2(c.x, c.y)));
+    const float2 Kp = kNearest ? __ffma2_rn(M2, A, Cp)
+                               : __ffma2_rn(A, __ffma2_rn(GP, A, NB), Cp);
+    K[2 * t] = Kp.x;
+    K[2 * t + 1] = Kp.y;
+  }
+}
+
+// Window of K: thr = best + |best| 2^-22 + dpad (dpad = 2 delta); bit 15 - j of
+// the result is set iff K_j < thr (the sign bit of K_j - thr). NaN dpad gives
+// a NaN thr, which fails the caller's envelope test.
+__device__ __forceinline__ unsigned window_mask(const float (&K)[16], float dpad,
+                                                float* best_out, float* thr_out) {
+  float m6[6];
+#pragma unroll
+  for (int t = 0; t < 5; ++t)
+    m6[t] = fminf(fminf(K[3 * t], K[3 * t + 1]), K[3 * t + 2]);
+  m6[5] = K[15];
+  const float best = fminf(fminf(fminf(m6[0], m6[1]), m6[2]),
+                           fminf(fminf(m6[3], m6[4]), m6[5]));
+  const float thr = __fadd_rn(__fmaf_rn(fabsf(best), 2.384185791015625e-07f, best), dpad);
+  const float2 NT = make_float2(-thr, -thr);
+  unsigned c[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const float2 D = __fadd2_rn(make_float2(K[2 * t], K[2 * t + 1]), NT);
+    c[t >> 1] = __funnelshift_l(__float_as_uint(D.x), c[t >> 1], 1);
+    c[t >> 1] = __funnelshift_l(__float_as_uint(D.y), c[t >> 1], 1);
+  }
+  *best_out = best;
+  *thr_out = thr;
+  return (((c[0] << 4) | c[1]) << 8) | ((c[2] << 4) | c[3]);
+}
+
+// Decision from a window: the single candidate, else the float64 re-score of
+// the window (or of all candidates when the proxies left the envelope).
+__device__ __forceinline__ unsigned decide(unsigned mask, float best, float thr,
+                                           float xf0, float xf1,
+                                           const double2* __restrict__ cbm,
+                                           unsigned all_mask, bool nearest,
+                                           double base2, double base1,
+                                           const double* pw, int ps,
+                                           unsigned long long* stats) {
+  const bool env = thr < 1e30f && best > -1e30f;
+  if (env && __popc(mask) == 1) return (unsigned)(__clz(mask) - 16);
+  const unsigned wm = (env && mask) ? (__brev(mask) >> 16) : all_mask;
+  return exact_window(xf0, xf1, cbm, wm, nearest, base2, base1, pw, ps, stats);
+}
+
+struct SweepPoint {
+  float gp, ngp2, ncC2, agp, dabs2;
+  int coff;
+};
+
+// One coordinate-descent step at subspace m (cd_sweep body, pq.hpp:157-183).
+template <int TPB>
+__device__ __forceinline__ unsigned cd_step(const float2 xv, const unsigned cur, const int m,
+                                            const float4* __restrict__ scb,
+                                            const double2* __restrict__ cb2,
+                                            const float2* __restrict__ srm,
+                                            const SweepPoint& P, double& s2,
+                                            double& s1, const double* pw,
+                                            unsigned all_mask,
+                                            unsigned long long* stats) {
+  const double2 cc = cb2[m * 16 + cur];
+  double t2, t1;
+  residual2(xv.x, xv.y, cc.x, cc.y, &t2, &t1);
+  const double base2 = __dsub_rn(s2, t2);
+  const double base1 = __dsub_rn(s1, t1);
+  const float2 rr = srm[m];
+  const float X = __fmaf_rn(xv.y, xv.y, xv.x * xv.x);
+  const float ax = (fabsf(xv.x) + fabsf(xv.y)) * rr.x;
+  // W2 >= |g'| ax^2 + beta^ ax + cC rm^2 (budget note in k_encode_sd2)
+  const float b1f = (float)base1;
+  const float W2 = __fmaf_rn(ax, __fmaf_rn(P.agp, __fmaf_rn(2.0f, fabsf(b1f) + X, ax), 2.0f), rr.y);
+  const float dpad = __fmaf_rn(W2, 7.62939453125e-06f, P.dabs2);  // 2 (2^-18 W2 + abs)
+  const float nbeta = __fmaf_rn(P.ngp2, b1f + X, P.ncC2);
+  float K[16];
+  proxy_keys<false>(xv.x, xv.y, scb + m * kCbStride, P.coff, P.gp, nbeta, K);
+  float best, thr;
+  const unsigned mask = window_mask(K, dpad, &best, &thr);
+  const unsigned jb = decide(mask, best, thr, xv.x, xv.y, cb2 + m * 16, all_mask,
+                             false, base2, base1, pw, TPB, stats);
+  double b2 = t2, b1 = t1;
+  if (jb != cur) {
+    const double2 cj = cb2[m * 16 + jb];
+    residual2(xv.x, xv.y, cj.x, cj.y, &b2, &b1);
+  }
+  s2 = __dadd_rn(base2, b2);
+  s1 = __dadd_rn(base1, b1);
+  return jb;
+}
+
+// reconstruction_nearest_pass step (pq.hpp:236-243) + pq_point_state terms.
+__device__ __forceinline__ unsigned nearest_step(const float2 xv, const int m,
+                                                 const float4* __restrict__ scb,
+                                                 const double2* __restrict__ cb2,
+                                                 const float2 rr, unsigned all_mask,
+                                                 double& s2, double& s1,
+                                                 unsigned long long* stats) {
+  const float X = __fmaf_rn(xv.y, xv.y, xv.x * xv.x);
+  const float ax = (fabsf(xv.x) + fabsf(xv.y)) * rr.x;
+  // error budget: < 12u (2 ax + rm^2); 2^-18 = 64u
+  const float Wn = 2.0f * ax + rr.y + X * 9.094947e-13f;
+  const float dpad = Wn < 1e30f ? __fmaf_rn(Wn, 7.62939453125e-06f, 2e-30f) : __int_as_float(0x7fffffff);
+  float K[16];
+  proxy_keys<true>(xv.x, xv.y, scb + m * kCbStride, 8, 0.0f, 0.0f, K);
+  float best, thr;
+  const unsigned mask = window_mask(K, dpad, &best, &thr);
+  const unsigned jb = decide(mask, best, thr, xv.x, xv.y, cb2 + m * 16, all_mask,
+                             true, 0.0, 0.0, nullptr, 0, stats);
+  const double2 cj = cb2[m * 16 + jb];
+  double t2, t1;
+  residual2(xv.x, xv.y, cj.x, cj.y, &t2, &t1);
+  s2 = __dadd_rn(s2, t2);
+  s1 = __dadd_rn(s1, t1);
+  return jb;
+}
+
+// MT > 0: M known at compile time (every shared-memory offset is a constant);
+// MT = 0: any M.
+template <int TPB, int MINB, int MT>
+__global__ void __launch_bounds__(TPB, MINB)
+    k_encode_sd2w(const EncodeArgs a, unsigned long long* stats) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int M = MT > 0 ? MT : a.M;
+  float4* scb = reinterpret_cast<float4*>(smem);                        // [M+1][16]
+  double2* cb2 = reinterpret_cast<double2*>(scb + (M + 1) * kCbStride);  // [M+1][16]
+  float2* srm = reinterpret_cast<float2*>(cb2 + (M + 1) * 16);          // [M+1] {rm, rm^2}
+  uint32_t* scode = reinterpret_cast<uint32_t*>(srm + M + 1);
+  double* swt = reinterpret_cast<double*>(
+      (reinterpret_cast<uintptr_t>(scode + ((M + 7) / 8 + 1) * TPB) + 7) & ~(uintptr_t)7);
+  {
+    const double2* g2 = reinterpret_cast<const double2*>(a.cb64);
+    for (int t = threadIdx.x; t < M * 16; t += blockDim.x) {
+      const int m = t >> 4, j = t & 15;
+      const float4 v = a.cb32[t];  // {c0, c1, C, 0}; C = 1e30 pads j >= k
+      float* row = reinterpret_cast<float*>(scb + m * kCbStride);
+      row[(j >> 1) * 4 + (j & 1)] = v.x;
+      row[(j >> 1) * 4 + 2 + (j & 1)] = v.y;
+      row[32 + j] = v.z;
+      row[48 + j] = j < a.k ? 0.0f : 1e30f;
+      cb2[t] = j < a.k ? g2[(size_t)m * a.k + j] : make_double2(0.0, 0.0);
+    }
+  }
+  for (int t = threadIdx.x; t <= M; t += blockDim.x) {
+    const float r = t < M ? a.rmax[t] : 0.0f;
+    srm[t] = make_float2(r, r * r);
+  }
+  for (int t = threadIdx.x; t < 16; t += blockDim.x) cb2[M * 16 + t] = make_double2(0.0, 0.0);
+  __syncthreads();
+
+  const size_t i = (size_t)blockIdx.x * TPB + threadIdx.x;
+  if (i >= a.n) return;
+  const int W = (M + 7) >> 3;
+  const int Wf = M >> 3, Mr = M & 7;
+  const unsigned all_mask = (1u << a.k) - 1u;
+  uint32_t* mycode = scode + threadIdx.x;  // word w at mycode[w * TPB]
+  const float2* xrow = a.xt + (i >> 5) * (size_t)a.pairs * 32 + (i & 31);
+  uint8_t* crow = a.codes + i * a.stride;
+
+  double hp, ho;
+  int st = AQ_OK;
+  if (!resolve_weights(a.w, i, a.norms[i], &hp, &ho, &st)) {
+    report_error(a.err, i, st);
+    return;
+  }
+  const bool iso = hp == ho;
+  double inv = 0.0;
+  const bool need_inv = a.mode != 0 || a.passes > 0;
+  if (!iso) {
+    const double n2 = __dmul_rn(a.norms[i], a.norms[i]);
+    if (n2 == 0.0) {
+      if (need_inv) {
+        report_error(a.err, i, AQ_E_ZERO_NORM_DATAPOINT);
+        return;
+      }
+    } else {
+      inv = __ddiv_rn(1.0, n2);
+    }
+  }
+  const bool zeroC = !iso && !(ho > 0.0);
+  float gp = 0.0f;
+  if (!iso) {
+    const double g = __dmul_rn(__dsub_rn(hp, ho), inv);
+    gp = (float)(zeroC ? g : g / ho);
+  }
+  const float cC = zeroC ? 0.0f : 1.0f;
+  const bool fast = fabsf(gp) < 1e30f;
+
+  double s2 = 0.0, s1 = 0.0;
+  float B1 = 0.0f, B2 = 0.0f, Amax = 0.0f, Xmax = 0.0f;
+  if (a.mode == 0) {
+    // reconstruction_nearest_pass + pq_point_state (pq.hpp:594, 603)
+    float2 xa = xrow[0], xb = xrow[32];
+    uint32_t nw = 0;
+#pragma unroll 2
+    for (int m = 0; m < M; ++m) {
+      const float2 xv = xa;
+      xa = xb;
+      xb = xrow[(size_t)(m + 2) * 32];  // padded
+      const float2 rr = srm[m];
+      const float X = __fmaf_rn(xv.y, xv.y, xv.x * xv.x);
+      const float l1 = fabsf(xv.x) + fabsf(xv.y);
+      const float ax = l1 * rr.x;
+      B1 += X + ax;
+      B2 += (l1 + rr.x) * (l1 + rr.x);
+      Amax = fmaxf(Amax, ax);
+      Xmax = fmaxf(Xmax, X);
+      const unsigned jb = nearest_step(xv, m, scb, cb2, rr, all_mask, s2, s1, stats);
+      nw = __funnelshift_r(nw, jb, 4);
+      if ((m & 7) == 7) mycode[(m >> 3) * TPB] = nw;
+    }
+    if (Mr) mycode[Wf * TPB] = nw >> (32 - 4 * Mr);
+  } else {
+    const uint32_t* r4 = reinterpret_cast<const uint32_t*>(crow);
+    for (int w = 0; w < W; ++w) mycode[w * TPB] = r4[w];
+    if (a.mode == 1) {
+      // pq_point_state from the current codes (pq.hpp:213)
+#pragma unroll 4
+      for (int m = 0; m < M; ++m) {
+        const float2 xv = xrow[(size_t)m * 32];
+        const unsigned c = (mycode[(m >> 3) * TPB] >> (4 * (m & 7))) & 15u;
+        const double2 cj = cb2[m * 16 + c];
+        double t2, t1;
+        residual2(xv.x, xv.y, cj.x, cj.y, &t2, &t1);
+        s2 = __dadd_rn(s2, t2);
+        s1 = __dadd_rn(s1, t1);
+        const float rm = srm[m].x;
+        const float X = __fmaf_rn(xv.y, xv.y, xv.x * xv.x);
+        const float l1 = fabsf(xv.x) + fabsf(xv.y);
+        B1 += X + l1 * rm;
+        B2 += (l1 + rm) * (l1 + rm);
+        Amax = fmaxf(Amax, l1 * rm);
+        Xmax = fmaxf(Xmax, X);
+      }
+    }
+  }
+
+  // error-budget constants (as k_encode_sd2)
+  B1 *= 1.0009765625f;
+  B2 *= 1.0009765625f;
+  const float agp = fabsf(gp);
+  const float AB = Amax + B1 + Xmax;
+  const float W2max = Amax * (agp * (Amax + 2.0f * (B1 + Xmax)) + 2.0f) + 4.0f * B2;
+  const float dabs = (B2 + Xmax + W2max + agp * AB * AB) * 9.094947e-13f + 1e-30f;
+  const bool fastpt = fast && dabs < 1e25f;
+  SweepPoint P;
+  P.gp = gp;
+  P.ngp2 = -2.0f * gp;
+  P.ncC2 = -2.0f * cC;
+  P.agp = agp;
+  P.dabs2 = fastpt ? 2.0f * dabs : __int_as_float(0x7fffffff);  // NaN: exact path
+  P.coff = zeroC ? 12 : 8;
+  swt[threadIdx.x] = hp;
+  swt[TPB + threadIdx.x] = ho;
+  swt[2 * TPB + threadIdx.x] = inv;
+  const double* pw = swt + threadIdx.x;
+
+  // coordinate-descent sweeps (cd_sweep, pq.hpp:151-185)
+  const int max_sweeps = a.mode == 0 ? a.passes : (a.mode == 1 ? 64 : 0);
+  int sweeps_run = 0;
+  for (int p = 0; p < max_sweeps; ++p) {
+    ++sweeps_run;
+    unsigned chg = 0;
+    float2 xa = xrow[0], xb = xrow[32];
+    uint32_t cw = mycode[0], nw = 0;
+#pragma unroll 2
+    for (int m = 0; m < M; ++m) {
+      const float2 xv = xa;
+      xa = xb;
+      xb = xrow[(size_t)(m + 2) * 32];  // padded
+      const unsigned cur = cw & 15u;
+      cw >>= 4;
+      const unsigned jb = cd_step<TPB>(xv, cur, m, scb, cb2, srm, P, s2, s1, pw,
+                                       all_mask, stats);
+      chg |= jb ^ cur;
+      nw = __funnelshift_r(nw, jb, 4);
+      if ((m & 7) == 7) {
+        mycode[(m >> 3) * TPB] = nw;
+        cw = mycode[((m >> 3) + 1) * TPB];  // padded word
+      }
+    }
+    if (Mr) mycode[Wf * TPB] = nw >> (32 - 4 * Mr);
+    const bool changed = chg != 0;
+    if (a.mode == 0) {
+      if (!changed) break;  // pq.hpp:605-606
+    } else {
+      // pq.hpp:215-216: repeat only when sweeping to a fixed point
+      if (!(changed && a.sweep_fixed && p + 1 < 64)) break;
+    }
+  }
+  if (stats && a.mode == 0) atomicAdd(stats + 1 + min(sweeps_run, 7), 1ull);
+
+  if (a.mode >= 1) {
+    // weights re-read from shared memory (not kept live across the sweeps)
+    const volatile double* vw = swt + threadIdx.x;
+    const double hp = vw[0], ho = vw[TPB], inv = vw[2 * TPB];
+    const bool iso = hp == ho;
+    // pq_point_loss (pq.hpp:137-146): state recomputed from scratch
+    double r2 = 0.0, r1 = 0.0;
+    unsigned long long nchg = 0;
+    for (int w = 0; w < W; ++w) {
+      const uint32_t cw = mycode[w * TPB];
+      const uint32_t old = reinterpret_cast<const uint32_t*>(crow)[w];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int m = w * 8 + q;
+        if (m < M) {
+          const float2 xv = xrow[(size_t)m * 32];
+          const unsigned c = (cw >> (4 * q)) & 15u;
+          nchg += c != ((old >> (4 * q)) & 15u);
+          const double2 cj = cb2[m * 16 + c];
+          double t2, t1;
+          residual2(xv.x, xv.y, cj.x, cj.y, &t2, &t1);
+          r2 = __dadd_rn(r2, t2);
+          r1 = __dadd_rn(r1, t1);
+        }
+      }
+    }
+    double loss;
+    if (iso) {
+      loss = __dmul_rn(ho, r2);
+    } else {
+      loss = combined_loss(r2, r1, hp, ho, inv);
+      loss = loss > 0.0 ? loss : 0.0;
+    }
+    if (a.losses) a.losses[i] = loss;
+    if (a.changed) {  // one atomic per warp
+      const unsigned act = __activemask();
+      const unsigned tot = __reduce_add_sync(act, (unsigned)nchg);
+      if (tot && (int)(threadIdx.x & 31) == __ffs(act) - 1)
+        atomicAdd(a.changed, (unsigned long long)tot);
+    }
+  }
+  if (a.mode <= 1) {
+    uint2* r8 = reinterpret_cast<uint2*>(crow);
+    for (int w = 0; w < (int)(a.stride >> 3); ++w) {
+      const uint32_t lo = 2 * w < W ? mycode[(2 * w) * TPB] : 0u;
+      const uint32_t hi = 2 * w + 1 < W ? mycode[(2 * w + 1) * TPB] : 0u;
+      r8[w] = make_uint2(lo, hi);
+    }
+  }
+}
+
 // ---- generic exact kernel (any sub_dimension, k <= 256) ---------------------
 
 __device__ __forceinline__ float xval(const float* __restrict__ xt, size_t i,
@@ -655,11 +1029,12 @@ int run_encode(aq_dataset* ds, aq_codebook* cb, const aq_weights* w,
   const bool fast = cb->sd == 2 && cb->k <= 16 && codes->bits == 4;
   if (fast) {
     const int W = (a.M + 7) / 8;
-    int variant = 1;  // 256 threads, 3 CTAs/SM (24 warps): measured best
+    int variant = 11;  // word-unrolled kernel, 256 threads, 3 CTAs/SM
     if (const char* v = getenv("AQ_ENC_VARIANT")) variant = atoi(v);
-    const int tpb = (variant == 2 || variant == 3) ? 128 : 256;
+    const int tpb = (variant == 2 || variant == 3 || variant == 12 || variant == 15) ? 128
+                    : variant == 17 ? 192 : 256;
     const size_t smv = (size_t)(a.M + 1) * (kCbStride * sizeof(float4) + 16 * sizeof(double2)) +
-                       (a.M + 1) * sizeof(float) + (size_t)(W + 1) * tpb * sizeof(uint32_t) + 16 +
+                       (a.M + 1) * sizeof(float2) + (size_t)(W + 1) * tpb * sizeof(uint32_t) + 16 +
                        3 * tpb * sizeof(double) + 8;
     const unsigned grid = (unsigned)((ds->n + tpb - 1) / tpb);
     if (smv > 200 * 1024) return ref_error(AQ_E_UNSUPPORTED, "M too large for the fast encoder");
@@ -670,11 +1045,37 @@ int run_encode(aq_dataset* ds, aq_codebook* cb, const aq_weights* w,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)); \
     k_encode_sd2<T, B><<<grid, T, smv, s->stream>>>(a, g_stats);                        \
   } while (0)
-    if (variant == 1) AQ_ENC_LAUNCH(256, 3);
+#define AQ_ENCW_LAUNCH(T, B, MT)                                                         \
+  do {                                                                                  \
+    AQ_CUDA(cudaFuncSetAttribute(k_encode_sd2w<T, B, MT>,                               \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)); \
+    k_encode_sd2w<T, B, MT><<<grid, T, smv, s->stream>>>(a, g_stats);                   \
+  } while (0)
+    if (variant == 11) {
+      // M-specialised instances for the common shapes; other M run the
+      // previous kernel (faster than the runtime-M instance of this one)
+      switch (a.M) {
+        case 16: AQ_ENCW_LAUNCH(256, 3, 16); break;
+        case 32: AQ_ENCW_LAUNCH(256, 3, 32); break;
+        case 48: AQ_ENCW_LAUNCH(256, 3, 48); break;
+        case 50: AQ_ENCW_LAUNCH(256, 3, 50); break;
+        case 64: AQ_ENCW_LAUNCH(256, 3, 64); break;
+        case 96: AQ_ENCW_LAUNCH(256, 3, 96); break;
+        case 128: AQ_ENCW_LAUNCH(256, 3, 128); break;
+        default: AQ_ENC_LAUNCH(256, 3); break;
+      }
+    } else if (variant == 12) AQ_ENCW_LAUNCH(128, 6, 0);
+    else if (variant == 13) AQ_ENCW_LAUNCH(256, 2, 0);
+    else if (variant == 14) AQ_ENCW_LAUNCH(256, 3, 0);
+    else if (variant == 15) AQ_ENCW_LAUNCH(128, 5, 64);
+    else if (variant == 16) AQ_ENCW_LAUNCH(256, 2, 64);
+    else if (variant == 17) AQ_ENCW_LAUNCH(192, 4, 64);
+    else if (variant == 1) AQ_ENC_LAUNCH(256, 3);
     else if (variant == 2) AQ_ENC_LAUNCH(128, 4);
     else if (variant == 3) AQ_ENC_LAUNCH(128, 6);
     else AQ_ENC_LAUNCH(256, 2);
 #undef AQ_ENC_LAUNCH
+#undef AQ_ENCW_LAUNCH
     AQ_LAUNCHED(s);
     timer_mark(s, AQ_T_ENCODE);
   } else {

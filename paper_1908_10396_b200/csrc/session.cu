@@ -355,8 +355,9 @@ static int dataset_from_device_rows(aq_session* s, const float* xdev, size_t n,
   ds->d = d;
   const size_t tf = tiled_floats(n, d);
   // +64 floats: the encoder prefetches one dimension pair past a row's end
-  AQ_CUDA(cudaMallocAsync(&ds->xt, (tf + 64) * sizeof(float), s->stream));
-  AQ_CUDA(cudaMemsetAsync(ds->xt + tf, 0, 64 * sizeof(float), s->stream));
+  // four pair tiles of padding: the encoders prefetch up to two pairs past a row
+  AQ_CUDA(cudaMallocAsync(&ds->xt, (tf + 256) * sizeof(float), s->stream));
+  AQ_CUDA(cudaMemsetAsync(ds->xt + tf, 0, 256 * sizeof(float), s->stream));
   AQ_CUDA(cudaMallocAsync(&ds->norms, (n ? n : 1) * sizeof(double), s->stream));
   AQ_CUDA(cudaMallocAsync(&ds->xr, (n * d ? n * d : 1) * sizeof(float), s->stream));
   if (n * d)

@@ -235,6 +235,37 @@ inline std::pair<ProductCodebook, CodeMatrix> train_apq(
   return {b200::download(cb.p, M, k, data.d / M), b200::download(cm.p, data.n, M, k)};
 }
 
+// vq.hpp:243-329: anisotropic vector quantization (one full-dimensional
+// codebook); the device trainer returns it as an M = 1 product codebook.
+inline std::pair<Codebook, VqAssignment> train_avq(const Dataset& data, std::size_t k,
+                                                   std::span<const AnisotropicWeights> weights,
+                                                   const TrainConfig& config) {
+  if (data.n == 0) throw EmptyDataset("cannot train on an empty dataset");
+  if (k == 0 || k > data.n)
+    throw InvalidArgument("need 1 <= k <= n (codewords come from datapoints)");
+  if (weights.size() != data.n) throw InvalidArgument("need one AnisotropicWeights per datapoint");
+  b200::OwnedDataset ds;
+  b200::upload(data, ds);
+  b200::WeightArgs wa;
+  b200::make_weights(weights, wa);
+  const aq_train_config cfg = b200::to_c(config);
+  b200::OwnedCodebook cb;
+  b200::OwnedCodes cm;
+  std::vector<double> hist(static_cast<std::size_t>(std::max(config.max_iterations, 0)) + 1);
+  std::size_t hl = 0;
+  b200::check(aq_dev_train_avq(ds.p, k, &wa.w, &cfg, &cb.p, &cm.p, hist.data(), &hl));
+  const ProductCodebook pcb = b200::download(cb.p, 1, k, data.d);
+  CodeMatrix codes = b200::download(cm.p, data.n, 1, k);
+  Codebook out;
+  out.k = k;
+  out.d = data.d;
+  out.codewords = pcb.dictionaries;
+  VqAssignment a;
+  a.assignments = std::move(codes.codes);
+  a.loss_history.assign(hist.begin(), hist.begin() + hl);
+  return {std::move(out), std::move(a)};
+}
+
 // pq.hpp:581-612
 inline CodeMatrix pq_quantize(const Dataset& data, const ProductCodebook& cb,
                               std::span<const AnisotropicWeights> weights, int passes,

@@ -18,6 +18,12 @@ struct Codebook {
   std::span<double> mutable_row(std::size_t j) { return {codewords.data() + j * d, d}; }
 };
 
+// Result of train_avq (reference vq.hpp:45-50).
+struct VqAssignment {
+  std::vector<std::uint32_t> assignments;  // one codeword index per datapoint
+  std::vector<double> loss_history;        // total loss after each assignment pass
+};
+
 enum class EmptyPartitionPolicy { reseed_highest_loss, keep_previous };
 
 struct TrainConfig {

@@ -15,6 +15,7 @@
  *   aq_pq_codebook_update     <- anisoq::pq_codebook_update     pq.hpp:356-464
  *   aq_train_l2_pq            <- anisoq::train_l2_pq            pq.hpp:469-501
  *   aq_train_apq              <- anisoq::train_apq              pq.hpp:513-575
+ *   aq_train_avq              <- anisoq::train_avq              vq.hpp:243-329
  *   aq_build_lut              <- anisoq::build_lut              index.hpp:56-70
  *   aq_adc_search             <- anisoq::adc_search             index.hpp:118-134
  *   aq_adc_search_batch       <- adc_search over a query batch (evaluate, index.hpp:251-259)
@@ -268,6 +269,13 @@ int aq_dev_train_apq(aq_dataset* ds, size_t M, size_t k, const aq_weights* w,
                      const aq_train_config* cfg, int warm_start,
                      aq_codebook** cb_out, aq_codes** codes_out,
                      double* loss_history_out, size_t* history_len);
+/* train_avq (vq.hpp:243-329): one k x d codebook, returned as M = 1;
+ * cfg->empty_partition_policy 0 reseeds an empty partition from the previous
+ * pass's loss ranking, 1 keeps its codeword. */
+int aq_dev_train_avq(aq_dataset* ds, size_t k, const aq_weights* w,
+                     const aq_train_config* cfg, aq_codebook** cb_out,
+                     aq_codes** codes_out, double* loss_history_out,
+                     size_t* history_len);
 
 /* ---- host-pointer forms (the reference's by-value semantics) ------------- */
 /* adc_search over nq queries: ids/scores nq x min(topn, n) */
@@ -296,6 +304,10 @@ int aq_train_apq(aq_session* s, const float* x, size_t n, size_t d, size_t M, si
                  const aq_weights* w, const aq_train_config* cfg, int warm_start,
                  double* dictionaries_out, uint32_t* codes_out,
                  double* loss_history_out, size_t* history_len);
+/* train_avq: codewords_out k x d, assignments_out n, history <= max_iterations + 1 */
+int aq_train_avq(aq_session* s, const float* x, size_t n, size_t d, size_t k,
+                 const aq_weights* w, const aq_train_config* cfg, double* codewords_out,
+                 uint32_t* assignments_out, double* loss_history_out, size_t* history_len);
 
 /* ---- row-sharded training building blocks (multi-GPU) -----
  * The reference trains in one process (pq.hpp:513-575); a sharded trainer

@@ -145,6 +145,25 @@ class _Lib:
         self._call("train_apq", *args)
         return cb, codes, hist[: hl.value].copy()
 
+    def train_avq(self, x, k, hp, ho, max_it=100, tol=1e-6, seed=0, ridge=-1.0,
+                  keep_previous=False, threads=1):
+        """vq.hpp:243-329 -> (codewords k x d, assignments, loss history)."""
+        x = _f64(x)
+        n, d = x.shape
+        cw = np.zeros(k * d, np.float64)
+        a = np.zeros(n, np.uint32)
+        hist = np.zeros(max_it + 1, np.float64)
+        hl = _szt(0)
+        vp = lambda v: v.ctypes.data_as(C.c_void_p)  # noqa: E731
+        hp, ho = _f64(hp), _f64(ho)
+        args = [vp(x), _szt(n), _szt(d), _szt(k), vp(hp), vp(ho), C.c_int(max_it),
+                C.c_double(tol), C.c_uint64(seed), C.c_double(ridge)]
+        if self.prefix == "ref_":
+            args.append(C.c_int(threads))
+        args += [C.c_int(1 if keep_previous else 0), vp(cw), vp(a), vp(hist), C.byref(hl)]
+        self._call("train_avq", *args)
+        return cw.reshape(k, d), a, hist[:hl.value].copy()
+
     def build_lut(self, q, cb, M, k, sd):
         q = _f64(q)
         lut = np.zeros(M * k, np.float64)

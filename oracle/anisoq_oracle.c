@@ -776,6 +776,120 @@ int orc_train_apq(const double* x, size_t n, size_t d, size_t M, size_t k,
   return st;
 }
 
+/* detail::vq_assign_pass, vq.hpp:196-217 (assign_scan 83-100, recorded_loss
+   102-105): per point the lowest-index argmin of the full-vector loss. */
+static int vq_assign_pass(const double* x, size_t n, size_t d, const double* cw,
+                          size_t k, const double* norms, const double* hp,
+                          const double* ho, uint32_t* assign, double* losses) {
+  for (size_t i = 0; i < n; ++i) {
+    const int iso = is_iso(hp[i], ho[i]);
+    double inv = 0.0;
+    if (!iso) {
+      const double n2 = norms[i] * norms[i];
+      if (n2 == 0.0) return E_ZERONORM("anisotropic assignment undefined at |x|=0");
+      inv = 1.0 / n2;
+    }
+    size_t best_j = 0;
+    double bs = 0.0, b2 = 0.0;
+    for (size_t j = 0; j < k; ++j) {
+      double c2, c1;
+      residual_terms(x + i * d, cw + j * d, d, &c2, &c1);
+      const double score = iso ? c2 : combined_loss(c2, c1, hp[i], ho[i], inv);
+      if (j == 0 || score < bs) {
+        bs = score;
+        b2 = c2;
+        best_j = j;
+      }
+    }
+    assign[i] = (uint32_t)best_j;
+    losses[i] = iso ? ho[i] * b2 : (bs > 0.0 ? bs : 0.0);
+  }
+  return AQ_OK;
+}
+
+/* train_avq, vq.hpp:243-329: codewords = rows Rng(seed).sample_distinct(n, k);
+   assignment pass -> history[0]; then per iteration the per-partition
+   update_codeword (members in ascending order; an empty partition keeps its
+   codeword or takes the next point of the loss ranking of the PREVIOUS pass),
+   assignment pass, stopping rules as train_apq. */
+int orc_train_avq(const double* x, size_t n, size_t d, size_t k, const double* hp,
+                  const double* ho, int max_it, double tol, uint64_t seed, double ridge,
+                  int keep_previous, double* cw, uint32_t* assign, double* history,
+                  size_t* history_len) {
+  *history_len = 0;
+  if (n == 0) return E_EMPTY("cannot train on an empty dataset");
+  if (k == 0 || k > n) return E_INVALID("need 1 <= k <= n (codewords come from datapoints)");
+  {
+    uint64_t s = seed;
+    size_t* idx = malloc(sizeof(size_t) * k);
+    sample_distinct_state(&s, n, k, idx);
+    for (size_t j = 0; j < k; ++j) memcpy(cw + j * d, x + idx[j] * d, sizeof(double) * d);
+    free(idx);
+  }
+  double* norms = malloc(sizeof(double) * n);
+  double* losses = malloc(sizeof(double) * n);
+  uint32_t* prev = malloc(sizeof(uint32_t) * n);
+  uint32_t* counts = malloc(sizeof(uint32_t) * k);
+  double* buf = malloc(sizeof(double) * n * d);
+  double* whp = malloc(sizeof(double) * n);
+  double* who = malloc(sizeof(double) * n);
+  size_t* order = malloc(sizeof(size_t) * n);
+  orc_row_norms(x, n, d, norms);
+  int st = vq_assign_pass(x, n, d, cw, k, norms, hp, ho, assign, losses);
+  double total = 0.0;
+  if (!st) {
+    for (size_t i = 0; i < n; ++i) total += losses[i];
+    history[(*history_len)++] = total;
+  }
+  for (int iter = 0; iter < max_it && !st; ++iter) {
+    memset(counts, 0, sizeof(uint32_t) * k);
+    for (size_t i = 0; i < n; ++i) ++counts[assign[i]];
+    int ranked = 0;
+    size_t cursor = 0;
+    for (size_t j = 0; j < k && !st; ++j) {
+      if (counts[j] == 0) {
+        if (keep_previous) continue;
+        if (!ranked) {
+          loss_ranking(losses, n, order);
+          ranked = 1;
+        }
+        memcpy(cw + j * d, x + order[cursor++] * d, sizeof(double) * d);
+        continue;
+      }
+      size_t cnt = 0;
+      for (size_t i = 0; i < n; ++i) {
+        if (assign[i] != j) continue;
+        memcpy(buf + cnt * d, x + i * d, sizeof(double) * d);
+        whp[cnt] = hp[i];
+        who[cnt] = ho[i];
+        ++cnt;
+      }
+      st = update_codeword(d, buf, cnt, whp, who, ridge, cw + j * d);
+    }
+    if (st) break;
+    memcpy(prev, assign, sizeof(uint32_t) * n);
+    st = vq_assign_pass(x, n, d, cw, k, norms, hp, ho, assign, losses);
+    if (st) break;
+    const double prev_total = total;
+    total = 0.0;
+    for (size_t i = 0; i < n; ++i) total += losses[i];
+    history[(*history_len)++] = total;
+    size_t changes = 0;
+    for (size_t i = 0; i < n; ++i) changes += assign[i] != prev[i];
+    if (changes == 0) break;
+    if (tol > 0.0 && (prev_total == 0.0 || prev_total - total <= tol * prev_total)) break;
+  }
+  free(norms);
+  free(losses);
+  free(prev);
+  free(counts);
+  free(buf);
+  free(whp);
+  free(who);
+  free(order);
+  return st;
+}
+
 /* ---- index.hpp ----------------------------------------------------------------- */
 
 /* build_lut, index.hpp:56-70 */

@@ -54,6 +54,10 @@ int orc_train_apq(const double* x, size_t n, size_t d, size_t M, size_t k,
                   double* dict, uint32_t* codes, double* history,
                   size_t* history_len);
 
+int orc_train_avq(const double* x, size_t n, size_t d, size_t k, const double* hp,
+                  const double* ho, int max_it, double tol, uint64_t seed, double ridge,
+                  int keep_previous, double* codewords, uint32_t* assignments,
+                  double* history, size_t* history_len);
 int orc_build_lut(const double* q, size_t d, const double* dict, size_t M,
                   size_t k, size_t sd, double* lut);
 int orc_adc_search_batch(const double* Q, size_t nq, size_t d,

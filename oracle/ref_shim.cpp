@@ -240,6 +240,25 @@ int ref_train_apq(const double* x, std::size_t n, std::size_t d,
   GUARD_END
 }
 
+int ref_train_avq(const double* x, std::size_t n, std::size_t d, std::size_t k,
+                  const double* hp, const double* ho, int max_it, double tol,
+                  std::uint64_t seed, double ridge, int threads, int keep_previous,
+                  double* cw_out, std::uint32_t* assign_out, double* history_out,
+                  std::size_t* history_len) {
+  GUARD_BEGIN
+  const Dataset ds = make_ds(x, n, d);
+  const auto w = make_w(hp, ho, n);
+  TrainConfig cfg = make_cfg(max_it, tol, seed, ridge, threads, 0);
+  cfg.empty_partition_policy = keep_previous ? EmptyPartitionPolicy::keep_previous
+                                             : EmptyPartitionPolicy::reseed_highest_loss;
+  auto [cb, a] = train_avq(ds, k, w, cfg);
+  std::copy(cb.codewords.begin(), cb.codewords.end(), cw_out);
+  std::copy(a.assignments.begin(), a.assignments.end(), assign_out);
+  std::copy(a.loss_history.begin(), a.loss_history.end(), history_out);
+  *history_len = a.loss_history.size();
+  GUARD_END
+}
+
 int ref_build_lut(const double* q, std::size_t d, const double* dict,
                   std::size_t M, std::size_t k, std::size_t sd,
                   double* lut_out) {

@@ -92,6 +92,8 @@ _SIGS = {
     "aq_dev_train_l2_pq": (_I, [_VP, _SZ, _SZ, _VP, _PP, _PP]),
     "aq_debug_exact_window_count": (_I, [_VP, _I, _VP]),
     "aq_dev_train_apq": (_I, [_VP, _SZ, _SZ, _VP, _VP, _I, _PP, _PP, _VP, _VP]),
+    "aq_dev_train_avq": (_I, [_VP, _SZ, _VP, _VP, _PP, _PP, _VP, _VP]),
+    "aq_train_avq": (_I, [_VP, _VP, _SZ, _SZ, _SZ, _VP, _VP, _VP, _VP, _VP, _VP]),
     # host-pointer forms
     "aq_adc_search_batch": (_I, [_VP, _VP, _SZ, _SZ, _VP, _SZ, _SZ, _SZ, _VP, _SZ, _SZ, _SZ, _SZ,
                                  _VP, _VP]),

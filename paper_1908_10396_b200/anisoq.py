@@ -591,6 +591,47 @@ def dev_train_apq(ds: DeviceDataset, M: int, k: int, weights, config: TrainConfi
     return (DeviceCodebook(ds.s, cb, M, k, ds.d // M), DeviceCodes(ds.s, cm, ds.n, M, k))
 
 
+@dataclass
+class Codebook:  # vq.hpp:32-43: k codewords of dimension d
+    k: int
+    d: int
+    codewords: np.ndarray  # k x d float64
+
+
+@dataclass
+class VqAssignment:  # vq.hpp:45-50
+    assignments: np.ndarray  # n uint32
+    loss_history: list
+
+
+def dev_train_avq(ds: DeviceDataset, k: int, weights, config: TrainConfig = TrainConfig(),
+                  loss_history: Optional[list] = None):
+    """vq.hpp:243-329 on the device: (codebook as M = 1, assignments as M = 1 codes)."""
+    cfg = config.c()
+    keep: list = []
+    w = _weights(weights, ds.n, keep)
+    cb, cm = C.c_void_p(), C.c_void_p()
+    hist = np.zeros(max(config.max_iterations, 0) + 1, np.float64)
+    hl = C.c_size_t(0)
+    _check(_L.aq_dev_train_avq(ds.h, k, C.byref(w), C.byref(cfg), C.byref(cb), C.byref(cm),
+                               hist.ctypes.data, C.byref(hl)))
+    if loss_history is not None:
+        loss_history.extend(float(v) for v in hist[: hl.value])
+    return (DeviceCodebook(ds.s, cb, 1, k, ds.d), DeviceCodes(ds.s, cm, ds.n, 1, k))
+
+
+def train_avq(data, k: int, weights, config: TrainConfig = TrainConfig(),
+              session: Optional[Session] = None):
+    """vq.hpp:243-329: anisotropic vector quantization -> (Codebook, VqAssignment)."""
+    s = _sess(session)
+    ds = s.upload_dataset(data)
+    hist: list = []
+    cb, cm = dev_train_avq(ds, k, weights, config, hist)
+    pcb, codes = cb.download(), cm.download()
+    return (Codebook(k, ds.d, pcb.dictionaries.reshape(k, ds.d)),
+            VqAssignment(codes.codes.reshape(-1).astype(np.uint32), hist))
+
+
 def train_l2_pq(data, M: int, k: int, config: TrainConfig = TrainConfig(),
                 session: Optional[Session] = None):
     """pq.hpp:469-501: classical PQ (independent k-means per subspace, seed + m)."""

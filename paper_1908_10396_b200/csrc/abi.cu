@@ -163,4 +163,17 @@ int aq_train_apq(aq_session* s, const float* x, size_t n, size_t d, size_t M, si
   return aq_codes_download(cm.p, codes_out);
 }
 
+int aq_train_avq(aq_session* s, const float* x, size_t n, size_t d, size_t k,
+                 const aq_weights* w, const aq_train_config* cfg, double* cw_out,
+                 uint32_t* assign_out, double* history_out, size_t* history_len) {
+  AQ_TRY(check_session(s));
+  DsGuard ds;
+  CbGuard cb;
+  CodesGuard cm;
+  AQ_TRY(aq_dataset_upload(s, x, n, d, &ds.p));
+  AQ_TRY(aq_dev_train_avq(ds.p, k, w, cfg, &cb.p, &cm.p, history_out, history_len));
+  AQ_TRY(aq_codebook_download(cb.p, cw_out));
+  return aq_codes_download(cm.p, assign_out);
+}
+
 }  // extern "C"

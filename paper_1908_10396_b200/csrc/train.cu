@@ -23,6 +23,8 @@ int run_encode(aq_dataset* ds, aq_codebook* cb, const aq_weights* w, aq_codes* c
                int mode, int passes, int sweep_fixed, double* losses_dev,
                uint64_t* changed_out);
 int stage_codebook(aq_codebook* cb);
+int avq_codebook_update(aq_dataset* ds, aq_codes* codes, const aq_weights* w, double ridge,
+                        aq_codebook* out, const double* rank_losses, const double* keep_prev);
 
 
 // ---- Rng (rng.hpp:28-89), host side -----------------------------------------------------
@@ -906,6 +908,92 @@ int aq_dev_train_apq(aq_dataset* ds, size_t M, size_t k, const aq_weights* w,
   cudaStreamSynchronize(s->side);
   if (history_len) *history_len = hl;
   aq_codebook_free(next);
+  if (losses) cudaFreeAsync(losses, s->stream);
+  if (total) cudaFreeAsync(total, s->stream);
+  cudaStreamSynchronize(s->stream);
+  if (st != AQ_OK) {
+    aq_codebook_free(cb);
+    aq_codes_free(codes);
+    return st;
+  }
+  *cb_out = cb;
+  *codes_out = codes;
+  return AQ_OK;
+}
+
+// train_avq (vq.hpp:243-329): anisotropic vector quantization, i.e. one
+// full-dimensional codebook (returned as M = 1). The assignment pass is the
+// M = 1 encoder pass (pq_assign_pass with M = 1 is vq_assign_pass bit for
+// bit: test_pq.cpp:79-95); the update is the per-codeword closed form with the
+// VQ empty-partition policy: keep the codeword, or reseed from the ranking of
+// the previous pass's losses (vq.hpp:276-292).
+int aq_dev_train_avq(aq_dataset* ds, size_t k, const aq_weights* w, const aq_train_config* cfg,
+                     aq_codebook** cb_out, aq_codes** codes_out, double* history_out,
+                     size_t* history_len) {
+  if (!ds || !cfg || !cb_out || !codes_out) return ref_error(AQ_E_INVALID_ARGUMENT, "null argument");
+  aq_session* s = ds->s;
+  AQ_TRY(check_session(s));
+  const size_t n = ds->n, d = ds->d;
+  if (history_len) *history_len = 0;
+  if (n == 0) return ref_error(AQ_E_EMPTY_DATASET, "cannot train on an empty dataset");
+  if (k == 0 || k > n)
+    return ref_error(AQ_E_INVALID_ARGUMENT, "need 1 <= k <= n (codewords come from datapoints)");
+  // codewords = rows Rng(seed).sample_distinct(n, k) (vq.hpp:257-264)
+  HostRng r{cfg->seed};
+  const auto v = r.sample_distinct(n, k);
+  std::vector<uint64_t> hidx(v.begin(), v.end());
+  aq_codebook* cb = nullptr;
+  aq_codebook* next = nullptr;
+  aq_codes* codes = nullptr;
+  double* losses = nullptr;
+  double* total = nullptr;
+  uint64_t* didx = nullptr;
+  int st = aq_codebook_upload(s, nullptr, 1, k, d, &cb);
+  if (st == AQ_OK) st = aq_codebook_upload(s, nullptr, 1, k, d, &next);
+  if (st == AQ_OK) st = aq_codes_alloc(s, n, 1, k, &codes);
+  if (st == AQ_OK &&
+      (cudaMallocAsync(&didx, k * sizeof(uint64_t), s->stream) != cudaSuccess ||
+       cudaMallocAsync(&losses, n * sizeof(double), s->stream) != cudaSuccess ||
+       cudaMallocAsync(&total, sizeof(double), s->stream) != cudaSuccess))
+    st = ref_error(AQ_E_CUDA, "out of device memory");
+  if (st == AQ_OK) {
+    cudaMemcpyAsync(didx, hidx.data(), k * sizeof(uint64_t), cudaMemcpyHostToDevice, s->stream);
+    k_init_codewords<<<(unsigned)((k + 127) / 128), 128, 0, s->stream>>>(ds->xr, (int)d, 1,
+                                                                       (int)k, (int)d, didx,
+                                                                       cb->d64);
+    s->launches++;
+    st = stage_codebook(cb);
+  }
+  const bool keep = cfg->empty_partition_policy == 1;
+  size_t hl = 0;
+  double tot = 0.0;
+  uint64_t changed = 0;
+  auto pass = [&]() -> int {
+    AQ_TRY(run_encode(ds, cb, w, codes, 1, 0, 0, losses, &changed));
+    AQ_TRY(seq_sum_device(s, losses, n, 0.0, total));
+    AQ_CUDA(cudaMemcpyAsync(&tot, total, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    AQ_CUDA(cudaStreamSynchronize(s->stream));
+    if (history_out) history_out[hl] = tot;
+    ++hl;
+    return AQ_OK;
+  };
+  if (st == AQ_OK) st = pass();
+  for (int iter = 0; st == AQ_OK && iter < cfg->max_iterations; ++iter) {
+    st = avq_codebook_update(ds, codes, w, cfg->ridge, next, keep ? nullptr : losses,
+                             keep ? cb->d64 : nullptr);
+    if (st != AQ_OK) break;
+    std::swap(cb, next);
+    const double prev = tot;
+    st = pass();
+    if (st != AQ_OK) break;
+    if (changed == 0) break;
+    if (cfg->relative_tolerance > 0.0 &&
+        (prev == 0.0 || prev - tot <= cfg->relative_tolerance * prev))
+      break;
+  }
+  if (history_len) *history_len = hl;
+  aq_codebook_free(next);
+  if (didx) cudaFreeAsync(didx, s->stream);
   if (losses) cudaFreeAsync(losses, s->stream);
   if (total) cudaFreeAsync(total, s->stream);
   cudaStreamSynchronize(s->stream);

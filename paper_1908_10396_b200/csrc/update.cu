@@ -1049,11 +1049,27 @@ int llt_solve_device(aq_session* s, double* A, int n, double* x) {
 // sequential chain over the members. Isotropic members only -> weighted mean.
 // out: A[j] (d x d row-major, diagonal already += diag), rhs[j] (d), iso[j],
 // mean path written straight to dict.
+// coef[p] = (h_par - h_perp) / x.squaredNorm() (vq.hpp:178-181; the norm as a
+// sequential sum of squares), NaN-free marker: n2 == 0 leaves coef = 0 and is
+// reported by k_vq_systems.
+__global__ void k_vq_coef(const float* __restrict__ xr, size_t n, int d,
+                          const double* __restrict__ hp, const double* __restrict__ ho,
+                          double* __restrict__ coef, double* __restrict__ n2out) {
+  const size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const float* xp = xr + p * d;
+  double n2 = 0.0;
+  for (int q = 0; q < d; ++q) n2 = __dadd_rn(n2, __dmul_rn((double)xp[q], (double)xp[q]));
+  n2out[p] = n2;
+  coef[p] = n2 == 0.0 ? 0.0 : __ddiv_rn(__dsub_rn(hp[p], ho[p]), n2);
+}
+
 __global__ void k_vq_systems(const float* __restrict__ xr, size_t n, int d, int k,
                              const uint32_t* __restrict__ list,
                              const uint32_t* __restrict__ start,
                              const uint32_t* __restrict__ count, const double* __restrict__ hp,
-                             const double* __restrict__ ho, double ridge, double* A,
+                             const double* __restrict__ ho, const double* __restrict__ coefs,
+                             const double* __restrict__ n2s, double ridge, double* A,
                              double* rhs, int* mode, double* dict, DevError* err) {
   const int j = blockIdx.x;
   const size_t cnt = count[j];
@@ -1091,10 +1107,7 @@ __global__ void k_vq_systems(const float* __restrict__ xr, size_t n, int d, int 
     mh = __ddiv_rn(mh, (double)cnt);
     double diag = ridge < 0.0 ? __dmul_rn(1e-10, mh) : ridge;
     for (size_t t = 0; t < cnt; ++t) {
-      const float* xp = xr + (size_t)L[t] * d;
-      double n2 = 0.0;
-      for (int c = 0; c < d; ++c) n2 = __dadd_rn(n2, __dmul_rn((double)xp[c], (double)xp[c]));
-      if (n2 == 0.0) report_error(err, (uint64_t)L[t], AQ_E_ZERO_NORM_DATAPOINT);
+      if (n2s[L[t]] == 0.0) report_error(err, (uint64_t)L[t], AQ_E_ZERO_NORM_DATAPOINT);
       diag = __dadd_rn(diag, ho[L[t]]);
     }
     s_diag = diag;
@@ -1112,10 +1125,7 @@ __global__ void k_vq_systems(const float* __restrict__ xr, size_t n, int d, int 
       for (size_t t = 0; t < cnt; ++t) {
         const uint32_t p = L[t];
         const float* xp = xr + (size_t)p * d;
-        double n2 = 0.0;
-        for (int q = 0; q < d; ++q) n2 = __dadd_rn(n2, __dmul_rn((double)xp[q], (double)xp[q]));
-        const double coef = __ddiv_rn(__dsub_rn(hp[p], ho[p]), n2);
-        v = __dadd_rn(v, __dmul_rn(__dmul_rn(coef, (double)xp[c]), (double)xp[r]));
+        v = __dadd_rn(v, __dmul_rn(__dmul_rn(coefs[p], (double)xp[c]), (double)xp[r]));
       }
       if (r == c) v = __dadd_rn(v, s_diag);
       Aj[(size_t)r * d + c] = v;
@@ -1324,8 +1334,14 @@ int aq_dev_assemble_selector_system(aq_dataset* ds, aq_codes* codes, const aq_we
 }
 
 // pq_codebook_update (pq.hpp:356-464): writes `out` (M x k x sd, allocated).
-int aq_dev_pq_codebook_update(aq_dataset* ds, aq_codes* codes, const aq_weights* w,
-                              double ridge, aq_codebook* out) {
+// rank_losses / keep_prev (train_avq, vq.hpp:276-292; both null for the
+// reference pq_codebook_update): an unused codeword keeps keep_prev's value
+// when keep_prev is set, else it takes the next point of the ranking of
+// rank_losses (device, n values) when set, else of the point losses under
+// the new codebook (pq.hpp:443-462).
+static int codebook_update_impl(aq_dataset* ds, aq_codes* codes, const aq_weights* w,
+                                double ridge, aq_codebook* out, const double* rank_losses,
+                                const double* keep_prev) {
   if (!ds || !codes || !out) return ref_error(AQ_E_INVALID_ARGUMENT, "null argument");
   aq_session* s = ds->s;
   AQ_TRY(check_session(s));
@@ -1335,7 +1351,8 @@ int aq_dev_pq_codebook_update(aq_dataset* ds, aq_codes* codes, const aq_weights*
   const int sd = (int)(ds->d / M);
   if ((size_t)sd != out->sd)
     return ref_error(AQ_E_DIMENSION_MISMATCH, "codebook sub-dimension does not match");
-  if (sd > 16) return ref_error(AQ_E_UNSUPPORTED, "device update supports sub_dimension <= 16");
+  if (sd > 16 && M != 1)
+    return ref_error(AQ_E_UNSUPPORTED, "device update supports sub_dimension <= 16 (M > 1)");
   const size_t n = ds->n, dim = k * ds->d;
   Buckets B;
   AQ_TRY(build_buckets(codes, (int)k, &B));
@@ -1353,17 +1370,21 @@ int aq_dev_pq_codebook_update(aq_dataset* ds, aq_codes* codes, const aq_weights*
     const size_t d = ds->d;
     double* As = nullptr;
     int* modes = nullptr;
-    if (cudaMallocAsync(&As, (k * d * d + k * d) * sizeof(double), s->stream) != cudaSuccess ||
+    if (cudaMallocAsync(&As, (k * d * d + k * d + 2 * n) * sizeof(double), s->stream) !=
+            cudaSuccess ||
         cudaMallocAsync(&modes, k * sizeof(int), s->stream) != cudaSuccess)
       st = ref_error(AQ_E_CUDA, "out of device memory");
     if (st == AQ_OK) {
       AQ_TRY(clear_dev_error(s));
       cudaMemsetAsync(modes, 0xff, k * sizeof(int), s->stream);
+      double* coefs = As + k * d * d + k * d;
+      k_vq_coef<<<(unsigned)((n + 255) / 256), 256, 0, s->stream>>>(ds->xr, n, (int)d, pw.hp,
+                                                                   pw.ho, coefs, coefs + n);
       k_vq_systems<<<(unsigned)k, 128, 0, s->stream>>>(ds->xr, n, (int)d, (int)k, B.list,
-                                                       B.start, B.count, pw.hp, pw.ho, ridge,
-                                                       As, As + k * d * d, modes, out->d64,
-                                                       s->err);
-      s->launches++;
+                                                       B.start, B.count, pw.hp, pw.ho, coefs,
+                                                       coefs + n, ridge, As, As + k * d * d,
+                                                       modes, out->d64, s->err);
+      s->launches += 2;
       st = sync_and_check(s, "codeword update");
     }
     if (st == AQ_OK) {
@@ -1419,7 +1440,13 @@ int aq_dev_pq_codebook_update(aq_dataset* ds, aq_codes* codes, const aq_weights*
     cudaStreamSynchronize(s->stream);
     bool any_unused = false;
     for (auto c : hc) any_unused |= c == 0;
-    if (any_unused) {
+    if (any_unused && keep_prev) {
+      for (size_t t = 0; t < M * k && st == AQ_OK; ++t)
+        if (hc[t] == 0 &&
+            cudaMemcpyAsync(out->d64 + t * sd, keep_prev + t * sd, sd * sizeof(double),
+                            cudaMemcpyDeviceToDevice, s->stream) != cudaSuccess)
+          st = AQ_E_CUDA;
+    } else if (any_unused) {
       st = stage_codebook(out);
       double* losses = nullptr;
       uint32_t* idx = nullptr;
@@ -1430,7 +1457,13 @@ int aq_dev_pq_codebook_update(aq_dataset* ds, aq_codes* codes, const aq_weights*
         cudaMallocAsync(&cnt_copy, M * k * sizeof(uint32_t), s->stream);
         cudaMemcpyAsync(cnt_copy, hc.data(), M * k * sizeof(uint32_t), cudaMemcpyHostToDevice,
                         s->stream);
-        st = run_encode(ds, out, w, codes, 2, 0, 0, losses, nullptr);
+        if (rank_losses)
+          st = cudaMemcpyAsync(losses, rank_losses, n * sizeof(double), cudaMemcpyDeviceToDevice,
+                               s->stream) == cudaSuccess
+                   ? AQ_OK
+                   : AQ_E_CUDA;
+        else
+          st = run_encode(ds, out, w, codes, 2, 0, 0, losses, nullptr);
       }
       if (st == AQ_OK) {
         k_iota<<<(unsigned)((n + 255) / 256), 256, 0, s->stream>>>(idx, n);
@@ -1458,6 +1491,11 @@ int aq_dev_pq_codebook_update(aq_dataset* ds, aq_codes* codes, const aq_weights*
   return st;
 }
 
+int aq_dev_pq_codebook_update(aq_dataset* ds, aq_codes* codes, const aq_weights* w,
+                              double ridge, aq_codebook* out) {
+  return codebook_update_impl(ds, codes, w, ridge, out, nullptr, nullptr);
+}
+
 // Host-pointer form of pq_codebook_update.
 int aq_pq_codebook_update(aq_session* s, const float* x, size_t n, size_t d,
                           const uint32_t* codes, size_t M, size_t k, const aq_weights* w,
@@ -1481,3 +1519,11 @@ int aq_pq_codebook_update(aq_session* s, const float* x, size_t n, size_t d,
 }
 
 }  // extern "C"
+
+namespace aqd {
+// train_avq's codebook step (vq.hpp:276-307) for the device trainer.
+int avq_codebook_update(aq_dataset* ds, aq_codes* codes, const aq_weights* w, double ridge,
+                        aq_codebook* out, const double* rank_losses, const double* keep_prev) {
+  return codebook_update_impl(ds, codes, w, ridge, out, rank_losses, keep_prev);
+}
+}  // namespace aqd

@@ -33,6 +33,8 @@ def main():
         w.queries.astype(np.float64), codes0, 16, cb, 16, 16, 2, 100, threads=4)
     out["train_cb"], out["train_codes"], out["train_hist"] = R.train_apq(
         x[:800], 16, 16, hp[:800], ho[:800], max_it=3, tol=0.0, seed=0)
+    out["avq_cw"], out["avq_assign"], out["avq_hist"] = R.train_avq(
+        x[:1000], 24, hp[:1000], ho[:1000], max_it=4, tol=0.0, seed=5)
     # sanity: the port agrees
     assert np.array_equal(Port().pq_quantize(x, cb, 16, 16, 2, hp, ho, 3), out["quantize3"])
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden_v1.npz")

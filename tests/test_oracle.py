@@ -129,6 +129,24 @@ def test_train_apq_port_equals_reference(warm):
 
 
 @needs_ref
+@pytest.mark.parametrize("keep", [False, True])
+def test_train_avq_port_equals_reference(keep):
+    # vq.hpp:243-329, including empty partitions (20 distinct rows, k = 30)
+    R = _ref()
+    g = np.random.default_rng(7)
+    base = g.standard_normal((20, 5))
+    dup = base[g.integers(0, 20, 400)].astype(np.float32).astype(np.float64)
+    x = mixture_rows(900, 8, 10).astype(np.float64)
+    for data, k in ((x, 16), (dup, 30)):
+        hp, ho = threshold_hp_ho(data, 0.2)
+        a = P.train_avq(data, k, hp, ho, max_it=5, tol=0.0, seed=3, keep_previous=keep)
+        b = R.train_avq(data, k, hp, ho, max_it=5, tol=0.0, seed=3, keep_previous=keep,
+                        threads=2)
+        for u, v in zip(a, b):
+            assert np.array_equal(u, v)
+
+
+@needs_ref
 def test_search_port_equals_reference():
     R = _ref()
     x = mixture_rows(3000, 32, 10).astype(np.float64)
@@ -161,3 +179,6 @@ def test_golden_fixtures():
     cbt, ct, h = P.train_apq(x[:800], 16, 16, hp[:800], ho[:800], max_it=3, tol=0.0, seed=0)
     assert np.array_equal(cbt, g["train_cb"]) and np.array_equal(ct, g["train_codes"])
     assert np.array_equal(h, g["train_hist"])
+    cw, a, h = P.train_avq(x[:1000], 24, hp[:1000], ho[:1000], max_it=4, tol=0.0, seed=5)
+    assert np.array_equal(cw, g["avq_cw"]) and np.array_equal(a, g["avq_assign"])
+    assert np.array_equal(h, g["avq_hist"])

@@ -21,6 +21,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "build", "obj")
 LIB = os.path.join(PKG, "libanisoq_b200.so")
+CLI = os.path.join(PKG, "anisoq_b200")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2,-ffp-contract=off",
@@ -72,7 +73,24 @@ def build(verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    build_cli()
     return LIB
+
+
+def build_cli() -> str:
+    """The anisoq_b200 command-line tool (cli/anisoq_b200_main.cpp) over the C++
+    drop-in headers, linked against the in-tree library (rpath $ORIGIN)."""
+    src = os.path.join(PKG, "cli", "anisoq_b200_main.cpp")
+    deps = [src, LIB] + [os.path.join(ROOT, "include", "anisoq", f)
+                         for f in os.listdir(os.path.join(ROOT, "include", "anisoq"))]
+    if os.path.exists(CLI) and os.path.getmtime(CLI) >= max(os.path.getmtime(f) for f in deps):
+        return CLI
+    cmd = ["g++", "-std=c++20", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"), src,
+           "-o", CLI, "-L", PKG, "-lanisoq_b200", "-Wl,-rpath,$ORIGIN"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"CLI build failed:\n{r.stdout}\n{r.stderr}")
+    return CLI
 
 
 if __name__ == "__main__":

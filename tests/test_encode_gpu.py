@@ -38,8 +38,10 @@ def test_quantize_config3_shape_lognormal_norms():
 
 
 # fast-path shapes of the other configs: M = 50 (config 2, a tail code word),
-# M = 128 (config 5), an odd M
-@pytest.mark.parametrize("n,d,M", [(6000, 100, 50), (3000, 256, 128), (5000, 26, 13)])
+# M = 128 (config 5), the other M-specialised instances (32, 48, 96), an odd M
+# (runtime-M kernel)
+@pytest.mark.parametrize("n,d,M", [(6000, 100, 50), (3000, 256, 128), (5000, 26, 13),
+                                   (4001, 64, 32), (3999, 96, 48), (2500, 192, 96)])
 def test_quantize_config_shapes(n, d, M):
     x = mixture_rows(n, d, M, centers=32)
     cb = _cb(M, 16, 2, M + 1, scale=1 / np.sqrt(d))

@@ -507,10 +507,17 @@ def bench_encode(args, aq, wl, sess, stream, flush, local, ws, pk):
     keep = []
     cw = aq._weights(wt, n, keep)
     xs = np.ascontiguousarray(w.base)
+
+    def e2e_call():
+        aq._check(L.aq_pq_quantize(sess.h, xs.ctypes.data, n, 128, w.codebook.ctypes.data, 64,
+                                   16, 2, C.byref(cw), 3, codes_h.ctypes.data))
+
+    e2e_call()  # warm-up: first-touch of the host buffers, device scratch
+    e2e_steps = max(2, min(args.steps, 3))
     t0 = time.perf_counter()
-    aq._check(L.aq_pq_quantize(sess.h, xs.ctypes.data, n, 128, w.codebook.ctypes.data, 64, 16, 2,
-                               C.byref(cw), 3, codes_h.ctypes.data))
-    e2e_s = time.perf_counter() - t0
+    for _ in range(e2e_steps):
+        e2e_call()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
     cpu = None
     if not args.no_cpu_baseline and int(os.environ.get("RANK", "0")) == 0 and ws == 1:
         cpu = encode_cpu_baseline(args, w)
@@ -530,7 +537,9 @@ def bench_encode(args, aq, wl, sess, stream, flush, local, ws, pk):
             "cpu_baseline": cpu,
             "e2e": {"value": round(n / e2e_s, 1), "unit": "points/s",
                     "h2d_bytes_per_step": int(n * 128 * 4), "d2h_bytes_per_step": int(n * 64 * 4),
-                    "note": "host wall clock of the synchronous aq_pq_quantize call"}}
+                    "note": f"host wall clock of the synchronous aq_pq_quantize call (host "
+                            f"rows in, host uint32 codes out), mean of {e2e_steps} calls after "
+                            f"one warm-up"}}
 
 
 def encode_cpu_baseline(args, w):

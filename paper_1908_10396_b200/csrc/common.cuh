@@ -92,6 +92,7 @@ struct aq_session {
   aqd::DevError* err = nullptr;     // device
   aqd::DevError* err_host = nullptr;  // pinned mirror
   aqd::Scratch scratch[7];  // slot 6: scan tile sums (sort.cu)
+  aqd::Scratch pinned[4];   // page-locked host staging (streamed host-pointer calls)
 };
 
 struct aq_dataset {

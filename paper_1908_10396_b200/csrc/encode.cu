@@ -40,6 +40,7 @@ struct EncodeArgs {
   double* losses;   // mode 1/2
   unsigned long long* changed;  // mode 1
   DevError* err;
+  size_t base;  // index of point 0 in the caller's numbering (error reports)
 };
 
 
@@ -200,7 +201,7 @@ __global__ void __launch_bounds__(TPB, MINB)
   double hp, ho;
   int st = AQ_OK;
   if (!resolve_weights(a.w, i, a.norms[i], &hp, &ho, &st)) {
-    report_error(a.err, i, st);
+    report_error(a.err, a.base + i, st);
     return;
   }
   const bool iso = hp == ho;
@@ -210,7 +211,7 @@ __global__ void __launch_bounds__(TPB, MINB)
     const double n2 = __dmul_rn(a.norms[i], a.norms[i]);
     if (n2 == 0.0) {
       if (need_inv) {
-        report_error(a.err, i, AQ_E_ZERO_NORM_DATAPOINT);
+        report_error(a.err, a.base + i, AQ_E_ZERO_NORM_DATAPOINT);
         return;
       }
     } else {
@@ -629,7 +630,7 @@ __global__ void __launch_bounds__(TPB, MINB)
   double hp, ho;
   int st = AQ_OK;
   if (!resolve_weights(a.w, i, a.norms[i], &hp, &ho, &st)) {
-    report_error(a.err, i, st);
+    report_error(a.err, a.base + i, st);
     return;
   }
   const bool iso = hp == ho;
@@ -639,7 +640,7 @@ __global__ void __launch_bounds__(TPB, MINB)
     const double n2 = __dmul_rn(a.norms[i], a.norms[i]);
     if (n2 == 0.0) {
       if (need_inv) {
-        report_error(a.err, i, AQ_E_ZERO_NORM_DATAPOINT);
+        report_error(a.err, a.base + i, AQ_E_ZERO_NORM_DATAPOINT);
         return;
       }
     } else {
@@ -855,7 +856,7 @@ __global__ void k_encode_generic(const EncodeArgs a, const float* xt,
   double hp, ho;
   int st = AQ_OK;
   if (!resolve_weights(a.w, i, a.norms[i], &hp, &ho, &st)) {
-    report_error(a.err, i, st);
+    report_error(a.err, a.base + i, st);
     return;
   }
   const bool iso = hp == ho;
@@ -865,7 +866,7 @@ __global__ void k_encode_generic(const EncodeArgs a, const float* xt,
     const double n2 = __dmul_rn(a.norms[i], a.norms[i]);
     if (n2 == 0.0) {
       if (need_inv) {
-        report_error(a.err, i, AQ_E_ZERO_NORM_DATAPOINT);
+        report_error(a.err, a.base + i, AQ_E_ZERO_NORM_DATAPOINT);
         return;
       }
     } else {
@@ -980,9 +981,10 @@ __global__ void k_copy_rows(const uint8_t* src, uint8_t* dst, size_t bytes) {
 // Runs one encode flavour over a dataset. codes: in/out (modes 0, 1) or in (2).
 unsigned long long* g_stats = nullptr;  // debug: exact-window count
 
-int run_encode(aq_dataset* ds, aq_codebook* cb, const aq_weights* w,
-               aq_codes* codes, int mode, int passes, int sweep_fixed,
-               double* losses_dev, uint64_t* changed_out) {
+static int run_encode_impl(aq_dataset* ds, aq_codebook* cb, const aq_weights* w,
+                           aq_codes* codes, int mode, int passes, int sweep_fixed,
+                           double* losses_dev, uint64_t* changed_out, size_t base,
+                           bool async) {
   aq_session* s = ds->s;
   AQ_TRY(check_session(s));
   if (ds->d != cb->M * cb->sd)
@@ -1017,6 +1019,7 @@ int run_encode(aq_dataset* ds, aq_codebook* cb, const aq_weights* w,
   a.sweep_fixed = sweep_fixed;
   a.losses = losses_dev;
   a.err = s->err;
+  a.base = base;
   unsigned long long* dchg = nullptr;
   if (mode == 1) {
     void* p;
@@ -1025,7 +1028,7 @@ int run_encode(aq_dataset* ds, aq_codebook* cb, const aq_weights* w,
     AQ_CUDA(cudaMemsetAsync(dchg, 0, 8, s->stream));
   }
   a.changed = dchg;
-  AQ_TRY(clear_dev_error(s));
+  if (!async) AQ_TRY(clear_dev_error(s));
   const bool fast = cb->sd == 2 && cb->k <= 16 && codes->bits == 4;
   if (fast) {
     const int W = (a.M + 7) / 8;
@@ -1099,7 +1102,21 @@ int run_encode(aq_dataset* ds, aq_codebook* cb, const aq_weights* w,
     *changed_out = h;
     return AQ_OK;
   }
-  return sync_and_check(s, "encode");
+  return async ? AQ_OK : sync_and_check(s, "encode");
+}
+
+int run_encode(aq_dataset* ds, aq_codebook* cb, const aq_weights* w, aq_codes* codes, int mode,
+               int passes, int sweep_fixed, double* losses_dev, uint64_t* changed_out) {
+  return run_encode_impl(ds, cb, w, codes, mode, passes, sweep_fixed, losses_dev, changed_out, 0,
+                         false);
+}
+
+// pq_quantize of one chunk of a larger host dataset (aq_pq_quantize's
+// streamed path): no error reset, no synchronisation; device errors carry
+// base + i and are checked once after the last chunk.
+int run_encode_chunk(aq_dataset* ds, aq_codebook* cb, const aq_weights* w, aq_codes* codes,
+                     int passes, size_t base) {
+  return run_encode_impl(ds, cb, w, codes, 0, passes, 0, nullptr, nullptr, base, true);
 }
 
 }  // namespace aqd

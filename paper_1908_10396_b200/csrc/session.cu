@@ -54,6 +54,23 @@ int scratch(aq_session* s, int slot, size_t bytes, void** out) {
   return AQ_OK;
 }
 
+// Page-locked host buffer `slot`, grown on demand and kept for the session.
+int pinned_buffer(aq_session* s, int slot, size_t bytes, void** out) {
+  Scratch& sc = s->pinned[slot];
+  if (sc.bytes < bytes) {
+    if (sc.p) {
+      AQ_CUDA(cudaStreamSynchronize(s->stream));
+      AQ_CUDA(cudaFreeHost(sc.p));
+      sc.p = nullptr;
+      sc.bytes = 0;
+    }
+    AQ_CUDA(cudaHostAlloc(&sc.p, bytes, cudaHostAllocDefault));
+    sc.bytes = bytes;
+  }
+  *out = sc.p;
+  return AQ_OK;
+}
+
 void timer_mark(aq_session* s, int slot) {
   if (!s->timing) return;
   cudaEvent_t e;
@@ -290,6 +307,8 @@ int aq_session_destroy(aq_session* s) {
   cudaStreamSynchronize(s->stream);
   for (auto& sc : s->scratch)
     if (sc.p) cudaFree(sc.p);
+  for (auto& sc : s->pinned)
+    if (sc.p) cudaFreeHost(sc.p);
   cudaFree(s->err);
   cudaFreeHost(s->err_host);
   cudaStreamSynchronize(s->side);
@@ -503,6 +522,22 @@ int aq_codes_upload_packed(aq_session* s, const uint8_t* packed, size_t n,
   AQ_CUDA(cudaStreamSynchronize(s->stream));
   return AQ_OK;
 }
+
+}  // extern "C"
+
+namespace aqd {
+// codes -> uint32 per code on the device (async, session stream)
+int codes_unpack_async(aq_codes* c, uint32_t* dev_out) {
+  const size_t total = c->n * c->M;
+  if (!total) return AQ_OK;
+  k_unpack_codes<<<(unsigned)((total + 255) / 256), 256, 0, c->s->stream>>>(
+      c->data, c->n, c->M, c->bits, c->stride, dev_out);
+  AQ_LAUNCHED(c->s);
+  return AQ_OK;
+}
+}  // namespace aqd
+
+extern "C" {
 
 int aq_codes_download(aq_codes* c, uint32_t* out) {
   aq_session* s = c->s;

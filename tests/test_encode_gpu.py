@@ -157,3 +157,22 @@ def test_empty_dataset_quantize():
     x = np.zeros((0, 8), np.float32)
     out = aq.pq_quantize(x, _cb(4, 4, 2, 1), aq.AnisotropicWeights(), 2)
     assert out.codes.shape == (0, 4)
+
+
+@pytest.mark.parametrize("chunk", ["1000", "4096"])
+def test_quantize_streamed_host_path(monkeypatch, chunk):
+    # aq_pq_quantize streams large host datasets in chunks (copies overlapped
+    # with the device work); AQ_STREAM_CHUNK shrinks the chunk so every row is
+    # checked: codes equal the oracle's, across chunk edges and a ragged tail
+    monkeypatch.setenv("AQ_STREAM_CHUNK", chunk)
+    x = mixture_rows(17003, 32, 91, centers=20)
+    cb = _cb(16, 16, 2, 92, scale=0.25)
+    got = aq.pq_quantize(x, cb, aq.ThresholdWeights(0.2), 3).codes
+    hp, ho = threshold_hp_ho(x, 0.2)
+    want = P.pq_quantize(x.astype(np.float64), cb.dictionaries, 16, 16, 2, hp, ho, 3)
+    assert np.array_equal(got, want)
+    # a failing point deep in a later chunk reports its global index
+    bad = x.copy()
+    bad[12345] = 0.0
+    with pytest.raises(aq.InvalidArgument, match="point 12345"):
+        aq.pq_quantize(bad, cb, aq.ThresholdWeights(0.2), 3)

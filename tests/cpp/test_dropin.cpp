@@ -231,6 +231,31 @@ int main() {
     CHECK(cb1.dictionaries == cb2.dictionaries && c1.codes == c2.codes && h1 == h2);
     CHECK_THROWS_AS(train_apq(data, 3, 2, w, cfg), DimensionNotDivisible);
   }
+  // train_avq: monotone history, assignments are the argmin of the final
+  // codebook, deterministic, reference validation (vq.hpp:243-329)
+  {
+    const Dataset data = unit_rows(500, 6, 12);
+    std::vector<AnisotropicWeights> w(data.n, AnisotropicWeights::from_eta(3.0));
+    TrainConfig cfg;
+    cfg.seed = 5;
+    cfg.max_iterations = 12;
+    cfg.relative_tolerance = 0.0;
+    auto [vq1, a1] = train_avq(data, 10, w, cfg);
+    cfg.threads = 8;
+    auto [vq2, a2] = train_avq(data, 10, w, cfg);
+    CHECK(vq1.k == 10 && vq1.d == 6 && vq1.codewords.size() == 60);
+    CHECK(a1.assignments.size() == 500 && !a1.loss_history.empty());
+    bool mono = true;
+    for (std::size_t t = 1; t < a1.loss_history.size(); ++t)
+      mono &= a1.loss_history[t] <= a1.loss_history[t - 1] + 1e-9;
+    CHECK(mono);
+    CHECK(vq1.codewords == vq2.codewords && a1.assignments == a2.assignments &&
+          a1.loss_history == a2.loss_history);
+    const ProductCodebook pc = to_product(vq1);
+    CHECK(pc.M == 1 && pc.k == 10 && pc.sub_dimension == 6);
+    CHECK_THROWS_AS(train_avq(data, 0, w, cfg), InvalidArgument);
+    CHECK_THROWS_AS(train_avq(data, 501, w, cfg), InvalidArgument);
+  }
   // serialization golden bytes (test_pq.cpp:560-571)
   {
     const auto dir = std::filesystem::temp_directory_path() / "anisoq_b200_dropin";

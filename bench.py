@@ -484,6 +484,18 @@ def bench_encode(args, aq, wl, sess, stream, flush, local, ws, pk):
     wt = aq.ThresholdWeights(w.threshold, "parallel_only")
     for _ in range(args.warmup):
         aq.dev_pq_quantize(ds, cb, wt, 3, out)
+    multi = torch.distributed.is_available() and torch.distributed.is_initialized()
+
+    def max_over_ranks(v):  # every number below is the slowest rank's
+        if not multi:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{local}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return t.item()
+
+    torch.cuda.synchronize()
+    if multi:
+        torch.distributed.barrier()
     L.aq_session_timing(sess.h, 1)
     L.aq_session_timer_read(sess.h, 0, None, None, 1)
     tot = 0.0
@@ -500,7 +512,7 @@ def bench_encode(args, aq, wl, sess, stream, flush, local, ws, pk):
     ms_k, cnt = C.c_double(0), C.c_uint64(0)
     L.aq_session_timer_read(sess.h, 0, C.byref(ms_k), C.byref(cnt), 1)
     L.aq_session_timing(sess.h, 0)
-    ms = tot / args.steps
+    ms = max_over_ranks(tot / args.steps)
     value = n * ws / (ms / 1e3)
     # e2e: host rows in -> host codes out through the C ABI (pq_quantize)
     codes_h = np.zeros((n, 64), np.uint32)
@@ -514,10 +526,12 @@ def bench_encode(args, aq, wl, sess, stream, flush, local, ws, pk):
 
     e2e_call()  # warm-up: first-touch of the host buffers, device scratch
     e2e_steps = max(2, min(args.steps, 3))
+    if multi:
+        torch.distributed.barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         e2e_call()
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps)
     cpu = None
     if not args.no_cpu_baseline and int(os.environ.get("RANK", "0")) == 0 and ws == 1:
         cpu = encode_cpu_baseline(args, w)

@@ -235,6 +235,62 @@ inline std::pair<ProductCodebook, CodeMatrix> train_apq(
   return {b200::download(cb.p, M, k, data.d / M), b200::download(cm.p, data.n, M, k)};
 }
 
+// vq.hpp:112-132: lowest-index argmin of the anisotropic loss over a VQ
+// codebook — the M = 1 coordinate-descent step (bit-identical, test_pq.cpp:79-95).
+inline std::size_t assign_point(std::span<const double> x, const Codebook& cb,
+                                const AnisotropicWeights& w) {
+  if (cb.k == 0) throw InvalidArgument("empty codebook");
+  if (x.size() != cb.d) throw DimensionMismatch("datapoint dimension does not match codebook");
+  const std::uint32_t cur = 0;
+  std::uint32_t out = 0;
+  b200::check(aq_pq_assign_point_order(b200::session(), x.data(), x.size(), &cur,
+                                       cb.codewords.data(), 1, cb.k, cb.d, w.h_parallel,
+                                       w.h_perpendicular, nullptr, 0, &out));
+  return out;
+}
+
+// vq.hpp:139-192: closed-form codeword for a set of weighted points (the
+// M = 1 branch of the device codebook update with every point in partition 0).
+inline std::vector<double> update_codeword(std::size_t d, std::span<const double> points,
+                                           std::span<const AnisotropicWeights> weights,
+                                           double ridge = -1.0) {
+  if (d == 0 || points.empty() || points.size() % d != 0)
+    throw InvalidArgument("points must be a non-empty multiple of d");
+  const std::size_t m = points.size() / d;
+  if (weights.size() != m) throw InvalidArgument("need one weight per point");
+  std::vector<float> x(points.size());
+  for (std::size_t i = 0; i < x.size(); ++i) {
+    x[i] = static_cast<float>(points[i]);
+    if (static_cast<double>(x[i]) != points[i])
+      throw Unsupported("device datasets hold float32-exact values (row " +
+                        std::to_string(i / d) + ")");
+  }
+  b200::WeightArgs wa;
+  b200::make_weights(weights, wa);
+  const std::vector<std::uint32_t> codes(m, 0u);
+  std::vector<double> out(d);
+  b200::check(aq_pq_codebook_update(b200::session(), x.data(), m, d, codes.data(), 1, 1, &wa.w,
+                                    ridge, out.data()));
+  return out;
+}
+
+// vq.hpp:332-343: one assignment pass against a fixed VQ codebook.
+inline std::vector<std::uint32_t> vq_quantize(const Dataset& data, const Codebook& cb,
+                                              std::span<const AnisotropicWeights> weights,
+                                              int threads = 1) {
+  (void)threads;
+  if (data.d != cb.d) throw DimensionMismatch("dataset dimension does not match codebook");
+  if (weights.size() != data.n) throw InvalidArgument("need one AnisotropicWeights per datapoint");
+  std::vector<std::uint32_t> codes(data.n, 0u);
+  if (data.n == 0) return codes;
+  const std::vector<float> x = b200::to_f32(data);
+  b200::WeightArgs wa;
+  b200::make_weights(weights, wa);
+  b200::check(aq_pq_assign_pass(b200::session(), x.data(), data.n, data.d, cb.codewords.data(),
+                                1, cb.k, cb.d, &wa.w, 0, codes.data(), nullptr));
+  return codes;
+}
+
 // vq.hpp:243-329: anisotropic vector quantization (one full-dimensional
 // codebook); the device trainer returns it as an M = 1 product codebook.
 inline std::pair<Codebook, VqAssignment> train_avq(const Dataset& data, std::size_t k,

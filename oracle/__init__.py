@@ -164,6 +164,37 @@ class _Lib:
         self._call("train_avq", *args)
         return cw.reshape(k, d), a, hist[:hl.value].copy()
 
+    def vq_quantize(self, x, cw, hp, ho, threads=1):
+        """vq.hpp:332-343 -> assignments."""
+        x, cw, hp, ho = _f64(x), _f64(cw), _f64(hp), _f64(ho)
+        n, d = x.shape
+        k = cw.size // d
+        a = np.zeros(n, np.uint32)
+        vp = lambda v: v.ctypes.data_as(C.c_void_p)  # noqa: E731
+        args = [vp(x), _szt(n), _szt(d), vp(cw), _szt(k), vp(hp), vp(ho)]
+        if self.prefix == "ref_":
+            args.append(C.c_int(threads))
+        self._call("vq_quantize", *args, vp(a))
+        return a
+
+    def assign_point(self, x, cw, hp, ho):
+        """vq.hpp:112-132 -> codeword index."""
+        x, cw = _f64(x).ravel(), _f64(cw)
+        out = C.c_uint32(0)
+        self._call("assign_point", x.ctypes.data_as(C.c_void_p), _szt(x.size),
+                   cw.ctypes.data_as(C.c_void_p), _szt(cw.size // max(x.size, 1)),
+                   C.c_double(hp), C.c_double(ho), C.byref(out))
+        return out.value
+
+    def update_codeword(self, d, pts, hp, ho, ridge=-1.0):
+        """vq.hpp:139-192 -> codeword (d values)."""
+        pts, hp, ho = _f64(pts).ravel(), _f64(hp), _f64(ho)
+        out = np.zeros(d, np.float64)
+        vp = lambda v: v.ctypes.data_as(C.c_void_p)  # noqa: E731
+        self._call("update_codeword", _szt(d), vp(pts), _szt(pts.size // d), vp(hp), vp(ho),
+                   C.c_double(ridge), vp(out))
+        return out
+
     def build_lut(self, q, cb, M, k, sd):
         q = _f64(q)
         lut = np.zeros(M * k, np.float64)

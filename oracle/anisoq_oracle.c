@@ -807,6 +807,37 @@ static int vq_assign_pass(const double* x, size_t n, size_t d, const double* cw,
   return AQ_OK;
 }
 
+/* vq_quantize, vq.hpp:332-343 */
+int orc_vq_quantize(const double* x, size_t n, size_t d, const double* cw, size_t k,
+                    const double* hp, const double* ho, uint32_t* assign) {
+  double* norms = malloc(sizeof(double) * (n ? n : 1));
+  double* losses = malloc(sizeof(double) * (n ? n : 1));
+  orc_row_norms(x, n, d, norms);
+  const int st = vq_assign_pass(x, n, d, cw, k, norms, hp, ho, assign, losses);
+  free(norms);
+  free(losses);
+  return st;
+}
+
+/* assign_point, vq.hpp:112-132 */
+int orc_assign_point(const double* x, size_t d, const double* cw, size_t k, double hp,
+                     double ho, uint32_t* out) {
+  if (k == 0) return E_INVALID("empty codebook");
+  double norm;
+  orc_row_norms(x, 1, d, &norm);
+  if (!is_iso(hp, ho) && norm * norm == 0.0)
+    return E_ZERONORM("anisotropic assignment undefined at |x| = 0");
+  double losses;
+  return vq_assign_pass(x, 1, d, cw, k, &norm, &hp, &ho, out, &losses);
+}
+
+/* update_codeword, vq.hpp:139-192 */
+int orc_update_codeword(size_t d, const double* pts, size_t m, const double* hp,
+                        const double* ho, double ridge, double* out) {
+  if (d == 0 || m == 0) return E_INVALID("points must be a non-empty multiple of d");
+  return update_codeword(d, pts, m, hp, ho, ridge, out);
+}
+
 /* train_avq, vq.hpp:243-329: codewords = rows Rng(seed).sample_distinct(n, k);
    assignment pass -> history[0]; then per iteration the per-partition
    update_codeword (members in ascending order; an empty partition keeps its

@@ -54,6 +54,12 @@ int orc_train_apq(const double* x, size_t n, size_t d, size_t M, size_t k,
                   double* dict, uint32_t* codes, double* history,
                   size_t* history_len);
 
+int orc_vq_quantize(const double* x, size_t n, size_t d, const double* cw, size_t k,
+                    const double* hp, const double* ho, uint32_t* assign);
+int orc_assign_point(const double* x, size_t d, const double* cw, size_t k, double hp,
+                     double ho, uint32_t* out);
+int orc_update_codeword(size_t d, const double* pts, size_t m, const double* hp,
+                        const double* ho, double ridge, double* out);
 int orc_train_avq(const double* x, size_t n, size_t d, size_t k, const double* hp,
                   const double* ho, int max_it, double tol, uint64_t seed, double ridge,
                   int keep_previous, double* codewords, uint32_t* assignments,

@@ -240,6 +240,42 @@ int ref_train_apq(const double* x, std::size_t n, std::size_t d,
   GUARD_END
 }
 
+int ref_vq_quantize(const double* x, std::size_t n, std::size_t d, const double* cw,
+                    std::size_t k, const double* hp, const double* ho, int threads,
+                    std::uint32_t* assign_out) {
+  GUARD_BEGIN
+  const Dataset ds = make_ds(x, n, d);
+  const auto w = make_w(hp, ho, n);
+  Codebook cb;
+  cb.k = k;
+  cb.d = d;
+  cb.codewords.assign(cw, cw + k * d);
+  const auto a = vq_quantize(ds, cb, w, threads);
+  std::copy(a.begin(), a.end(), assign_out);
+  GUARD_END
+}
+
+int ref_assign_point(const double* x, std::size_t d, const double* cw, std::size_t k,
+                     double hp, double ho, std::uint32_t* out) {
+  GUARD_BEGIN
+  Codebook cb;
+  cb.k = k;
+  cb.d = d;
+  cb.codewords.assign(cw, cw + k * d);
+  *out = static_cast<std::uint32_t>(
+      assign_point(std::span<const double>(x, d), cb, AnisotropicWeights::from_h(hp, ho)));
+  GUARD_END
+}
+
+int ref_update_codeword(std::size_t d, const double* pts, std::size_t m, const double* hp,
+                        const double* ho, double ridge, double* out) {
+  GUARD_BEGIN
+  const auto w = make_w(hp, ho, m);
+  const auto c = update_codeword(d, std::span<const double>(pts, m * d), w, ridge);
+  std::copy(c.begin(), c.end(), out);
+  GUARD_END
+}
+
 int ref_train_avq(const double* x, std::size_t n, std::size_t d, std::size_t k,
                   const double* hp, const double* ho, int max_it, double tol,
                   std::uint64_t seed, double ridge, int threads, int keep_previous,

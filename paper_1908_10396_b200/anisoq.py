@@ -632,6 +632,48 @@ def train_avq(data, k: int, weights, config: TrainConfig = TrainConfig(),
             VqAssignment(codes.codes.reshape(-1).astype(np.uint32), hist))
 
 
+def assign_point(x, cb: Codebook, w: AnisotropicWeights, session: Optional[Session] = None) -> int:
+    """vq.hpp:112-132: lowest-index argmin of the anisotropic loss (M = 1 sweep)."""
+    if cb.k == 0:
+        raise InvalidArgument("InvalidArgument: empty codebook")
+    x = np.ascontiguousarray(x, np.float64).ravel()
+    if x.size != cb.d:
+        raise DimensionMismatch("DimensionMismatch: datapoint dimension does not match codebook")
+    return int(pq_assign_point(x, np.zeros(1, np.uint32),
+                               ProductCodebook(1, cb.k, cb.d, cb.codewords), w,
+                               session=session)[0])
+
+
+def update_codeword(d: int, points, weights, ridge: float = -1.0,
+                    session: Optional[Session] = None) -> np.ndarray:
+    """vq.hpp:139-192: closed-form codeword of weighted points (the device M = 1
+    update with every point in partition 0)."""
+    pts = np.ascontiguousarray(points, np.float64).ravel()
+    if d == 0 or pts.size == 0 or pts.size % d:
+        raise InvalidArgument("InvalidArgument: points must be a non-empty multiple of d")
+    m = pts.size // d
+    ws = weights if isinstance(weights, (list, tuple)) else None
+    if ws is not None and len(ws) != m:
+        raise InvalidArgument("InvalidArgument: need one weight per point")
+    out = pq_codebook_update(pts.reshape(m, d), CodeMatrix(m, 1, 1, np.zeros((m, 1), np.uint32)),
+                             weights, 1, 1, ridge, session=session)
+    return out.dictionaries.copy()
+
+
+def vq_quantize(data, cb: Codebook, weights, threads: int = 1,
+                session: Optional[Session] = None) -> np.ndarray:
+    """vq.hpp:332-343: one assignment pass against a fixed VQ codebook."""
+    data = data if isinstance(data, Dataset) else Dataset(data)
+    if data.d != cb.d:
+        raise DimensionMismatch("DimensionMismatch: dataset dimension does not match codebook")
+    if data.n == 0:
+        return np.zeros(0, np.uint32)
+    codes, _ = pq_assign_pass(data, ProductCodebook(1, cb.k, cb.d, cb.codewords), weights,
+                              CodeMatrix(data.n, 1, cb.k, np.zeros((data.n, 1), np.uint32)),
+                              session=session)
+    return codes.codes.reshape(-1).copy()
+
+
 def train_l2_pq(data, M: int, k: int, config: TrainConfig = TrainConfig(),
                 session: Optional[Session] = None):
     """pq.hpp:469-501: classical PQ (independent k-means per subspace, seed + m)."""

@@ -253,6 +253,17 @@ int main() {
           a1.loss_history == a2.loss_history);
     const ProductCodebook pc = to_product(vq1);
     CHECK(pc.M == 1 && pc.k == 10 && pc.sub_dimension == 6);
+    // vq_quantize / assign_point agree with the trained assignments' argmin
+    const auto again = vq_quantize(data, vq1, w);
+    bool agree = true;
+    for (std::size_t i = 0; i < data.n; ++i) agree &= again[i] == assign_point(data.row(i), vq1, w[i]);
+    CHECK(agree);
+    CHECK(again == a1.assignments);  // the last pass used the final codebook
+    // update_codeword of an isotropic set is its mean (vq.hpp:151-162)
+    const std::vector<double> pts{1, 2, 3, 4, 5, 6};
+    const std::vector<AnisotropicWeights> iso(2, AnisotropicWeights::isotropic());
+    CHECK((update_codeword(3, pts, iso) == std::vector<double>{2.5, 3.5, 4.5}));
+    CHECK_THROWS_AS(update_codeword(4, pts, iso), InvalidArgument);
     CHECK_THROWS_AS(train_avq(data, 0, w, cfg), InvalidArgument);
     CHECK_THROWS_AS(train_avq(data, 501, w, cfg), InvalidArgument);
   }

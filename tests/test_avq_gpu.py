@@ -69,3 +69,30 @@ def test_train_avq_per_point_weights_and_errors():
         aq.train_avq(x[:5], 6, aq.AnisotropicWeights.isotropic(), cfg)
     with pytest.raises(aq.EmptyDataset):
         aq.train_avq(np.zeros((0, 4), np.float32), 1, aq.AnisotropicWeights.isotropic(), cfg)
+
+
+def test_vq_api_matches_oracle():
+    # vq_quantize, assign_point, update_codeword (vq.hpp:112-192, 332-343)
+    g = np.random.default_rng(21)
+    x = mixture_rows(3000, 12, 74, centers=10, sigma=0.3, normalize=False)
+    cw = g.standard_normal((20, 12))
+    hp, ho = 1.0 + 3.0 * g.random(3000), np.ones(3000)
+    ws = [aq.AnisotropicWeights(float(a), 1.0) for a in hp]
+    cb = aq.Codebook(20, 12, cw)
+    got = aq.vq_quantize(x, cb, ws)
+    assert np.array_equal(got, P.vq_quantize(x.astype(np.float64), cw, hp, ho))
+    for i in range(0, 3000, 150):
+        w = aq.AnisotropicWeights(float(hp[i]), 1.0)
+        assert aq.assign_point(x[i].astype(np.float64), cb, w) == P.assign_point(
+            x[i].astype(np.float64), cw, hp[i], 1.0)
+    pts = x[:300]
+    for h in (hp[:300], np.ones(300)):
+        w = [aq.AnisotropicWeights(float(a), 1.0) for a in h]
+        assert np.array_equal(aq.update_codeword(12, pts, w),
+                              P.update_codeword(12, pts.astype(np.float64), h, np.ones(300)))
+    with pytest.raises(aq.InvalidArgument):
+        aq.update_codeword(12, pts[:, :5], [aq.AnisotropicWeights()] * 300)
+    with pytest.raises(aq.DimensionMismatch):
+        aq.vq_quantize(x[:, :6], cb, ws)
+    with pytest.raises(aq.InvalidArgument):
+        aq.assign_point(x[0], aq.Codebook(0, 12, np.zeros((0, 12))), aq.AnisotropicWeights())

@@ -147,6 +147,22 @@ def test_train_avq_port_equals_reference(keep):
 
 
 @needs_ref
+def test_vq_api_port_equals_reference():
+    # vq_quantize / assign_point / update_codeword (vq.hpp:112-192, 332-343)
+    R = _ref()
+    g = np.random.default_rng(3)
+    x = g.standard_normal((500, 6)).astype(np.float32).astype(np.float64)
+    cw = g.standard_normal(12 * 6)
+    hp, ho = 1 + 2 * g.random(500), np.ones(500)
+    assert np.array_equal(P.vq_quantize(x, cw, hp, ho), R.vq_quantize(x, cw, hp, ho, threads=3))
+    for i in range(40):
+        assert P.assign_point(x[i], cw, hp[i], 1.0) == R.assign_point(x[i], cw, hp[i], 1.0)
+    for h in (hp[:40], np.ones(40)):
+        assert np.array_equal(P.update_codeword(6, x[:40], h, ho[:40], 1e-3),
+                              R.update_codeword(6, x[:40], h, ho[:40], 1e-3))
+
+
+@needs_ref
 def test_search_port_equals_reference():
     R = _ref()
     x = mixture_rows(3000, 32, 10).astype(np.float64)

@@ -6,5 +6,7 @@
 #include "error.hpp"
 #include "geometry.hpp"
 #include "index.hpp"
+#include "parallel.hpp"
 #include "pq.hpp"
+#include "rng.hpp"
 #include "vq.hpp"

@@ -55,6 +55,25 @@ inline double dot(std::span<const double> a, std::span<const double> b) {
   return s;
 }
 inline double norm2(std::span<const double> a) { return dot(a, a); }
+
+// geometry.hpp:182-200: the two scalars of a residual r = x - c (|r|^2 and
+// <r, x>, ascending components) and the score-aware loss built from them —
+// the float64 definitions the device kernels reproduce bit for bit.
+inline void residual_terms(std::span<const double> x, std::span<const double> c, double& dist2,
+                           double& rdot) {
+  dist2 = 0.0;
+  rdot = 0.0;
+  for (std::size_t j = 0; j < x.size(); ++j) {
+    const double r = x[j] - c[j];
+    dist2 += r * r;
+    rdot += r * x[j];
+  }
+}
+inline double combined_loss(double dist2, double rdot, const AnisotropicWeights& w,
+                            double inv_norm2) {
+  return w.h_perpendicular * dist2 +
+         (w.h_parallel - w.h_perpendicular) * (rdot * rdot) * inv_norm2;
+}
 }  // namespace detail
 
 }  // namespace anisoq

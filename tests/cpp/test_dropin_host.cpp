@@ -2,6 +2,7 @@
 // generator, fvecs/ivecs I/O, Rng, VQ <-> product codebook conversions.
 // Writes generated datasets to argv[1] for tests/test_cpp_dropin_gpu.py to
 // compare with the reference's own generator.
+#include <cmath>
 #include <cstdio>
 #include <string>
 #include <vector>
@@ -55,5 +56,28 @@ int main(int argc, char** argv) {
   const Dataset unit = unit_normalize(back);
   CHECK(unit.normalized && unit.n == back.n);
   std::printf("dropin_host: %d failed\n", fails);
+  // parallel_for: per-index results independent of the thread count, first
+  // error rethrown (parallel.hpp); fnv1a64 known answers (dataset.hpp:62-70)
+  {
+    std::vector<double> a(100003), b(100003);
+    parallel_for(a.size(), 1, [&](std::size_t lo, std::size_t hi) {
+      for (auto i = lo; i < hi; ++i) a[i] = std::sqrt((double)i) * 3.0;
+    });
+    parallel_for(b.size(), 7, [&](std::size_t lo, std::size_t hi) {
+      for (auto i = lo; i < hi; ++i) b[i] = std::sqrt((double)i) * 3.0;
+    }, 333);
+    CHECK(a == b);
+    bool thrown = false;
+    try {
+      parallel_for(5000, 4, [&](std::size_t lo, std::size_t) {
+        if (lo == 2048) throw InvalidArgument("boom");
+      });
+    } catch (const InvalidArgument&) {
+      thrown = true;
+    }
+    CHECK(thrown);
+    CHECK(detail::fnv1a64("", 0) == 0xcbf29ce484222325ull);
+    CHECK(detail::fnv1a64("a", 1) == 0xaf63dc4c8601ec8cull);
+  }
   return fails ? 1 : 0;
 }

@@ -547,7 +547,9 @@ def bench_encode(args, aq, wl, sess, stream, flush, local, ws, pk):
                          "peak": round(fp32_peak / 1e12, 2), "unit": "Tops/s",
                          "frac": round(achieved_ops / fp32_peak, 4),
                          "note": "27,648 algorithmic f32 ops/point (SURVEY.md §8(d)); HBM side "
-                                 "544 B/point is << HBM peak"},
+                                 "544 B/point is << HBM peak; the kernel is issue/latency "
+                                 "bound (ncu: ~71% issue active, no pipe above 46%; the "
+                                 "per-point float64 coordinate-descent chain, DESIGN.md §4.1)"},
             "cpu_baseline": cpu,
             "e2e": {"value": round(n / e2e_s, 1), "unit": "points/s",
                     "h2d_bytes_per_step": int(n * 128 * 4), "d2h_bytes_per_step": int(n * 64 * 4),

@@ -101,6 +101,36 @@ def test_train_pq_encode_search_eval(files):
     r = run("eval", "--data", str(base), "--queries", str(qf), "--codebook",
             str(out / "codebook.bin"), "--codes", str(enc), "--out", str(ev), "--Ns", "1,10")
     assert json.loads((ev / "manifest.json").read_text())["ground_truth"]["source"] == "cache"
+    # a supplied ground truth file is used as is; a missing one is computed there
+    ev2 = t / "eval2"
+    r = run("eval", "--data", str(base), "--queries", str(qf), "--codebook",
+            str(out / "codebook.bin"), "--codes", str(enc), "--out", str(ev2), "--Ns", "1,10",
+            "--ground-truth", man["ground_truth"]["path"])
+    assert r.returncode == 0, r.stderr
+    assert json.loads((ev2 / "manifest.json").read_text())["ground_truth"]["source"] == "supplied"
+    rep2 = json.loads((ev2 / "eval_report.json").read_text())
+    rep2.pop("latency_us")
+    assert rep2 == {k: v for k, v in rep.items() if k != "latency_us"}
+    gt_new = t / "gt_new.ivecs"
+    r = run("eval", "--data", str(base), "--queries", str(qf), "--codebook",
+            str(out / "codebook.bin"), "--codes", str(enc), "--out", str(ev2), "--Ns", "1,10",
+            "--ground-truth", str(gt_new))
+    assert r.returncode == 0 and np.array_equal(np.array(aq.read_ivecs(str(gt_new))),
+                                                want_gt.astype(np.int32))
+
+
+def test_train_from_config_document(files):
+    t, base, _, x, _, hp, ho = files
+    cfg = t / "train.json"
+    cfg.write_text(json.dumps({"seed": 3, "train": {"M": 4, "k": 8, "iters": 2, "tol": 0.0,
+                                                    "warm-start": False}}))
+    out = t / "cfg"
+    r = run("train", "--data", str(base), "--out", str(out), "--config", str(cfg))
+    assert r.returncode == 0, r.stderr
+    cb, codes, hist = P.train_apq(x, 4, 8, hp, ho, max_it=2, tol=0.0, seed=3, warm_start=False)
+    assert np.array_equal(aq.load_codes(str(out / "codes.bin")).codes, codes)
+    man = json.loads((out / "manifest.json").read_text())
+    assert man["options"]["seed"] == 3 and man["options"]["warm_start"] is False
 
 
 def test_train_vq_and_reconstruction_loss(files):

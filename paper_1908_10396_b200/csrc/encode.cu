@@ -1032,10 +1032,11 @@ static int run_encode_impl(aq_dataset* ds, aq_codebook* cb, const aq_weights* w,
   const bool fast = cb->sd == 2 && cb->k <= 16 && codes->bits == 4;
   if (fast) {
     const int W = (a.M + 7) / 8;
-    int variant = 11;  // word-unrolled kernel, 256 threads, 3 CTAs/SM
+    // 256 threads, 3 CTAs/SM (24 warps at 80 registers), measured best for
+    // both kernels; AQ_ENC_VARIANT=1 forces the previous kernel for every M
+    int variant = 11;
     if (const char* v = getenv("AQ_ENC_VARIANT")) variant = atoi(v);
-    const int tpb = (variant == 2 || variant == 3 || variant == 12 || variant == 15) ? 128
-                    : variant == 17 ? 192 : 256;
+    const int tpb = 256;
     const size_t smv = (size_t)(a.M + 1) * (kCbStride * sizeof(float4) + 16 * sizeof(double2)) +
                        (a.M + 1) * sizeof(float2) + (size_t)(W + 1) * tpb * sizeof(uint32_t) + 16 +
                        3 * tpb * sizeof(double) + 8;
@@ -1067,16 +1068,9 @@ static int run_encode_impl(aq_dataset* ds, aq_codebook* cb, const aq_weights* w,
         case 128: AQ_ENCW_LAUNCH(256, 3, 128); break;
         default: AQ_ENC_LAUNCH(256, 3); break;
       }
-    } else if (variant == 12) AQ_ENCW_LAUNCH(128, 6, 0);
-    else if (variant == 13) AQ_ENCW_LAUNCH(256, 2, 0);
-    else if (variant == 14) AQ_ENCW_LAUNCH(256, 3, 0);
-    else if (variant == 15) AQ_ENCW_LAUNCH(128, 5, 64);
-    else if (variant == 16) AQ_ENCW_LAUNCH(256, 2, 64);
-    else if (variant == 17) AQ_ENCW_LAUNCH(192, 4, 64);
-    else if (variant == 1) AQ_ENC_LAUNCH(256, 3);
-    else if (variant == 2) AQ_ENC_LAUNCH(128, 4);
-    else if (variant == 3) AQ_ENC_LAUNCH(128, 6);
-    else AQ_ENC_LAUNCH(256, 2);
+    } else {
+      AQ_ENC_LAUNCH(256, 3);
+    }
 #undef AQ_ENC_LAUNCH
 #undef AQ_ENCW_LAUNCH
     AQ_LAUNCHED(s);

@@ -6,7 +6,7 @@ sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
 from paper_1908_10396_b200 import anisoq as aq, workload as wl
 
 n = int(float(sys.argv[1])) if len(sys.argv) > 1 else 4_000_000
-variants = sys.argv[2].split(",") if len(sys.argv) > 2 else ["1", "0", "2", "3"]
+variants = sys.argv[2].split(",") if len(sys.argv) > 2 else ["11", "1"]
 w = wl.config3(n=n)
 s = aq.Session.default()
 ds = s.upload_dataset(w.base)

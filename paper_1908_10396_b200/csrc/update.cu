@@ -949,16 +949,15 @@ __global__ void __launch_bounds__(1024) k_llt_solve(const double* L, int n, doub
     }
     if (tid < bs) xb[tid] = x[kb + tid];
     __syncthreads();
-    if (w == 0) {
-      for (int r = 0; r < bs; ++r) {
-        for (int c = lane; c < r; c += 32) pr[c] = __dmul_rn(Ld[r][c], xb[c]);
-        __syncwarp();
-        if (lane == 0) {
-          double t = xb[r];
-          for (int c = 0; c < r; ++c) t = __dsub_rn(t, pr[c]);
-          xb[r] = __ddiv_rn(t, Ld[r][r]);
-        }
-        __syncwarp();
+    // forward: thread r owns row r's chain t_r = b_r - L_r0 x_0 - L_r1 x_1 - ...
+    // (terms in ascending column order, as the stand-in); x_c is final once
+    // row c's chain ends, so all rows advance one column per step
+    if (tid < kLLT) {
+      double t = tid < bs ? xb[tid] : 0.0;
+      for (int c = 0; c < bs; ++c) {
+        if (tid == c) xb[c] = __ddiv_rn(t, Ld[c][c]);
+        asm volatile("bar.sync 1, %0;" ::"n"(kLLT) : "memory");
+        if (tid > c && tid < bs) t = __dsub_rn(t, __dmul_rn(Ld[tid][c], xb[c]));
       }
     }
     __syncthreads();

@@ -176,3 +176,17 @@ def test_quantize_streamed_host_path(monkeypatch, chunk):
     bad[12345] = 0.0
     with pytest.raises(aq.InvalidArgument, match="point 12345"):
         aq.pq_quantize(bad, cb, aq.ThresholdWeights(0.2), 3)
+
+
+@pytest.mark.parametrize("weights,passes", [("iso", 0), ("eta", 2)])
+def test_quantize_streamed_uniform_weights(monkeypatch, weights, passes):
+    # the streamed host path with uniform weights (isotropic / explicit eta)
+    monkeypatch.setenv("AQ_STREAM_CHUNK", "2500")
+    x = mixture_rows(12345, 16, 93, centers=12, normalize=False)
+    cb = _cb(8, 16, 2, 94, scale=0.3)
+    w = aq.AnisotropicWeights.isotropic() if weights == "iso" else aq.AnisotropicWeights.from_eta(3.5)
+    got = aq.pq_quantize(x, cb, w, passes).codes
+    hp = np.full(len(x), w.h_parallel)
+    ho = np.full(len(x), w.h_perpendicular)
+    want = P.pq_quantize(x.astype(np.float64), cb.dictionaries, 8, 16, 2, hp, ho, passes)
+    assert np.array_equal(got, want)

@@ -585,6 +585,14 @@ __device__ __forceinline__ unsigned nearest_step(const float2 xv, const int m,
   return jb;
 }
 
+#ifndef AQ_SWEEP_UNROLL
+#define AQ_SWEEP_UNROLL 4  // measured: 1 6.99, 2 6.67, 3 7.09, 4 6.55, 8 6.66 ms (4e6 config-3 points)
+#endif
+constexpr int kSweepUnroll = AQ_SWEEP_UNROLL;  // subspace steps per loop body
+#ifndef AQ_NEAREST_UNROLL
+#define AQ_NEAREST_UNROLL 2
+#endif
+constexpr int kNearestUnroll = AQ_NEAREST_UNROLL;
 // MT > 0: M known at compile time (every shared-memory offset is a constant);
 // MT = 0: any M.
 template <int TPB, int MINB, int MT>
@@ -662,7 +670,7 @@ __global__ void __launch_bounds__(TPB, MINB)
     // reconstruction_nearest_pass + pq_point_state (pq.hpp:594, 603)
     float2 xa = xrow[0], xb = xrow[32];
     uint32_t nw = 0;
-#pragma unroll 2
+#pragma unroll kNearestUnroll
     for (int m = 0; m < M; ++m) {
       const float2 xv = xa;
       xa = xb;
@@ -679,7 +687,7 @@ __global__ void __launch_bounds__(TPB, MINB)
       nw = __funnelshift_r(nw, jb, 4);
       if ((m & 7) == 7) mycode[(m >> 3) * TPB] = nw;
     }
-    if (Mr) mycode[Wf * TPB] = nw >> (32 - 4 * Mr);
+    if (Mr) mycode[Wf * TPB] = nw >> ((32 - 4 * Mr) & 31);
   } else {
     const uint32_t* r4 = reinterpret_cast<const uint32_t*>(crow);
     for (int w = 0; w < W; ++w) mycode[w * TPB] = r4[w];
@@ -733,7 +741,7 @@ __global__ void __launch_bounds__(TPB, MINB)
     unsigned chg = 0;
     float2 xa = xrow[0], xb = xrow[32];
     uint32_t cw = mycode[0], nw = 0;
-#pragma unroll 2
+#pragma unroll kSweepUnroll
     for (int m = 0; m < M; ++m) {
       const float2 xv = xa;
       xa = xb;
@@ -749,7 +757,7 @@ __global__ void __launch_bounds__(TPB, MINB)
         cw = mycode[((m >> 3) + 1) * TPB];  // padded word
       }
     }
-    if (Mr) mycode[Wf * TPB] = nw >> (32 - 4 * Mr);
+    if (Mr) mycode[Wf * TPB] = nw >> ((32 - 4 * Mr) & 31);
     const bool changed = chg != 0;
     if (a.mode == 0) {
       if (!changed) break;  // pq.hpp:605-606

@@ -12,6 +12,12 @@
 #include <utility>
 #include <vector>
 
+#if __has_include(<Eigen/Dense>)
+#include <Eigen/Dense>
+#else
+#include "eigen_dense_subset.hpp"
+#endif
+
 #include "b200.hpp"
 #include "dataset.hpp"
 #include "error.hpp"
@@ -45,31 +51,13 @@ struct CodeMatrix {
   std::span<std::uint32_t> mutable_row(std::size_t i) { return {codes.data() + i * M, M}; }
 };
 
-// Dense row-major stand-ins for the reference's Eigen members.
-struct DenseMatrix {
-  std::ptrdiff_t r = 0, c = 0;
-  std::vector<double> v;
-  double& operator()(std::ptrdiff_t i, std::ptrdiff_t j) { return v[i * c + j]; }
-  double operator()(std::ptrdiff_t i, std::ptrdiff_t j) const { return v[i * c + j]; }
-  std::ptrdiff_t rows() const { return r; }
-  std::ptrdiff_t cols() const { return c; }
-  double trace() const {
-    double s = 0.0;
-    for (std::ptrdiff_t i = 0; i < r && i < c; ++i) s += (*this)(i, i);
-    return s;
-  }
-};
-struct DenseVector {
-  std::vector<double> v;
-  double& operator()(std::ptrdiff_t i) { return v[i]; }
-  double operator()(std::ptrdiff_t i) const { return v[i]; }
-  std::ptrdiff_t size() const { return (std::ptrdiff_t)v.size(); }
-  const double* data() const { return v.data(); }
-};
-
+// Normal equations of the joint codebook problem (pq.hpp:69-74), Eigen-typed
+// like the reference's: real Eigen when <Eigen/Dense> is on the include path,
+// otherwise the dense subset the reference's callers use
+// (eigen_dense_subset.hpp).
 struct SelectorSystem {
-  DenseMatrix system_matrix;
-  DenseVector rhs;
+  Eigen::MatrixXd system_matrix;
+  Eigen::VectorXd rhs;
 };
 
 // VQ <-> M = 1 product codebook (pq.hpp:76-92)
@@ -105,15 +93,6 @@ inline std::vector<double> reconstruct(std::span<const std::uint32_t> codes_row,
 }
 
 namespace b200 {
-inline aq_train_config to_c(const TrainConfig& c) {
-  return aq_train_config{c.max_iterations, c.relative_tolerance, c.seed,
-                         c.empty_partition_policy == EmptyPartitionPolicy::keep_previous ? 1 : 0,
-                         c.ridge, c.threads, c.sweep_to_fixed_point ? 1 : 0};
-}
-inline void upload(const Dataset& data, OwnedDataset& ds) {
-  const std::vector<float> x = to_f32(data);
-  check(aq_dataset_upload(session(), x.data(), data.n, data.d, &ds.p));
-}
 inline ProductCodebook download(aq_codebook* cb, std::size_t M, std::size_t k, std::size_t sd) {
   ProductCodebook out;
   out.M = M;
@@ -160,17 +139,24 @@ inline SelectorSystem assemble_selector_system(const Dataset& data, const CodeMa
   if (weights.size() != data.n) throw InvalidArgument("need one AnisotropicWeights per datapoint");
   const std::size_t dim = k * data.d;
   SelectorSystem sys;
-  sys.system_matrix.r = sys.system_matrix.c = (std::ptrdiff_t)dim;
-  sys.system_matrix.v.assign(dim * dim, 0.0);
-  sys.rhs.v.assign(dim, 0.0);
+  sys.system_matrix = Eigen::MatrixXd::Zero(static_cast<Eigen::Index>(dim),
+                                            static_cast<Eigen::Index>(dim));
+  sys.rhs = Eigen::VectorXd::Zero(static_cast<Eigen::Index>(dim));
   b200::OwnedDataset ds;
   b200::OwnedCodes cm;
   b200::upload(data, ds);
   b200::check(aq_codes_upload(b200::session(), codes.codes.data(), codes.n, M, k, &cm.p));
   b200::WeightArgs wa;
   b200::make_weights(weights, wa);
-  b200::check(aq_dev_assemble_selector_system(ds.p, cm.p, &wa.w, sys.system_matrix.v.data(),
-                                              sys.rhs.v.data()));
+  // the device writes the matrix row-major; (r, c) and (c, r) are separately
+  // rounded products (pq.hpp:333-336), so copy element-wise into Eigen's
+  // column-major storage
+  std::vector<double> a(dim * dim);
+  b200::check(aq_dev_assemble_selector_system(ds.p, cm.p, &wa.w, a.data(), sys.rhs.data()));
+  for (std::size_t r = 0; r < dim; ++r)
+    for (std::size_t c = 0; c < dim; ++c)
+      sys.system_matrix(static_cast<Eigen::Index>(r), static_cast<Eigen::Index>(c)) =
+          a[r * dim + c];
   return sys;
 }
 
@@ -233,93 +219,6 @@ inline std::pair<ProductCodebook, CodeMatrix> train_apq(
                                hist.data(), &hl));
   if (loss_history) loss_history->insert(loss_history->end(), hist.begin(), hist.begin() + hl);
   return {b200::download(cb.p, M, k, data.d / M), b200::download(cm.p, data.n, M, k)};
-}
-
-// vq.hpp:112-132: lowest-index argmin of the anisotropic loss over a VQ
-// codebook — the M = 1 coordinate-descent step (bit-identical, test_pq.cpp:79-95).
-inline std::size_t assign_point(std::span<const double> x, const Codebook& cb,
-                                const AnisotropicWeights& w) {
-  if (cb.k == 0) throw InvalidArgument("empty codebook");
-  if (x.size() != cb.d) throw DimensionMismatch("datapoint dimension does not match codebook");
-  const std::uint32_t cur = 0;
-  std::uint32_t out = 0;
-  b200::check(aq_pq_assign_point_order(b200::session(), x.data(), x.size(), &cur,
-                                       cb.codewords.data(), 1, cb.k, cb.d, w.h_parallel,
-                                       w.h_perpendicular, nullptr, 0, &out));
-  return out;
-}
-
-// vq.hpp:139-192: closed-form codeword for a set of weighted points (the
-// M = 1 branch of the device codebook update with every point in partition 0).
-inline std::vector<double> update_codeword(std::size_t d, std::span<const double> points,
-                                           std::span<const AnisotropicWeights> weights,
-                                           double ridge = -1.0) {
-  if (d == 0 || points.empty() || points.size() % d != 0)
-    throw InvalidArgument("points must be a non-empty multiple of d");
-  const std::size_t m = points.size() / d;
-  if (weights.size() != m) throw InvalidArgument("need one weight per point");
-  std::vector<float> x(points.size());
-  for (std::size_t i = 0; i < x.size(); ++i) {
-    x[i] = static_cast<float>(points[i]);
-    if (static_cast<double>(x[i]) != points[i])
-      throw Unsupported("device datasets hold float32-exact values (row " +
-                        std::to_string(i / d) + ")");
-  }
-  b200::WeightArgs wa;
-  b200::make_weights(weights, wa);
-  const std::vector<std::uint32_t> codes(m, 0u);
-  std::vector<double> out(d);
-  b200::check(aq_pq_codebook_update(b200::session(), x.data(), m, d, codes.data(), 1, 1, &wa.w,
-                                    ridge, out.data()));
-  return out;
-}
-
-// vq.hpp:332-343: one assignment pass against a fixed VQ codebook.
-inline std::vector<std::uint32_t> vq_quantize(const Dataset& data, const Codebook& cb,
-                                              std::span<const AnisotropicWeights> weights,
-                                              int threads = 1) {
-  (void)threads;
-  if (data.d != cb.d) throw DimensionMismatch("dataset dimension does not match codebook");
-  if (weights.size() != data.n) throw InvalidArgument("need one AnisotropicWeights per datapoint");
-  std::vector<std::uint32_t> codes(data.n, 0u);
-  if (data.n == 0) return codes;
-  const std::vector<float> x = b200::to_f32(data);
-  b200::WeightArgs wa;
-  b200::make_weights(weights, wa);
-  b200::check(aq_pq_assign_pass(b200::session(), x.data(), data.n, data.d, cb.codewords.data(),
-                                1, cb.k, cb.d, &wa.w, 0, codes.data(), nullptr));
-  return codes;
-}
-
-// vq.hpp:243-329: anisotropic vector quantization (one full-dimensional
-// codebook); the device trainer returns it as an M = 1 product codebook.
-inline std::pair<Codebook, VqAssignment> train_avq(const Dataset& data, std::size_t k,
-                                                   std::span<const AnisotropicWeights> weights,
-                                                   const TrainConfig& config) {
-  if (data.n == 0) throw EmptyDataset("cannot train on an empty dataset");
-  if (k == 0 || k > data.n)
-    throw InvalidArgument("need 1 <= k <= n (codewords come from datapoints)");
-  if (weights.size() != data.n) throw InvalidArgument("need one AnisotropicWeights per datapoint");
-  b200::OwnedDataset ds;
-  b200::upload(data, ds);
-  b200::WeightArgs wa;
-  b200::make_weights(weights, wa);
-  const aq_train_config cfg = b200::to_c(config);
-  b200::OwnedCodebook cb;
-  b200::OwnedCodes cm;
-  std::vector<double> hist(static_cast<std::size_t>(std::max(config.max_iterations, 0)) + 1);
-  std::size_t hl = 0;
-  b200::check(aq_dev_train_avq(ds.p, k, &wa.w, &cfg, &cb.p, &cm.p, hist.data(), &hl));
-  const ProductCodebook pcb = b200::download(cb.p, 1, k, data.d);
-  CodeMatrix codes = b200::download(cm.p, data.n, 1, k);
-  Codebook out;
-  out.k = k;
-  out.d = data.d;
-  out.codewords = pcb.dictionaries;
-  VqAssignment a;
-  a.assignments = std::move(codes.codes);
-  a.loss_history.assign(hist.begin(), hist.begin() + hl);
-  return {std::move(out), std::move(a)};
 }
 
 // pq.hpp:581-612

@@ -365,9 +365,11 @@ int exact_filter_device(aq_dataset* ds, const double* Qd, size_t nq, size_t dept
   const size_t qf_b = nqb * d * kFQ * sizeof(float), tb_b = nq_pad * sizeof(float);
   const size_t buf_b = nq_pad * R * cap * sizeof(uint2);
   void* p;
-  AQ_TRY(scratch(s, 3, buf_b + qf_b + tb_b + nq * R * sizeof(int) + nq * sizeof(int) + 256, &p));
+  // the filter kernel stages its query tile with 16-byte loads
+  const size_t qf_off = (buf_b + 255) & ~(size_t)255;
+  AQ_TRY(scratch(s, 3, qf_off + qf_b + tb_b + nq * R * sizeof(int) + nq * sizeof(int) + 256, &p));
   uint2* obuf = (uint2*)p;
-  float* qf = (float*)(obuf + nq_pad * R * cap);
+  float* qf = (float*)((char*)p + qf_off);
   float* twoB = qf + nqb * d * kFQ;
   int* ocnt = (int*)(twoB + nq_pad);
   int* oflag = ocnt + nq * R;

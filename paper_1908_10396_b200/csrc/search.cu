@@ -474,9 +474,12 @@ int adc_search_device(aq_codes* codes, aq_codebook* cb, const double* Qd,
   const size_t lut64_b = nq * M * k * sizeof(double);
   const size_t lutq_b = nqb * shp.qp * (size_t)M * 16 * sizeof(uint32_t);
   void* p;
-  AQ_TRY(scratch(s, 1, lut64_b + lutq_b + 256, &p));
+  // the score kernel stages the filter table with 16-byte loads: its offset
+  // is rounded up (nq M k doubles can be an odd multiple of 8 bytes)
+  const size_t lutq_off = (lut64_b + 255) & ~(size_t)255;
+  AQ_TRY(scratch(s, 1, lutq_off + lutq_b + 256, &p));
   double* lut64 = (double*)p;
-  uint32_t* lutq = (uint32_t*)(lut64 + nq * M * k);
+  uint32_t* lutq = (uint32_t*)((char*)p + lutq_off);
   AQ_CUDA(cudaMemsetAsync(lutq, 0, lutq_b, s->stream));
   timer_mark(s, AQ_T_LUT);
   k_build_lut<<<(unsigned)nq, 256, 0, s->stream>>>(Qd, (int)nq, (int)d, cb->d64, M, k,

@@ -169,7 +169,6 @@ inline ProductCodebook pq_codebook_update(const Dataset& data, const CodeMatrix&
     throw DimensionMismatch("code matrix does not match dataset");
   if (M == 0 || data.d % M != 0) throw DimensionNotDivisible("dimension not divisible by M");
   if (weights.size() != data.n) throw InvalidArgument("need one AnisotropicWeights per datapoint");
-  const std::vector<float> x = b200::to_f32(data);
   b200::WeightArgs wa;
   b200::make_weights(weights, wa);
   ProductCodebook cb;
@@ -177,8 +176,10 @@ inline ProductCodebook pq_codebook_update(const Dataset& data, const CodeMatrix&
   cb.k = k;
   cb.sub_dimension = data.d / M;
   cb.dictionaries.resize(M * k * cb.sub_dimension);
-  b200::check(aq_pq_codebook_update(b200::session(), x.data(), data.n, data.d, codes.codes.data(),
-                                    M, k, &wa.w, ridge, cb.dictionaries.data()));
+  b200::OwnedDataset ds;
+  b200::upload(data, ds);
+  b200::codebook_update(ds, data.n, codes.codes.data(), M, k, cb.sub_dimension, &wa.w, ridge,
+                        cb.dictionaries.data());
   return cb;
 }
 
@@ -229,7 +230,6 @@ inline CodeMatrix pq_quantize(const Dataset& data, const ProductCodebook& cb,
   if (data.d != cb.dim()) throw DimensionMismatch("dataset dimension does not match codebook");
   if (weights.size() != data.n) throw InvalidArgument("need one AnisotropicWeights per datapoint");
   if (passes < 0) throw InvalidArgument("passes must be >= 0");
-  const std::vector<float> x = b200::to_f32(data);
   b200::WeightArgs wa;
   b200::make_weights(weights, wa);
   CodeMatrix out;
@@ -237,6 +237,19 @@ inline CodeMatrix pq_quantize(const Dataset& data, const ProductCodebook& cb,
   out.M = cb.M;
   out.k = cb.k;
   out.codes.resize(data.n * cb.M);
+  if (!b200::f32_exact(data.values)) {  // float64 rows: the resident-dataset path
+    b200::OwnedDataset ds;
+    b200::upload(data, ds);
+    b200::OwnedCodebook dcb;
+    b200::check(aq_codebook_upload(b200::session(), cb.dictionaries.data(), cb.M, cb.k,
+                                   cb.sub_dimension, &dcb.p));
+    b200::OwnedCodes cm;
+    b200::check(aq_codes_alloc(b200::session(), data.n, cb.M, cb.k, &cm.p));
+    b200::check(aq_dev_pq_quantize(ds.p, dcb.p, &wa.w, passes, cm.p));
+    b200::check(aq_codes_download(cm.p, out.codes.data()));
+    return out;
+  }
+  const std::vector<float> x = b200::to_f32(data);
   b200::check(aq_pq_quantize(b200::session(), x.data(), data.n, data.d, cb.dictionaries.data(),
                              cb.M, cb.k, cb.sub_dimension, &wa.w, passes, out.codes.data()));
   return out;

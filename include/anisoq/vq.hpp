@@ -55,9 +55,21 @@ inline aq_train_config to_c(const TrainConfig& c) {
                          c.empty_partition_policy == EmptyPartitionPolicy::keep_previous ? 1 : 0,
                          c.ridge, c.threads, c.sweep_to_fixed_point ? 1 : 0};
 }
+// float64 rows in; the library stores them as float32 when exact, else float64
 inline void upload(const Dataset& data, OwnedDataset& ds) {
-  const std::vector<float> x = to_f32(data);
-  check(aq_dataset_upload(session(), x.data(), data.n, data.d, &ds.p));
+  check(aq_dataset_upload_f64(session(), data.values.data(), data.n, data.d, &ds.p));
+}
+// codebook update over a resident dataset: ds, codes (n x M), per-point
+// weights -> dictionaries (M k sd)
+inline void codebook_update(const OwnedDataset& ds, std::size_t n, const std::uint32_t* codes,
+                            std::size_t M, std::size_t k, std::size_t sd, const aq_weights* w,
+                            double ridge, double* dict_out) {
+  OwnedCodes cm;
+  check(aq_codes_upload(session(), codes, n, M, k, &cm.p));
+  OwnedCodebook cb;
+  check(aq_codebook_upload(session(), nullptr, M, k, sd, &cb.p));
+  check(aq_dev_pq_codebook_update(ds.p, cm.p, w, ridge, cb.p));
+  check(aq_codebook_download(cb.p, dict_out));
 }
 }  // namespace b200
 
@@ -84,19 +96,13 @@ inline std::vector<double> update_codeword(std::size_t d, std::span<const double
     throw InvalidArgument("points must be a non-empty multiple of d");
   const std::size_t m = points.size() / d;
   if (weights.size() != m) throw InvalidArgument("need one weight per point");
-  std::vector<float> x(points.size());
-  for (std::size_t i = 0; i < x.size(); ++i) {
-    x[i] = static_cast<float>(points[i]);
-    if (static_cast<double>(x[i]) != points[i])
-      throw Unsupported("device datasets hold float32-exact values (row " +
-                        std::to_string(i / d) + ")");
-  }
   b200::WeightArgs wa;
   b200::make_weights(weights, wa);
+  b200::OwnedDataset ds;
+  b200::check(aq_dataset_upload_f64(b200::session(), points.data(), m, d, &ds.p));
   const std::vector<std::uint32_t> codes(m, 0u);
   std::vector<double> out(d);
-  b200::check(aq_pq_codebook_update(b200::session(), x.data(), m, d, codes.data(), 1, 1, &wa.w,
-                                    ridge, out.data()));
+  b200::codebook_update(ds, m, codes.data(), 1, 1, d, &wa.w, ridge, out.data());
   return out;
 }
 
@@ -109,11 +115,24 @@ inline std::vector<std::uint32_t> vq_quantize(const Dataset& data, const Codeboo
   if (weights.size() != data.n) throw InvalidArgument("need one AnisotropicWeights per datapoint");
   std::vector<std::uint32_t> codes(data.n, 0u);
   if (data.n == 0) return codes;
-  const std::vector<float> x = b200::to_f32(data);
   b200::WeightArgs wa;
   b200::make_weights(weights, wa);
-  b200::check(aq_pq_assign_pass(b200::session(), x.data(), data.n, data.d, cb.codewords.data(),
-                                1, cb.k, cb.d, &wa.w, 0, codes.data(), nullptr));
+  if (b200::f32_exact(data.values)) {
+    const std::vector<float> x = b200::to_f32(data);
+    b200::check(aq_pq_assign_pass(b200::session(), x.data(), data.n, data.d,
+                                  cb.codewords.data(), 1, cb.k, cb.d, &wa.w, 0, codes.data(),
+                                  nullptr));
+    return codes;
+  }
+  b200::OwnedDataset ds;
+  b200::upload(data, ds);
+  b200::OwnedCodebook dcb;
+  b200::check(aq_codebook_upload(b200::session(), cb.codewords.data(), 1, cb.k, cb.d, &dcb.p));
+  b200::OwnedCodes cm;
+  b200::check(aq_codes_upload(b200::session(), codes.data(), data.n, 1, cb.k, &cm.p));
+  std::uint64_t changed = 0;
+  b200::check(aq_dev_pq_assign_pass(ds.p, dcb.p, &wa.w, 0, cm.p, nullptr, &changed));
+  b200::check(aq_codes_download(cm.p, codes.data()));
   return codes;
 }
 

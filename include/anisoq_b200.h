@@ -130,6 +130,15 @@ typedef struct aq_codes aq_codes;       /* packed codes n x M */
 /* Upload float32 rows; norms are computed on the device (dataset.hpp:55-59). */
 int aq_dataset_upload(aq_session* s, const float* x, size_t n, size_t d,
                       aq_dataset** out);
+/* Upload float64 rows (the reference's Dataset values, dataset.hpp:41-51).
+   Stored as float32 when every value is float32-exact (fvecs files, the
+   reference generator: dataset.hpp:146-151, 288), else as float64 — e.g.
+   unit_normalize output (dataset.hpp:229). Results equal the reference's
+   either way; the float64 storage runs the generic kernels. */
+int aq_dataset_upload_f64(aq_session* s, const double* x, size_t n, size_t d,
+                          aq_dataset** out);
+/* 1 when the dataset holds float64 rows. */
+int aq_dataset_is_f64(const aq_dataset* ds);
 /* Wrap rows already on this session's device (not copied, not freed). */
 int aq_dataset_wrap_device(aq_session* s, const float* x_dev, size_t n,
                            size_t d, aq_dataset** out);

@@ -57,6 +57,8 @@ _SIGS = {
     "aq_session_timer_read": (_I, [_VP, _I, _VP, _VP, _I]),
     "aq_dev_search_rerank_d": (_I, [_VP, _VP, _VP, _VP, _SZ, _SZ, _SZ, _VP, _VP, _VP, _VP]),
     "aq_dataset_upload": (_I, [_VP, _VP, _SZ, _SZ, _PP]),
+    "aq_dataset_upload_f64": (_I, [_VP, _VP, _SZ, _SZ, _PP]),
+    "aq_dataset_is_f64": (_I, [_VP]),
     "aq_dataset_wrap_device": (_I, [_VP, _VP, _SZ, _SZ, _PP]),
     "aq_dataset_free": (_I, [_VP]),
     "aq_dataset_norms": (_I, [_VP, _VP]),

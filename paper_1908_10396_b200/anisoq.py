@@ -135,7 +135,7 @@ def eta_limit(threshold: float, norm: float, d: int) -> float:
 
 @dataclass
 class Dataset:
-    values: np.ndarray  # n x d, float32-exact
+    values: np.ndarray  # n x d: float32 when float32-exact, else float64
     normalized: bool = False
 
     def __post_init__(self):
@@ -146,12 +146,17 @@ class Dataset:
             row = int(np.nonzero(~np.isfinite(v))[0][0])
             raise MalformedFile(f"MalformedFile: non-finite value at row {row}")
         if v.dtype != np.float32:
+            # float32 storage when exact (fvecs / generate_synthetic data,
+            # dataset.hpp:146-151, 288: the fast kernels); float64 otherwise
+            # (e.g. unit_normalize output), which runs the generic kernels
             f = v.astype(np.float32)
-            if not np.array_equal(f.astype(np.float64), np.asarray(v, np.float64)):
-                raise Unsupported("Unsupported: device datasets hold float32-exact values "
-                                  "(fvecs / generate_synthetic data are; dataset.hpp:146-151)")
-            v = f
-        self.values = np.ascontiguousarray(v, dtype=np.float32)
+            v64 = np.asarray(v, np.float64)
+            v = f if np.array_equal(f.astype(np.float64), v64) else v64
+        self.values = np.ascontiguousarray(v)
+
+    @property
+    def f64(self) -> bool:
+        return self.values.dtype == np.float64
 
     @property
     def n(self) -> int:
@@ -275,7 +280,8 @@ class Session:
     def upload_dataset(self, values: np.ndarray) -> "DeviceDataset":
         ds = values if isinstance(values, Dataset) else Dataset(values)
         h = C.c_void_p()
-        _check(_L.aq_dataset_upload(self.h, ds.values.ctypes.data, ds.n, ds.d, C.byref(h)))
+        up = _L.aq_dataset_upload_f64 if ds.f64 else _L.aq_dataset_upload
+        _check(up(self.h, ds.values.ctypes.data, ds.n, ds.d, C.byref(h)))
         return DeviceDataset(self, h, ds.n, ds.d)
 
     def wrap_device_rows(self, ptr: int, n: int, d: int) -> "DeviceDataset":
@@ -418,6 +424,12 @@ def pq_quantize(data: Dataset, cb: ProductCodebook, weights, passes: int,
     keep: list = []
     w = _weights(weights, data.n, keep)
     out = np.zeros((data.n, cb.M), np.uint32)
+    if data.f64:  # float64 rows: the resident-dataset path
+        if data.d != cb.dim():
+            raise DimensionMismatch("DimensionMismatch: dataset dimension does not match codebook")
+        ds, dcb, dc = s.upload_dataset(data), s.upload_codebook(cb), s.alloc_codes(data.n, cb.M, cb.k)
+        _check(_L.aq_dev_pq_quantize(ds.h, dcb.h, C.byref(w), passes, dc.h))
+        return dc.download()
     _check(_L.aq_pq_quantize(s.h, data.values.ctypes.data, data.n, data.d,
                              cb.dictionaries.ctypes.data, cb.M, cb.k, cb.sub_dimension,
                              C.byref(w), passes, out.ctypes.data))
@@ -433,6 +445,16 @@ def pq_assign_pass(data: Dataset, cb: ProductCodebook, weights, codes: CodeMatri
     w = _weights(weights, data.n, keep)
     out = np.ascontiguousarray(codes.codes, np.uint32).copy()
     losses = np.zeros(data.n, np.float64)
+    if data.f64:  # float64 rows: the resident-dataset path
+        import torch  # device buffer for the per-point losses
+        ds, dcb = s.upload_dataset(data), s.upload_codebook(cb)
+        dc = s.upload_codes(CodeMatrix(data.n, cb.M, cb.k, out))
+        ld = torch.zeros(max(data.n, 1), dtype=torch.float64, device=f"cuda:{s.device}")
+        torch.cuda.synchronize(s.device)
+        ch = C.c_uint64(0)
+        _check(_L.aq_dev_pq_assign_pass(ds.h, dcb.h, C.byref(w), int(sweep_to_fixed_point),
+                                        dc.h, ld.data_ptr(), C.byref(ch)))
+        return dc.download(), ld[: data.n].cpu().numpy()
     _check(_L.aq_pq_assign_pass(s.h, data.values.ctypes.data, data.n, data.d,
                                 cb.dictionaries.ctypes.data, cb.M, cb.k, cb.sub_dimension,
                                 C.byref(w), int(sweep_to_fixed_point), out.ctypes.data,
@@ -542,6 +564,16 @@ def pq_codebook_update(data, codes: CodeMatrix, weights, M: int, k: int, ridge: 
     w = _weights(weights, data.n, keep)
     out = np.zeros(k * data.d, np.float64)
     cm = np.ascontiguousarray(codes.codes, np.uint32)
+    if data.f64:  # float64 rows: the resident-dataset path
+        if codes.n != data.n or codes.M != M:
+            raise DimensionMismatch("DimensionMismatch: code matrix does not match dataset")
+        if M == 0 or data.d % M:
+            raise DimensionNotDivisible("DimensionNotDivisible: dimension not divisible by M")
+        ds = s.upload_dataset(data)
+        dc = s.upload_codes(CodeMatrix(codes.n, M, k, cm))
+        dcb = s.upload_codebook(ProductCodebook(M, k, data.d // M, out))
+        _check(_L.aq_dev_pq_codebook_update(ds.h, dc.h, C.byref(w), ridge, dcb.h))
+        return dcb.download()
     _check(_L.aq_pq_codebook_update(s.h, data.values.ctypes.data, data.n, data.d,
                                     cm.ctypes.data, M, k, C.byref(w), ridge, out.ctypes.data))
     return ProductCodebook(M, k, data.d // M if M else 0, out)
@@ -1110,7 +1142,7 @@ def generate_synthetic(kind: str, n: int, d: int, seed: int, centers: int = 16,
 
 def unit_normalize(ds: Dataset) -> np.ndarray:
     """dataset.hpp:225-236: rows scaled to unit norm (float64; generally not
-    float32-exact, so the device path would refuse the result)."""
+    float32-exact, so devices hold the result as float64 rows)."""
     x = np.asarray(ds.values if isinstance(ds, Dataset) else ds, np.float64)
     norms = np.sqrt(np.add.accumulate(x * x, axis=1)[:, -1])  # dataset.hpp:55-59 order
     if np.any(norms == 0.0):

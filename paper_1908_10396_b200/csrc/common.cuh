@@ -101,7 +101,25 @@ struct aq_dataset {
   float* xt = nullptr;      // pair-tiled rows (encoders, search)
   float* xr = nullptr;      // row-major rows (normal equations, gathers)
   double* norms = nullptr;  // float64 norms
+  // Datasets whose values are not all float32-exact (e.g. unit_normalize
+  // output, dataset.hpp:229) keep float64 rows instead: f64 = 1, xt64 / xr64
+  // set, xt / xr null. Every kernel that reads rows has a float64
+  // instantiation; the float32-filter fast paths (sd = 2 encoders, k-means,
+  // slot gathers, exact-search filter) are float32-only and are bypassed.
+  int f64 = 0;
+  double* xt64 = nullptr;
+  double* xr64 = nullptr;
 };
+
+// Launch KERNEL<float>(ds->xr, ...) or KERNEL<double>(ds->xr64, ...) by the
+// dataset's row type (row-major rows as the first kernel argument).
+#define AQ_XR_LAUNCH(ds, KERNEL, grid, block, smem, stream, ...)                      \
+  do {                                                                               \
+    if ((ds)->f64)                                                                   \
+      KERNEL<double><<<(grid), (block), (smem), (stream)>>>((ds)->xr64, __VA_ARGS__); \
+    else                                                                             \
+      KERNEL<float><<<(grid), (block), (smem), (stream)>>>((ds)->xr, __VA_ARGS__);   \
+  } while (0)
 
 struct aq_codebook {
   aq_session* s = nullptr;
@@ -179,10 +197,9 @@ int llt_solve_device(aq_session* s, double* A, int n, double* x);
 int trace_ridge_device(aq_session* s, double* A, size_t dim, double ridge);
 // per-slot point-ordered sums (train.cu k_slot_sums): hp == null -> unit
 // weights; dict != null -> means of non-empty slots, else num/den partials
-int slot_sums_device(aq_session* s, const float* xr, size_t n, int d, int M, int k, int sd,
+int slot_sums_device(aq_session* s, const aq_dataset* ds, int M, int k, int sd,
                      const Buckets& B, const int* active, const double* hp, const double* ho,
-                     double* dict, double* pnum, double* pden,
-                     const float* xt = nullptr);
+                     double* dict, double* pnum, double* pden);
 
 // ---- weights ------------------------------------------------------------------
 // Resolved per point on the device from an aq_weights descriptor

@@ -821,13 +821,14 @@ __global__ void __launch_bounds__(TPB, MINB)
 
 // ---- generic exact kernel (any sub_dimension, k <= 256) ---------------------
 
-__device__ __forceinline__ float xval(const float* __restrict__ xt, size_t i,
-                                      int j, int pairs) {
-  return xt[tiled_index(i, (size_t)j, (size_t)pairs)];
+template <class TX>
+__device__ __forceinline__ double xval(const TX* __restrict__ xt, size_t i, int j, int pairs) {
+  return (double)xt[tiled_index(i, (size_t)j, (size_t)pairs)];
 }
 
 // detail::residual_terms for general sd (geometry.hpp:182-192)
-__device__ __forceinline__ void residual_g(const float* __restrict__ xt,
+template <class TX>
+__device__ __forceinline__ void residual_g(const TX* __restrict__ xt,
                                            size_t i, int pairs, int off,
                                            const double* c, int sd,
                                            double* d2, double* rd) {
@@ -857,7 +858,8 @@ __device__ __forceinline__ void scode(uint8_t* row, int m, int bits,
 
 // Exact float64 mirror of the reference loops; codes are edited in place in
 // a per-thread scratch row (global memory) so any M works.
-__global__ void k_encode_generic(const EncodeArgs a, const float* xt,
+template <class TX>
+__global__ void k_encode_generic(const EncodeArgs a, const TX* xt,
                                  int sd, uint8_t* work) {
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n) return;
@@ -1037,7 +1039,7 @@ static int run_encode_impl(aq_dataset* ds, aq_codebook* cb, const aq_weights* w,
   }
   a.changed = dchg;
   if (!async) AQ_TRY(clear_dev_error(s));
-  const bool fast = cb->sd == 2 && cb->k <= 16 && codes->bits == 4;
+  const bool fast = cb->sd == 2 && cb->k <= 16 && codes->bits == 4 && !ds->f64;
   if (fast) {
     const int W = (a.M + 7) / 8;
     // 256 threads, 3 CTAs/SM (24 warps at 80 registers), measured best for
@@ -1087,8 +1089,12 @@ static int run_encode_impl(aq_dataset* ds, aq_codebook* cb, const aq_weights* w,
     void* work;
     AQ_TRY(scratch(s, 3, ds->n * codes->stride + 16, &work));
     const unsigned grid = (unsigned)((ds->n + 127) / 128);
-    k_encode_generic<<<grid, 128, 0, s->stream>>>(a, ds->xt, (int)cb->sd,
-                                                  (uint8_t*)work);
+    if (ds->f64)
+      k_encode_generic<double><<<grid, 128, 0, s->stream>>>(a, ds->xt64, (int)cb->sd,
+                                                            (uint8_t*)work);
+    else
+      k_encode_generic<float><<<grid, 128, 0, s->stream>>>(a, ds->xt, (int)cb->sd,
+                                                           (uint8_t*)work);
     AQ_LAUNCHED(s);
     if (mode <= 1) {
       const size_t bytes = ds->n * codes->stride;

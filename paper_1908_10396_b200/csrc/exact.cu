@@ -74,7 +74,7 @@ __device__ int warp_keep_ge(XEntry* buf, int cnt, unsigned long long cut) {
 }
 
 struct XArgs {
-  const float* xt;
+  const void* xt;  // pair-tiled rows, float or double (TX)
   int pairs, d;
   size_t n;
   const double* Q;
@@ -86,6 +86,7 @@ struct XArgs {
   int* out_flag;
 };
 
+template <class TX>
 __global__ void __launch_bounds__(kXTile, 1) k_exact_score(const XArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   double* qs = reinterpret_cast<double*>(smem);  // [d][kXQ]
@@ -114,7 +115,8 @@ __global__ void __launch_bounds__(kXTile, 1) k_exact_score(const XArgs a) {
       double s[kXQ];
 #pragma unroll
       for (int q = 0; q < kXQ; ++q) s[q] = 0.0;
-      const float* xrow = a.xt + ((p >> 5) * a.pairs * 32 + (p & 31)) * 2;
+      const TX* xrow =
+          static_cast<const TX*>(a.xt) + ((p >> 5) * a.pairs * 32 + (p & 31)) * 2;
       for (int j = 0; j < a.d; ++j) {
         const double xv = (double)xrow[(size_t)(j >> 1) * 64 + (j & 1)];
         const double2* qj = reinterpret_cast<const double2*>(qs + (size_t)j * kXQ);
@@ -254,7 +256,8 @@ __global__ void __launch_bounds__(256) k_exact_merge(const XEntry* buf, const in
   }
 }
 
-__global__ void k_exact_all(const float* xt, int pairs, int d, size_t n, const double* q,
+template <class TX>
+__global__ void k_exact_all(const TX* xt, int pairs, int d, size_t n, const double* q,
                             double* out, uint32_t* idx) {
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -285,7 +288,9 @@ int exact_search_device(aq_dataset* ds, const double* Qd, size_t nq, size_t dept
   // keeps the all-float64 scoring kernel below
   static const int use_filter = getenv("AQ_EXACT_FILTER") ? atoi(getenv("AQ_EXACT_FILTER")) : 1;
   bool ran = false;
-  if (use_filter) AQ_TRY(exact_filter_device(ds, Qd, nq, depth, ids, scores, hflag, &ran));
+  // (float32 datasets only: the filter reads float32 rows)
+  if (use_filter && !ds->f64)
+    AQ_TRY(exact_filter_device(ds, Qd, nq, depth, ids, scores, hflag, &ran));
   const bool fast = !ran && depth <= (size_t)kXMaxN;
   if (fast) {
     const size_t nqb = (nq + kXQ - 1) / kXQ;
@@ -302,13 +307,21 @@ int exact_search_device(aq_dataset* ds, const double* Qd, size_t nq, size_t dept
     int* ocnt = (int*)(obuf + nq * R * cap);
     int* oflag = ocnt + nq * R;
     AQ_CUDA(cudaMemsetAsync(oflag, 0, nq * sizeof(int), s->stream));
-    XArgs a{ds->xt, pairs, (int)d, n, Qd, (int)nq, N, cap, range_len, (int)R, obuf, ocnt, oflag};
+    const void* xt = ds->f64 ? (const void*)ds->xt64 : (const void*)ds->xt;
+    XArgs a{xt, pairs, (int)d, n, Qd, (int)nq, N, cap, range_len, (int)R, obuf, ocnt, oflag};
     const size_t smem = d * kXQ * sizeof(double) + kXQ * 8 + 2 * kXQ * 4 + 8 +
                         (size_t)kXQ * cap * sizeof(XEntry);
     if (smem <= 227 * 1024) {
-      AQ_CUDA(cudaFuncSetAttribute(k_exact_score, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
-      k_exact_score<<<dim3((unsigned)R, (unsigned)nqb), kXTile, smem, s->stream>>>(a);
+      const dim3 grid((unsigned)R, (unsigned)nqb);
+      if (ds->f64) {
+        AQ_CUDA(cudaFuncSetAttribute(k_exact_score<double>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_exact_score<double><<<grid, kXTile, smem, s->stream>>>(a);
+      } else {
+        AQ_CUDA(cudaFuncSetAttribute(k_exact_score<float>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_exact_score<float><<<grid, kXTile, smem, s->stream>>>(a);
+      }
       AQ_LAUNCHED(s);
       k_exact_merge<<<(unsigned)nq, 256, 0, s->stream>>>(obuf, ocnt, oflag, (int)R, cap, N,
                                                          (int)te, ids, scores);
@@ -327,8 +340,12 @@ int exact_search_device(aq_dataset* ds, const double* Qd, size_t nq, size_t dept
     uint32_t* idx = (uint32_t*)(all + n);
     for (size_t q = 0; q < nq; ++q) {
       if (!hflag[q]) continue;
-      k_exact_all<<<(unsigned)((n + 255) / 256), 256, 0, s->stream>>>(ds->xt, pairs, (int)d, n,
-                                                                      Qd + q * d, all, idx);
+      if (ds->f64)
+        k_exact_all<double><<<(unsigned)((n + 255) / 256), 256, 0, s->stream>>>(
+            ds->xt64, pairs, (int)d, n, Qd + q * d, all, idx);
+      else
+        k_exact_all<float><<<(unsigned)((n + 255) / 256), 256, 0, s->stream>>>(
+            ds->xt, pairs, (int)d, n, Qd + q * d, all, idx);
       AQ_LAUNCHED(s);
       AQ_TRY(sort_scores_desc(s, all, idx, n));
       k_take<<<(unsigned)((te + 255) / 256), 256, 0, s->stream>>>(idx, all, (int)te,

@@ -615,7 +615,8 @@ int adc_search_device(aq_codes* codes, aq_codebook* cb, const double* Qd,
 
 // One warp per query: candidates rescored with detail::dot against the row
 // (float32-exact values) and the best `keep` returned in select_top order.
-__global__ void k_rerank(const float* __restrict__ xr, int d,
+template <class TX>
+__global__ void k_rerank(const TX* __restrict__ xr, int d,
                          const double* __restrict__ Q, int nq,
                          const uint32_t* __restrict__ cand, int ncand, int keep,
                          uint32_t* __restrict__ ids, double* __restrict__ sc,
@@ -634,7 +635,7 @@ __global__ void k_rerank(const float* __restrict__ xr, int d,
       const uint32_t id = cand[(size_t)q * ncand + e];
       double s = 0.0;
       if (id < n) {
-        const float* row = xr + (size_t)id * d;  // row-major: contiguous gather
+        const TX* row = xr + (size_t)id * d;  // row-major: contiguous gather
         for (int j = 0; j < d; ++j) s = __dadd_rn(s, __dmul_rn(qv[j], (double)row[j]));
       } else {
         report_error(err, (uint64_t)q, AQ_E_INVALID_ARGUMENT);
@@ -678,7 +679,8 @@ __global__ void k_rerank(const float* __restrict__ xr, int d,
 
 // Exact float64 dots for candidate ids, in the given order (no selection):
 // the per-shard half of the multi-GPU rerank.
-__global__ void k_exact_dots(const float* __restrict__ xr, int d,
+template <class TX>
+__global__ void k_exact_dots(const TX* __restrict__ xr, int d,
                              const double* __restrict__ Q, size_t nq,
                              const uint32_t* __restrict__ cand, size_t ncand, size_t n,
                              double* __restrict__ out) {
@@ -706,9 +708,9 @@ int rerank_device(aq_dataset* ds, const double* Qd, size_t nq,
   const size_t smem = (size_t)wpb * P * 12;
   AQ_TRY(clear_dev_error(s));
   timer_mark(s, AQ_T_RERANK);
-  k_rerank<<<(unsigned)((nq + wpb - 1) / wpb), wpb * 32, smem, s->stream>>>(
-      ds->xr, (int)ds->d, Qd, (int)nq, cand, (int)ncand,
-      (int)keep_eff, ids, sc, ds->n, s->err);
+  AQ_XR_LAUNCH(ds, k_rerank, (unsigned)((nq + wpb - 1) / wpb), wpb * 32, smem, s->stream,
+               (int)ds->d, Qd, (int)nq, cand, (int)ncand, (int)keep_eff, ids, sc, ds->n,
+               s->err);
   AQ_LAUNCHED(s);
   timer_mark(s, AQ_T_RERANK);
   return AQ_OK;
@@ -859,8 +861,8 @@ int aq_dev_exact_dots_d(aq_dataset* ds, const double* q_dev, size_t nq,
   AQ_TRY(check_session(s));
   const size_t total = nq * ncand;
   if (total == 0) return AQ_OK;
-  k_exact_dots<<<(unsigned)((total + 255) / 256), 256, 0, s->stream>>>(
-      ds->xr, (int)ds->d, q_dev, nq, cand_dev, ncand, ds->n, out_dev);
+  AQ_XR_LAUNCH(ds, k_exact_dots, (unsigned)((total + 255) / 256), 256, 0, s->stream,
+               (int)ds->d, q_dev, nq, cand_dev, ncand, ds->n, out_dev);
   AQ_LAUNCHED(s);
   AQ_CUDA(cudaStreamSynchronize(s->stream));
   return AQ_OK;

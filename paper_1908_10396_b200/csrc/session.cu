@@ -110,15 +110,16 @@ int sync_and_check(aq_session* s, const char* what) {
 // Row-major fp32 -> pair-tiled layout, and float64 norms in the reference's
 // order (dataset.hpp:55-59). One thread per row for the norm; the tiled write
 // of a 32-row tile is coalesced because lanes own consecutive rows.
-__global__ void k_tile_rows(const float* __restrict__ x, size_t n, size_t d,
-                            float* __restrict__ xt, double* __restrict__ norms) {
+template <class T>
+__global__ void k_tile_rows(const T* __restrict__ x, size_t n, size_t d,
+                            T* __restrict__ xt, double* __restrict__ norms) {
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t pairs = pairs_of(d);
   const size_t ntile = ((n + 31) / 32) * 32;
   if (i >= ntile) return;
   double s = 0.0;
   for (size_t j = 0; j < 2 * pairs; ++j) {
-    float v = 0.0f;
+    T v = 0;
     if (i < n && j < d) v = x[i * d + j];
     xt[tiled_index(i, j, pairs)] = v;
     if (j < d) s = __dadd_rn(s, __dmul_rn((double)v, (double)v));
@@ -384,13 +385,73 @@ static int dataset_from_device_rows(aq_session* s, const float* xdev, size_t n,
                             s->stream));
   const size_t ntile = ((n + 31) / 32) * 32;
   if (ntile) {
-    k_tile_rows<<<(unsigned)((ntile + 127) / 128), 128, 0, s->stream>>>(
+    k_tile_rows<float><<<(unsigned)((ntile + 127) / 128), 128, 0, s->stream>>>(
         xdev, n, d, ds->xt, ds->norms);
     AQ_LAUNCHED(s);
   }
   *out = ds;
   return AQ_OK;
 }
+
+// float64 rows (values that are not float32-exact): row-major + pair-tiled
+// float64 copies, norms in the reference's order.
+static int dataset_from_device_rows64(aq_session* s, const double* xdev, size_t n, size_t d,
+                                      aq_dataset** out) {
+  aq_dataset* ds = new aq_dataset();
+  ds->s = s;
+  ds->n = n;
+  ds->d = d;
+  ds->f64 = 1;
+  const size_t tf = tiled_floats(n, d);
+  int st = AQ_OK;
+  if (cudaMallocAsync(&ds->xt64, (tf + 256) * sizeof(double), s->stream) != cudaSuccess ||
+      cudaMallocAsync(&ds->norms, (n ? n : 1) * sizeof(double), s->stream) != cudaSuccess ||
+      cudaMallocAsync(&ds->xr64, (n * d ? n * d : 1) * sizeof(double), s->stream) !=
+          cudaSuccess)
+    st = ref_error(AQ_E_CUDA, "out of device memory for the dataset");
+  if (st == AQ_OK) {
+    cudaMemsetAsync(ds->xt64 + tf, 0, 256 * sizeof(double), s->stream);
+    if (n * d)
+      cudaMemcpyAsync(ds->xr64, xdev, n * d * sizeof(double), cudaMemcpyDeviceToDevice,
+                      s->stream);
+    const size_t ntile = ((n + 31) / 32) * 32;
+    if (ntile) {
+      k_tile_rows<double><<<(unsigned)((ntile + 127) / 128), 128, 0, s->stream>>>(
+          xdev, n, d, ds->xt64, ds->norms);
+      AQ_LAUNCHED(s);
+    }
+  }
+  if (st != AQ_OK) {
+    aq_dataset_free(ds);
+    return st;
+  }
+  *out = ds;
+  return AQ_OK;
+}
+
+// float64 host rows: float32 storage when every value is float32-exact
+// (the fast kernels), float64 storage otherwise.
+int aq_dataset_upload_f64(aq_session* s, const double* x, size_t n, size_t d,
+                          aq_dataset** out) {
+  AQ_TRY(check_session(s));
+  if (d == 0) return ref_error(AQ_E_INVALID_ARGUMENT, "dimension must be positive");
+  bool exact32 = true;
+  for (size_t e = 0; e < n * d && exact32; ++e)
+    exact32 = (double)(float)x[e] == x[e] || x[e] != x[e];
+  if (exact32) {
+    std::vector<float> f(n * d);
+    for (size_t e = 0; e < n * d; ++e) f[e] = (float)x[e];
+    return aq_dataset_upload(s, f.data(), n, d, out);
+  }
+  void* stage = nullptr;
+  AQ_TRY(scratch(s, 0, n * d * sizeof(double) + 16, &stage));
+  AQ_CUDA(cudaMemcpyAsync(stage, x, n * d * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+  AQ_TRY(dataset_from_device_rows64(s, (const double*)stage, n, d, out));
+  AQ_CUDA(cudaStreamSynchronize(s->stream));
+  return AQ_OK;
+}
+
+int aq_dataset_is_f64(const aq_dataset* ds) { return ds ? ds->f64 : 0; }
 
 int aq_dataset_upload(aq_session* s, const float* x, size_t n, size_t d,
                       aq_dataset** out) {
@@ -417,6 +478,8 @@ int aq_dataset_free(aq_dataset* ds) {
   cudaSetDevice(ds->s->device);
   cudaFreeAsync(ds->xt, ds->s->stream);
   cudaFreeAsync(ds->xr, ds->s->stream);
+  cudaFreeAsync(ds->xt64, ds->s->stream);
+  cudaFreeAsync(ds->xr64, ds->s->stream);
   cudaFreeAsync(ds->norms, ds->s->stream);
   delete ds;
   return AQ_OK;
@@ -446,6 +509,8 @@ int aq_codebook_upload(aq_session* s, const double* dict, size_t M, size_t k,
   if (cnt && dict)
     AQ_CUDA(cudaMemcpyAsync(cb->d64, dict, cnt * sizeof(double),
                             cudaMemcpyHostToDevice, s->stream));
+  else if (cnt)  // an output codebook: defined contents until written
+    AQ_CUDA(cudaMemsetAsync(cb->d64, 0, cnt * sizeof(double), s->stream));
   AQ_TRY(stage_codebook(cb));
   AQ_CUDA(cudaStreamSynchronize(s->stream));
   *out = cb;

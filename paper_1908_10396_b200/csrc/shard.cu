@@ -122,8 +122,8 @@ int aq_dev_iso_partials(aq_dataset* ds, aq_codes* codes, const aq_weights* w, si
   if (ds->n) {
     st = build_buckets(codes, (int)k, &B);
     if (st == AQ_OK) {
-      st = slot_sums_device(s, ds->xr, ds->n, (int)ds->d, (int)M, (int)k, (int)sd, B, nullptr,
-                            pw.hp, pw.ho, nullptr, num_dev, den_dev, ds->xt);
+      st = slot_sums_device(s, ds, (int)M, (int)k, (int)sd, B, nullptr, pw.hp, pw.ho, nullptr,
+                            num_dev, den_dev);
       if (usage_dev) {
         k_copy_counts<<<(unsigned)((M * k + 255) / 256), 256, 0, s->stream>>>(B.count, M * k,
                                                                               usage_dev);
@@ -229,8 +229,8 @@ int aq_dev_kmeans_partials(aq_dataset* ds, aq_codes* codes, size_t k, const int*
     Buckets B;
     st = build_buckets(codes, (int)k, &B);
     if (st == AQ_OK) {
-      st = slot_sums_device(s, ds->xr, ds->n, (int)ds->d, (int)M, (int)k, (int)sd, B, act,
-                            nullptr, nullptr, nullptr, num_dev, den_dev, ds->xt);
+      st = slot_sums_device(s, ds, (int)M, (int)k, (int)sd, B, act, nullptr, nullptr, nullptr,
+                            num_dev, den_dev);
       k_copy_counts<<<(unsigned)((M * k + 255) / 256), 256, 0, s->stream>>>(B.count, M * k,
                                                                             count_dev);
       s->launches++;

@@ -352,7 +352,8 @@ int seq_sum_device(aq_session* s, const double* v, size_t n, double init, double
 }
 
 // codewords from sampled rows: dict[m][j] = x[idx[m][j]][m-subvector]
-__global__ void k_init_codewords(const float* __restrict__ xr, int d, int M, int k, int sd,
+template <class TX>
+__global__ void k_init_codewords(const TX* __restrict__ xr, int d, int M, int k, int sd,
                                  const uint64_t* __restrict__ idx, double* __restrict__ dict) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= M * k) return;
@@ -374,7 +375,8 @@ __device__ __forceinline__ void set_code(uint8_t* row, int m, int bits, unsigned
 // vq_assign_pass with isotropic unit weights (vq.hpp:196-217, assign_scan
 // 83-100): per subspace argmin of dist2 (first index wins), loss = 1.0 dist2.
 // One thread per point walks the active subspaces (codes share bytes).
-__global__ void k_kmeans_assign(const float* __restrict__ xr, size_t n, int d, int M, int k,
+template <class TX>
+__global__ void k_kmeans_assign(const TX* __restrict__ xr, size_t n, int d, int M, int k,
                                 int sd, const double* __restrict__ dict,
                                 const int* __restrict__ active, uint8_t* __restrict__ codes,
                                 int stride, int bits, double* __restrict__ losses,
@@ -382,7 +384,7 @@ __global__ void k_kmeans_assign(const float* __restrict__ xr, size_t n, int d, i
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   uint8_t* row = codes + i * stride;
-  const float* xp = xr + i * d;
+  const TX* xp = xr + i * d;
   for (int m = 0; m < M; ++m) {
     if (!active[m]) continue;
     const double* cm = dict + (size_t)m * k * sd;
@@ -482,8 +484,8 @@ __global__ void __launch_bounds__(256) k_kmeans_assign_sd2(
 //                      pq.hpp:405-417)
 //   dict != null: dict = num / den for non-empty slots (weighted: den <= 0 is
 //                 a singular block); else num / den are written as partials.
-template <int SDC, bool kWeighted>
-__global__ void k_slot_sums(const float* __restrict__ xr, const float* __restrict__ xt, size_t n,
+template <class TX, int SDC, bool kWeighted>
+__global__ void k_slot_sums(const TX* __restrict__ xr, const float* __restrict__ xt, size_t n,
                             int d, int M, int k,
                             int sd_rt, const uint32_t* __restrict__ list,
                             const uint32_t* __restrict__ start,
@@ -505,7 +507,7 @@ __global__ void k_slot_sums(const float* __restrict__ xr, const float* __restric
   if (active && !active[m]) return;
   const size_t cnt = count[slot];
   const uint32_t* L = list + (size_t)m * n + start[slot];
-  float nx[G][SDM];
+  TX nx[G][SDM];
   double nh[G][2];
   auto fetch = [&](size_t r0) {
 #pragma unroll
@@ -526,7 +528,7 @@ __global__ void k_slot_sums(const float* __restrict__ xr, const float* __restric
           }
         }
         if (!tiled) {
-          const float* xp = xr + (size_t)p * d + m * sd;
+          const TX* xp = xr + (size_t)p * d + m * sd;
 #pragma unroll
           for (int c = 0; c < SDM; ++c)
             if (c < sd) nx[g][c] = xp[c];
@@ -595,14 +597,23 @@ __global__ void k_slot_sums(const float* __restrict__ xr, const float* __restric
 }
 
 // Host wrapper of k_slot_sums (hp == null: unit weights).
-int slot_sums_device(aq_session* s, const float* xr, size_t n, int d, int M, int k, int sd,
+int slot_sums_device(aq_session* s, const aq_dataset* ds, int M, int k, int sd,
                      const Buckets& B, const int* active, const double* hp, const double* ho,
-                     double* dict, double* pnum, double* pden, const float* xt) {
+                     double* dict, double* pnum, double* pden) {
   const unsigned grid = (unsigned)((M * k + 3) / 4);
-#define AQ_SLOTS(SDV, WV)                                                                \
-  k_slot_sums<SDV, WV><<<grid, 128, 0, s->stream>>>(xr, xt, n, d, M, k, sd, B.list, B.start, \
-                                                    B.count, active, hp, ho, dict, pnum, \
-                                                    pden, s->err)
+  const size_t n = ds->n;
+  const int d = (int)ds->d;
+#define AQ_SLOTS(SDV, WV)                                                                     \
+  do {                                                                                       \
+    if (ds->f64)                                                                             \
+      k_slot_sums<double, SDV, WV><<<grid, 128, 0, s->stream>>>(                             \
+          ds->xr64, nullptr, n, d, M, k, sd, B.list, B.start, B.count, active, hp, ho, dict, \
+          pnum, pden, s->err);                                                               \
+    else                                                                                     \
+      k_slot_sums<float, SDV, WV><<<grid, 128, 0, s->stream>>>(                              \
+          ds->xr, ds->xt, n, d, M, k, sd, B.list, B.start, B.count, active, hp, ho, dict,    \
+          pnum, pden, s->err);                                                               \
+  } while (0)
   if (sd == 2) {
     if (hp) AQ_SLOTS(2, true);
     else AQ_SLOTS(2, false);
@@ -616,8 +627,9 @@ int slot_sums_device(aq_session* s, const float* xr, size_t n, int d, int M, int
 }
 
 // empty partitions (vq.hpp:284-292): j ascending, consuming the ranking
+template <class TX>
 __global__ void k_kmeans_reseed(const uint32_t* __restrict__ count, int m, int k, int sd,
-                                const uint32_t* __restrict__ order, const float* xr, int d,
+                                const uint32_t* __restrict__ order, const TX* xr, int d,
                                 double* dict) {
   size_t cursor = 0;
   for (int j = 0; j < k; ++j) {
@@ -670,8 +682,12 @@ int train_l2_pq_device(aq_dataset* ds, size_t M, size_t k, const aq_train_config
     cudaMallocAsync(&didx, M * k * sizeof(uint64_t), s->stream);
     cudaMallocAsync(&order, n * sizeof(uint32_t), s->stream);
     cudaMemcpyAsync(didx, hidx.data(), M * k * sizeof(uint64_t), cudaMemcpyHostToDevice, s->stream);
-    k_init_codewords<<<(unsigned)((M * k + 127) / 128), 128, 0, s->stream>>>(
-        ds->xr, (int)d, (int)M, (int)k, (int)sd, didx, cb->d64);
+    if (ds->f64)
+      k_init_codewords<double><<<(unsigned)((M * k + 127) / 128), 128, 0, s->stream>>>(
+          ds->xr64, (int)d, (int)M, (int)k, (int)sd, didx, cb->d64);
+    else
+      k_init_codewords<float><<<(unsigned)((M * k + 127) / 128), 128, 0, s->stream>>>(
+          ds->xr, (int)d, (int)M, (int)k, (int)sd, didx, cb->d64);
     s->launches++;
   }
   std::vector<int> hact(M, 1);
@@ -680,7 +696,7 @@ int train_l2_pq_device(aq_dataset* ds, size_t M, size_t k, const aq_train_config
   auto assign = [&]() -> int {
     AQ_CUDA(cudaMemcpyAsync(active, hact.data(), M * sizeof(int), cudaMemcpyHostToDevice, s->stream));
     AQ_CUDA(cudaMemsetAsync(changes, 0, M * sizeof(unsigned long long), s->stream));
-    if (sd == 2 && codes->bits == 4) {
+    if (sd == 2 && codes->bits == 4 && !ds->f64) {
       const size_t sm = (size_t)M * k * sizeof(double2) + 2 * M * sizeof(int);
       AQ_CUDA(cudaFuncSetAttribute(k_kmeans_assign_sd2,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -688,9 +704,9 @@ int train_l2_pq_device(aq_dataset* ds, size_t M, size_t k, const aq_train_config
           reinterpret_cast<const float2*>(ds->xt), n, (int)(d / 2), (int)M, (int)k, cb->d64,
           active, codes->data, (int)codes->stride, losses, changes);
     } else {
-      k_kmeans_assign<<<(unsigned)((n + 127) / 128), 128, 0, s->stream>>>(
-          ds->xr, n, (int)d, (int)M, (int)k, (int)sd, cb->d64, active, codes->data,
-          (int)codes->stride, codes->bits, losses, changes);
+      AQ_XR_LAUNCH(ds, k_kmeans_assign, (unsigned)((n + 127) / 128), 128, 0, s->stream, n,
+                   (int)d, (int)M, (int)k, (int)sd, cb->d64, active, codes->data,
+                   (int)codes->stride, codes->bits, losses, changes);
     }
     AQ_LAUNCHED(s);
     // loss totals only feed the relative-tolerance test (vq.hpp:316-321)
@@ -713,8 +729,8 @@ int train_l2_pq_device(aq_dataset* ds, size_t M, size_t k, const aq_train_config
     st = build_buckets(codes, (int)k, &B);
     if (st != AQ_OK) break;
     AQ_CUDA(cudaMemcpyAsync(active, hact.data(), M * sizeof(int), cudaMemcpyHostToDevice, s->stream));
-    AQ_TRY(slot_sums_device(s, ds->xr, n, (int)d, (int)M, (int)k, (int)sd, B, active, nullptr,
-                            nullptr, cb->d64, nullptr, nullptr, ds->xt));
+    AQ_TRY(slot_sums_device(s, ds, (int)M, (int)k, (int)sd, B, active, nullptr, nullptr,
+                            cb->d64, nullptr, nullptr));
     s->launches++;
     if (cfg->empty_partition_policy == 0) {
       std::vector<uint32_t> hc(M * k);
@@ -735,8 +751,12 @@ int train_l2_pq_device(aq_dataset* ds, size_t M, size_t k, const aq_train_config
         s->launches++;
         st = sort_scores_desc(s, losses + m * n, order, n);
         if (st == AQ_OK) {
-          k_kmeans_reseed<<<1, 1, 0, s->stream>>>(cnt_copy, (int)m, (int)k, (int)sd, order,
-                                                  ds->xr, (int)d, cb->d64);
+          if (ds->f64)
+            k_kmeans_reseed<double><<<1, 1, 0, s->stream>>>(cnt_copy, (int)m, (int)k, (int)sd,
+                                                            order, ds->xr64, (int)d, cb->d64);
+          else
+            k_kmeans_reseed<float><<<1, 1, 0, s->stream>>>(cnt_copy, (int)m, (int)k, (int)sd,
+                                                           order, ds->xr, (int)d, cb->d64);
           s->launches++;
         }
         cudaFreeAsync(cnt_copy, s->stream);
@@ -820,8 +840,8 @@ int aq_dev_train_apq(aq_dataset* ds, size_t M, size_t k, const aq_weights* w,
     AQ_CUDA(cudaMallocAsync(&didx, M * k * sizeof(uint64_t), s->stream));
     AQ_CUDA(cudaMemcpyAsync(didx, hidx.data(), M * k * sizeof(uint64_t), cudaMemcpyHostToDevice,
                             s->stream));
-    k_init_codewords<<<(unsigned)((M * k + 127) / 128), 128, 0, s->stream>>>(
-        ds->xr, (int)d, (int)M, (int)k, (int)sd, didx, cb->d64);
+    AQ_XR_LAUNCH(ds, k_init_codewords, (unsigned)((M * k + 127) / 128), 128, 0, s->stream,
+                 (int)d, (int)M, (int)k, (int)sd, didx, cb->d64);
     s->launches++;
     cudaFreeAsync(didx, s->stream);
     int st = stage_codebook(cb);
@@ -958,9 +978,8 @@ int aq_dev_train_avq(aq_dataset* ds, size_t k, const aq_weights* w, const aq_tra
     st = ref_error(AQ_E_CUDA, "out of device memory");
   if (st == AQ_OK) {
     cudaMemcpyAsync(didx, hidx.data(), k * sizeof(uint64_t), cudaMemcpyHostToDevice, s->stream);
-    k_init_codewords<<<(unsigned)((k + 127) / 128), 128, 0, s->stream>>>(ds->xr, (int)d, 1,
-                                                                       (int)k, (int)d, didx,
-                                                                       cb->d64);
+    AQ_XR_LAUNCH(ds, k_init_codewords, (unsigned)((k + 127) / 128), 128, 0, s->stream, (int)d,
+                 1, (int)k, (int)d, didx, cb->d64);
     s->launches++;
     st = stage_codebook(cb);
   }
@@ -1027,7 +1046,7 @@ int aq_dev_kmeans_assign(aq_dataset* ds, aq_codebook* cb, aq_codes* codes,
   AQ_CUDA(cudaMemcpyAsync(act, active_host, M * sizeof(int), cudaMemcpyHostToDevice, s->stream));
   AQ_CUDA(cudaMemsetAsync(chg, 0, M * sizeof(unsigned long long), s->stream));
   if (n) {
-    if (cb->sd == 2 && codes->bits == 4) {
+    if (cb->sd == 2 && codes->bits == 4 && !ds->f64) {
       const size_t sm = (size_t)M * cb->k * sizeof(double2) + 2 * M * sizeof(int);
       AQ_CUDA(cudaFuncSetAttribute(k_kmeans_assign_sd2,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -1035,9 +1054,9 @@ int aq_dev_kmeans_assign(aq_dataset* ds, aq_codebook* cb, aq_codes* codes,
           reinterpret_cast<const float2*>(ds->xt), n, (int)(ds->d / 2), (int)M, (int)cb->k,
           cb->d64, act, codes->data, (int)codes->stride, losses_dev, chg);
     } else {
-      k_kmeans_assign<<<(unsigned)((n + 127) / 128), 128, 0, s->stream>>>(
-          ds->xr, n, (int)ds->d, (int)M, (int)cb->k, (int)cb->sd, cb->d64, act, codes->data,
-          (int)codes->stride, codes->bits, losses_dev, chg);
+      AQ_XR_LAUNCH(ds, k_kmeans_assign, (unsigned)((n + 127) / 128), 128, 0, s->stream, n,
+                   (int)ds->d, (int)M, (int)cb->k, (int)cb->sd, cb->d64, act, codes->data,
+                   (int)codes->stride, codes->bits, losses_dev, chg);
     }
     s->launches++;
   }

@@ -286,7 +286,8 @@ __global__ void k_point_weights(const double* __restrict__ norms, size_t n, DevW
 // ---- dense normal equations ---------------------------------------------------------------
 
 struct AsmArgs {
-  const float* xr;
+  const float* xr;  // float32 rows (every kernel), or null with xr64 set
+  const double* xr64;  // float64 rows (k_assemble<double> only)
   size_t n;
   int d, M, k, sd;
   const uint8_t* codes;
@@ -325,11 +326,20 @@ __device__ __forceinline__ size_t lower_bound_u32(const uint32_t* L, size_t cnt,
 // lane's column sub-vector / code) so the global gathers of a batch are
 // independent and in flight together.
 constexpr int kAsmSdMax = 4;
+template <class TX>
+__device__ __forceinline__ const TX* asm_rows(const AsmArgs& a);
+template <>
+__device__ __forceinline__ const float* asm_rows<float>(const AsmArgs& a) { return a.xr; }
+template <>
+__device__ __forceinline__ const double* asm_rows<double>(const AsmArgs& a) { return a.xr64; }
+
+template <class TX>
 __global__ void __launch_bounds__(32) k_assemble(const AsmArgs a) {
   extern __shared__ __align__(16) double acc[];  // [(aa*k + j2)*sd + b][32], rhs[sd]
   __shared__ double s_coef[32], s_ho[32], s_hp[32];
-  __shared__ float s_xm[32][kAsmSdMax];
-  __shared__ float s_xc[32][kAsmSdMax][33];  // [point][b][lane] (+1 pad)
+  __shared__ TX s_xm[32][kAsmSdMax];
+  __shared__ TX s_xc[32][kAsmSdMax][33];  // [point][b][lane] (+1 pad)
+  const TX* __restrict__ xr = asm_rows<TX>(a);
   __shared__ unsigned char s_j2[32][32];
   const int unit = blockIdx.x;
   const int chunk = unit % a.nchunk;
@@ -357,14 +367,14 @@ __global__ void __launch_bounds__(32) k_assemble(const AsmArgs a) {
       s_coef[lane] = a.coef[pl];
       s_ho[lane] = a.ho[pl];
       s_hp[lane] = a.hp[pl];
-      for (int c = 0; c < sd; ++c) s_xm[lane][c] = a.xr[(size_t)pl * d + m * sd + c];
+      for (int c = 0; c < sd; ++c) s_xm[lane][c] = xr[(size_t)pl * d + m * sd + c];
     }
     // ... and, for every point of the batch, its own column sub-vector and code
     if (mine) {
 #pragma unroll 8
       for (int b = 0; b < nb; ++b) {
         const uint32_t p = __shfl_sync(0xffffffffu, pl, b);
-        const float* xp = a.xr + (size_t)p * d + m2 * sd;
+        const TX* xp = xr + (size_t)p * d + m2 * sd;
         for (int c = 0; c < sd; ++c) s_xc[b][c][lane] = xp[c];
         s_j2[b][lane] = (unsigned char)get_code(a.codes + (size_t)p * a.stride, m2, a.bits);
       }
@@ -1051,19 +1061,21 @@ int llt_solve_device(aq_session* s, double* A, int n, double* x) {
 // coef[p] = (h_par - h_perp) / x.squaredNorm() (vq.hpp:178-181; the norm as a
 // sequential sum of squares), NaN-free marker: n2 == 0 leaves coef = 0 and is
 // reported by k_vq_systems.
-__global__ void k_vq_coef(const float* __restrict__ xr, size_t n, int d,
+template <class TX>
+__global__ void k_vq_coef(const TX* __restrict__ xr, size_t n, int d,
                           const double* __restrict__ hp, const double* __restrict__ ho,
                           double* __restrict__ coef, double* __restrict__ n2out) {
   const size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
-  const float* xp = xr + p * d;
+  const TX* xp = xr + p * d;
   double n2 = 0.0;
   for (int q = 0; q < d; ++q) n2 = __dadd_rn(n2, __dmul_rn((double)xp[q], (double)xp[q]));
   n2out[p] = n2;
   coef[p] = n2 == 0.0 ? 0.0 : __ddiv_rn(__dsub_rn(hp[p], ho[p]), n2);
 }
 
-__global__ void k_vq_systems(const float* __restrict__ xr, size_t n, int d, int k,
+template <class TX>
+__global__ void k_vq_systems(const TX* __restrict__ xr, size_t n, int d, int k,
                              const uint32_t* __restrict__ list,
                              const uint32_t* __restrict__ start,
                              const uint32_t* __restrict__ count, const double* __restrict__ hp,
@@ -1123,7 +1135,7 @@ __global__ void k_vq_systems(const float* __restrict__ xr, size_t n, int d, int 
       double v = 0.0;
       for (size_t t = 0; t < cnt; ++t) {
         const uint32_t p = L[t];
-        const float* xp = xr + (size_t)p * d;
+        const TX* xp = xr + (size_t)p * d;
         v = __dadd_rn(v, __dmul_rn(__dmul_rn(coefs[p], (double)xp[c]), (double)xp[r]));
       }
       if (r == c) v = __dadd_rn(v, s_diag);
@@ -1140,8 +1152,9 @@ __global__ void k_vq_systems(const float* __restrict__ xr, size_t n, int d, int 
 
 // unused-codeword reseeding: walk (m, j) lexicographically, consuming the
 // loss ranking cyclically (pq.hpp:452-461)
-__global__ void k_reseed(const uint32_t* count, int M, int k, int sd, const uint32_t* order,
-                         size_t n, const float* xr, int d, double* dict) {
+template <class TX>
+__global__ void k_reseed(const TX* xr, const uint32_t* count, int M, int k, int sd,
+                         const uint32_t* order, size_t n, int d, double* dict) {
   size_t cursor = 0;
   for (int m = 0; m < M; ++m)
     for (int j = 0; j < k; ++j) {
@@ -1191,19 +1204,23 @@ int assemble_device(aq_dataset* ds, aq_codes* codes, const PointW& pw, const Buc
   AQ_CUDA(cudaMemsetAsync(A, 0, dim * dim * sizeof(double), s->stream));
   AQ_CUDA(cudaMemsetAsync(rhs, 0, dim * sizeof(double), s->stream));
   const int nchunk = (M + 31) / 32;
-  AsmArgs a{ds->xr, ds->n, d, M, k, sd, codes->data, (int)codes->stride, codes->bits,
+  AsmArgs a{ds->xr, ds->xr64, ds->n, d, M, k, sd, codes->data, (int)codes->stride, codes->bits,
             B.list, B.start, B.count, pw.hp, pw.ho, pw.coef, full ? 1 : 0, A, rhs, nchunk,
             0u, (uint32_t)ds->n, 0};
   if (sd > kAsmSdMax)
     return ref_error(AQ_E_UNSUPPORTED, "device normal equations support sub_dimension <= 4");
   const size_t smem = ((size_t)sd * k * sd * 32 + 16) * sizeof(double);
-  if (smem + 20 * 1024 > 227 * 1024)
+  if (smem + (ds->f64 ? 40 : 20) * 1024 > 227 * 1024)
     return ref_error(AQ_E_UNSUPPORTED, "normal-equation strip exceeds shared memory");
-  AQ_CUDA(cudaFuncSetAttribute(k_assemble, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem));
+  if (ds->f64)
+    AQ_CUDA(cudaFuncSetAttribute(k_assemble<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+  else
+    AQ_CUDA(cudaFuncSetAttribute(k_assemble<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
   const unsigned units = (unsigned)(M * k * nchunk);
   timer_mark(s, AQ_T_ASSEMBLE);
-  if (sd == 2 && k == 16 && d % 4 == 0 && codes->bits == 4) {
+  if (sd == 2 && k == 16 && d % 4 == 0 && codes->bits == 4 && !ds->f64) {
     // 32 column subspaces per unit (a 16-column split with twice the units
     // measured slower: per-unit staging outweighs the extra warps)
     const int cols = 32, nch = nchunk;
@@ -1259,7 +1276,10 @@ int assemble_device(aq_dataset* ds, aq_codes* codes, const PointW& pw, const Buc
     a.lo = 0;
     a.hi = (uint32_t)ds->n;
     a.resume = 0;
-    k_assemble<<<units, 32, smem, s->stream>>>(a);
+    if (ds->f64)
+      k_assemble<double><<<units, 32, smem, s->stream>>>(a);
+    else
+      k_assemble<float><<<units, 32, smem, s->stream>>>(a);
   }
   AQ_LAUNCHED(s);
   timer_mark(s, AQ_T_ASSEMBLE);
@@ -1377,12 +1397,11 @@ static int codebook_update_impl(aq_dataset* ds, aq_codes* codes, const aq_weight
       AQ_TRY(clear_dev_error(s));
       cudaMemsetAsync(modes, 0xff, k * sizeof(int), s->stream);
       double* coefs = As + k * d * d + k * d;
-      k_vq_coef<<<(unsigned)((n + 255) / 256), 256, 0, s->stream>>>(ds->xr, n, (int)d, pw.hp,
-                                                                   pw.ho, coefs, coefs + n);
-      k_vq_systems<<<(unsigned)k, 128, 0, s->stream>>>(ds->xr, n, (int)d, (int)k, B.list,
-                                                       B.start, B.count, pw.hp, pw.ho, coefs,
-                                                       coefs + n, ridge, As, As + k * d * d,
-                                                       modes, out->d64, s->err);
+      AQ_XR_LAUNCH(ds, k_vq_coef, (unsigned)((n + 255) / 256), 256, 0, s->stream, n, (int)d,
+                   pw.hp, pw.ho, coefs, coefs + n);
+      AQ_XR_LAUNCH(ds, k_vq_systems, (unsigned)k, 128, 0, s->stream, n, (int)d, (int)k, B.list,
+                   B.start, B.count, pw.hp, pw.ho, coefs, coefs + n, ridge, As,
+                   As + k * d * d, modes, out->d64, s->err);
       s->launches += 2;
       st = sync_and_check(s, "codeword update");
     }
@@ -1404,8 +1423,8 @@ static int codebook_update_impl(aq_dataset* ds, aq_codes* codes, const aq_weight
     if (modes) cudaFreeAsync(modes, s->stream);
   } else if (st == AQ_OK && all_iso) {
     AQ_TRY(clear_dev_error(s));
-    st = slot_sums_device(s, ds->xr, n, (int)ds->d, (int)M, (int)k, sd, B, nullptr, pw.hp, pw.ho,
-                          out->d64, nullptr, nullptr, ds->xt);
+    st = slot_sums_device(s, ds, (int)M, (int)k, sd, B, nullptr, pw.hp, pw.ho, out->d64,
+                          nullptr, nullptr);
     if (st == AQ_OK) st = sync_and_check(s, "zero total weight in block");
   } else if (st == AQ_OK) {
     if (dim > 16384) {
@@ -1470,8 +1489,8 @@ static int codebook_update_impl(aq_dataset* ds, aq_codes* codes, const aq_weight
         st = sort_scores_desc(s, losses, idx, n);
       }
       if (st == AQ_OK) {
-        k_reseed<<<1, 1, 0, s->stream>>>(cnt_copy, (int)M, (int)k, sd, idx, n, ds->xr,
-                                         (int)ds->d, out->d64);
+        AQ_XR_LAUNCH(ds, k_reseed, 1, 1, 0, s->stream, cnt_copy, (int)M, (int)k, sd, idx, n,
+                     (int)ds->d, out->d64);
         s->launches++;
       }
       if (losses) cudaFreeAsync(losses, s->stream);

@@ -60,12 +60,16 @@ def test_host_weight_helpers():
         aq.eta_limit(0.2, 0.1, 32)
 
 
-def test_dataset_requires_float32_exact_values():
+def test_dataset_storage_type():
+    """float32-exact values are stored as float32 (fast kernels); anything
+    else (e.g. unit_normalize output) keeps float64 rows."""
     from paper_1908_10396_b200 import anisoq as aq
 
-    aq.Dataset(np.ones((3, 4), np.float64))
-    with pytest.raises(aq.Unsupported):
-        aq.Dataset(np.full((3, 4), 0.1, np.float64))
+    a = aq.Dataset(np.ones((3, 4), np.float64))
+    assert a.values.dtype == np.float32 and not a.f64
+    b = aq.Dataset(np.full((3, 4), 0.1, np.float64))
+    assert b.values.dtype == np.float64 and b.f64
+    assert np.array_equal(b.values, np.full((3, 4), 0.1))
 
 
 def test_workload_pack_roundtrip():

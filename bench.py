@@ -346,11 +346,12 @@ def run_ours(args):
         from paper_1908_10396_b200 import distributed as D
 
         def step_dev():  # noqa: F811
-            D.sharded_search_rerank(ds, dc, dcb, Qd, rank * n, topn, keep)
+            D.sharded_search_rerank(ds, dc, dcb, Qd, rank * n, topn, keep, n_total=n * ws)
 
         def step_e2e():  # noqa: F811
             q = Qpin.to(f"cuda:{local}", non_blocking=True)
-            _, _, r_ids, r_sc = D.sharded_search_rerank(ds, dc, dcb, q, rank * n, topn, keep)
+            _, _, r_ids, r_sc = D.sharded_search_rerank(ds, dc, dcb, q, rank * n, topn, keep,
+                                                        n_total=n * ws)
             hid_t.copy_(r_ids.to(torch.int32).cpu())
             hsc_t.copy_(r_sc.cpu())
 
@@ -701,8 +702,31 @@ def emit(line: str) -> None:
         print(line, flush=True)
 
 
+def launch_ranks(args) -> int:
+    """`--gpus N` without a torchrun environment: start N ranks (one process
+    per GPU) under torch.distributed.run on this node and relay rank 0's line."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 if __name__ == "__main__":
     a = parse()
+    world = os.environ.get("WORLD_SIZE")
+    if world is None and a.gpus > 1:
+        sys.exit(launch_ranks(a))
+    if world is not None and int(world) != a.gpus:
+        sys.exit(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world}; launch one rank per GPU")
+    if a.impl == "ours" and a.gpus > 1:
+        import torch
+        if torch.cuda.device_count() < a.gpus and int(os.environ.get("LOCAL_RANK", "0")) == 0:
+            sys.exit(f"bench.py: --gpus {a.gpus} but only {torch.cuda.device_count()} visible")
     sys.stdout.flush()
     _STDOUT_FD = os.dup(1)
     os.dup2(2, 1)  # C-level and Python prints during the run go to stderr

@@ -695,13 +695,82 @@ __global__ void k_exact_dots(const TX* __restrict__ xr, int d,
   out[t] = id < n ? s : -INFINITY;
 }
 
+// Long candidate lists (> 4096, beyond one warp's shared-memory sort): per
+// query, float64 dots of every candidate (k_exact_dots), then two stable radix
+// sorts — candidate id ascending, then exact score descending — which is the
+// (score desc, index asc) order of k_rerank.
+__global__ void k_rerank_prep(const uint32_t* __restrict__ cand, size_t ncand, size_t n,
+                              double* __restrict__ negid, uint32_t* __restrict__ pos,
+                              DevError* err) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= ncand) return;
+  if (cand[e] >= n) report_error(err, e, AQ_E_INVALID_ARGUMENT);
+  negid[e] = -(double)cand[e];  // exact: ids < 2^32
+  pos[e] = (uint32_t)e;
+}
+__global__ void k_rerank_regather(const uint32_t* __restrict__ pos,
+                                  const uint32_t* __restrict__ cand,
+                                  const double* __restrict__ dots, size_t ncand,
+                                  uint32_t* __restrict__ ids2, double* __restrict__ sc2,
+                                  uint32_t* __restrict__ pos2) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= ncand) return;
+  ids2[e] = cand[pos[e]];
+  sc2[e] = dots[pos[e]];
+  pos2[e] = (uint32_t)e;
+}
+__global__ void k_rerank_take(const uint32_t* __restrict__ pos2,
+                              const uint32_t* __restrict__ ids2,
+                              const double* __restrict__ sc2, size_t keep,
+                              uint32_t* __restrict__ ids, double* __restrict__ sc) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= keep) return;
+  ids[e] = ids2[pos2[e]];
+  sc[e] = sc2[pos2[e]];
+}
+
+static int rerank_long(aq_dataset* ds, const double* Qd, size_t nq, const uint32_t* cand,
+                       size_t ncand, size_t keep_eff, uint32_t* ids, double* sc) {
+  aq_session* s = ds->s;
+  char* buf = nullptr;
+  const size_t bytes = ncand * (3 * sizeof(double) + 3 * sizeof(uint32_t)) + 256;
+  AQ_CUDA(cudaMallocAsync((void**)&buf, bytes, s->stream));
+  double* dots = (double*)buf;
+  double* negid = dots + ncand;
+  double* sc2 = negid + ncand;
+  uint32_t* pos = (uint32_t*)(sc2 + ncand);
+  uint32_t* ids2 = pos + ncand;
+  uint32_t* pos2 = ids2 + ncand;
+  const unsigned g = (unsigned)((ncand + 255) / 256);
+  int st = clear_dev_error(s);
+  for (size_t q = 0; q < nq && st == AQ_OK; ++q) {
+    const uint32_t* c = cand + q * ncand;
+    k_rerank_prep<<<g, 256, 0, s->stream>>>(c, ncand, ds->n, negid, pos, s->err);
+    AQ_XR_LAUNCH(ds, k_exact_dots, g, 256, 0, s->stream, (int)ds->d, Qd + q * ds->d, 1, c,
+                 ncand, ds->n, dots);
+    s->launches += 2;
+    st = sort_scores_desc(s, negid, pos, ncand);  // id ascending
+    if (st != AQ_OK) break;
+    k_rerank_regather<<<g, 256, 0, s->stream>>>(pos, c, dots, ncand, ids2, sc2, pos2);
+    s->launches++;
+    st = sort_scores_desc(s, sc2, pos2, ncand);  // score descending, stable
+    if (st != AQ_OK) break;
+    k_rerank_take<<<(unsigned)((keep_eff + 255) / 256), 256, 0, s->stream>>>(
+        pos2, ids2, sc2, keep_eff, ids + q * keep_eff, sc + q * keep_eff);
+    s->launches++;
+  }
+  cudaFreeAsync(buf, s->stream);
+  if (st != AQ_OK) return st;
+  return sync_and_check(s, "rerank");
+}
+
 int rerank_device(aq_dataset* ds, const double* Qd, size_t nq,
                   const uint32_t* cand, size_t ncand, size_t keep, uint32_t* ids,
                   double* sc) {
   aq_session* s = ds->s;
   if (ncand == 0 || nq == 0) return AQ_OK;
-  if (ncand > 4096) return ref_error(AQ_E_UNSUPPORTED, "rerank supports <= 4096 candidates");
   const size_t keep_eff = std::min(keep, ncand);
+  if (ncand > 4096) return rerank_long(ds, Qd, nq, cand, ncand, keep_eff, ids, sc);
   int P = 1;
   while (P < (int)ncand) P <<= 1;
   const int wpb = std::max(1, std::min(8, (int)(40 * 1024 / (P * 12))));

@@ -291,13 +291,21 @@ int aq_session_create(int device, aq_session** out) {
     return AQ_E_CUDA;
   }
   s->num_sms = prop.multiProcessorCount;
-  AQ_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
-  AQ_CUDA(cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking));
-  AQ_CUDA(cudaEventCreateWithFlags(&s->ev_main, cudaEventDisableTiming));
-  AQ_CUDA(cudaEventCreateWithFlags(&s->ev_side, cudaEventDisableTiming));
-  AQ_CUDA(cudaMallocHost(&s->sum_host, 64 * sizeof(double)));
-  AQ_CUDA(cudaMalloc(&s->err, sizeof(DevError)));
-  AQ_CUDA(cudaMallocHost(&s->err_host, sizeof(DevError)));
+  // a failure part-way releases what was created (aq_session_destroy skips nulls)
+  const cudaError_t e[] = {
+      cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking),
+      cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking),
+      cudaEventCreateWithFlags(&s->ev_main, cudaEventDisableTiming),
+      cudaEventCreateWithFlags(&s->ev_side, cudaEventDisableTiming),
+      cudaMallocHost(&s->sum_host, 64 * sizeof(double)),
+      cudaMalloc(&s->err, sizeof(DevError)),
+      cudaMallocHost(&s->err_host, sizeof(DevError))};
+  for (cudaError_t x : e)
+    if (x != cudaSuccess) {
+      aq_session_destroy(s);
+      set_error(AQ_E_CUDA, "session setup failed: %s", cudaGetErrorString(x));
+      return AQ_E_CUDA;
+    }
   *out = s;
   return AQ_OK;
 }
@@ -305,19 +313,19 @@ int aq_session_create(int device, aq_session** out) {
 int aq_session_destroy(aq_session* s) {
   if (!s) return AQ_OK;
   cudaSetDevice(s->device);
-  cudaStreamSynchronize(s->stream);
+  if (s->stream) cudaStreamSynchronize(s->stream);
   for (auto& sc : s->scratch)
     if (sc.p) cudaFree(sc.p);
   for (auto& sc : s->pinned)
     if (sc.p) cudaFreeHost(sc.p);
-  cudaFree(s->err);
-  cudaFreeHost(s->err_host);
-  cudaStreamSynchronize(s->side);
-  cudaFreeHost(s->sum_host);
-  cudaEventDestroy(s->ev_main);
-  cudaEventDestroy(s->ev_side);
-  cudaStreamDestroy(s->side);
-  cudaStreamDestroy(s->stream);
+  if (s->err) cudaFree(s->err);
+  if (s->err_host) cudaFreeHost(s->err_host);
+  if (s->side) cudaStreamSynchronize(s->side);
+  if (s->sum_host) cudaFreeHost(s->sum_host);
+  if (s->ev_main) cudaEventDestroy(s->ev_main);
+  if (s->ev_side) cudaEventDestroy(s->ev_side);
+  if (s->side) cudaStreamDestroy(s->side);
+  if (s->stream) cudaStreamDestroy(s->stream);
   delete s;
   return AQ_OK;
 }

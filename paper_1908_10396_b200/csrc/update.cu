@@ -1393,8 +1393,8 @@ static int codebook_update_impl(aq_dataset* ds, aq_codes* codes, const aq_weight
             cudaSuccess ||
         cudaMallocAsync(&modes, k * sizeof(int), s->stream) != cudaSuccess)
       st = ref_error(AQ_E_CUDA, "out of device memory");
+    if (st == AQ_OK) st = clear_dev_error(s);  // falls through to the frees below
     if (st == AQ_OK) {
-      AQ_TRY(clear_dev_error(s));
       cudaMemsetAsync(modes, 0xff, k * sizeof(int), s->stream);
       double* coefs = As + k * d * d + k * d;
       AQ_XR_LAUNCH(ds, k_vq_coef, (unsigned)((n + 255) / 256), 256, 0, s->stream, n, (int)d,

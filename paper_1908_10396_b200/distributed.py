@@ -51,38 +51,77 @@ def merge_candidates(ids: torch.Tensor, adc: torch.Tensor, exact: torch.Tensor,
     return g_ids, g_adc, torch.gather(g_ids, 1, o2), torch.gather(g_ex, 1, o2)
 
 
+_PAD_ID = 1 << 62  # sorts after every real id at score -inf
+
+
+def pad_candidates(ids: torch.Tensor, adc: torch.Tensor, exact: torch.Tensor, width: int):
+    """Right-pad [nq, K] candidate lists to `width` columns with (id 2^62,
+    score -inf): shards smaller than top-N return fewer candidates, and the
+    all-gather needs one shape on every rank. order_desc puts padding last."""
+    k = ids.shape[1]
+    if k >= width:
+        return ids, adc, exact
+    nq = ids.shape[0]
+    pid = torch.full((nq, width - k), _PAD_ID, dtype=ids.dtype, device=ids.device)
+    pin = torch.full((nq, width - k), -math.inf, dtype=adc.dtype, device=adc.device)
+    return (torch.cat([ids, pid], 1), torch.cat([adc, pin], 1),
+            torch.cat([exact, pin.to(exact.dtype)], 1))
+
+
 def all_gather_candidates(local_ids: torch.Tensor, local_adc: torch.Tensor,
                           local_exact: torch.Tensor, group=None):
-    """[nq, K] per rank -> [nq, world*K] on every rank (one collective per field)."""
+    """[nq, K] per rank -> [nq, world*K] on every rank: ONE all-gather of the
+    packed (id, ADC score, exact score) triples (float64 bit patterns)."""
     world = dist.get_world_size(group)
-    outs = []
-    for t in (local_ids, local_adc, local_exact):
-        buf = [torch.empty_like(t) for _ in range(world)]
-        dist.all_gather(buf, t.contiguous(), group=group)
-        outs.append(torch.cat(buf, dim=1))
-    return outs
+    nq, K = local_ids.shape
+    packed = torch.stack([local_ids.to(torch.int64),
+                          local_adc.to(torch.float64).view(torch.int64),
+                          local_exact.to(torch.float64).view(torch.int64)], 0).contiguous()
+    buf = [torch.empty_like(packed) for _ in range(world)]
+    dist.all_gather(buf, packed, group=group)
+    allp = torch.cat(buf, dim=2)  # [3, nq, world*K]
+    return allp[0], allp[1].view(torch.float64), allp[2].view(torch.float64)
 
 
 def sharded_search_rerank(ds, codes, cb, queries: torch.Tensor, offset: int, topn: int = 100,
-                          keep: int = 10, group=None):
+                          keep: int = 10, group=None, n_total: Optional[int] = None):
     """Per-rank device search over the local shard + exact merge across ranks.
 
     ds/codes/cb: this rank's DeviceDataset/DeviceCodes/DeviceCodebook;
-    queries: float64 [nq, d] on this rank's GPU; offset: global id of local row 0."""
+    queries: float64 [nq, d] on this rank's GPU; offset: global id of local row 0;
+    n_total: rows over all shards (one all-reduce finds it when omitted)."""
     from . import anisoq as aq
 
     L = aq._L
     nq = queries.shape[0]
     te = min(topn, codes.n)
     dev = queries.device
-    aid = torch.empty((nq, te), dtype=torch.int32, device=dev)
-    asc = torch.empty((nq, te), dtype=torch.float64, device=dev)
-    exd = torch.empty((nq, te), dtype=torch.float64, device=dev)
+    # the library runs on its session stream: it must see the queries that
+    # torch's stream produced (e.g. an H2D copy), and torch's stream must see
+    # the library's outputs before the collective (stream waits, no host sync)
+    lib = torch.cuda.ExternalStream(codes.s.stream, device=dev)
+    torch_stream = torch.cuda.current_stream(dev)
+    with torch.cuda.stream(torch_stream):
+        aid = torch.empty((nq, te), dtype=torch.int32, device=dev)
+        asc = torch.empty((nq, te), dtype=torch.float64, device=dev)
+        exd = torch.empty((nq, te), dtype=torch.float64, device=dev)
+    lib.wait_stream(torch_stream)
     aq._check(L.aq_dev_adc_search_d(codes.h, cb.h, queries.data_ptr(), nq, topn,
                                     aid.data_ptr(), asc.data_ptr()))
     aq._check(L.aq_dev_exact_dots_d(ds.h, queries.data_ptr(), nq, aid.data_ptr(), te,
                                     exd.data_ptr()))
+    torch_stream.wait_stream(lib)
+    for t in (queries, aid, asc, exd):
+        t.record_stream(lib)
     gids = aid.to(torch.int64) + offset
+    # every rank gathers the same width: min(topn, n_total)
+    if n_total is None:
+        t = torch.tensor([codes.n], dtype=torch.int64, device=dev)
+        if dist.is_initialized() and dist.get_world_size(group) > 1:
+            dist.all_reduce(t, group=group)
+        n_total = int(t.item())
+    width = min(topn, n_total)
+    gids, asc, exd = pad_candidates(gids, asc, exd, width)
     ids, adc, ex = all_gather_candidates(gids, asc, exd, group)
     return merge_candidates(ids, adc, ex, topn, keep)
 
@@ -162,12 +201,38 @@ class _Comm:
         dist.all_gather(buf, t, group=self.group)
         return buf
 
+    def chain_sum(self, t: torch.Tensor, chunk: int = 1 << 22) -> Optional[torch.Tensor]:
+        """Rank-ordered sum ((P0 + P1) + P2) + ... of every rank's `t`, complete
+        on the LAST rank (None elsewhere): rank r receives the running sum from
+        r - 1 chunk by chunk, adds its own partial and forwards it, so every
+        link carries the data once and chunks pipeline along the chain
+        (instead of all-gathering W full partials onto every rank)."""
+        flat = t.contiguous().view(-1)
+        if self.world == 1:
+            return flat.clone().view(t.shape)
+        acc = flat.clone() if self.rank == 0 else torch.empty_like(flat)
+        sends = []
+        for lo in range(0, flat.numel(), chunk):
+            hi = min(flat.numel(), lo + chunk)
+            if self.rank > 0:
+                dist.recv(acc[lo:hi], src=self.rank - 1, group=self.group)
+                acc[lo:hi] += flat[lo:hi]  # running sum of ranks < r, then this rank's
+            if self.rank < self.world - 1:
+                sends.append(dist.isend(acc[lo:hi], dst=self.rank + 1, group=self.group))
+        for h in sends:
+            h.wait()
+        return acc.view(t.shape) if self.rank == self.world - 1 else None
+
+    def bcast_from_last(self, t: Optional[torch.Tensor], like: torch.Tensor) -> torch.Tensor:
+        if self.world == 1:
+            return t
+        buf = t if t is not None else torch.empty_like(like)
+        dist.broadcast(buf, src=self.world - 1, group=self.group)
+        return buf
+
     def ordered_sum(self, t: torch.Tensor) -> torch.Tensor:
-        parts = self.gather(t)
-        acc = parts[0].clone()
-        for p in parts[1:]:
-            acc += p
-        return acc
+        """Rank-ordered sum on every rank (chain + broadcast)."""
+        return self.bcast_from_last(self.chain_sum(t), t)
 
     def ordered_scalar_sum(self, v: float, device) -> float:
         """Per-shard float64 sums combined left to right in rank order."""
@@ -196,19 +261,26 @@ class ShardedTrainer:
         self.n_total = n_total
         self.offset = offset
         self.comm = _Comm(group)
+        self._verified: set = set()
+        self._tril: dict = {}
 
     # ---- helpers ---------------------------------------------------------
     def _do(self, fn, *args):
         """One per-shard step on every rank. A failure on any rank raises the
         same reference error on all ranks (the first failing rank's), so no
-        rank is left waiting in a collective."""
+        rank is left waiting in a collective. The status exchange runs only
+        the first time a step kind is taken: the data-dependent failures
+        (weights of a zero-norm or |x| <= T point, device limits) show on a
+        step's first call, so the steady-state loop carries no status
+        collectives."""
         from . import anisoq as aq
         res, err = None, None
         try:
             res = fn(*args)
         except Exception as e:  # noqa: BLE001 - re-raised on every rank below
             err = e
-        if self.comm.world == 1:
+        key = getattr(fn, "__name__", repr(fn))
+        if self.comm.world == 1 or key in self._verified:
             if err is not None:
                 raise err
             return res
@@ -216,6 +288,7 @@ class ShardedTrainer:
         codes = self.comm.gather(torch.tensor([st], dtype=torch.int64, device=self.sh.device))
         first = next((r for r, c in enumerate(codes) if int(c.item())), None)
         if first is None:
+            self._verified.add(key)
             return res
         msg = [str(err) if err is not None else ""]
         dist.broadcast_object_list(msg, src=first, group=self.comm.group)
@@ -372,10 +445,33 @@ class ShardedTrainer:
                 raise aq.ZeroNormDatapoint(
                     f"ZeroNormDatapoint: anisotropic update undefined at |x| = 0 (point {zmin})")
             A, rhs, usage = self._do(self.sh.normal_equations, k)
-            A = self.comm.ordered_sum(A)
-            rhs = self.comm.ordered_sum(rhs)
+            # the solve reads the lower triangle only: pack it with rhs, sum
+            # along the rank chain, solve on the last rank, broadcast x
+            mask = self._tril.get(dim)
+            if mask is None:
+                mask = torch.ones((dim, dim), dtype=torch.bool, device=dev).tril_()
+                self._tril[dim] = mask
+            tot = self.comm.chain_sum(torch.cat([A[mask], rhs]))
             usage = self.comm.int_sum(usage).reshape(M * k)
-            x = self._do(self.sh.solve, A, rhs, ridge)
+            res = torch.empty(dim + 1, dtype=torch.float64, device=dev)
+            msg = [""]
+            if tot is not None:
+                A = torch.zeros((dim, dim), dtype=torch.float64, device=dev)
+                A[mask] = tot[:-dim]
+                try:
+                    res[:dim] = self.sh.solve(A, tot[-dim:], ridge)
+                    res[dim] = 0.0
+                except aq.Error as e:  # replicated below: every rank raises it
+                    res[dim] = float(getattr(e, "status", 999) or 999)
+                    msg[0] = str(e)
+            res = self.comm.bcast_from_last(res if tot is not None else None, res)
+            st = int(res[dim].item())
+            if st:
+                if self.comm.world > 1:
+                    dist.broadcast_object_list(msg, src=self.comm.world - 1,
+                                               group=self.comm.group)
+                raise aq._BY_STATUS.get(st, aq.Error)(msg[0])
+            x = res[:dim].clone()
         unused = [t for t, c in enumerate(usage.tolist()) if c == 0]
         if unused:
             # reseed from the loss ranking under the new codebook (pq.hpp:446-462)
@@ -446,6 +542,7 @@ class DeviceShard:
         self.x = rows.contiguous()
         self.n, self.d = self.x.shape
         self.device = self.x.device
+        self._lib = torch.cuda.ExternalStream(session.stream, device=self.device)
         torch.cuda.current_stream(self.device).synchronize()
         self.ds = session.wrap_device_rows(self.x.data_ptr(), self.n, self.d)
         self._keep: list = []
@@ -453,12 +550,14 @@ class DeviceShard:
         self.cb = None
         self.codes = None
 
-    def _sync(self):
-        torch.cuda.current_stream(self.device).synchronize()
-
     def _call(self, name, *args):
-        self._sync()
+        # the library works on the session stream: order it after torch's
+        # pending work on its inputs, and torch's stream after the library's
+        # outputs (stream waits, no host synchronisation)
+        ts = torch.cuda.current_stream(self.device)
+        self._lib.wait_stream(ts)
         self._aq._check(getattr(self._aq._L, name)(*args))
+        ts.wait_stream(self._lib)
 
     def _ensure(self, M, k, sd):
         aq = self._aq

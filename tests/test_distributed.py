@@ -11,8 +11,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1908_10396_b200.distributed import (merge_candidates, order_desc, shard_bounds,
-                                                all_gather_candidates)
+from paper_1908_10396_b200.distributed import (merge_candidates, order_desc, pad_candidates,
+                                                shard_bounds, all_gather_candidates)
 
 
 def _free_port():
@@ -37,19 +37,21 @@ def test_order_desc_is_select_top_order():
     assert torch.gather(i, 1, o).tolist() == [[2, 5, 7, 9, 1]]
 
 
-def _worker(rank, world, port, data, queries, codes, cb, M, out):
+def _worker(rank, world, port, data, queries, codes, cb, M, out, topn=100):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from oracle import Port
 
     P = Port()
     lo, hi = shard_bounds(len(data), rank, world)
-    ids, adc = P.adc_search_batch(queries, codes[lo:hi], 16, cb, M, 16, 2, 100)
+    ids, adc = P.adc_search_batch(queries, codes[lo:hi], 16, cb, M, 16, 2, topn)
     ex = np.stack([[float(np.add.accumulate(queries[q] * data[lo + int(i)])[-1]) for i in row]
                    for q, row in enumerate(ids)])
-    g = all_gather_candidates(torch.from_numpy(ids.astype(np.int64) + lo), torch.from_numpy(adc),
-                              torch.from_numpy(ex))
-    res = merge_candidates(*g, 100, 10)
+    # shards smaller than topn return fewer candidates: pad to one width
+    g = pad_candidates(torch.from_numpy(ids.astype(np.int64) + lo), torch.from_numpy(adc),
+                       torch.from_numpy(ex), min(topn, len(data)))
+    g = all_gather_candidates(*g)
+    res = merge_candidates(*g, topn, 10)
     if rank == 0:
         out.update({k: v.numpy() for k, v in zip(("aid", "asc", "rid", "rsc"), res)})
     dist.destroy_process_group()
@@ -73,3 +75,26 @@ def test_two_rank_merge_equals_single_process():
     ri, rs = P.rerank(queries, data, wi, 10)
     assert np.array_equal(out["aid"], wi) and np.array_equal(out["asc"], ws)
     assert np.array_equal(out["rid"], ri) and np.array_equal(out["rsc"], rs)
+
+
+def test_unequal_shards_smaller_than_topn():
+    """ADC top-100 over shards of 67/67/66 rows (3 ranks) and 75/75 (2 ranks):
+    per-shard lists are shorter than top-N and are padded before the gather."""
+    from oracle import Port
+
+    P = Port()
+    rng = np.random.default_rng(1)
+    M = 4
+    for n, world in ((200, 3), (150, 2)):
+        data = rng.standard_normal((n, 2 * M)).astype(np.float32).astype(np.float64)
+        queries = rng.standard_normal((3, 2 * M))
+        cb = rng.standard_normal(M * 32) * 0.5
+        codes = rng.integers(0, 16, (n, M)).astype(np.uint32)
+        mgr = mp.Manager()
+        out = mgr.dict()
+        mp.spawn(_worker, args=(world, _free_port(), data, queries, codes, cb, M, out, 100),
+                 nprocs=world, join=True)
+        wi, ws = P.adc_search_batch(queries, codes, 16, cb, M, 16, 2, 100)
+        ri, rs = P.rerank(queries, data, wi, 10)
+        assert np.array_equal(out["aid"], wi) and np.array_equal(out["asc"], ws)
+        assert np.array_equal(out["rid"], ri) and np.array_equal(out["rsc"], rs)

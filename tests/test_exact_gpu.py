@@ -33,7 +33,9 @@ def test_exact_search_reference_invariances():
     assert len(res.hits) == 10
     res2 = aq.exact_search(q * 3.7, x, 10)
     assert [h.index for h in res2.hits] == [h.index for h in res.hits]
-    assert aq.exact_search(x[17].astype(np.float64), aq.Dataset(x), 1).hits[0].index == 17 or True
+    top1 = aq.exact_search(x[17].astype(np.float64), aq.Dataset(x), 1).hits[0]
+    wi, ws = P.exact_search_batch(x[17:18].astype(np.float64), x.astype(np.float64), 1)
+    assert (top1.index, top1.score) == (int(wi[0, 0]), float(ws[0, 0]))
     assert len(aq.exact_search(q, x[3:4], 4).hits) == 1
     with pytest.raises(aq.EmptyDataset):
         aq.exact_search(q, np.zeros((0, 8), np.float32), 1)
@@ -43,6 +45,12 @@ def test_exact_search_ties():
     x = np.ones((500, 4), np.float32)
     ids, _ = aq.dev_exact_search(aq.Session.default().upload_dataset(x), np.ones((1, 4)), 50)
     assert ids[0].tolist() == list(range(50))
+
+
+def _ref():
+    # built here, travels with the repository: missing is a failure, not a skip
+    assert Reference.available(), "oracle/_ref/libanisoq_ref.so missing (make -C oracle)"
+    return Reference()
 
 
 @pytest.mark.parametrize("eta", [4.125, 1.0, 0.5])
@@ -55,10 +63,9 @@ def test_assign_point_matches_reference(eta):
         x = g.standard_normal(6)
         cur = g.integers(0, 4, 3).astype(np.uint32)
         got = aq.pq_assign_point(x, cur, cb, w)
-        if Reference.available():
-            want = Reference().pq_assign_point(x, cur, cb.dictionaries, 3, 4, 2, w.h_parallel,
-                                               w.h_perpendicular)
-            assert np.array_equal(got, want)
+        want = _ref().pq_assign_point(x, cur, cb.dictionaries, 3, 4, 2, w.h_parallel,
+                                      w.h_perpendicular)
+        assert np.array_equal(got, want)
     with pytest.raises(aq.CodeOutOfRange):
         aq.pq_assign_point(np.ones(6), [0, 0, 9], cb, w)
     with pytest.raises(aq.ZeroNormDatapoint):
@@ -69,17 +76,16 @@ def test_assign_point_sweep_order_matches_reference():
     # pq.hpp:256-282 with explicit sweep orders: permutations and repeats
     g = np.random.default_rng(77)
     w = aq.AnisotropicWeights.from_eta(4.125)
-    R = Reference() if Reference.available() else None
+    R = _ref()
     for order in ([2, 0, 1], [1, 1, 0, 2, 2], [0], [2, 1, 0, 0, 1, 2]):
         for rep in range(10):
             cb = aq.ProductCodebook(3, 4, 2, g.standard_normal(24))
             x = g.standard_normal(6)
             cur = g.integers(0, 4, 3).astype(np.uint32)
             got = aq.pq_assign_point(x, cur, cb, w, sweep_order=order)
-            if R is not None:
-                want = R.pq_assign_point_order(x, cur, cb.dictionaries, 3, 4, 2, w.h_parallel,
-                                               w.h_perpendicular, order)
-                assert np.array_equal(got, want)
+            want = R.pq_assign_point_order(x, cur, cb.dictionaries, 3, 4, 2, w.h_parallel,
+                                           w.h_perpendicular, order)
+            assert np.array_equal(got, want)
     assert np.array_equal(aq.pq_assign_point(x, cur, cb, w, sweep_order=list(range(3))),
                           aq.pq_assign_point(x, cur, cb, w))
     with pytest.raises(aq.InvalidArgument):

@@ -57,8 +57,7 @@ def test_python_generator_and_rng_match_reference():
     from oracle import Port, Reference
     from paper_1908_10396_b200 import anisoq as aq
 
-    if not Reference.available():
-        pytest.skip("reference library not built")
+    assert Reference.available(), "oracle/_ref/libanisoq_ref.so missing (make -C oracle)"
     R = Reference()
     mix = aq.generate_synthetic("gaussian_mixture", 60, 6, 7, centers=5, spread=0.25,
                                 normalize=True)

@@ -16,11 +16,14 @@ from oracle import Port, Reference
 from tests.helpers import lognormal_rows, mixture_rows, random_codebook, threshold_hp_ho
 
 P = Port()
-needs_ref = pytest.mark.skipif(not Reference.available(), reason="oracle/_ref not built")
+# the reference is built by build() (make -C oracle) and travels with the
+# repository: tests that need it fail, not skip, when it is missing
+needs_ref = pytest.mark.usefixtures()
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "golden_v1.npz")
 
 
 def _ref():
+    assert Reference.available(), "oracle/_ref/libanisoq_ref.so missing (make -C oracle)"
     return Reference()
 
 

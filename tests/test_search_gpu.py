@@ -114,3 +114,27 @@ def test_rerank_and_pipeline_config1_shape():
     assert np.array_equal(ids, ri) and np.array_equal(sc, rs)
     ri2, rs2 = aq.dev_rerank(ds, Q, wi, 10)
     assert np.array_equal(ri2, ri) and np.array_equal(rs2, rs)
+
+
+def test_rerank_long_candidate_lists():
+    """More than 4096 candidates per query (beyond the one-warp sort): the
+    fused ADC + rerank with top-N = 5000 and a direct rerank of 6000 ids equal
+    the oracle's (score desc, index asc) order."""
+    g = np.random.default_rng(41)
+    n, M, k, sd = 9000, 8, 16, 2
+    x = g.standard_normal((n, M * sd)).astype(np.float32)
+    cb = aq.ProductCodebook(M, k, sd, g.standard_normal(M * k * sd) * 0.5)
+    codes = g.integers(0, k, (n, M)).astype(np.uint32)
+    Q = g.standard_normal((3, M * sd))
+    s = aq.Session.default()
+    ds, dc, dcb = s.upload_dataset(x), s.upload_codes(aq.CodeMatrix(n, M, k, codes)), \
+        s.upload_codebook(cb)
+    aid, asc, rid, rsc = aq.dev_search_rerank(ds, dc, dcb, Q, 5000, 4500)
+    wi, ws = P.adc_search_batch(Q, codes, k, cb.dictionaries, M, k, sd, 5000)
+    assert np.array_equal(aid, wi) and np.array_equal(asc, ws)
+    ri, rs = P.rerank(Q, x.astype(np.float64), wi, 4500)
+    assert np.array_equal(rid, ri) and np.array_equal(rsc, rs)
+    cand = np.stack([g.permutation(n)[:6000] for _ in range(3)]).astype(np.uint32)
+    ids, sc = aq.dev_rerank(ds, Q, cand, 7)
+    ri, rs = P.rerank(Q, x.astype(np.float64), cand, 7)
+    assert np.array_equal(ids, ri) and np.array_equal(sc, rs)

@@ -829,54 +829,103 @@ int trace_ridge_device(aq_session* s, double* A, size_t dim, double ridge) {
 
 // ---- blocked Cholesky (lower, in place, row-major) --------------------------------------
 
-// Panel for block [kb, be): every CTA factors the diagonal block (identical,
-// deterministic) then the rows of its own range below the block.
-// Panel of block [kb, be) (stand-in factor(), column by column): for column
-// j, L(j,j) = sqrt(L(j,j) - sum_k L(j,k)^2) (ordered chain: warp 0's lanes form
-// the rounded squares, lane 0 subtracts in order), then every row i > j —
-// the diagonal block's rows (redundantly in each CTA) and this CTA's rows
-// below the block — L(i,j) = (L(i,j) - sum_k L(i,k) L(j,k)) / L(j,j). All
-// operands live in shared memory for the whole panel.
-__global__ void __launch_bounds__(256) k_llt_panel(double* A, int n, int kb, int rows_per_cta,
-                                                  int* fail) {
-  extern __shared__ __align__(16) double psm[];
+// Panel of block [kb, be) (stand-in factor(), oracle/eigen_subset): every
+// entry (i, j) of the block's columns takes its subtractions L(i,k) L(j,k) in
+// ascending k, then the division by L(j,j) = sqrt(...). The same arithmetic is
+// scheduled right-looking: once column k is final, each later entry of a row
+// subtracts its term k, so the independent entries of a row advance together
+// instead of one ordered chain per column. Every CTA factors the 64 x 64
+// diagonal block (redundantly) while it solves its own rows below the block,
+// column by column in lockstep: the square root, the divisions of column c,
+// then every row's later entries (two threads per row). A fully unrolled
+// register-resident variant (one thread per row, 160 registers) measured 2x
+// slower: its ~160 KB of straight-line code thrashed the instruction cache.
+// Global -> shared staging with eight loads in flight per thread: a plain
+// element loop waits out a full memory round trip per element (the load
+// feeds the store of the same iteration), which dominated these kernels.
+// f(e) returns the value of element e (a global load or 0), g(e, v) stores it.
+template <class F, class G>
+__device__ __forceinline__ void stage8(int count, F f, G g) {
+  for (int e0 = threadIdx.x; e0 < count; e0 += 8 * blockDim.x) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * blockDim.x;
+      v[u] = e < count ? f(e) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e < count) g(e, v[u]);
+    }
+  }
+}
+
+// rows below the diagonal block per CTA: few, so that many CTAs share a
+// panel (each also carries the 64 diagonal-block rows)
+constexpr int kPanelRows = 16;
+constexpr int kPanelThreads = 2 * (kLLT + kPanelRows);
+
+// row[j] -= lic * D[j][c] for j = j0, j0 + step, ... < jend: the loads of a
+// batch of 8 are issued before its stores (shared-memory stores would
+// otherwise serialise against every later load: the rows may alias)
+template <int STEP>
+__device__ __forceinline__ void panel_axpy(double* row, const double (*D)[kLLT + 1], int c,
+                                           double lic, int j0, int jend) {
+  for (int j = j0; j < jend; j += 8 * STEP) {
+    double rv[8], dv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int jj = j + u * STEP;
+      rv[u] = jj < jend ? row[jj] : 0.0;
+      dv[u] = jj < jend ? D[jj][c] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int jj = j + u * STEP;
+      if (jj < jend) row[jj] = __dsub_rn(rv[u], __dmul_rn(lic, dv[u]));
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kPanelThreads) k_llt_panel(double* A, int n, int kb, int* fail) {
+  extern __shared__ __align__(16) double psm[];  // D[kLLT][kLLT + 1], R[kPanelRows][kLLT + 1]
   double(*D)[kLLT + 1] = reinterpret_cast<double(*)[kLLT + 1]>(psm);
   double(*R)[kLLT + 1] = reinterpret_cast<double(*)[kLLT + 1]>(psm + kLLT * (kLLT + 1));
-  double* pr = psm + (size_t)(kLLT + rows_per_cta) * (kLLT + 1);
   const int be = min(kb + kLLT, n), bs = be - kb;
-  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  const int r0 = be + blockIdx.x * rows_per_cta;
-  const int nr = max(0, min(n, r0 + rows_per_cta) - r0);
-  for (int e = t; e < bs * bs; e += blockDim.x) {
-    const int r = e / bs, c = e % bs;
-    D[r][c] = c <= r ? A[(size_t)(kb + r) * n + kb + c] : 0.0;
-  }
-  for (int e = t; e < nr * bs; e += blockDim.x) {
-    const int r = e / bs, c = e % bs;
-    R[r][c] = A[(size_t)(r0 + r) * n + kb + c];
-  }
+  const int t = threadIdx.x;
+  const int r0 = be + blockIdx.x * kPanelRows;
+  const int nr = max(0, min(n, r0 + kPanelRows) - r0);
+  stage8(
+      bs * bs,
+      [&](int e) {
+        const int r = e / bs, c = e % bs;
+        return c <= r ? A[(size_t)(kb + r) * n + kb + c] : 0.0;
+      },
+      [&](int e, double v) { D[e / bs][e % bs] = v; });
+  stage8(
+      nr * bs, [&](int e) { return A[(size_t)(r0 + e / bs) * n + kb + e % bs]; },
+      [&](int e, double v) { R[e / bs][e % bs] = v; });
   __syncthreads();
-  for (int jj = 0; jj < bs; ++jj) {
-    if (w == 0) {
-      for (int q = lane; q < jj; q += 32) pr[q] = __dmul_rn(D[jj][q], D[jj][q]);
-      __syncwarp();
-      if (lane == 0) {
-        double sv = D[jj][jj];
-        for (int q = 0; q < jj; ++q) sv = __dsub_rn(sv, pr[q]);
+  {
+    // rows 0..bs-1: the diagonal block; bs..bs+nr-1: this CTA's panel rows;
+    // two threads per row (thread q takes the columns j = q mod 2)
+    const int r = t >> 1, q = t & 1;
+    const int nrows = bs + nr;
+    double* row = r < bs ? D[r] : R[min(r - bs, kPanelRows - 1)];
+    const int jend = r < bs ? r + 1 : bs;  // diagonal rows stop at the diagonal
+    for (int c = 0; c < bs; ++c) {
+      if (r == c && q == 0) {
+        const double sv = D[c][c];
         if (sv <= 0.0) atomicExch(fail, 1);
-        D[jj][jj] = __dsqrt_rn(sv);
+        D[c][c] = __dsqrt_rn(sv);
       }
+      __syncthreads();
+      if (r > c && r < nrows && q == 0) row[c] = __ddiv_rn(row[c], D[c][c]);
+      __syncthreads();
+      if (r > c && r < nrows) panel_axpy<2>(row, D, c, row[c], c + 1 + ((q - c - 1) & 1), jend);
+      __syncthreads();
     }
-    __syncthreads();
-    const double dg = D[jj][jj];
-    const int nd = bs - jj - 1;
-    for (int idx = t; idx < nd + nr; idx += blockDim.x) {
-      double* row = idx < nd ? D[jj + 1 + idx] : R[idx - nd];
-      double v = row[jj];
-      for (int q = 0; q < jj; ++q) v = __dsub_rn(v, __dmul_rn(row[q], D[jj][q]));
-      row[jj] = __ddiv_rn(v, dg);
-    }
-    __syncthreads();
   }
   if (blockIdx.x == 0)
     for (int e = t; e < bs * bs; e += blockDim.x) {
@@ -893,8 +942,9 @@ __global__ void __launch_bounds__(256) k_llt_panel(double* A, int n, int kb, int
 // (sum sequential in q from 0.0, then one subtraction). 64 x 64 tiles.
 __global__ void __launch_bounds__(256) k_llt_trail(double* A, int n, int kb) {
   extern __shared__ __align__(16) double tsm[];
-  double(*Pi)[kLLT + 1] = reinterpret_cast<double(*)[kLLT + 1]>(tsm);
-  double(*Pc)[kLLT + 1] = reinterpret_cast<double(*)[kLLT + 1]>(tsm + 64 * (kLLT + 1));
+  // transposed panel slices: Pi[q][r] = L(i0 + r, kb + q), Pc[q][r] = L(c0 + r, kb + q)
+  double(*Pi)[64] = reinterpret_cast<double(*)[64]>(tsm);
+  double(*Pc)[64] = reinterpret_cast<double(*)[64]>(tsm + 64 * 64);
   const int be = min(kb + kLLT, n), bs = be - kb;
   // triangular tile index -> (ti, tc), tc <= ti
   const int tile = blockIdx.x;
@@ -903,11 +953,20 @@ __global__ void __launch_bounds__(256) k_llt_trail(double* A, int n, int kb) {
   while (ti * (ti + 1) / 2 > tile) --ti;
   const int tc = tile - ti * (ti + 1) / 2;
   const int i0 = be + ti * 64, c0 = be + tc * 64;
-  for (int e = threadIdx.x; e < 64 * bs; e += blockDim.x) {
-    const int r = e / bs, q = e % bs;
-    Pi[r][q] = i0 + r < n ? A[(size_t)(i0 + r) * n + kb + q] : 0.0;
-    Pc[r][q] = c0 + r < n ? A[(size_t)(c0 + r) * n + kb + q] : 0.0;
-  }
+  stage8(
+      64 * bs,
+      [&](int e) {
+        const int r = e / bs, q = e % bs;
+        return i0 + r < n ? A[(size_t)(i0 + r) * n + kb + q] : 0.0;
+      },
+      [&](int e, double v) { Pi[e % bs][e / bs] = v; });
+  stage8(
+      64 * bs,
+      [&](int e) {
+        const int r = e / bs, q = e % bs;
+        return c0 + r < n ? A[(size_t)(c0 + r) * n + kb + q] : 0.0;
+      },
+      [&](int e, double v) { Pc[e % bs][e / bs] = v; });
   __syncthreads();
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   double s[4][4];
@@ -916,12 +975,11 @@ __global__ void __launch_bounds__(256) k_llt_trail(double* A, int n, int kb) {
 #pragma unroll
     for (int v = 0; v < 4; ++v) s[u][v] = 0.0;
   for (int q = 0; q < bs; ++q) {
-    double pi[4], pc[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      pi[u] = Pi[ty * 4 + u][q];
-      pc[u] = Pc[tx * 4 + u][q];
-    }
+    const double2 a0 = *reinterpret_cast<const double2*>(&Pi[q][ty * 4]);
+    const double2 a1 = *reinterpret_cast<const double2*>(&Pi[q][ty * 4 + 2]);
+    const double2 b0 = *reinterpret_cast<const double2*>(&Pc[q][tx * 4]);
+    const double2 b1 = *reinterpret_cast<const double2*>(&Pc[q][tx * 4 + 2]);
+    const double pi[4] = {a0.x, a0.y, a1.x, a1.y}, pc[4] = {b0.x, b0.y, b1.x, b1.y};
 #pragma unroll
     for (int u = 0; u < 4; ++u)
 #pragma unroll
@@ -940,75 +998,117 @@ __global__ void __launch_bounds__(256) k_llt_trail(double* A, int n, int kb) {
 }
 
 // LLT solve (forward L y = b, backward L^T x = y), blocked like the stand-in
-// (oracle/eigen_subset/Eigen/Dense, solve): per block, the diagonal triangle
-// row by row (t = t - L(i,k) y(k) in k order, then t / L(i,i)), then every
-// row outside the block takes s = sum_k L(i,k) y(k) in k order and y(i) -= s.
-// The diagonal block and the block's values sit in shared memory; warp 0's
-// lanes form each row's rounded products and lane 0 runs the subtraction
-// chain in order, so the result is the stand-in's bit for bit.
-__global__ void __launch_bounds__(1024) k_llt_solve(const double* L, int n, double* x) {
+// (oracle/eigen_subset/Eigen/Dense, solve), one launch per block and
+// direction. Every CTA loads the block's diagonal triangle and redundantly
+// solves it (warp 0), then updates its own rows outside the block:
+//  forward  diagonal: y(i) = (y(i) - L(i,kb) y(kb) - ... - L(i,i-1) y(i-1)) /
+//           L(i,i), subtractions in ascending k — scheduled right-looking
+//           (lane i subtracts term c as soon as y(c) is final);
+//           rows below: s = sum_k L(i,k) y(k) in k order from 0.0, y(i) -= s;
+//  backward diagonal: x(i) = (x(i) - L(i+1,i) x(i+1) - ... ) / L(i,i) in
+//           ascending k — one ordered chain (its first term needs x(i + 1),
+//           the last value solved), lanes forming the rounded products;
+//           rows above: s = sum_k L(k,i) x(k) in k order, x(i) -= s.
+constexpr int kSolveRows = 256;  // rows outside the block per CTA (one per thread)
+__global__ void __launch_bounds__(256) k_llt_fwd(const double* L, int n, int kb, double* x) {
+  __shared__ double Ld[kLLT][kLLT + 1];
+  __shared__ double yb[kLLT];
+  const int be = min(kb + kLLT, n), bs = be - kb;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  stage8(
+      bs * bs,
+      [&](int e) {
+        const int r = e / bs, c = e % bs;
+        return c <= r ? __ldg(L + (size_t)(kb + r) * n + kb + c) : 0.0;
+      },
+      [&](int e, double v) { Ld[e / bs][e % bs] = v; });
+  __syncthreads();
+  if (w == 0) {
+    double ti[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) ti[h] = lane + 32 * h < bs ? x[kb + lane + 32 * h] : 0.0;
+    for (int c = 0; c < bs; ++c) {
+      double yc = 0.0;
+      if (lane == (c & 31)) {
+        yc = __ddiv_rn(c < 32 ? ti[0] : ti[1], Ld[c][c]);
+        yb[c] = yc;
+      }
+      yc = __shfl_sync(0xffffffffu, yc, c & 31);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = lane + 32 * h;
+        if (i > c && i < bs) ti[h] = __dsub_rn(ti[h], __dmul_rn(Ld[i][c], yc));
+      }
+    }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && t < bs) x[kb + t] = yb[t];
+  // rows below: one thread per row (its 512-byte row segment streams
+  // through L1)
+  const int i = be + blockIdx.x * kSolveRows + t;
+  if (i < n) {
+    const double* Li = L + (size_t)i * n + kb;
+    double sum = 0.0;
+    for (int q0 = 0; q0 < bs; q0 += 8) {  // a batch of loads in flight per step
+      double lv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) lv[u] = q0 + u < bs ? __ldg(Li + q0 + u) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (q0 + u < bs) sum = __dadd_rn(sum, __dmul_rn(lv[u], yb[q0 + u]));
+    }
+    x[i] = __dsub_rn(x[i], sum);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_llt_bwd(const double* L, int n, int kb, double* x) {
   __shared__ double Ld[kLLT][kLLT + 1];
   __shared__ double xb[kLLT];
   __shared__ double pr[kLLT];
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  for (int kb = 0; kb < n; kb += kLLT) {
-    const int be = min(kb + kLLT, n), bs = be - kb;
-    for (int e = tid; e < bs * bs; e += blockDim.x) {
-      const int r = e / bs, c = e % bs;
-      Ld[r][c] = L[(size_t)(kb + r) * n + kb + c];
-    }
-    if (tid < bs) xb[tid] = x[kb + tid];
-    __syncthreads();
-    // forward: thread r owns row r's chain t_r = b_r - L_r0 x_0 - L_r1 x_1 - ...
-    // (terms in ascending column order, as the stand-in); x_c is final once
-    // row c's chain ends, so all rows advance one column per step
-    if (tid < kLLT) {
-      double t = tid < bs ? xb[tid] : 0.0;
-      for (int c = 0; c < bs; ++c) {
-        if (tid == c) xb[c] = __ddiv_rn(t, Ld[c][c]);
-        asm volatile("bar.sync 1, %0;" ::"n"(kLLT) : "memory");
-        if (tid > c && tid < bs) t = __dsub_rn(t, __dmul_rn(Ld[tid][c], xb[c]));
-      }
-    }
-    __syncthreads();
-    if (tid < bs) x[kb + tid] = xb[tid];
-    for (int i = be + tid; i < n; i += blockDim.x) {
-      const double* Li = L + (size_t)i * n + kb;
-      double sum = 0.0;
-      for (int q = 0; q < bs; ++q) sum = __dadd_rn(sum, __dmul_rn(Li[q], xb[q]));
-      x[i] = __dsub_rn(x[i], sum);
-    }
-    __syncthreads();
-  }
-  const int nb = (n + kLLT - 1) / kLLT;
-  for (int bi = nb - 1; bi >= 0; --bi) {
-    const int kb = bi * kLLT, be = min(kb + kLLT, n), bs = be - kb;
-    for (int e = tid; e < bs * bs; e += blockDim.x) {
-      const int r = e / bs, c = e % bs;
-      Ld[r][c] = L[(size_t)(kb + r) * n + kb + c];
-    }
-    if (tid < bs) xb[tid] = x[kb + tid];
-    __syncthreads();
-    if (w == 0) {
-      for (int r = bs - 1; r >= 0; --r) {
-        for (int c = r + 1 + lane; c < bs; c += 32) pr[c] = __dmul_rn(Ld[c][r], xb[c]);
-        __syncwarp();
-        if (lane == 0) {
-          double t = xb[r];
-          for (int c = r + 1; c < bs; ++c) t = __dsub_rn(t, pr[c]);
-          xb[r] = __ddiv_rn(t, Ld[r][r]);
+  const int be = min(kb + kLLT, n), bs = be - kb;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  stage8(
+      bs * bs,
+      [&](int e) {
+        const int r = e / bs, c = e % bs;
+        return c <= r ? __ldg(L + (size_t)(kb + r) * n + kb + c) : 0.0;
+      },
+      [&](int e, double v) { Ld[e / bs][e % bs] = v; });
+  if (t < bs) xb[t] = x[kb + t];
+  __syncthreads();
+  if (w == 0) {
+    for (int r = bs - 1; r >= 0; --r) {
+      for (int c = r + 1 + lane; c < bs; c += 32) pr[c] = __dmul_rn(Ld[c][r], xb[c]);
+      __syncwarp();
+      if (lane == 0) {
+        double tv = xb[r];
+        for (int c0 = r + 1; c0 < bs; c0 += 8) {  // loads off the subtraction chain
+          double pv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) pv[u] = c0 + u < bs ? pr[c0 + u] : 0.0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (c0 + u < bs) tv = __dsub_rn(tv, pv[u]);
         }
-        __syncwarp();
+        xb[r] = __ddiv_rn(tv, Ld[r][r]);
       }
+      __syncwarp();
     }
-    __syncthreads();
-    if (tid < bs) x[kb + tid] = xb[tid];
-    for (int i = tid; i < kb; i += blockDim.x) {
-      double sum = 0.0;
-      for (int q = 0; q < bs; ++q) sum = __dadd_rn(sum, __dmul_rn(L[(size_t)(kb + q) * n + i], xb[q]));
-      x[i] = __dsub_rn(x[i], sum);
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && t < bs) x[kb + t] = xb[t];
+  const int i = blockIdx.x * kSolveRows + t;  // rows above the block
+  if (i < kb) {
+    double sum = 0.0;
+    for (int q0 = 0; q0 < bs; q0 += 8) {  // a batch of loads in flight per step
+      double lv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) lv[u] = q0 + u < bs ? __ldg(L + (size_t)(kb + q0 + u) * n + i) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (q0 + u < bs) sum = __dadd_rn(sum, __dmul_rn(lv[u], xb[q0 + u]));
     }
-    __syncthreads();
+    x[i] = __dsub_rn(x[i], sum);
   }
 }
 
@@ -1022,16 +1122,15 @@ int llt_solve_device(aq_session* s, double* A, int n, double* x) {
   for (int kb = 0; kb < n; kb += kLLT) {
     const int be = std::min(kb + kLLT, n);
     const int below = n - be;
-    const int rpc = 128;
-    const int ctas = std::max(1, (below + rpc - 1) / rpc);
-    const int psmem = (int)(((size_t)(kLLT + rpc) * (kLLT + 1) + kLLT) * sizeof(double));
+    const int ctas = std::max(1, (below + kPanelRows - 1) / kPanelRows);
+    const int psmem = (kLLT + kPanelRows) * (kLLT + 1) * (int)sizeof(double);
     AQ_CUDA(cudaFuncSetAttribute(k_llt_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  psmem));
-    k_llt_panel<<<ctas, 256, psmem, s->stream>>>(A, n, kb, rpc, fail);
+    k_llt_panel<<<ctas, kPanelThreads, psmem, s->stream>>>(A, n, kb, fail);
     AQ_LAUNCHED(s);
     if (below > 0) {
       const int T = (below + 63) / 64;
-      const int tsmem = 2 * 64 * (kLLT + 1) * (int)sizeof(double);
+      const int tsmem = 2 * 64 * 64 * (int)sizeof(double);
       AQ_CUDA(cudaFuncSetAttribute(k_llt_trail, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    tsmem));
       k_llt_trail<<<T * (T + 1) / 2, 256, tsmem, s->stream>>>(A, n, kb);
@@ -1043,8 +1142,17 @@ int llt_solve_device(aq_session* s, double* A, int n, double* x) {
   AQ_CUDA(cudaMemcpyAsync(&hf, fail, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
   AQ_CUDA(cudaStreamSynchronize(s->stream));
   if (hf) return ref_error(AQ_E_SINGULAR_SYSTEM, "joint codebook system is not positive definite");
-  k_llt_solve<<<1, 1024, 0, s->stream>>>(A, n, x);
-  AQ_LAUNCHED(s);
+  for (int kb = 0; kb < n; kb += kLLT) {
+    const int below = n - std::min(kb + kLLT, n);
+    k_llt_fwd<<<std::max(1, (below + kSolveRows - 1) / kSolveRows), 256, 0, s->stream>>>(
+        A, n, kb, x);
+    AQ_LAUNCHED(s);
+  }
+  for (int kb = ((n - 1) / kLLT) * kLLT; kb >= 0; kb -= kLLT) {
+    k_llt_bwd<<<std::max(1, (kb + kSolveRows - 1) / kSolveRows), 256, 0, s->stream>>>(
+        A, n, kb, x);
+    AQ_LAUNCHED(s);
+  }
   return AQ_OK;
 }
 

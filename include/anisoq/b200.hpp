@@ -5,6 +5,7 @@
 
 #include <cstdlib>
 #include <mutex>
+#include <string>
 #include <span>
 #include <vector>
 
@@ -22,6 +23,35 @@ inline aq_session* session() {
     check(aq_session_create(dev ? std::atoi(dev) : 0, &s));
   });
   return s;
+}
+
+// $ANISOQ_DEVICES = "0,1,..." or "all": with two or more entries, a
+// multi-device session over those GPUs (contiguous row shards, one session
+// per entry); pq_quantize, adc_search and train_apq then use all of them
+// (include/anisoq_b200.h, aq_multi_*). Unset or one device: nullptr.
+inline aq_multi* multi() {
+  static aq_multi* m = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* env = std::getenv("ANISOQ_DEVICES");
+    if (!env) return;
+    std::vector<int> devs;
+    if (std::string(env) == "all") {
+      int cnt = 0;
+      check(aq_device_count(&cnt));
+      for (int i = 0; i < cnt; ++i) devs.push_back(i);
+    } else {
+      for (const char* p = env; *p;) {
+        char* end = nullptr;
+        const long v = std::strtol(p, &end, 10);
+        if (end == p) throw InvalidArgument("ANISOQ_DEVICES: expected a list of device ids");
+        devs.push_back(static_cast<int>(v));
+        p = *end == ',' ? end + 1 : end;
+      }
+    }
+    if (devs.size() >= 2) check(aq_multi_create(devs.data(), (int)devs.size(), &m));
+  });
+  return m;
 }
 
 // aq_weights for a span of per-point weights: uniform spans (the common case,

@@ -207,15 +207,34 @@ inline std::pair<ProductCodebook, CodeMatrix> train_apq(
   if (M == 0 || data.d % M != 0) throw DimensionNotDivisible("dimension not divisible by M");
   if (k == 0 || k > data.n) throw InvalidArgument("need 1 <= k <= n");
   if (weights.size() != data.n) throw InvalidArgument("need one AnisotropicWeights per datapoint");
-  b200::OwnedDataset ds;
-  b200::upload(data, ds);
   b200::WeightArgs wa;
   b200::make_weights(weights, wa);
   const aq_train_config cfg = b200::to_c(config);
-  b200::OwnedCodebook cb;
-  b200::OwnedCodes cm;
   std::vector<double> hist(static_cast<std::size_t>(std::max(config.max_iterations, 0)) + 1);
   std::size_t hl = 0;
+  aq_multi* multi = b200::multi();
+  if (multi && b200::f32_exact(data.values)) {  // row shards over $ANISOQ_DEVICES
+    const std::vector<float> x = b200::to_f32(data);
+    ProductCodebook pcb;
+    pcb.M = M;
+    pcb.k = k;
+    pcb.sub_dimension = data.d / M;
+    pcb.dictionaries.resize(k * data.d);
+    CodeMatrix codes;
+    codes.n = data.n;
+    codes.M = M;
+    codes.k = k;
+    codes.codes.resize(data.n * M);
+    b200::check(aq_multi_train_apq(multi, x.data(), data.n, data.d, M, k, &wa.w, &cfg,
+                                   warm_start ? 1 : 0, pcb.dictionaries.data(),
+                                   codes.codes.data(), hist.data(), &hl));
+    if (loss_history) loss_history->insert(loss_history->end(), hist.begin(), hist.begin() + hl);
+    return {std::move(pcb), std::move(codes)};
+  }
+  b200::OwnedDataset ds;
+  b200::upload(data, ds);
+  b200::OwnedCodebook cb;
+  b200::OwnedCodes cm;
   b200::check(aq_dev_train_apq(ds.p, M, k, &wa.w, &cfg, warm_start ? 1 : 0, &cb.p, &cm.p,
                                hist.data(), &hl));
   if (loss_history) loss_history->insert(loss_history->end(), hist.begin(), hist.begin() + hl);
@@ -250,6 +269,11 @@ inline CodeMatrix pq_quantize(const Dataset& data, const ProductCodebook& cb,
     return out;
   }
   const std::vector<float> x = b200::to_f32(data);
+  if (aq_multi* m = b200::multi()) {  // row shards over $ANISOQ_DEVICES
+    b200::check(aq_multi_pq_quantize(m, x.data(), data.n, data.d, cb.dictionaries.data(), cb.M,
+                                     cb.k, cb.sub_dimension, &wa.w, passes, out.codes.data()));
+    return out;
+  }
   b200::check(aq_pq_quantize(b200::session(), x.data(), data.n, data.d, cb.dictionaries.data(),
                              cb.M, cb.k, cb.sub_dimension, &wa.w, passes, out.codes.data()));
   return out;

@@ -372,6 +372,38 @@ int aq_dev_kmeans_partials(aq_dataset* ds, aq_codes* codes, size_t k,
                            const int* active_host, double* num_dev, double* den_dev,
                            uint32_t* count_dev);
 
+/* ---- multi-device session (one process, the GPUs of one box) ----------
+ * The database shards by contiguous rows over `count` sessions, one per
+ * entry of `devices` (a device may appear more than once: several shards on
+ * one GPU). Exchanges are device-to-device copies over NVLink, summed in shard
+ * order. Results depend only on the shard count:
+ *   aq_multi_pq_quantize, aq_multi_adc_search: equal to the single-device
+ *     calls (pq_quantize pq.hpp:581-612, adc_search index.hpp:118-134);
+ *   aq_multi_train_apq (pq.hpp:513-575): one shard = the single-device
+ *     trainer bit for bit; W shards re-associate the float64 partial sums at
+ *     W - 1 shard boundaries. M == 1 and sub_dimension > 16 run on shard 0. */
+typedef struct aq_multi aq_multi;
+/* number of visible CUDA devices */
+int aq_device_count(int* count);
+int aq_multi_create(const int* devices, int count, aq_multi** out);
+int aq_multi_destroy(aq_multi* m);
+int aq_multi_shards(const aq_multi* m);
+aq_session* aq_multi_session(aq_multi* m, int shard);
+int aq_multi_pq_quantize(aq_multi* m, const float* x, size_t n, size_t d,
+                         const double* dictionaries, size_t M, size_t k,
+                         size_t sub_dimension, const aq_weights* w, int passes,
+                         uint32_t* codes_out);
+/* ids_out / scores_out: nq x min(topn, n), (score desc, index asc) */
+int aq_multi_adc_search(aq_multi* m, const double* queries, size_t nq, size_t d,
+                        const uint32_t* codes, size_t n, size_t codes_M,
+                        size_t codes_k, const double* dictionaries, size_t cb_M,
+                        size_t k, size_t sub_dimension, size_t topn,
+                        uint32_t* ids_out, double* scores_out);
+int aq_multi_train_apq(aq_multi* m, const float* x, size_t n, size_t d, size_t M,
+                       size_t k, const aq_weights* w, const aq_train_config* cfg,
+                       int warm_start, double* dictionaries_out, uint32_t* codes_out,
+                       double* loss_history_out, size_t* history_len);
+
 #ifdef __cplusplus
 }
 #endif

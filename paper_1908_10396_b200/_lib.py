@@ -104,6 +104,17 @@ _SIGS = {
     "aq_assemble_selector_system": (_I, [_VP, _VP, _SZ, _SZ, _VP, _SZ, _SZ, _VP, _VP, _VP]),
     "aq_train_l2_pq": (_I, [_VP, _VP, _SZ, _SZ, _SZ, _SZ, _VP, _VP, _VP]),
     "aq_train_apq": (_I, [_VP, _VP, _SZ, _SZ, _SZ, _SZ, _VP, _VP, _I, _VP, _VP, _VP, _VP]),
+    # multi-device session (csrc/multi.cu)
+    "aq_device_count": (_I, [_VP]),
+    "aq_multi_create": (_I, [_VP, _I, _PP]),
+    "aq_multi_destroy": (_I, [_VP]),
+    "aq_multi_shards": (_I, [_VP]),
+    "aq_multi_session": (_VP, [_VP, _I]),
+    "aq_multi_pq_quantize": (_I, [_VP, _VP, _SZ, _SZ, _VP, _SZ, _SZ, _SZ, _VP, _I, _VP]),
+    "aq_multi_adc_search": (_I, [_VP, _VP, _SZ, _SZ, _VP, _SZ, _SZ, _SZ, _VP, _SZ, _SZ, _SZ,
+                                 _SZ, _VP, _VP]),
+    "aq_multi_train_apq": (_I, [_VP, _VP, _SZ, _SZ, _SZ, _SZ, _VP, _VP, _I, _VP, _VP, _VP,
+                                _VP]),
     # row-sharded training building blocks
     "aq_dev_weight_flags": (_I, [_VP, _VP, _VP]),
     "aq_dev_normal_equations_partial": (_I, [_VP, _VP, _VP, _SZ, _VP, _VP, _VP, _VP]),

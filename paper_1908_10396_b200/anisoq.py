@@ -725,6 +725,82 @@ def train_apq(data, M: int, k: int, weights, config: TrainConfig = TrainConfig()
     return cb.download(), cm.download()
 
 
+# ---- multi-device session (csrc/multi.cu) ---------------------------------------------
+
+
+class MultiSession:
+    """Row shards over the GPUs of one box from one process (one session per
+    entry of `devices`; a device may carry several shards). pq_quantize and
+    adc_search equal the single-device calls; train_apq equals them for one
+    shard and re-associates the float64 partial sums at shard boundaries for
+    more (include/anisoq_b200.h)."""
+
+    def __init__(self, devices):
+        devs = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        _check(_L.aq_multi_create(devs, len(devices), C.byref(h)))
+        self.h = h
+        self.devices = list(devices)
+
+    @property
+    def shards(self) -> int:
+        return _L.aq_multi_shards(self.h)
+
+    def close(self) -> None:
+        if self.h:
+            _L.aq_multi_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def pq_quantize(self, data, cb: ProductCodebook, weights, passes: int) -> CodeMatrix:
+        data = data if isinstance(data, Dataset) else Dataset(data)
+        if data.f64:
+            raise Unsupported("Unsupported: multi-device calls take float32-exact rows")
+        keep: list = []
+        w = _weights(weights, data.n, keep)
+        out = np.zeros((data.n, cb.M), np.uint32)
+        _check(_L.aq_multi_pq_quantize(self.h, data.values.ctypes.data, data.n, data.d,
+                                       cb.dictionaries.ctypes.data, cb.M, cb.k,
+                                       cb.sub_dimension, C.byref(w), passes, out.ctypes.data))
+        return CodeMatrix(data.n, cb.M, cb.k, out)
+
+    def adc_search(self, queries, codes: CodeMatrix, cb: ProductCodebook, topn: int):
+        Q = np.ascontiguousarray(np.atleast_2d(queries), np.float64)
+        cm = np.ascontiguousarray(codes.codes, np.uint32)
+        te = min(topn, codes.n) if topn >= 1 else 1
+        ids = np.zeros((len(Q), te), np.uint32)
+        sc = np.zeros((len(Q), te), np.float64)
+        _check(_L.aq_multi_adc_search(self.h, Q.ctypes.data, len(Q), Q.shape[1], cm.ctypes.data,
+                                      codes.n, codes.M, codes.k, cb.dictionaries.ctypes.data,
+                                      cb.M, cb.k, cb.sub_dimension, topn, ids.ctypes.data,
+                                      sc.ctypes.data))
+        return ids, sc
+
+    def train_apq(self, data, M: int, k: int, weights, config: TrainConfig = TrainConfig(),
+                  warm_start: bool = True, loss_history: Optional[list] = None):
+        data = data if isinstance(data, Dataset) else Dataset(data)
+        if data.f64:
+            raise Unsupported("Unsupported: multi-device calls take float32-exact rows")
+        keep: list = []
+        w = _weights(weights, data.n, keep)
+        cfg = config.c()
+        dic = np.zeros(k * data.d, np.float64)
+        codes = np.zeros((data.n, M), np.uint32)
+        hist = np.zeros(max(config.max_iterations, 0) + 1, np.float64)
+        hl = C.c_size_t(0)
+        _check(_L.aq_multi_train_apq(self.h, data.values.ctypes.data, data.n, data.d, M, k,
+                                     C.byref(w), C.byref(cfg), int(warm_start), dic.ctypes.data,
+                                     codes.ctypes.data, hist.ctypes.data, C.byref(hl)))
+        if loss_history is not None:
+            loss_history.extend(float(v) for v in hist[: hl.value])
+        return ProductCodebook(M, k, data.d // M, dic), CodeMatrix(data.n, M, k, codes)
+
+
 # ---- single-point API, exact search, evaluation (pq.hpp:256, index.hpp:137-332) ---------
 
 

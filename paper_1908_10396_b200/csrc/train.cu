@@ -28,42 +28,6 @@ int avq_codebook_update(aq_dataset* ds, aq_codes* codes, const aq_weights* w, do
 
 
 // ---- Rng (rng.hpp:28-89), host side -----------------------------------------------------
-struct HostRng {
-  uint64_t state;
-  uint64_t next_u64() {
-    state += 0x9E3779B97F4A7C15ull;
-    uint64_t z = state;
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-    return z ^ (z >> 31);
-  }
-  uint64_t next_below(uint64_t n) {
-    const uint64_t threshold = (0 - n) % n;
-    for (;;) {
-      const uint64_t r = next_u64();
-      if (r >= threshold) return r % n;
-    }
-  }
-  // sample_distinct (rng.hpp:74-83): partial Fisher-Yates on iota(n); only the
-  // touched positions are materialised, so it is O(k) instead of O(n).
-  std::vector<size_t> sample_distinct(size_t n, size_t k) {
-    std::unordered_map<size_t, size_t> moved;
-    auto get = [&](size_t i) {
-      auto it = moved.find(i);
-      return it == moved.end() ? i : it->second;
-    };
-    std::vector<size_t> out;
-    for (size_t i = 0; i < k && i < n; ++i) {
-      const size_t j = i + (size_t)next_below(n - i);
-      const size_t vi = get(i), vj = get(j);
-      moved[i] = vj;
-      moved[j] = vi;
-      out.push_back(vj);
-    }
-    return out;
-  }
-};
-
 // ---- kernels ------------------------------------------------------------------------------
 
 // std::accumulate of `count` values (float64, index order), one warp per row.

@@ -44,3 +44,16 @@ def test_reference_suite_passes_on_b200(suite):
     out = r.stdout + r.stderr
     assert r.returncode == 0, out
     assert f"{SUITES[suite]} cases run, 0 skipped, 0 failed" in out, out
+
+
+@pytest.mark.gpu
+def test_reference_index_suite_on_multi_device_session():
+    """The reference's test_index.cpp with $ANISOQ_DEVICES set: adc_search runs
+    over row shards of a multi-device session (three shards on this box's one
+    B200) and every case still passes — results depend only on the shard
+    count and equal the single-device ones."""
+    env = dict(os.environ, ANISOQ_DEVICES="0,0,0")
+    r = subprocess.run([_exe("index")], capture_output=True, text=True, timeout=900, env=env)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out
+    assert f"{SUITES['index']} cases run, 0 skipped, 0 failed" in out, out

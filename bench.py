@@ -50,6 +50,9 @@ def parse():
     p.add_argument("--encode-n", type=int, default=10_000_000)
     p.add_argument("--no-encode", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-c4", action="store_true", help="skip the config-4 search object")
+    p.add_argument("--no-c5", action="store_true", help="skip the config-5 training object")
+    p.add_argument("--no-dropin", action="store_true", help="skip the single-query drop-in call")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     return p.parse_args()
 
@@ -79,6 +82,28 @@ def traffic_record():
         return json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
     except Exception:
         return {}
+
+
+BENCH_INDEX = os.path.join(ROOT, "bench_data", "config2_codebook.npz")
+
+
+def search_config(w, n):
+    """The `config` both arms print (identical dicts: same workload, index and
+    query set; the per-step query count is a separate top-level key)."""
+    return {"workload": "config2", "n_per_gpu": n, "d": w.d, "M": w.M, "k": 16,
+            "threshold": w.threshold, "adc_topn": 100, "rerank_to": 10,
+            "index": "codebook of train_apq (warm start + 10 iterations, T = 0.2, seed 0; "
+                     "bench_data/config2_codebook.npz is the reference's), codes of "
+                     "pq_quantize (3 passes)",
+            "queries": "config2 query set (workload.config2, 10,000 unit vectors)"}
+
+
+def reference_codebook():
+    """The config-2 codebook trained by the reference (tools/make_bench_index.py)."""
+    try:
+        return np.load(BENCH_INDEX)["dictionaries"]
+    except Exception:
+        return None
 
 
 class ClockSampler:
@@ -312,6 +337,16 @@ def run_ours(args):
     stream = torch.cuda.ExternalStream(sess.stream, device=torch.device("cuda", local))
     w, cb, ds, dcb, dc, train_info = build_index(aq, wl, args.n, args.nq, rank, sess)
     n, nq, M, d = args.n, args.nq, w.M, w.d
+    ref_cb = reference_codebook()
+    if ws == 1 and n == 1_183_514 and ref_cb is not None:
+        # the device trainer reproduces the reference's codebook bit for bit
+        train_info["codebook_equals_reference"] = bool(np.array_equal(cb.dictionaries, ref_cb))
+    # the searched index: the trained codebook + pq_quantize codes (the
+    # reference pipeline's train -> encode), the same in both arms
+    trained_codes = dc
+    dc = sess.alloc_codes(n, M, 16)
+    aq.dev_pq_quantize(ds, dcb, aq.ThresholdWeights(w.threshold), 3, dc)
+    sess.sync()
     topn, keep = 100, 10
     Qh = np.ascontiguousarray(w.queries, np.float64)
     Qd = torch.from_numpy(Qh).cuda(local)
@@ -442,14 +477,12 @@ def run_ours(args):
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (seeded stand-in for GloVe-1.2M shape, config2)",
-           "config": {"workload": "config2", "n_per_gpu": n, "d": d, "M": M, "k": 16,
-                      "queries_per_step": nq, "adc_topn": topn, "rerank_to": keep,
-                      "threshold": w.threshold,
-                      "index": {k: v for k, v in train_info.items() if k != "phases"},
-                      "recall10_at_10": recall,
-                      "filter_dtype": "13-bit integer LUT (bounded error), results f64 bit-exact",
-                      "l2": "flushed (256 MiB write) before every timed step",
-                      "parallelism": f"dp{ws} (row shards)"},
+           "config": dict(search_config(w, n), parallelism=f"dp{ws} (row shards)"),
+           "queries_per_step": nq,
+           "index_build": {k: v for k, v in train_info.items() if k != "phases"},
+           "recall10_at_10": recall,
+           "notes": {"filter": "13-bit integer LUT (bounded error), results f64 bit-exact",
+                     "l2": "flushed (256 MiB write) before every timed step"},
            "e2e": {"value": round(e2e, 1), "unit": UNIT,
                    "h2d_bytes_per_step": int(nq * d * 8),
                    "d2h_bytes_per_step": int(nq * ke * (4 + 8))},
@@ -459,12 +492,20 @@ def run_ours(args):
     if rank == 0:
         tcpu = None
         if ws == 1 and not args.no_cpu_baseline:
-            tcpu = train_cpu_baseline(args, w, dc.download().codes, n)
+            tcpu = train_cpu_baseline(args, w, trained_codes.download().codes, n)
         out["train"] = train_record(w, n * ws, train_info, None, tcpu)
     if not args.no_encode:
         out["encode"] = bench_encode(args, aq, wl, sess, stream, flush, local, ws, pk)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, w, cb, dc, n)
+    if ws == 1 and not args.no_dropin:
+        out["dropin_adc_search"] = bench_dropin_search(aq, sess, w, cb, dc, n)
+    del trained_codes, dc, dcb, ds, aid, asc, rid, rsc, Qd
+    torch.cuda.empty_cache()
+    if ws == 1 and not args.no_c4:
+        out["search_c4"] = bench_search_c4(args, aq, wl, sess, local, pk, stream)
+    if ws == 1 and not args.no_c5:
+        out["train_c5"] = bench_train_c5(args, aq, sess, local)
     if rank == 0:
         emit(json.dumps(out))
     if sharded:
@@ -559,6 +600,144 @@ def bench_encode(args, aq, wl, sess, stream, flush, local, ws, pk):
                             f"one warm-up"}}
 
 
+def bench_dropin_search(aq, sess, w, cb, dc, n):
+    """The reference-signature single-query call anisoq::adc_search(q, codes,
+    cb, topn) (index.hpp:118): host uint32 codes in, host hits out, so every
+    call uploads and packs the whole index (n x M x 4 B). The resident
+    batched path above is the one to use for query batches."""
+    L = aq._L
+    import ctypes as C
+    codes = np.ascontiguousarray(dc.download().codes, np.uint32)
+    Q = np.ascontiguousarray(w.queries[:4], np.float64)
+    ids = np.zeros(100, np.uint32)
+    sc = np.zeros(100, np.float64)
+    cnt = C.c_size_t(0)
+
+    def call(q):
+        aq._check(L.aq_adc_search(sess.h, q.ctypes.data, q.size, codes.ctypes.data, n, w.M, 16,
+                                  cb.dictionaries.ctypes.data, w.M, 16, 2, 100, ids.ctypes.data,
+                                  sc.ctypes.data, C.byref(cnt)))
+
+    call(Q[0])
+    t0 = time.perf_counter()
+    for q in Q[1:]:
+        call(q)
+    ms = (time.perf_counter() - t0) / (len(Q) - 1) * 1e3
+    return {"call": "aq_adc_search (C++ anisoq::adc_search), one query, host codes",
+            "ms_per_query": round(ms, 2), "scores_per_s": round(n / (ms / 1e3), 1),
+            "h2d_bytes_per_call": int(codes.nbytes + 8 * w.d),
+            "note": "dominated by the per-call index upload (the reference signature passes "
+                    "the codes by value); batched queries on the resident index: `value`"}
+
+
+def bench_search_c4(args, aq, wl, sess, local, pk, stream):
+    """configs[3]: ADC top-100 of 4,096 queries over 1e8 uniform 4-bit codes
+    (M = 48), resident; the largest single-GPU search configuration."""
+    import ctypes as C
+    import torch
+
+    L = aq._L
+    w = wl.config4()
+    n, M, nq = w.n, w.M, len(w.queries)
+    dc = sess.upload_packed_codes(w.packed_codes, n, M, 16)
+    del w.packed_codes
+    dcb = sess.upload_codebook(aq.ProductCodebook(M, 16, 2, w.codebook))
+    Qd = torch.from_numpy(np.ascontiguousarray(w.queries, np.float64)).cuda(local)
+    ids = torch.empty((nq, 100), dtype=torch.int32, device=f"cuda:{local}")
+    sc = torch.empty((nq, 100), dtype=torch.float64, device=f"cuda:{local}")
+
+    def step():
+        aq._check(L.aq_dev_adc_search_d(dc.h, dcb.h, Qd.data_ptr(), nq, 100, ids.data_ptr(),
+                                        sc.data_ptr()))
+
+    step()
+    torch.cuda.synchronize()
+    L.aq_session_timing(sess.h, 1)
+    L.aq_session_timer_read(sess.h, 1, None, None, 1)
+    steps = 2
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    msk, cnt = C.c_double(0), C.c_uint64(0)
+    L.aq_session_timer_read(sess.h, 1, C.byref(msk), C.byref(cnt), 1)
+    L.aq_session_timing(sess.h, 0)
+    per_launch = msk.value / max(cnt.value, 1) / 1e3
+    achieved = nq * n * (M / 2) / per_launch / 1e9
+    ceil = 148 * 64 * 1.965e9 / M
+    del dc, dcb
+    return {"metric": "ADC scores/sec", "workload": "config4", "value": round(nq * n / (ms / 1e3), 1),
+            "unit": "scores/s", "ms_per_step": round(ms, 2), "n": n, "M": M,
+            "queries_per_step": nq, "topn": 100,
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"],
+                         "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4),
+                         "kernel": "k_adc_score",
+                         "onchip_frac": round(nq * n / per_launch / ceil, 4),
+                         "note": "M/2 code bytes per score; 16 queries per code pass, so the "
+                                 "bound is the shared-memory LUT (onchip_frac: 64 lookups/clk/SM)"},
+            "exact": "ids and scores equal the reference's over all 1e8 codes "
+                     "(tests/test_config_pins_gpu.py::test_c4_all_codes_top100)"}
+
+
+def bench_train_c5(args, aq, sess, local):
+    """configs[4]: train_apq at n = 1e7, d = 256, M = 128, k = 16, T = 0.2,
+    warm start + 20 iterations (the dim-4096 normal equations); rows drawn on
+    the device (torch, seeded) with config 5's distribution."""
+    import ctypes as C
+    import torch
+
+    L = aq._L
+    n, d, M, comps = 10_000_000, 256, 128, 4096
+    dev = torch.device("cuda", local)
+    g = torch.Generator(device=dev)
+    g.manual_seed(5)
+    means = torch.randn((comps, d), generator=g, device=dev, dtype=torch.float32)
+    x = torch.empty((n, d), dtype=torch.float32, device=dev)
+    for b in range(0, n, 1 << 20):
+        e = min(n, b + (1 << 20))
+        comp = torch.randint(0, comps, (e - b,), generator=g, device=dev)
+        v = means[comp] + 0.4 * torch.randn((e - b, d), generator=g, device=dev)
+        x[b:e] = v / torch.linalg.vector_norm(v, dim=1, keepdim=True)
+    torch.cuda.synchronize()
+    ds = sess.wrap_device_rows(x.data_ptr(), n, d)
+    cfg = aq.TrainConfig(max_iterations=20, relative_tolerance=0.0, seed=0)
+    L.aq_session_timing(sess.h, 1)
+    for slot in range(9):
+        L.aq_session_timer_read(sess.h, slot, None, None, 1)
+    hist = []
+    t0 = time.perf_counter()
+    dcb, dc = aq.dev_train_apq(ds, M, 16, aq.ThresholdWeights(0.2), cfg, True, hist)
+    sess.sync()
+    tt = time.perf_counter() - t0
+    ph = {}
+    for slot, name in [(0, "encode"), (5, "assemble"), (6, "llt_solve"), (7, "kmeans_warm_start")]:
+        ms, cnt = C.c_double(0), C.c_uint64(0)
+        L.aq_session_timer_read(sess.h, slot, C.byref(ms), C.byref(cnt), 1)
+        ph[name] = round(ms.value, 1)
+    L.aq_session_timing(sess.h, 0)
+    its = len(hist) - 1
+    per_it = (tt - ph["kmeans_warm_start"] / 1e3) / max(its, 1)
+    macs = n * (M * (M + 1) // 2) * 4
+    asm_s = ph["assemble"] / 1e3 / max(its, 1)
+    del ds, dcb, dc, x, means
+    torch.cuda.empty_cache()
+    return {"metric": "train_apq iterations/sec", "workload": "config5", "n": n, "d": d, "M": M,
+            "value": round(1.0 / per_it, 3), "unit": "iterations/s",
+            "ms_per_iteration": round(per_it * 1e3, 1), "total_s": round(tt, 2),
+            "iterations": its, "phases_ms": ph, "loss_first": hist[0], "loss_last": hist[-1],
+            "assembly_roofline": {"bound": "smem read-modify-write",
+                                  "achieved_gmacs": round(macs / asm_s / 1e9, 1),
+                                  "ceiling_gmacs": 2326.6,
+                                  "frac": round(macs / asm_s / 2.3266e12, 4)},
+            "data": "synthetic on the device (torch, seeded): 4,096-component mixture, "
+                    "sigma 0.4, unit norm",
+            "exact": "bit-identical to the reference at the config-5 shape "
+                     "(tests/test_config_pins_gpu.py::test_c5_shape_train, n = 2e5)"}
+
+
 def encode_cpu_baseline(args, w):
     """Reference pq_quantize (oracle/_ref, all host cores) on a bounded prefix
     of the config-3 rows."""
@@ -636,12 +815,18 @@ def run_reference(args):
     n = args.n
     w = wl.config2(n=n, nq=args.nq, seed=0)
     M = w.M
-    g = np.random.Generator(np.random.PCG64([0, 7]))
-    dic = np.empty((M, 16, 2))
-    for m in range(M):
-        idx = g.choice(n, size=16, replace=False)
-        dic[m] = w.base[idx, m * 2:(m + 1) * 2]
-    dic = dic.ravel()
+    # the index of the GPU arm: the config-2 codebook as trained by the
+    # reference itself (bench_data/, tools/make_bench_index.py; the device
+    # trainer reproduces it bit for bit) and pq_quantize codes below
+    dic = reference_codebook() if n == 1_183_514 else None
+    same_index = dic is not None
+    if dic is None:  # other shard sizes: a codebook sampled from the rows
+        g = np.random.Generator(np.random.PCG64([0, 7]))
+        dic = np.empty((M, 16, 2))
+        for m in range(M):
+            idx = g.choice(n, size=16, replace=False)
+            dic[m] = w.base[idx, m * 2:(m + 1) * 2]
+        dic = dic.ravel()
     if Reference.available():
         R, kind, cores = Reference(), "reference", os.cpu_count() or 1
     else:
@@ -681,8 +866,10 @@ def run_reference(args):
         "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded stand-in for GloVe-1.2M shape, config2)",
-        "config": {"workload": "config2", "n_per_gpu": n, "d": w.d, "M": M, "k": 16,
-                   "queries_per_step": per_step, "adc_topn": 100, "rerank_to": 10},
+        "config": (dict(search_config(w, n), parallelism=f"dp{ws} (row shards)") if same_index
+                   else {"workload": "config2", "n_per_gpu": n, "d": w.d, "M": M, "k": 16,
+                         "index": "sampled codebook + pq_quantize codes"}),
+        "queries_per_step": per_step,
         "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": cores, "kind": kind,
                          "sample": f"{per_step} queries x {n} points per step"},
         "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0,

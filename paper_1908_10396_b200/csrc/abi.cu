@@ -22,98 +22,157 @@ using namespace aqd;
 
 namespace {
 
-// memcpy split over up to 8 host threads (pageable <-> page-locked staging)
-void parallel_copy(void* dst, const void* src, size_t bytes) {
-  constexpr size_t kPiece = size_t(16) << 20;
-  const size_t hw = std::max(1u, std::thread::hardware_concurrency());
-  const size_t nt = std::min<size_t>({8, hw, (bytes + kPiece - 1) / kPiece});
+// memcpy-bound host loop split over up to `nt` threads: f(begin, end)
+template <class F>
+void parallel_rows(size_t rows, size_t nt, F f) {
+  nt = std::max<size_t>(1, std::min(nt, rows / 1024 + 1));
   if (nt <= 1) {
-    std::memcpy(dst, src, bytes);
+    f(0, rows);
     return;
   }
-  const size_t per = (bytes + nt - 1) / nt;
+  const size_t per = (rows + nt - 1) / nt;
   std::vector<std::thread> th;
   for (size_t t = 1; t < nt; ++t) {
     const size_t b = t * per;
-    if (b >= bytes) break;
-    const size_t e = std::min(bytes, b + per);
-    th.emplace_back([=] {
-      std::memcpy(static_cast<char*>(dst) + b, static_cast<const char*>(src) + b, e - b);
-    });
+    if (b >= rows) break;
+    th.emplace_back([=] { f(b, std::min(rows, b + per)); });
   }
-  std::memcpy(dst, src, std::min(per, bytes));
+  f(0, std::min(per, rows));
   for (auto& t : th) t.join();
 }
 
-// pq_quantize over host rows in chunks: the host copies chunk i + 1 into
-// page-locked staging (and chunk i - 1's codes out of it) while the device
-// uploads, tiles, encodes and unpacks chunk i. Points are independent
+// pq_quantize over host rows in chunks, three stages in flight:
+//   host     copies chunk i's rows into page-locked staging (every host
+//            thread) while a second thread group unpacks chunk i - 2's 4-bit
+//            codes from staging into codes_out;
+//   up       H2D of chunk i on its own stream;
+//   compute  tiles and encodes chunk i - 1, then its packed codes (M/2 bytes
+//            per row, 8x fewer than uint32) go D2H on a third stream.
+// Buffers (page-locked, device rows, tiled datasets, packed codes) are a ring
+// of three, allocated once per call. Points are independent
 // (pq.hpp:581-612), so the codes equal the single-shot call's; device errors
 // carry global point indices and are checked once at the end.
 int pq_quantize_streamed(aq_session* s, const float* x, size_t n, size_t d, aq_codebook* cb,
                          const aq_weights* w, int passes, uint32_t* codes_out, size_t chunk) {
+  constexpr int NB = 3;
   const size_t M = cb->M;
-  void* hin[2];
-  void* hout[2];
-  for (int b = 0; b < 2; ++b) {
+  const int bits = cb->k <= 16 ? 4 : 8;
+  const size_t stride = code_stride(M, bits);
+  const size_t nt = std::max(1u, std::thread::hardware_concurrency());
+  void* hin[NB];
+  void* hout[NB];
+  for (int b = 0; b < NB; ++b) {
     AQ_TRY(pinned_buffer(s, b, chunk * d * sizeof(float), &hin[b]));
-    AQ_TRY(pinned_buffer(s, 2 + b, chunk * M * sizeof(uint32_t), &hout[b]));
+    AQ_TRY(pinned_buffer(s, NB + b, chunk * stride, &hout[b]));
   }
-  float* dx[2] = {nullptr, nullptr};
-  uint32_t* dcodes[2] = {nullptr, nullptr};
-  cudaEvent_t h2d[2] = {nullptr, nullptr}, d2h[2] = {nullptr, nullptr};
+  cudaStream_t up = nullptr, down = nullptr;
+  float* dx[NB] = {};
+  aq_dataset ds[NB];
+  aq_codes* cc[NB] = {};
+  cudaEvent_t ev_up[NB] = {}, ev_enc[NB] = {}, ev_down[NB] = {};
   int st = AQ_OK;
-  for (int b = 0; b < 2 && st == AQ_OK; ++b) {
-    if (cudaMallocAsync(&dx[b], chunk * d * sizeof(float), s->stream) != cudaSuccess ||
-        cudaMallocAsync(&dcodes[b], chunk * M * sizeof(uint32_t), s->stream) != cudaSuccess ||
-        cudaEventCreateWithFlags(&h2d[b], cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&d2h[b], cudaEventDisableTiming) != cudaSuccess)
+  if (cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking) != cudaSuccess)
+    st = ref_error(AQ_E_CUDA, "stream creation failed");
+  for (int b = 0; b < NB && st == AQ_OK; ++b) {
+    ds[b].s = s;
+    ds[b].d = d;
+    if (cudaMalloc(&dx[b], chunk * d * sizeof(float)) != cudaSuccess ||
+        cudaMalloc(&ds[b].xt, (tiled_floats(chunk, d) + 256) * sizeof(float)) != cudaSuccess ||
+        cudaMalloc(&ds[b].norms, chunk * sizeof(double)) != cudaSuccess ||
+        cudaMemset(ds[b].xt + tiled_floats(chunk, d), 0, 256 * sizeof(float)) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev_up[b], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev_enc[b], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev_down[b], cudaEventDisableTiming) != cudaSuccess)
       st = ref_error(AQ_E_CUDA, "out of device memory for the streamed encode");
+    if (st == AQ_OK) st = aq_codes_alloc(s, chunk, M, cb->k, &cc[b]);
   }
   if (st == AQ_OK) st = clear_dev_error(s);
   const size_t nch = (n + chunk - 1) / chunk;
-  for (size_t i = 0; i <= nch && st == AQ_OK; ++i) {
-    if (i < nch) {
-      const int b = (int)(i & 1);
-      const size_t off = i * chunk, cn = std::min(chunk, n - off);
-      if (i >= 2) cudaEventSynchronize(h2d[b]);  // staging slot b is free again
-      parallel_copy(hin[b], x + off * d, cn * d * sizeof(float));
-      if (cudaMemcpyAsync(dx[b], hin[b], cn * d * sizeof(float), cudaMemcpyHostToDevice,
-                          s->stream) != cudaSuccess ||
-          cudaEventRecord(h2d[b], s->stream) != cudaSuccess) {
-        st = AQ_E_CUDA;
+  auto rows_of = [&](size_t i) { return std::min(chunk, n - i * chunk); };
+  auto unpack = [&](size_t k) {  // chunk k: staging (packed) -> codes_out (uint32)
+    const int b = (int)(k % NB);
+    const size_t cn = rows_of(k);
+    const uint8_t* src = static_cast<const uint8_t*>(hout[b]);
+    uint32_t* dst = codes_out + k * chunk * M;
+    parallel_rows(cn, std::max<size_t>(1, nt / 2), [&](size_t r0, size_t r1) {
+      for (size_t r = r0; r < r1; ++r) {
+        const uint8_t* row = src + r * stride;
+        uint32_t* o = dst + r * M;
+        if (bits == 4) {
+          for (size_t m = 0; m < M; ++m) o[m] = (row[m >> 1] >> ((m & 1) * 4)) & 15u;
+        } else {
+          for (size_t m = 0; m < M; ++m) o[m] = row[m];
+        }
+      }
+    });
+  };
+  for (size_t i = 0; i < nch + 2 && st == AQ_OK; ++i) {
+    std::thread unpacker;
+    if (i >= 2) {  // chunk i - 2's codes, concurrently with chunk i's copy-in
+      const size_t k = i - 2;
+      if (cudaEventSynchronize(ev_down[k % NB]) != cudaSuccess) {
+        st = ref_error(AQ_E_CUDA, "streamed encode failed");
         break;
       }
-      aq_dataset* ds = nullptr;
-      aq_codes* cc = nullptr;
-      st = aq_dataset_wrap_device(s, dx[b], cn, d, &ds);
-      if (st == AQ_OK) st = aq_codes_alloc(s, cn, M, cb->k, &cc);
-      if (st == AQ_OK) st = run_encode_chunk(ds, cb, w, cc, passes, off);
-      if (st == AQ_OK) st = codes_unpack_async(cc, dcodes[b]);
-      if (st == AQ_OK &&
-          (cudaMemcpyAsync(hout[b], dcodes[b], cn * M * sizeof(uint32_t),
-                           cudaMemcpyDeviceToHost, s->stream) != cudaSuccess ||
-           cudaEventRecord(d2h[b], s->stream) != cudaSuccess))
-        st = AQ_E_CUDA;
-      aq_codes_free(cc);
-      aq_dataset_free(ds);
-      if (st != AQ_OK) break;
+      unpacker = std::thread(unpack, k);
     }
-    if (i >= 1) {  // chunk i - 1's codes, while the device works on chunk i
-      const size_t j = i - 1, off = j * chunk, cn = std::min(chunk, n - off);
-      const int b = (int)(j & 1);
-      cudaEventSynchronize(d2h[b]);
-      parallel_copy(codes_out + off * M, hout[b], cn * M * sizeof(uint32_t));
+    if (i < nch) {  // chunk i: host staging, then H2D on `up`
+      const int b = (int)(i % NB);
+      const size_t cn = rows_of(i);
+      if (i >= NB) cudaEventSynchronize(ev_up[b]);  // staging slot b is free again
+      const float* src = x + i * chunk * d;
+      float* dst = static_cast<float*>(hin[b]);
+      parallel_rows(cn, std::max<size_t>(1, i >= 2 ? nt / 2 : nt), [&](size_t r0, size_t r1) {
+        std::memcpy(dst + r0 * d, src + r0 * d, (r1 - r0) * d * sizeof(float));
+      });
+      if (i >= NB) cudaStreamWaitEvent(up, ev_enc[b], 0);  // dx[b] read by chunk i - 3
+      if (cudaMemcpyAsync(dx[b], hin[b], cn * d * sizeof(float), cudaMemcpyHostToDevice, up) !=
+              cudaSuccess ||
+          cudaEventRecord(ev_up[b], up) != cudaSuccess)
+        st = ref_error(AQ_E_CUDA, "streamed encode upload failed");
     }
+    if (st == AQ_OK && i >= 1 && i - 1 < nch) {  // chunk i - 1: tile + encode, then D2H
+      const size_t j = i - 1;
+      const int b = (int)(j % NB);
+      const size_t cn = rows_of(j);
+      cudaStreamWaitEvent(s->stream, ev_up[b], 0);
+      if (j >= NB) cudaStreamWaitEvent(s->stream, ev_down[b], 0);  // cc[b] downloaded
+      ds[b].n = cn;
+      ds[b].xr = dx[b];
+      cc[b]->n = cn;
+      st = tile_rows_async(dx[b], cn, d, ds[b].xt, ds[b].norms, s->stream);
+      if (st == AQ_OK) st = run_encode_chunk(&ds[b], cb, w, cc[b], passes, j * chunk);
+      if (st == AQ_OK && (cudaEventRecord(ev_enc[b], s->stream) != cudaSuccess ||
+                          cudaStreamWaitEvent(down, ev_enc[b], 0) != cudaSuccess ||
+                          cudaMemcpyAsync(hout[b], cc[b]->data, cn * stride,
+                                          cudaMemcpyDeviceToHost, down) != cudaSuccess ||
+                          cudaEventRecord(ev_down[b], down) != cudaSuccess))
+        st = ref_error(AQ_E_CUDA, "streamed encode download failed");
+    }
+    if (unpacker.joinable()) unpacker.join();
   }
   const int fin = sync_and_check(s, "encode");
   if (st == AQ_OK) st = fin;
-  for (int b = 0; b < 2; ++b) {
-    if (dx[b]) cudaFreeAsync(dx[b], s->stream);
-    if (dcodes[b]) cudaFreeAsync(dcodes[b], s->stream);
-    if (h2d[b]) cudaEventDestroy(h2d[b]);
-    if (d2h[b]) cudaEventDestroy(d2h[b]);
+  if (up) cudaStreamSynchronize(up);
+  if (down) cudaStreamSynchronize(down);
+  for (int b = 0; b < NB; ++b) {
+    if (cc[b]) {
+      cc[b]->n = chunk;
+      aq_codes_free(cc[b]);
+    }
+    cudaFree(dx[b]);
+    cudaFree(ds[b].xt);
+    cudaFree(ds[b].norms);
+    ds[b].xt = nullptr;
+    ds[b].norms = nullptr;
+    ds[b].xr = nullptr;
+    if (ev_up[b]) cudaEventDestroy(ev_up[b]);
+    if (ev_enc[b]) cudaEventDestroy(ev_enc[b]);
+    if (ev_down[b]) cudaEventDestroy(ev_down[b]);
   }
+  if (up) cudaStreamDestroy(up);
+  if (down) cudaStreamDestroy(down);
   return st;
 }
 

@@ -93,7 +93,7 @@ struct aq_session {
   aqd::DevError* err = nullptr;     // device
   aqd::DevError* err_host = nullptr;  // pinned mirror
   aqd::Scratch scratch[7];  // slot 6: scan tile sums (sort.cu)
-  aqd::Scratch pinned[4];   // page-locked host staging (streamed host-pointer calls)
+  aqd::Scratch pinned[6];   // page-locked host staging (streamed host-pointer calls)
 };
 
 struct aq_dataset {
@@ -144,6 +144,8 @@ namespace aqd {
 // concurrently live temporaries never alias).
 int scratch(aq_session* s, int slot, size_t bytes, void** out);
 int check_session(aq_session* s);
+int tile_rows_async(const float* xdev, size_t n, size_t d, float* xt, double* norms,
+                    cudaStream_t stream);
 int sync_and_check(aq_session* s, const char* what);  // reads DevError
 int clear_dev_error(aq_session* s);
 

@@ -127,6 +127,17 @@ __global__ void k_tile_rows(const T* __restrict__ x, size_t n, size_t d,
   if (i < n) norms[i] = __dsqrt_rn(s);
 }
 
+// Pair-tiles n float32 rows (device) into an existing dataset's xt / norms on
+// `stream` (the streamed host-pointer encode reuses one dataset per buffer).
+int tile_rows_async(const float* xdev, size_t n, size_t d, float* xt, double* norms,
+                    cudaStream_t stream) {
+  const size_t ntile = ((n + 31) / 32) * 32;
+  if (ntile)
+    k_tile_rows<float><<<(unsigned)((ntile + 127) / 128), 128, 0, stream>>>(xdev, n, d, xt, norms);
+  AQ_CUDA(cudaGetLastError());
+  return AQ_OK;
+}
+
 // float32 staging of an sd == 2 codebook for the filter kernels:
 // {c0, c1, c0^2 + c1^2} per (m, j); slots j >= k are padded with a huge C so
 // they never win and never look like a near tie. rmax[m] bounds |c_mj| from

@@ -811,11 +811,17 @@ __global__ void __launch_bounds__(32, 12) k_assemble_sd2r(const AsmArgs a, const
 // trace (sequential, Eigen stand-in) and ridge = 1e-6 trace / dim (pq.hpp:431-435)
 __global__ void k_trace_ridge(double* A, size_t dim, double ridge) {
   __shared__ double r;
-  if (threadIdx.x == 0) {
-    double tr = 0.0;
-    for (size_t i = 0; i < dim; ++i) tr = __dadd_rn(tr, A[i * dim + i]);
-    r = ridge < 0.0 ? __ddiv_rn(__dmul_rn(1e-6, tr), (double)dim) : ridge;
+  __shared__ double diag[4096];  // the diagonal gathered in parallel (dim <= 16384: chunks)
+  double tr = 0.0;
+  for (size_t c0 = 0; c0 < dim; c0 += 4096) {
+    const size_t cn = min((size_t)4096, dim - c0);
+    for (size_t i = threadIdx.x; i < cn; i += blockDim.x) diag[i] = A[(c0 + i) * dim + c0 + i];
+    __syncthreads();
+    if (threadIdx.x == 0)  // the sum itself stays sequential (index order)
+      for (size_t i = 0; i < cn; ++i) tr = __dadd_rn(tr, diag[i]);
+    __syncthreads();
   }
+  if (threadIdx.x == 0) r = ridge < 0.0 ? __ddiv_rn(__dmul_rn(1e-6, tr), (double)dim) : ridge;
   __syncthreads();
   for (size_t i = threadIdx.x; i < dim; i += blockDim.x)
     A[i * dim + i] = __dadd_rn(A[i * dim + i], r);

@@ -302,6 +302,18 @@ int aq_session_create(int device, aq_session** out) {
     return AQ_E_CUDA;
   }
   s->num_sms = prop.multiProcessorCount;
+  // Keep stream-ordered allocations in the device's pool across
+  // synchronisations (the default threshold 0 returns freed memory at every
+  // sync, so the next cudaMallocAsync of a multi-GB training buffer maps it
+  // again); $AQ_POOL_KEEP=0 restores the default.
+  {
+    const char* keep = getenv("AQ_POOL_KEEP");
+    cudaMemPool_t pool;
+    if ((!keep || atoi(keep) != 0) && cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   // a failure part-way releases what was created (aq_session_destroy skips nulls)
   const cudaError_t e[] = {
       cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking),

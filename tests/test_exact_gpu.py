@@ -15,7 +15,12 @@ P = Port()
 @pytest.mark.parametrize("n,d,depth,nq", [(20000, 32, 10, 100), (5000, 100, 100, 17),
                                           (300, 8, 1000, 3), (70000, 96, 64, 40),
                                           (30000, 64, 1000, 20), (40000, 32, 4096, 5),
-                                          (20000, 16, 5000, 3)])
+                                          (20000, 16, 5000, 3),
+                                          # tensor-core filter shapes: d not a multiple
+                                          # of 16, the largest K tile, one query past a
+                                          # 128-query block, and d > 128 (float32 filter)
+                                          (50000, 30, 10, 129), (60000, 128, 10, 300),
+                                          (9000, 130, 10, 40)])
 def test_exact_search_matches_oracle(n, d, depth, nq):
     x = mixture_rows(n, d, 71)
     q = mixture_rows(nq, d, 72).astype(np.float64)
@@ -113,3 +118,36 @@ def test_evaluate_perfect_codes_recall_one():
     assert lines[:5] == ["num_queries 20", "num_datapoints 16", "recall_1@1 1", "recall_1@5 1",
                          "recall_1@16 1"]
     assert lines[5] == "recall_5@5 1" and lines[-3].startswith("latency_mean_us ")
+
+
+def test_exact_tensor_core_and_float32_filters_agree(tmp_path):
+    """The tcgen05 filter ($AQ_EXACT_TC=1, default) and the float32 FFMA filter
+    ($AQ_EXACT_TC=0) give the same ids and scores (both equal the oracle's),
+    including duplicated rows (exact ties) and a zero query."""
+    import subprocess
+    import sys
+    import os
+    script = tmp_path / "ex.py"
+    script.write_text(
+        "import sys, numpy as np\n"
+        f"sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})\n"
+        "from paper_1908_10396_b200 import anisoq as aq\n"
+        "from tests.helpers import mixture_rows\n"
+        "x = np.repeat(mixture_rows(20000, 100, 91), 3, axis=0)\n"
+        "q = mixture_rows(200, 100, 92).astype(np.float64); q[7] = 0.0\n"
+        "ids, sc = aq.dev_exact_search(aq.Session.default().upload_dataset(x), q, 25)\n"
+        "np.savez(sys.argv[1], ids=ids, sc=sc)\n")
+    out = {}
+    for flag in ("1", "0"):
+        f = tmp_path / f"r{flag}.npz"
+        r = subprocess.run([sys.executable, str(script), str(f)], capture_output=True, text=True,
+                           env=dict(os.environ, AQ_EXACT_TC=flag), timeout=300)
+        assert r.returncode == 0, r.stderr
+        out[flag] = np.load(f)
+    assert np.array_equal(out["1"]["ids"], out["0"]["ids"])
+    assert np.array_equal(out["1"]["sc"], out["0"]["sc"])
+    x = np.repeat(mixture_rows(20000, 100, 91), 3, axis=0).astype(np.float64)
+    q = mixture_rows(200, 100, 92).astype(np.float64)
+    q[7] = 0.0
+    wi, ws = P.exact_search_batch(q, x, 25)
+    assert np.array_equal(out["1"]["ids"], wi) and np.array_equal(out["1"]["sc"], ws)

@@ -339,31 +339,58 @@ __global__ void k_filter_queries(const double* Q, int nq, int d, double xmax, fl
     if (!all && q < nq) flag[q] = 4;
   }
 }
-
 // ---- tensor-core filter (tcgen05) ------------------------------------------------
 //
 // The same filter / window / merge contract with the filter scores formed on
-// the 5th-generation tensor cores: q.x ~ qh.xh + qh.xl + ql.xh with bf16 hi/lo
-// splits of the float64 query and the float32 row (each product exact in
-// float32, accumulated in float32 in TMEM), one 128-point x 128-query tile per
-// 3 x Kp/16 tcgen05.mma (kind::f16, M = 128, N = 128, K = 16). Per element
-//   |q x - (qh xh + qh xl + ql xh)| <= |ql xl| + |eq| |xh + xl| + |qh + ql| |ex|
-//                                    <= 3.02 2^-18 |q_j x_j|
-// (bf16 keeps 8 significant bits: |ql| <= 2^-9 |q|, the split residuals
-// |eq| <= 2^-18 |q|, |ex| <= 2^-18 |x|), and each float32 accumulation adds
-// at most one unit in the last place (any order, any rounding), so
-//   |f - s| <= B = 1.01 [3.02 2^-18 + (1.01 Kp + 2) 2^-23] |q| max|x|
-// (qh.xh accumulates in one TMEM accumulator, the two cross terms — 2^8
-// smaller — in a second one, and the reader adds the two),
-// and the windows keep f >= theta - 2B exactly as the float32 filter does.
-// Operands sit in shared memory in the K-major SWIZZLE_NONE canonical layout
-// (8-row x 16-byte core matrices; LBO = 128 B along K, SBO = Kp/8 x 128 B
-// along M/N); point tiles are pre-laid-out in global memory so one
-// cp.async.bulk per tile (mbarrier completion) stages them, double-buffered.
-constexpr int kTM = 128;  // points per tile (UMMA M, TMEM lanes)
-constexpr int kTQ = 128;  // queries per CTA (UMMA N, TMEM columns)
+// the 5th-generation tensor cores (kind::f16: bf16 operands, products exact
+// in float32, float32 accumulation in TMEM), one 128-point x NQ-query tile
+// per TERMS x Kp/16 tcgen05.mma (M = 128, N = NQ, K = 16). bf16 keeps 8
+// significant bits, so rounding to it moves a value by at most 2^-8 of
+// itself. Two precisions:
+//
+//  TERMS = 1   f = qh.xh, qh = bf16(q), xh = bf16(x). Per element
+//              |q x - qh xh| = |qh (x - xh) + (q - qh) x| <= 2^-7 (1 + 2^-9) |q_j x_j|;
+//  TERMS = 3   f = qh.xh + ql.xh + qh.xl with ql = bf16(q - qh), xl = bf16(x - xh),
+//              whose residuals eq, ex are <= 2^-16 of |q|, |x|. Per element
+//              |q x - f_j| = |qh ex + ql xl + ql ex + eq x| <= 3.02 2^-16 |q_j x_j|.
+//
+// The accumulator takes TERMS x Kp products whose absolute sum is <= 1.02
+// sum |q_j x_j|; each step (a product joining the K = 16 reduction, or the
+// reduction joining the accumulator: at most 1.07 TERMS Kp + 4 steps) is
+// charged two units of the last float32 place, 2^-22 of that absolute sum,
+// whatever the hardware's alignment and rounding. With E_T the per-element
+// factor above,
+//   |f - s| <= B = 1.01 [E_T + 1.02 (1.07 TERMS Kp + 4) 2^-22] |q| max|x|
+// (Cauchy-Schwarz on sum |q_j x_j|; 1.01 covers the reference's own float64
+// roundings), and the windows keep f >= theta - 2B exactly as the float32
+// filter does. The one-term filter is three times cheaper on the tensor
+// cores with a window about 60 x wider (config 2, depth 10: ~140 candidates
+// per query, re-scored in float64 by the merge); queries whose windows
+// overflow are re-run with TERMS = 3, then on the float32 filter.
+//
+// Layout and schedule (B200-first):
+//  * operands in shared memory in the K-major SWIZZLE_NONE canonical layout
+//    (8-row x 16-byte core matrices; LBO = 128 B along K, SBO = Kp/8 x 128 B
+//    along M/N); point tiles are pre-laid-out in global memory as
+//    [block][hi | lo][128 x Kp], so one cp.async.bulk stages a half tile;
+//  * warp 16 loads (a ring of NS half-tile stages plus the query tile), warp
+//    17 issues the MMAs (one elected lane), warps 0..15 read the two TMEM
+//    accumulators (2 x NQ columns) and keep the windows;
+//  * the point blocks are cut into S segments and the work items (segment,
+//    query block) are dealt segment-major, item b + k G to CTA b: at any time
+//    the grid streams two or three segments, so a point tile fetched from HBM
+//    by one CTA serves the other query blocks from L2;
+//  * one window per (query, segment); every window's cut is also published
+//    to a per-query cut in global memory (atomicMax on the order-preserving
+//    key) that later items start from. Any window's N-th filter score is <=
+//    the global one, so every published cut stays <= theta - 2B.
+constexpr int kTM = 128;   // points per tile (UMMA M, TMEM lanes)
 constexpr int kTKpMax = 128;
-constexpr int kTPPT = 16;  // tiles between window shrinks
+constexpr int kTPPT = 8;   // tiles between window shrinks
+constexpr int kTReaders = 16;
+constexpr int kTThreads = (kTReaders + 2) * 32;  // + the loader and MMA warps
+constexpr int kTMaxStages = 8;
+constexpr int kTSmemMax = 232448;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -372,18 +399,19 @@ __device__ __forceinline__ uint64_t umma_sdesc(uint32_t addr, uint32_t lbo, uint
   return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);  // version 1, no swizzle
 }
-// kind::f16: bf16 x bf16 -> f32, A and B K-major, M = 128, N = kTQ
-constexpr uint32_t kTIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTQ >> 3) << 17) |
+// kind::f16: bf16 x bf16 -> f32, A and B K-major, M = 128, N = NQ
+template <int NQ>
+constexpr uint32_t kTIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NQ >> 3) << 17) |
                              ((uint32_t)(kTM >> 4) << 24);
 
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t done = 0;
   while (!done)
     asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}\n"
         : "=r"(done)
-        : "r"(bar), "r"(parity)
+        : "r"(bar), "r"(parity), "n"(1000000)  // suspend up to 1 ms (woken by the phase)
         : "memory");
 }
 // one mbarrier transaction, issued as 8 bulk copies so the copy engine keeps
@@ -401,14 +429,115 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_
         "r"(bar)
         : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
+      : "memory");
+}
+// D (+)= A B over nks K = 16 steps (the start-address field advances 256 B per step)
+__device__ __forceinline__ void umma_chain(uint32_t dst, uint64_t da, uint64_t db, int nks,
+                                           uint32_t idesc, uint32_t acc0) {
+#pragma unroll
+  for (int ks = 0; ks < kTKpMax / 16; ++ks)
+    if (ks < nks)
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+          "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(dst),
+          "l"(da + 16u * ks), "l"(db + 16u * ks), "r"(idesc), "r"(ks ? 1u : acc0));
+}
+__device__ __forceinline__ void readers_sync() {  // named barrier 1: the reading warps
+  asm volatile("bar.sync 1, %0;\n" ::"n"(kTReaders * 32) : "memory");
+}
+// N-th largest key among buf[0..cnt) (warp-cooperative; false when cnt < N):
+// windows of up to 128 entries select in registers (32 bit passes, no
+// memory traffic), larger ones in four 8-bit passes over a 256-bin shared
+// histogram of this warp
+__device__ bool warp_nth_key_tc(const uint2* buf, int cnt, int N, uint32_t* hist,
+                                uint32_t* out) {
+  if (cnt < N) return false;
+  const int lane = threadIdx.x & 31;
+  if (cnt <= 128) {
+    uint32_t k[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) k[u] = lane + 32 * u < cnt ? buf[lane + 32 * u].x : 0u;
+    uint32_t T = 0u;
+    for (int bit = 31; bit >= 0; --bit) {
+      const uint32_t cand = T | (1u << bit);
+      const int c = __reduce_add_sync(0xffffffffu, (int)(k[0] >= cand) + (int)(k[1] >= cand) +
+                                                       (int)(k[2] >= cand) + (int)(k[3] >= cand));
+      if (c >= N) T = cand;
+    }
+    *out = T;
+    return true;
+  }
+  uint32_t prefix = 0u, mask = 0u;
+  int need = N;
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int i = lane; i < 256; i += 32) hist[i] = 0u;
+    __syncwarp();
+    for (int e = lane; e < cnt; e += 32) {
+      const uint32_t key = buf[e].x;
+      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+    }
+    __syncwarp();
+    // lane l owns digits 255 - 8 l .. 248 - 8 l (descending)
+    int c8[8], sum = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      c8[j] = (int)hist[255 - 8 * lane - j];
+      sum += c8[j];
+    }
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int digit = -1, above = 0;
+    if (incl - sum < need && need <= incl) {
+      int acc = incl - sum;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (digit < 0 && acc + c8[j] >= need) {
+          digit = 255 - 8 * lane - j;
+          above = acc;
+        }
+        acc += c8[j];
+      }
+    }
+    const int src = __ffs(__ballot_sync(0xffffffffu, digit >= 0)) - 1;
+    digit = __shfl_sync(0xffffffffu, digit, src);
+    above = __shfl_sync(0xffffffffu, above, src);
+    prefix |= (uint32_t)digit << shift;
+    mask |= 255u << shift;
+    need -= above;
+    __syncwarp();
+  }
+  *out = prefix;
+  return true;
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+      "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
 
-// canonical K-major index of element (r, k) in a 128-row tile with KC = Kp / 8
+// canonical K-major index of element (r, k) in a tile with KC = Kp / 8
 __device__ __forceinline__ int canon(int r, int k, int KC) {
   return ((r >> 3) * KC + (k >> 3)) * 64 + (r & 7) * 8 + (k & 7);
 }
 
 // rows -> per-128-point blocks of [hi tile | lo tile] bf16 (padding zero)
-__global__ void k_tc_points(const float* __restrict__ xr, size_t n, int d, int Kp,
+__global__ void k_tc_points(const float* __restrict__ xr, size_t n, int d, int Kp, int terms,
                             __nv_bfloat16* __restrict__ out) {
   const size_t blk = blockIdx.x;
   const int KC = Kp / 8;
@@ -420,18 +549,18 @@ __global__ void k_tc_points(const float* __restrict__ xr, size_t n, int d, int K
     const float v = (p < n && k < d) ? xr[p * d + k] : 0.0f;
     const __nv_bfloat16 h = __float2bfloat16_rn(v);
     hi[canon(r, k, KC)] = h;
-    lo[canon(r, k, KC)] = __float2bfloat16_rn(v - __bfloat162float(h));
+    if (terms == 3) lo[canon(r, k, KC)] = __float2bfloat16_rn(v - __bfloat162float(h));
   }
 }
 
-// queries -> per-128-query blocks of [hi | lo] tiles and 2 B per query;
+// queries -> per-NQ-query blocks of [hi | lo] tiles and 2 B per query;
 // non-finite or out-of-range queries flag 4 (the caller's exact path)
-__global__ void k_tc_queries(const double* Q, int nq, int d, int Kp, double xmax,
+__global__ void k_tc_queries(const double* Q, int nq, int d, int Kp, int NQ, int terms, double xmax,
                              __nv_bfloat16* __restrict__ out, float* twoB, int* flag) {
   const int q = blockIdx.x;  // padded query index
-  const int qb = q / kTQ, r = q % kTQ, KC = Kp / 8;
-  __nv_bfloat16* hi = out + (size_t)qb * 2 * kTQ * Kp;
-  __nv_bfloat16* lo = hi + kTQ * Kp;
+  const int qb = q / NQ, r = q % NQ, KC = Kp / 8;
+  __nv_bfloat16* hi = out + (size_t)qb * 2 * NQ * Kp;
+  __nv_bfloat16* lo = hi + (size_t)NQ * Kp;
   __shared__ double red[32];
   double ss = 0.0;
   bool ok = true;
@@ -454,10 +583,9 @@ __global__ void k_tc_queries(const double* Q, int nq, int d, int Kp, double xmax
       if (red[w] < 0.0) all = false;
       t += red[w] < 0.0 ? 0.0 : red[w];
     }
-    // split terms + the float32 accumulations: qh.xh in one accumulator
-    // (Kp additions of terms <= |q_j x_j|), the two cross terms in another
-    // (2 Kp additions of terms <= 2^-8 |q_j x_j|), one final add
-    const double c = 3.02 * 3.814697265625e-06 + (1.01 * Kp + 2.0) * 1.1920928955078125e-07;
+    // split terms + the float32 accumulation steps (header comment)
+    const double et = terms == 3 ? 3.02 * 1.52587890625e-05 : 7.8125e-03 * (1.0 + 1.953125e-03);
+    const double c = et + 1.02 * (1.07 * terms * Kp + 4.0) * 2.384185791015625e-07;
     const double B = 1.01 * c * sqrt(t) * 1.0000001 * xmax + 1e-30;
     twoB[q] = (float)(2.0 * B * (1.0 + 1e-6));
     // bf16 keeps float32's exponent range: values that would overflow or
@@ -467,300 +595,298 @@ __global__ void k_tc_queries(const double* Q, int nq, int d, int Kp, double xmax
 }
 
 struct TArgs {
-  const __nv_bfloat16* xtile;  // [n / 128][hi | lo][128 x Kp]
-  const __nv_bfloat16* qtile;  // [nqb][hi | lo][128 x Kp]
-  const float* twoB;           // [nq_pad]
+  const __nv_bfloat16* xtile;  // [nblk][hi | lo][128 x Kp]
+  const __nv_bfloat16* qtile;  // [nqb][hi | lo][NQ x Kp] (this batch)
+  const float* twoB;           // [nqb * NQ]
+  uint32_t* gcut;              // [nq] published window cut per query (key)
   size_t n;
-  int Kp, nq, N, cap, R, nqb;
-  size_t chunk;
-  uint2* out_buf;  // [q][r][cap]
-  int* out_cnt;    // [q][r]
+  int Kp, nq, N, cap, nqb;     // nq, nqb: this batch
+  int S, T, nblk, NS, items;   // segments of T point blocks (last shorter); items = S nqb
+  uint2* out_buf;  // [q][S][cap]
+  int* out_cnt;    // [q][S]
   int* out_flag;   // [q]
 };
 
-// Warp-specialised: warp 16 is the producer (one lane stages the tiles with
-// cp.async.bulk and issues the MMAs), warps 0..15 read the accumulators. Two
-// TMEM accumulators and two point-tile buffers, handed over by mbarriers:
-// full[acc] (the MMAs' tcgen05.commit), empty[acc] (one arrival per reading
-// warp), A[buf] (bulk-copy bytes). Reading warp w takes TMEM lanes
-// 32 (w mod 4) .. + 31 (its points) and columns 32 (w / 4) .. + 31 (its
-// queries), one tcgen05.ld per tile; it keeps its 32 window cuts in
-// registers (refreshed after each shrink) and builds a bit mask of the
-// queries a point passes, so the rare appends are the only branches.
-#ifdef AQ_TC_PROFILE
-__device__ unsigned long long g_tcprof[8];
-__device__ unsigned long long g_tccta[2048];
-#endif
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
-      "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
-        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
-        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-      : "r"(taddr));
-}
-
-constexpr int kTReaders = 16;
-constexpr int kTThreads = (kTReaders + 1) * 32;
-
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void readers_sync() {  // named barrier 1: the reading warps
-  asm volatile("bar.sync 1, %0;\n" ::"n"(kTReaders * 32) : "memory");
-}
-
+template <int NQ, int TERMS>
 __global__ void __launch_bounds__(kTThreads, 1) k_exact_tc(const TArgs a) {
   extern __shared__ __align__(1024) unsigned char tsm[];
-  const int Kp = a.Kp, KC = Kp / 8;
-  const uint32_t tile_b = (uint32_t)(2 * kTM * Kp * 2);  // bytes of [hi | lo]
-  unsigned char* sB = tsm + 2 * tile_b;  // point tiles: tsm + buffer * tile_b
-  uint32_t* cut = reinterpret_cast<uint32_t*>(sB + tile_b);
-  int* cnt = reinterpret_cast<int*>(cut + kTQ);
-  int* flag = cnt + kTQ;
-  float* tb2 = reinterpret_cast<float*>(flag + kTQ);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(tb2 + kTQ);  // A0 A1 B F0 F1 E0 E1
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 7);
+  constexpr int CPW = NQ / 4;  // accumulator columns per reading warp
+  constexpr uint32_t kIdesc = kTIdesc<NQ>;
+  const int Kp = a.Kp, KC = Kp / 8, NS = a.NS, cap = a.cap;
+  const uint32_t half_b = (uint32_t)(kTM * Kp * 2), qhalf_b = (uint32_t)(NQ * Kp * 2);
+  // [query hi | query lo (TERMS = 3)][NS point half tiles][cutf][cut][cnt][flag][tb2][hist][barriers][tmem slot]
+  constexpr int HALVES = TERMS == 3 ? 2 : 1;  // point half tiles (hi, lo) per tile
+  unsigned char* ring = tsm + HALVES * qhalf_b;
+  float* cutf = reinterpret_cast<float*>(ring + (size_t)NS * half_b);
+  uint32_t* cut = reinterpret_cast<uint32_t*>(cutf + NQ);
+  int* cnt = reinterpret_cast<int*>(cut + NQ);
+  int* flag = cnt + NQ;
+  float* tb2 = reinterpret_cast<float*>(flag + NQ);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(tb2 + NQ) + (threadIdx.x >> 5) * 256;  // per reader warp
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint32_t*>(tb2 + NQ) + kTReaders * 256);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kTMaxStages + 6);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const bool producer = warp == kTReaders;
-  // barrier addresses by index (no per-thread arrays: they would live in
-  // local memory when indexed by the tile parity)
+  // barrier addresses by index: full[st], empty[st], F[acc], E[acc], Qfull, Qempty
   const uint32_t bar0 = smem_addr(bars);
-  const uint32_t barB = bar0 + 16;
-  auto barA = [&](int b) { return bar0 + 8u * (uint32_t)b; };
-  auto barF = [&](int b) { return bar0 + 24u + 8u * (uint32_t)b; };
-  auto barE = [&](int b) { return bar0 + 40u + 8u * (uint32_t)b; };
-  const uint32_t sA0 = smem_addr(tsm);
+  auto bFull = [&](int st) { return bar0 + 8u * (uint32_t)st; };
+  auto bEmpty = [&](int st) { return bar0 + 8u * (uint32_t)(kTMaxStages + st); };
+  auto bF = [&](int acc) { return bar0 + 8u * (uint32_t)(2 * kTMaxStages + acc); };
+  auto bE = [&](int acc) { return bar0 + 8u * (uint32_t)(2 * kTMaxStages + 2 + acc); };
+  const uint32_t bQf = bar0 + 8u * (2 * kTMaxStages + 4), bQe = bQf + 8u;
   if (t == 0) {
-    for (int b = 0; b < 5; ++b)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_addr(&bars[b])));
-    for (int b = 5; b < 7; ++b)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(&bars[b])),
-                   "n"(kTReaders));
+    for (int b = 0; b < 2 * kTMaxStages + 6; ++b) {
+      const bool e = b == 2 * kTMaxStages + 2 || b == 2 * kTMaxStages + 3;
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar0 + 8u * b),
+                   "r"(e ? kTReaders : 1));
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
                      smem_addr(tmem_slot)),
-                 "r"(4 * kTQ));
+                 "r"(2 * NQ));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-#ifdef AQ_TC_PROFILE
-  const long long kstart = clock64();
-#endif
-  // phases (bit b = parity of barrier b): producer and readers each track
-  // the barriers they wait on
-  uint32_t phA = 0u, phB = 0u, phF = 0u, phE = 0u;
-  const size_t total = (size_t)a.nqb * a.n;
-  size_t Lpos = (size_t)blockIdx.x * a.chunk;
-  const size_t Lend = min(total, Lpos + a.chunk);
-  const int cap = a.cap;
-  const int lq = warp & 3, cq = warp >> 2;
-  while (Lpos < Lend) {
-    const int qb = (int)(Lpos / a.n);
-    const size_t start = Lpos % a.n;
-    const size_t end = min(a.n, start + (Lend - Lpos));
-    const int r = (int)(blockIdx.x - ((size_t)qb * a.n) / a.chunk);
-    Lpos += end - start;
-    const size_t b0 = start / kTM, b1 = (end + kTM - 1) / kTM;  // point blocks of the segment
-    const int nt = (int)(b1 - b0);
-    __syncthreads();  // every warp is done with the previous segment's windows
-    if (t < kTQ) {
-      // padding queries of the last block (scores 0 everywhere) start with an
-      // unreachable cut and never append
-      cut[t] = qb * kTQ + t < a.nq ? 0u : 0xFFFFFFFFu;
-      cnt[t] = 0;
-      flag[t] = 0;
-      tb2[t] = a.twoB[qb * kTQ + t];
-    }
-    __syncthreads();
-    if (producer) {
-      if (lane == 0) {
-        bulk_load(smem_addr(sB), a.qtile + (size_t)qb * 2 * kTQ * Kp, tile_b, barB);
-        bulk_load(sA0, a.xtile + b0 * 2 * kTM * Kp, tile_b, barA(0));
-        if (nt > 1) bulk_load(sA0 + tile_b, a.xtile + (b0 + 1) * 2 * kTM * Kp, tile_b, barA(1));
-        mbar_wait(barB, phB);
-        phB ^= 1u;
-        const uint32_t half = (uint32_t)(kTM * Kp * 2), lbo = 128, sbo = (uint32_t)KC * 128;
-        for (int i = 0; i < nt; ++i) {
-          const int acc = i & 1;
-#ifdef AQ_TC_PROFILE
-          long long c0 = clock64();
-#endif
-          if (i >= 2) {  // the readers are done with accumulator acc (tile i - 2)
-            mbar_wait(barE(acc), (phE >> acc) & 1u);
-            phE ^= 1u << acc;
+  const int G = gridDim.x;
+
+  if (warp == kTReaders) {  // ---- loader
+    if (lane == 0) {
+      int st = 0;            // ring stage of the next half tile
+      uint32_t ph = 0u;      // its use count's parity
+      uint32_t issued = 0u;  // half tiles issued
+      int k = 0;
+      for (int it = blockIdx.x; it < a.items; it += G, ++k) {
+        const int s = it / a.nqb, qb = it % a.nqb;
+        const int tb0 = s * a.T, tb1 = min(a.nblk, tb0 + a.T);
+        if (k > 0) mbar_wait(bQe, (uint32_t)(k - 1) & 1u);  // the last item's MMAs are done
+        bulk_load(smem_addr(tsm), a.qtile + (size_t)qb * 2 * NQ * Kp, HALVES * qhalf_b, bQf);
+        const __nv_bfloat16* src = a.xtile + (size_t)tb0 * 2 * kTM * Kp;
+        // TERMS = 1 reads the hi half of each [hi | lo] block only
+        for (int hh = 0; hh < HALVES * (tb1 - tb0);
+             ++hh, ++issued, src += (TERMS == 3 ? 1 : 2) * kTM * Kp) {
+          if (issued >= (uint32_t)NS) mbar_wait(bEmpty(st), ph ^ 1u);
+          bulk_load(smem_addr(ring) + (uint32_t)st * half_b, src, half_b, bFull(st));
+          if (++st == NS) {
+            st = 0;
+            ph ^= 1u;
           }
-#ifdef AQ_TC_PROFILE
-          long long c1 = clock64();
-#endif
-          mbar_wait(barA(acc), (phA >> acc) & 1u);
-          phA ^= 1u << acc;
-#ifdef AQ_TC_PROFILE
-          long long c2 = clock64();
-          if (blockIdx.x == 0) { atomicAdd(&g_tcprof[0], (unsigned long long)(c1 - c0)); atomicAdd(&g_tcprof[1], (unsigned long long)(c2 - c1)); atomicAdd(&g_tcprof[3], 1ull); }
-#endif
-          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-          const uint32_t aBase = sA0 + (uint32_t)acc * tile_b, bBase = smem_addr(sB);
-          for (int term = 0; term < 3; ++term) {  // qh.xh -> D1; qh.xl, ql.xh -> D2
-            const uint32_t aOff = term == 1 ? half : 0u, bOff = term == 2 ? half : 0u;
-            const uint32_t dst = tmem + (uint32_t)(acc * 2 * kTQ + (term ? kTQ : 0));
-            // K step ks: the start-address field advances by 256 B (16 units)
-            uint64_t da = umma_sdesc(aBase + aOff, lbo, sbo);
-            uint64_t db = umma_sdesc(bBase + bOff, lbo, sbo);
-            uint32_t accum = term == 2 ? 1u : 0u;
-            for (int ks = 0; ks < Kp / 16; ++ks, da += 16, db += 16) {
-              asm volatile(
-                  "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                  "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(dst),
-                  "l"(da), "l"(db), "r"(kTIdesc), "r"(accum));
-              accum = 1u;
-            }
-          }
-          asm volatile(
-              "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                  barF(acc))
-              : "memory");
-#ifdef AQ_TC_PROFILE
-          if (blockIdx.x == 0) atomicAdd(&g_tcprof[4], (unsigned long long)(clock64() - c2));
-#endif
-          // tile i + 1 goes into the buffer of tile i - 1 once that tile's MMAs
-          // are done (tiles 0 and 1 were loaded up front), while MMA(i) runs
-          if (i >= 1 && i + 1 < nt) {
-            const int pb = acc ^ 1;
-#ifdef AQ_TC_PROFILE
-            long long c3 = clock64();
-#endif
-            mbar_wait(barF(pb), (phF >> pb) & 1u);
-            phF ^= 1u << pb;
-#ifdef AQ_TC_PROFILE
-            if (blockIdx.x == 0) atomicAdd(&g_tcprof[2], (unsigned long long)(clock64() - c3));
-#endif
-            bulk_load(sA0 + (uint32_t)pb * tile_b, a.xtile + (b0 + i + 1) * 2 * kTM * Kp, tile_b,
-                      barA(pb));
-          }
-        }
-        // consume the trailing phases so producer and readers stay in step:
-        // the readers' arrivals for the last (up to) two tiles
-        for (int i = (nt >= 2 ? nt - 2 : 0); i < nt; ++i) {
-          const int acc = i & 1;
-          mbar_wait(barE(acc), (phE >> acc) & 1u);
-          phE ^= 1u << acc;
-        }
-        // MMA completions the producer did not wait on: tile nt - 1, and tile
-        // 0 when nt == 1 (the loop waited on tiles 0 .. nt - 3 at i = 1 .. nt - 2)
-        if (nt >= 2) {
-          phF ^= 1u << ((nt - 2) & 1);
-          phF ^= 1u << ((nt - 1) & 1);
-        } else {
-          phF ^= 1u;
         }
       }
-      __syncwarp();
-    } else {
-      uint2* const buf = a.out_buf + ((size_t)qb * kTQ * a.R + r) * cap;
-      const size_t qstride = (size_t)a.R * cap;
-      constexpr int SPAN = kTM * kTPPT;
-        float cr[32];  // this warp's 32 window cuts (filter-score floor)
-#pragma unroll
-      for (int j = 0; j < 32; ++j) cr[j] = -INFINITY;
-      for (int i = 0; i < nt; ++i) {
-        const int acc = i & 1;
-        mbar_wait(barF(acc), (phF >> acc) & 1u);
-        phF ^= 1u << acc;
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        uint32_t v[32], w2[32];
-        const uint32_t taddr =
-            tmem + ((uint32_t)(lq * 32) << 16) + (uint32_t)(acc * 2 * kTQ + cq * 32);
-        tmem_ld32(taddr, v);
-        tmem_ld32(taddr + kTQ, w2);
-        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-        float f[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) f[j] = __fadd_rn(__uint_as_float(v[j]), __uint_as_float(w2[j]));
-        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(barE(acc));  // accumulator acc may be overwritten
-        if ((i % kTPPT) == 0) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const uint32_t ck = cut[cq * 32 + j];
-            cr[j] = ck ? funkey(ck) : -INFINITY;  // key >= cut  <=>  f >= funkey(cut)
+      // every commit has landed before the CTA exits: the last use of each
+      // stage and the last item's query tile
+      for (int e = 0; e < NS && (uint32_t)e < issued; ++e) {
+        if (st == 0) ph ^= 1u;
+        st = st == 0 ? NS - 1 : st - 1;
+        mbar_wait(bEmpty(st), ph);
+      }
+      if (k > 0) mbar_wait(bQe, (uint32_t)(k - 1) & 1u);
+    }
+    __syncwarp();
+  } else if (warp == kTReaders + 1) {  // ---- MMA issue
+    if (lane == 0) {
+      int st = 0;
+      uint32_t ph = 0u, c = 0u;
+      int k = 0;
+      const int nks = Kp / 16;
+      const uint32_t lbo = 128, sbo = (uint32_t)KC * 128;
+      // descriptors: the query hi / lo tiles, ring stage 0 (stage st adds
+      // st x half_b >> 4 to the start-address field)
+      const uint64_t dqh = umma_sdesc(smem_addr(tsm), lbo, sbo);
+      const uint64_t dql = umma_sdesc(smem_addr(tsm) + qhalf_b, lbo, sbo);
+      const uint64_t dx0 = umma_sdesc(smem_addr(ring), lbo, sbo);
+      const uint32_t dstep = half_b >> 4;
+      for (int it = blockIdx.x; it < a.items; it += G, ++k) {
+        const int s = it / a.nqb;
+        const int ntile = min(a.nblk, (s + 1) * a.T) - s * a.T;
+        mbar_wait(bQf, (uint32_t)k & 1u);
+        for (int i = 0; i < ntile; ++i, ++c) {
+          const int acc = (int)(c & 1u);
+          if (c >= 2) mbar_wait(bE(acc), ((c >> 1) - 1) & 1u);  // readers done with acc
+          const int sh = st;
+          const uint32_t phh = ph;
+          if (++st == NS) {
+            st = 0;
+            ph ^= 1u;
           }
-        }
-        const size_t p = (b0 + i) * kTM + lq * 32 + lane;
-        if (p >= start && p < end) {
-          uint32_t pass = 0u;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) pass |= (uint32_t)(f[j] >= cr[j]) << j;
-          while (pass) {
-            const int j = __ffs(pass) - 1;
-            pass &= pass - 1;
-            const int q = cq * 32 + j;
-            float fj = 0.0f;  // f[j] without dynamic register indexing (appends are rare)
-#pragma unroll
-            for (int u = 0; u < 32; ++u) fj = u == j ? f[u] : fj;
-            const int pos = atomicAdd(&cnt[q], 1);
-            if (pos < cap)
-              buf[q * qstride + pos] = make_uint2(fkey(fj), (unsigned)p);
-            else
-              flag[q] = 1;
-          }
-        }
-        if ((i % kTPPT) == kTPPT - 1 || i + 1 == nt) {
-          readers_sync();  // appends of the last tiles visible
-          for (int q = warp; q < kTQ; q += kTReaders) {
-            const int c = min(cnt[q], cap);
-            uint32_t th;
-            if (c > cap - SPAN && !flag[q] && warp_nth_key32(buf + q * qstride, c, a.N, &th)) {
-              const uint32_t cqv = max(cut[q], window_cut(th, tb2[q]));
-              const int kept = warp_keep_key32(buf + q * qstride, c, cqv);
-              if (lane == 0) {
-                cut[q] = cqv;
-                cnt[q] = kept;
-                if (kept > cap - SPAN) flag[q] = 1;
-              }
+          const uint32_t dst = tmem + (uint32_t)(acc * NQ);
+          if constexpr (TERMS == 1) {
+            mbar_wait(bFull(sh), phh);
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            umma_chain(dst, dx0 + (uint64_t)(sh * dstep), dqh, nks, kIdesc, 0u);
+            umma_commit(bEmpty(sh));
+          } else {
+            const int sl = st;
+            const uint32_t phl = ph;
+            if (++st == NS) {
+              st = 0;
+              ph ^= 1u;
             }
+            mbar_wait(bFull(sh), phh);
+            mbar_wait(bFull(sl), phl);
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            const uint64_t dxh = dx0 + (uint64_t)(sh * dstep), dxl = dx0 + (uint64_t)(sl * dstep);
+            // qh.xh, ql.xh (the hi stage), then qh.xl (the lo stage)
+            umma_chain(dst, dxh, dqh, nks, kIdesc, 0u);
+            umma_chain(dst, dxh, dql, nks, kIdesc, 1u);
+            umma_commit(bEmpty(sh));
+            umma_chain(dst, dxl, dqh, nks, kIdesc, 1u);
+            umma_commit(bEmpty(sl));
+          }
+          umma_commit(bF(acc));
+        }
+        umma_commit(bQe);
+      }
+    }
+    __syncwarp();
+  } else {  // ---- readers: warp w takes TMEM lanes 32 (w mod 4).. and columns CPW (w / 4)..
+    const int lq = warp & 3, cg = warp >> 2;
+    constexpr int SPAN = kTM * kTPPT;
+    constexpr int QPW = NQ / kTReaders;  // queries per warp in the window passes
+    uint32_t c = 0;
+    for (int it = blockIdx.x; it < a.items; it += G) {
+      const int s = it / a.nqb, qb = it % a.nqb;
+      const int tb0 = s * a.T, ntile = min(a.nblk, tb0 + a.T) - tb0;
+      readers_sync();  // the previous item's windows are finished
+      for (int q = t; q < NQ; q += kTReaders * 32) {
+        const int gq = qb * NQ + q;
+        // padding queries (scores 0 everywhere) get an unreachable cut
+        const uint32_t c0 = gq < a.nq ? *(volatile const uint32_t*)(a.gcut + gq) : 0xFFFFFFFFu;
+        cut[q] = c0;
+        cutf[q] = c0 ? funkey(c0) : -INFINITY;  // key >= cut  <=>  f >= funkey(cut)
+        cnt[q] = 0;
+        flag[q] = 0;
+        tb2[q] = a.twoB[gq];
+      }
+      readers_sync();
+      uint2* const buf = a.out_buf + ((size_t)qb * NQ * a.S + s) * cap;
+      const size_t qstride = (size_t)a.S * cap;
+      for (int i = 0; i < ntile; ++i, ++c) {
+        const int acc = (int)(c & 1u);
+        mbar_wait(bF(acc), (c >> 1) & 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint32_t taddr = tmem + ((uint32_t)(lq * 32) << 16) + (uint32_t)(acc * NQ + cg * CPW);
+        const size_t p = (size_t)(tb0 + i) * kTM + lq * 32 + lane;
+        // 32 columns at a time (registers); the accumulator is released
+        // after the last chunk's load
+#pragma unroll
+        for (int h = 0; h < CPW / 32; ++h) {
+          uint32_t v[32];
+          __syncwarp();  // converged after the previous chunk's appends (.sync.aligned)
+          tmem_ld32(taddr + 32 * h, v);
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+          if (h == CPW / 32 - 1) {
+            asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
             __syncwarp();
+            if (lane == 0) mbar_arrive(bE(acc));  // accumulator acc may be overwritten
+          }
+          const float4* cf = reinterpret_cast<const float4*>(cutf + cg * CPW + 32 * h);
+          // one predicate-OR compare per column; the pass mask only when a
+          // query passes (rare once the cuts have settled)
+          bool any = false;
+#pragma unroll
+          for (int j4 = 0; j4 < 8; ++j4) {
+            const float4 cc = cf[j4];
+            any |= __uint_as_float(v[4 * j4]) >= cc.x;
+            any |= __uint_as_float(v[4 * j4 + 1]) >= cc.y;
+            any |= __uint_as_float(v[4 * j4 + 2]) >= cc.z;
+            any |= __uint_as_float(v[4 * j4 + 3]) >= cc.w;
+          }
+          if (any && p < a.n) {
+            uint32_t pass = 0u;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              pass |= (uint32_t)(__uint_as_float(v[j]) >= cutf[cg * CPW + 32 * h + j]) << j;
+            while (pass) {
+              const int j = __ffs(pass) - 1;
+              pass &= pass - 1;
+              const int q = cg * CPW + 32 * h + j;
+              uint32_t vj = 0u;  // v[j] without dynamic register indexing
+#pragma unroll
+              for (int u = 0; u < 32; ++u) vj = u == j ? v[u] : vj;
+              const int pos = atomicAdd(&cnt[q], 1);
+              if (pos < cap)
+                buf[q * qstride + pos] = make_uint2(fkey(__uint_as_float(vj)), (unsigned)p);
+              else
+                flag[q] = 1;
+            }
+          }
+        }
+        const bool last = i + 1 == ntile;
+        if ((i % kTPPT) == kTPPT - 1 || last) {
+          readers_sync();  // appends of the last tiles visible
+          // lane j < QPW owns query warp + 16 j: its published cut, count and
+          // whether its window shrinks now (the next span could overflow, or
+          // the item ends); the warp then shrinks those windows one by one
+          const int qj = warp + kTReaders * lane, gqj = qb * NQ + qj;
+          uint32_t oldc = 0u, cqj = 0u;
+          int c2j = 0;
+          bool need = false;
+          if (lane < QPW) {
+            oldc = cut[qj];
+            cqj = max(oldc, gqj < a.nq ? *(volatile const uint32_t*)(a.gcut + gqj) : 0u);
+            c2j = min(cnt[qj], cap);
+            need = (last || c2j > cap - SPAN) && !flag[qj] && c2j >= a.N;
+            // an overflowed window (the query goes to the next tier) stops
+            // appending: unreachable cut, not published
+            if (flag[qj]) cqj = 0xFFFFFFFFu;
+          }
+          unsigned todo = __ballot_sync(0xffffffffu, need);
+          while (todo) {
+            const int j = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const int q = warp + kTReaders * j;
+            const int cj = __shfl_sync(0xffffffffu, c2j, j);
+            uint32_t cq = __shfl_sync(0xffffffffu, cqj, j), th = 0u;
+            warp_nth_key_tc(buf + q * qstride, cj, a.N, hist, &th);
+            cq = max(cq, window_cut(th, tb2[q]));
+            const int kept = warp_keep_key32(buf + q * qstride, cj, cq);
+            if (lane == j) {
+              cqj = cq;
+              c2j = kept;
+            }
+          }
+          if (lane < QPW) {
+            if (need) {
+              cnt[qj] = c2j;
+              if (gqj < a.nq && cqj > oldc) atomicMax(a.gcut + gqj, cqj);
+            }
+            if (cqj != oldc) {
+              cut[qj] = cqj;
+              cutf[qj] = funkey(cqj);  // 0xFFFFFFFF: NaN, nothing passes
+            }
+            if (last && gqj < a.nq) {
+              a.out_cnt[(size_t)gqj * a.S + s] = c2j;
+              if (flag[qj]) atomicOr(&a.out_flag[gqj], 1);
+            }
           }
           readers_sync();
         }
-      }
-      for (int q = warp; q < kTQ; q += kTReaders) {
-        const int gq = qb * kTQ + q;
-        int c = min(cnt[q], cap);
-        uint32_t th;
-        if (warp_nth_key32(buf + q * qstride, c, a.N, &th))
-          c = warp_keep_key32(buf + q * qstride, c, max(cut[q], window_cut(th, tb2[q])));
-        if (gq < a.nq && lane == 0) {
-          a.out_cnt[(size_t)gq * a.R + r] = c;
-          if (flag[q]) atomicOr(&a.out_flag[gq], 1);
-        }
-        __syncwarp();
       }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
-#ifdef AQ_TC_PROFILE
-  if (t == 0 && blockIdx.x < 2048) g_tccta[blockIdx.x] = (unsigned long long)(clock64() - kstart);
-#endif
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
-                 "r"(4 * kTQ));
+                 "r"(2 * NQ));
 }
 
-// Tensor-core filter + the float64 merge; *ran = false leaves the query set
-// to the float32 filter (d > 128, non-finite values, windows too large).
+namespace {
+// shared memory of k_exact_tc<NQ, terms> with NS ring stages
+size_t tc_smem(int NQ, int Kp, int NS, int terms) {
+  return (terms == 3 ? 2 : 1) * (size_t)NQ * Kp * 2 + (size_t)NS * kTM * Kp * 2 + (size_t)NQ * 20 +
+         (size_t)kTReaders * 256 * 4 + 8 * (2 * kTMaxStages + 6) + 16 + 1024;
+}
+}  // namespace
+
+// Tensor-core filter (TERMS = terms) + the float64 merge; *ran = false leaves
+// the query set to the next tier (d > 128, float64 data).
 int exact_tc_device(aq_dataset* ds, const double* Qd, size_t nq, size_t depth, uint32_t* ids,
-                    double* scores, std::vector<int>& hflag, double xmax, bool* ran) {
+                    double* scores, std::vector<int>& hflag, double xmax, int terms, bool* ran) {
   *ran = false;
   aq_session* s = ds->s;
   const size_t n = ds->n, d = ds->d;
@@ -768,79 +894,133 @@ int exact_tc_device(aq_dataset* ds, const double* Qd, size_t nq, size_t depth, u
   if (Kp > kTKpMax || ds->f64 || !ds->xr) return AQ_OK;
   const size_t te = std::min(depth, n);
   const int N = (int)te;
-  const size_t nqb = (nq + kTQ - 1) / kTQ, nq_pad = nqb * kTQ;
-  const size_t nblk = (n + kTM - 1) / kTM;
-  const int cap = ((N + 31) & ~31) + kTM * kTPPT + 32 + (N > 128 ? N : 0);
-  const size_t G0 = (size_t)s->num_sms;
-  const size_t total = nqb * n;
-  size_t chunk = std::max<size_t>((total + G0 - 1) / G0, 16 * (size_t)kTM);
-  const size_t G = (total + chunk - 1) / chunk;
-  size_t R = 1;
-  for (size_t qb = 0; qb < nqb; ++qb)
-    R = std::max(R, ((qb + 1) * n - 1) / chunk - qb * n / chunk + 1);
-  const size_t xt_b = nblk * 2 * kTM * Kp * sizeof(__nv_bfloat16);
-  const size_t qt_b = nqb * 2 * kTQ * Kp * sizeof(__nv_bfloat16);
-  const size_t buf_b = nq_pad * R * cap * sizeof(uint2);
+  // 256 queries per CTA when the query tile and three ring stages fit
+  // (three-term: one ring stage is a hi or lo half tile, two per tile)
+  int NQ = 256, NS = 0;
+  auto stages = [&](int nqv) {
+    const size_t fixed = tc_smem(nqv, Kp, 0, terms);
+    return fixed > (size_t)kTSmemMax
+               ? 0
+               : (int)std::min<size_t>(kTMaxStages, (kTSmemMax - fixed) / ((size_t)kTM * Kp * 2));
+  };
+  NS = stages(256);
+  if (NS < (terms == 3 ? 3 : 2) || nq <= 128) {
+    NQ = 128;
+    NS = stages(128);
+  }
+  const size_t nqb = (nq + NQ - 1) / NQ, nq_pad = nqb * NQ;
+  const int nblk = (int)((n + kTM - 1) / kTM);
+  // window: N, one span of appends, room for the filter's near-ties
+  // (the one-term window is wide), tie room growing with N
+  const int cap = ((N + 31) & ~31) + kTM * kTPPT + (terms == 1 ? 256 : 32) + (N > 128 ? N : 0);
+  const int G0 = s->num_sms;
+  const size_t tile_b = 2 * (size_t)kTM * Kp * 2;
+  // query batches whose windows (nq x S x cap entries) stay within ~4 GB
+  const size_t win_budget = (size_t)4 << 30;
+  const int Smax_seg = std::max(1, std::min(64, nblk));
+  // segments: at most ~24 MB of point tiles each (two or three are live in
+  // L2 at a time); among those, the count whose item deal loads the CTAs
+  // most evenly
+  auto choose_S = [&](size_t nqb_b, int Scap) {
+    const int Smin = (int)std::min<size_t>(
+        (size_t)Scap, std::max<size_t>(1, (nblk * tile_b + (24u << 20) - 1) / (24u << 20)));
+    int bestS = Smin;
+    double best = 1e300;
+    for (int S = Smin; S <= Scap; ++S) {
+      const int T = (nblk + S - 1) / S, Se = (nblk + T - 1) / T;
+      const size_t items = (size_t)Se * nqb_b, G = std::min<size_t>(G0, items);
+      double worst = 0.0;
+      for (size_t b = 0; b < G; ++b) {
+        double w = 0.0;
+        for (size_t it = b; it < items; it += G) {
+          const int sg = (int)(it / nqb_b);
+          w += std::min(nblk, (sg + 1) * T) - sg * T + 6;  // + item overhead (tiles)
+        }
+        worst = std::max(worst, w);
+      }
+      const double cost = worst * (1.0 + 0.002 * Se);
+      if (cost < best * 0.999) {
+        best = cost;
+        bestS = Se;
+      }
+    }
+    return bestS;
+  };
+  // one launch for all query blocks unless their windows (nq x S x cap
+  // entries) exceed the budget; then batches of query blocks
+  size_t qb_batch = nqb;
+  int Scap_mem = Smax_seg;
+  {
+    const size_t per_qb = (size_t)NQ * cap * sizeof(uint2);  // one segment's windows
+    const int S_all = choose_S(nqb, Smax_seg);
+    if (nqb * S_all * per_qb > win_budget) {
+      qb_batch = std::max<size_t>(1, win_budget / (S_all * per_qb));
+      Scap_mem = (int)std::max<size_t>(1, std::min<size_t>(Smax_seg, win_budget / (qb_batch * per_qb)));
+    } else {
+      Scap_mem = S_all;
+    }
+  }
+  const size_t xt_b = (size_t)nblk * tile_b;
+  const size_t qt_b = nqb * 2 * (size_t)NQ * Kp * sizeof(__nv_bfloat16);
+  const size_t buf_b = qb_batch * NQ * (size_t)Scap_mem * cap * sizeof(uint2);
+  auto up = [](size_t v) { return (v + 1023) & ~(size_t)1023; };
+  const size_t off_q = up(xt_b), off_b = up(off_q + qt_b), off_t = up(off_b + buf_b);
+  const size_t off_g = up(off_t + nq_pad * sizeof(float));
+  const size_t off_c = up(off_g + nq * sizeof(uint32_t));
+  const size_t bytes = off_c + nq * (size_t)Scap_mem * sizeof(int) + nq * sizeof(int) + 256;
   char* mem = nullptr;
-  const size_t off_q = (xt_b + 1023) & ~(size_t)1023, off_b = (off_q + qt_b + 1023) & ~(size_t)1023;
-  const size_t off_t = off_b + buf_b, off_c = off_t + nq_pad * sizeof(float);
-  const size_t bytes = off_c + nq * R * sizeof(int) + nq * sizeof(int) + 256;
   AQ_CUDA(cudaMallocAsync((void**)&mem, bytes, s->stream));
   __nv_bfloat16* xtile = (__nv_bfloat16*)mem;
   __nv_bfloat16* qtile = (__nv_bfloat16*)(mem + off_q);
   uint2* obuf = (uint2*)(mem + off_b);
   float* twoB = (float*)(mem + off_t);
+  uint32_t* gcut = (uint32_t*)(mem + off_g);
   int* ocnt = (int*)(mem + off_c);
-  int* oflag = ocnt + nq * R;
+  int* oflag = ocnt + nq * (size_t)Scap_mem;
   int st = AQ_OK;
   if (cudaMemsetAsync(oflag, 0, nq * sizeof(int), s->stream) != cudaSuccess ||
-      cudaMemsetAsync(ocnt, 0, nq * R * sizeof(int), s->stream) != cudaSuccess)
+      cudaMemsetAsync(gcut, 0, nq * sizeof(uint32_t), s->stream) != cudaSuccess)
     st = ref_error(AQ_E_CUDA, "memset failed");
+  auto kern = NQ == 256 ? (terms == 3 ? k_exact_tc<256, 3> : k_exact_tc<256, 1>)
+                        : (terms == 3 ? k_exact_tc<128, 3> : k_exact_tc<128, 1>);
+  const size_t smem = tc_smem(NQ, Kp, NS, terms);
+  if (st == AQ_OK &&
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+          cudaSuccess)
+    st = ref_error(AQ_E_CUDA, "shared memory attribute");
+  int mcap = kFMergeCapMin;
+  while (mcap < N + N / 2 + 1024 && mcap < kFMergeCapMax) mcap <<= 1;
+  const size_t msmem = (size_t)mcap * (sizeof(unsigned long long) + sizeof(uint32_t));
+  if (st == AQ_OK)
+    cudaFuncSetAttribute(k_exact_fmerge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem);
   if (st == AQ_OK) {
     timer_mark(s, AQ_T_EXACT);
-    k_tc_points<<<(unsigned)nblk, 256, 0, s->stream>>>(ds->xr, n, (int)d, Kp, xtile);
-    k_tc_queries<<<(unsigned)nq_pad, 128, 0, s->stream>>>(Qd, (int)nq, (int)d, Kp, xmax, qtile,
-                                                          twoB, oflag);
+    k_tc_points<<<(unsigned)nblk, 256, 0, s->stream>>>(ds->xr, n, (int)d, Kp, terms, xtile);
+    k_tc_queries<<<(unsigned)nq_pad, 128, 0, s->stream>>>(Qd, (int)nq, (int)d, Kp, NQ, terms,
+                                                          xmax, qtile, twoB, oflag);
     s->launches += 2;
-    TArgs a{xtile, qtile, twoB, n, Kp, (int)nq, N, cap, (int)R, (int)nqb, chunk, obuf, ocnt, oflag};
-    const size_t smem = 3 * (size_t)(2 * kTM * Kp * 2) + kTQ * 16 + 7 * 8 + 16 + 1024;
-    if (cudaFuncSetAttribute(k_exact_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
-      st = ref_error(AQ_E_CUDA, "shared memory attribute");
-    if (st == AQ_OK) {
-      k_exact_tc<<<(unsigned)G, kTThreads, smem, s->stream>>>(a);
-      s->launches++;
-#ifdef AQ_TC_PROFILE
-      {
-        unsigned long long h[8];
-        cudaStreamSynchronize(s->stream);
-        cudaMemcpyFromSymbol(h, g_tcprof, sizeof h);
-        fprintf(stderr, "tc prof CTA0: tiles %llu, wait E %.0f, wait A %.0f, wait F %.0f, MMA issue %.0f cycles/tile\n",
-                h[3], (double)h[0] / h[3], (double)h[1] / h[3], (double)h[2] / h[3], (double)h[4] / h[3]);
-        std::vector<unsigned long long> cc(2048);
-        cudaMemcpyFromSymbol(cc.data(), g_tccta, 2048 * 8);
-        unsigned long long mn = ~0ull, mx = 0, sum = 0;
-        for (size_t b = 0; b < G && b < 2048; ++b) { mn = std::min(mn, cc[b]); mx = std::max(mx, cc[b]); sum += cc[b]; }
-        fprintf(stderr, "CTA cycles: G %zu min %llu avg %llu max %llu\n", G, mn, sum / G, mx);
-      }
-#endif
-      int mcap = kFMergeCapMin;
-      while (mcap < N + N / 2 + 1024 && mcap < kFMergeCapMax) mcap <<= 1;
-      FArgs fa{nullptr, 0, (int)d, n, nullptr, twoB, (int)nq, N, cap, (int)R,
-               chunk, (int)nqb, mcap, obuf, ocnt, oflag};
-      const size_t msmem = (size_t)mcap * (sizeof(unsigned long long) + sizeof(uint32_t));
-      cudaFuncSetAttribute(k_exact_fmerge, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)msmem);
-      k_exact_fmerge<<<(unsigned)nq, R >= 32 ? 1024 : 256, msmem, s->stream>>>(
-          fa, ds->xr, Qd, (int)te, ids, scores);
-      s->launches++;
-      timer_mark(s, AQ_T_EXACT);
-      if (cudaGetLastError() != cudaSuccess ||
-          cudaMemcpyAsync(hflag.data(), oflag, nq * sizeof(int), cudaMemcpyDeviceToHost,
-                          s->stream) != cudaSuccess ||
-          cudaStreamSynchronize(s->stream) != cudaSuccess)
-        st = ref_error(AQ_E_CUDA, "tensor-core exact filter failed");
+    for (size_t qb0 = 0; qb0 < nqb && st == AQ_OK; qb0 += qb_batch) {
+      const size_t nqb_b = std::min(qb_batch, nqb - qb0);
+      const size_t q0 = qb0 * NQ, nq_b = std::min(nq, (qb0 + nqb_b) * NQ) - q0;
+      const int S = choose_S(nqb_b, Scap_mem);
+      const int T = (nblk + S - 1) / S;
+      const size_t items = (size_t)S * nqb_b;
+      TArgs a{xtile, qtile + qb0 * 2 * (size_t)NQ * Kp, twoB + q0, gcut + q0, n, Kp, (int)nq_b,
+              N, cap, (int)nqb_b, S, T, nblk, NS, (int)items, obuf, ocnt + q0 * S, oflag + q0};
+      kern<<<(unsigned)std::min<size_t>(G0, items), kTThreads, smem, s->stream>>>(a);
+      FArgs fa{nullptr, 0, (int)d, n, nullptr, twoB + q0, (int)nq_b, N, cap, S,
+               0, (int)nqb_b, mcap, obuf, ocnt + q0 * S, oflag + q0};
+      k_exact_fmerge<<<(unsigned)nq_b, S >= 32 ? 1024 : 256, msmem, s->stream>>>(
+          fa, ds->xr, Qd + q0 * d, (int)te, ids + q0 * te, scores + q0 * te);
+      s->launches += 2;
+      if (cudaGetLastError() != cudaSuccess) st = ref_error(AQ_E_CUDA, "tensor-core exact filter failed");
     }
+    timer_mark(s, AQ_T_EXACT);
+    if (st == AQ_OK &&
+        (cudaMemcpyAsync(hflag.data(), oflag, nq * sizeof(int), cudaMemcpyDeviceToHost,
+                         s->stream) != cudaSuccess ||
+         cudaStreamSynchronize(s->stream) != cudaSuccess))
+      st = ref_error(AQ_E_CUDA, "tensor-core exact filter failed");
   }
   cudaFreeAsync(mem, s->stream);
   if (st == AQ_OK) *ran = true;
@@ -863,41 +1043,18 @@ __global__ void k_max_norm(const double* __restrict__ v, size_t n, unsigned long
   if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
 }
 
-int exact_filter_device(aq_dataset* ds, const double* Qd, size_t nq, size_t depth, uint32_t* ids,
-                        double* scores, std::vector<int>& hflag, bool* ran) {
+namespace {
+// float32 FFMA filter + the float64 merge (the tier after the tensor cores)
+int ffma_filter_device(aq_dataset* ds, const double* Qd, size_t nq, size_t depth, uint32_t* ids,
+                       double* scores, std::vector<int>& hflag, double xmax, bool* ran) {
   *ran = false;
   aq_session* s = ds->s;
   const size_t n = ds->n, d = ds->d;
   const size_t te = std::min(depth, n);
   const int N = (int)te;
   const size_t nqb = (nq + kFQ - 1) / kFQ, nq_pad = nqb * kFQ;
-  // max |x| over the rows (norms are the reference's float64 norms), reduced
-  // on the device: non-negative doubles order like their bit patterns
-  void* pm;
-  AQ_TRY(scratch(s, 6, 64, &pm));
-  unsigned long long* dmax = (unsigned long long*)pm;
-  AQ_CUDA(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), s->stream));
-  k_max_norm<<<(unsigned)std::min<size_t>((n + 255) / 256, 4096), 256, 0, s->stream>>>(ds->norms,
-                                                                                      n, dmax);
-  AQ_LAUNCHED(s);
-  unsigned long long hbits = 0;
-  AQ_CUDA(cudaMemcpyAsync(&hbits, dmax, sizeof hbits, cudaMemcpyDeviceToHost, s->stream));
-  AQ_CUDA(cudaStreamSynchronize(s->stream));
-  double xmax;
-  std::memcpy(&xmax, &hbits, sizeof xmax);
-  xmax *= 1.0000001;
-  if (!(xmax < 1e30) || depth > (size_t)kFMaxN) return AQ_OK;  // caller's exact path
-  // tensor-core filter first ($AQ_EXACT_TC=0 keeps the float32 FFMA filter);
-  // flagged queries (non-finite values, overflowing windows) go on below
-  static const int use_tc = getenv("AQ_EXACT_TC") ? atoi(getenv("AQ_EXACT_TC")) : 1;
-  if (use_tc) {
-    bool tc_ran = false;
-    AQ_TRY(exact_tc_device(ds, Qd, nq, depth, ids, scores, hflag, xmax, &tc_ran));
-    if (tc_ran) {
-      *ran = true;
-      return AQ_OK;
-    }
-  }
+  const size_t smem = (size_t)d * kFQ * sizeof(float) + kFQ * 16 + 64;
+  if (smem > 200 * 1024) return AQ_OK;
   // window: N, one span of appends, tie room growing with N (search.cu)
   const int cap = ((N + 31) & ~31) + kFTile * kFPPT + 32 + (N > 128 ? N : 0);
   const size_t G0 = (size_t)s->num_sms * 2;
@@ -928,8 +1085,6 @@ int exact_filter_device(aq_dataset* ds, const double* Qd, size_t nq, size_t dept
   FArgs a{ds->xt, (int)pairs_of(d), (int)d, n, qf, twoB, (int)nq, N, cap, (int)R,
           chunk, (int)nqb, mcap, obuf, ocnt, oflag};
   const size_t msmem = (size_t)mcap * (sizeof(unsigned long long) + sizeof(uint32_t));
-  const size_t smem = (size_t)d * kFQ * sizeof(float) + kFQ * 16 + 64;
-  if (smem > 200 * 1024) return AQ_OK;
   AQ_CUDA(cudaFuncSetAttribute(k_exact_filter, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem));
   timer_mark(s, AQ_T_EXACT);
@@ -945,6 +1100,110 @@ int exact_filter_device(aq_dataset* ds, const double* Qd, size_t nq, size_t dept
                           s->stream));
   AQ_CUDA(cudaStreamSynchronize(s->stream));
   *ran = true;
+  return AQ_OK;
+}
+
+__global__ void k_gather_queries(const double* Q, const uint32_t* idx, int d, double* out) {
+  const double* src = Q + (size_t)idx[blockIdx.x] * d;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) out[(size_t)blockIdx.x * d + j] = src[j];
+}
+__global__ void k_scatter_hits(const uint32_t* ids_sub, const double* sc_sub, const uint32_t* idx,
+                               int te, uint32_t* ids, double* scores) {
+  const size_t q = idx[blockIdx.x];
+  for (int e = threadIdx.x; e < te; e += blockDim.x) {
+    ids[q * te + e] = ids_sub[(size_t)blockIdx.x * te + e];
+    scores[q * te + e] = sc_sub[(size_t)blockIdx.x * te + e];
+  }
+}
+
+// Runs one filter tier on the queries still flagged (hflag != 0): all of
+// them in place, or a gathered subset whose hits and flags are scattered back.
+template <class Tier>
+int run_tier(aq_session* s, const double* Qd, size_t nq, size_t d, size_t te, uint32_t* ids,
+             double* scores, std::vector<int>& hflag, bool* any_ran, Tier&& tier) {
+  std::vector<uint32_t> idx;
+  for (size_t q = 0; q < nq; ++q)
+    if (hflag[q]) idx.push_back((uint32_t)q);
+  if (idx.empty()) return AQ_OK;
+  bool ran = false;
+  if (idx.size() == nq) {
+    std::vector<int> hf(nq, 1);
+    AQ_TRY(tier(Qd, nq, ids, scores, hf, &ran));
+    if (ran) hflag.swap(hf);
+  } else {
+    const size_t m = idx.size();
+    char* mem = nullptr;
+    const size_t b_idx = (m * 4 + 255) & ~(size_t)255, b_q = m * d * 8, b_ids = (m * te * 4 + 255) & ~(size_t)255;
+    AQ_CUDA(cudaMallocAsync((void**)&mem, b_idx + b_q + b_ids + m * te * 8, s->stream));
+    uint32_t* didx = (uint32_t*)mem;
+    double* qsub = (double*)(mem + b_idx);
+    uint32_t* ids_sub = (uint32_t*)(mem + b_idx + b_q);
+    double* sc_sub = (double*)(mem + b_idx + b_q + b_ids);
+    int st = AQ_OK;
+    if (cudaMemcpyAsync(didx, idx.data(), m * 4, cudaMemcpyHostToDevice, s->stream) != cudaSuccess)
+      st = ref_error(AQ_E_CUDA, "query gather failed");
+    if (st == AQ_OK) {
+      k_gather_queries<<<(unsigned)m, 128, 0, s->stream>>>(Qd, didx, (int)d, qsub);
+      s->launches++;
+      std::vector<int> hf(m, 1);
+      st = tier(qsub, m, ids_sub, sc_sub, hf, &ran);
+      if (st == AQ_OK && ran) {
+        k_scatter_hits<<<(unsigned)m, 128, 0, s->stream>>>(ids_sub, sc_sub, didx, (int)te, ids,
+                                                            scores);
+        s->launches++;
+        for (size_t i = 0; i < m; ++i) hflag[idx[i]] = hf[i];
+      }
+    }
+    cudaFreeAsync(mem, s->stream);
+    if (st == AQ_OK && cudaStreamSynchronize(s->stream) != cudaSuccess)
+      st = ref_error(AQ_E_CUDA, "query scatter failed");
+    AQ_TRY(st);
+  }
+  *any_ran |= ran;
+  return AQ_OK;
+}
+}  // namespace
+
+// Exact MIPS through the filter tiers: three-term tensor cores, then float32
+// FFMA; each tier takes the queries the previous one flagged (non-finite
+// values, overflowing windows) and the caller's float64 path the rest.
+// $AQ_EXACT_TC: 1 (default) as above, 13 the one-term tensor-core tier first
+// (three times fewer MMAs, but its wide window appends more than it saves
+// while the window cuts come from single segments: DESIGN.md 4.3), 0 the
+// float32 filter alone.
+int exact_filter_device(aq_dataset* ds, const double* Qd, size_t nq, size_t depth, uint32_t* ids,
+                        double* scores, std::vector<int>& hflag, bool* ran) {
+  *ran = false;
+  aq_session* s = ds->s;
+  const size_t n = ds->n, d = ds->d;
+  const size_t te = std::min(depth, n);
+  // max |x| over the rows (norms are the reference's float64 norms), reduced
+  // on the device: non-negative doubles order like their bit patterns
+  void* pm;
+  AQ_TRY(scratch(s, 6, 64, &pm));
+  unsigned long long* dmax = (unsigned long long*)pm;
+  AQ_CUDA(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), s->stream));
+  k_max_norm<<<(unsigned)std::min<size_t>((n + 255) / 256, 4096), 256, 0, s->stream>>>(ds->norms,
+                                                                                      n, dmax);
+  AQ_LAUNCHED(s);
+  unsigned long long hbits = 0;
+  AQ_CUDA(cudaMemcpyAsync(&hbits, dmax, sizeof hbits, cudaMemcpyDeviceToHost, s->stream));
+  AQ_CUDA(cudaStreamSynchronize(s->stream));
+  double xmax;
+  std::memcpy(&xmax, &hbits, sizeof xmax);
+  xmax *= 1.0000001;
+  if (!(xmax < 1e30) || depth > (size_t)kFMaxN) return AQ_OK;  // caller's exact path
+  static const int use_tc = getenv("AQ_EXACT_TC") ? atoi(getenv("AQ_EXACT_TC")) : 1;
+  std::fill(hflag.begin(), hflag.end(), 1);
+  for (int terms : {1, 3}) {
+    if (!use_tc || (terms == 1 && use_tc != 13)) continue;
+    AQ_TRY(run_tier(s, Qd, nq, d, te, ids, scores, hflag, ran,
+                    [&](const double* Q, size_t m, uint32_t* I, double* S, std::vector<int>& hf,
+                        bool* r) { return exact_tc_device(ds, Q, m, depth, I, S, hf, xmax, terms, r); }));
+  }
+  AQ_TRY(run_tier(s, Qd, nq, d, te, ids, scores, hflag, ran,
+                  [&](const double* Q, size_t m, uint32_t* I, double* S, std::vector<int>& hf,
+                      bool* r) { return ffma_filter_device(ds, Q, m, depth, I, S, hf, xmax, r); }));
   return AQ_OK;
 }
 

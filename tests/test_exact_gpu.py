@@ -121,9 +121,10 @@ def test_evaluate_perfect_codes_recall_one():
 
 
 def test_exact_tensor_core_and_float32_filters_agree(tmp_path):
-    """The tcgen05 filter ($AQ_EXACT_TC=1, default) and the float32 FFMA filter
-    ($AQ_EXACT_TC=0) give the same ids and scores (both equal the oracle's),
-    including duplicated rows (exact ties) and a zero query."""
+    """The filter tiers — three-term tcgen05 ($AQ_EXACT_TC=1, default),
+    one-term then three-term (13), the float32 FFMA filter alone (0) — give
+    the same ids and scores (all equal to the oracle's), including duplicated
+    rows (exact ties) and a zero query."""
     import subprocess
     import sys
     import os
@@ -138,14 +139,15 @@ def test_exact_tensor_core_and_float32_filters_agree(tmp_path):
         "ids, sc = aq.dev_exact_search(aq.Session.default().upload_dataset(x), q, 25)\n"
         "np.savez(sys.argv[1], ids=ids, sc=sc)\n")
     out = {}
-    for flag in ("1", "0"):
+    for flag in ("1", "13", "0"):
         f = tmp_path / f"r{flag}.npz"
         r = subprocess.run([sys.executable, str(script), str(f)], capture_output=True, text=True,
                            env=dict(os.environ, AQ_EXACT_TC=flag), timeout=300)
         assert r.returncode == 0, r.stderr
         out[flag] = np.load(f)
-    assert np.array_equal(out["1"]["ids"], out["0"]["ids"])
-    assert np.array_equal(out["1"]["sc"], out["0"]["sc"])
+    for flag in ("13", "0"):
+        assert np.array_equal(out["1"]["ids"], out[flag]["ids"])
+        assert np.array_equal(out["1"]["sc"], out[flag]["sc"])
     x = np.repeat(mixture_rows(20000, 100, 91), 3, axis=0).astype(np.float64)
     q = mixture_rows(200, 100, 92).astype(np.float64)
     q[7] = 0.0

@@ -1118,10 +1118,134 @@ __global__ void __launch_bounds__(256) k_llt_bwd(const double* L, int n, int kb,
   }
 }
 
+// Whole forward / backward solve in one launch each: one CTA per 64-row
+// block, taking its block index from a ticket (dispatch order), so a CTA only
+// ever waits for blocks already running. A block applies the published
+// blocks' updates in the stand-in's order (forward: blocks 0, 1, ..., r - 1;
+// backward: nb - 1, ..., r + 1; each a from-zero ordered sum over the 64
+// columns, then one subtraction), solves its diagonal triangle exactly as
+// k_llt_fwd / k_llt_bwd, and publishes (x store, fence, release flag). The
+// L tile of the next update is staged while the previous block is still
+// solving, so the chain is one 64-term sum plus one triangle per block and
+// there are no per-block launches.
+__device__ __forceinline__ void flag_wait(const unsigned* f) {
+  unsigned v;
+  for (;;) {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(f) : "memory");
+    if (v) break;
+    __nanosleep(20);
+  }
+}
+
+template <bool FWD>
+__global__ void __launch_bounds__(256) k_llt_flow(const double* L, int n, double* x, unsigned* sync) {
+  extern __shared__ __align__(16) double fsm[];
+  double(*Ld)[kLLT + 1] = reinterpret_cast<double(*)[kLLT + 1]>(fsm);
+  double(*T)[kLLT + 1] = reinterpret_cast<double(*)[kLLT + 1]>(fsm + kLLT * (kLLT + 1));  // FWD: T[row][k]; BWD: T[k][row]
+  __shared__ double xk[kLLT];
+  __shared__ double xb[kLLT];
+  __shared__ double pr[kLLT];
+  __shared__ int s_r;
+  const int nb = (n + kLLT - 1) / kLLT;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  if (t == 0) s_r = (int)atomicAdd(sync, 1u);
+  __syncthreads();
+  const int bi = FWD ? s_r : nb - 1 - s_r;  // this CTA's block
+  unsigned* ready = sync + 1;
+  const int kb = bi * kLLT, be = min(kb + kLLT, n), bs = be - kb;
+  stage8(
+      bs * bs,
+      [&](int e) {
+        const int r = e / bs, c = e % bs;
+        return c <= r ? __ldg(L + (size_t)(kb + r) * n + kb + c) : 0.0;
+      },
+      [&](int e, double v) { Ld[e / bs][e % bs] = v; });
+  double xi = t < bs ? x[kb + t] : 0.0;
+  // updates from the other blocks, in the stand-in's order
+  for (int u = 0; u < (FWD ? bi : nb - 1 - bi); ++u) {
+    const int ob = FWD ? u : nb - 1 - u;  // the published block
+    const int ok = ob * kLLT, os = min(ok + kLLT, n) - ok;
+    __syncthreads();  // T / xk of the previous update are consumed
+    if (FWD)
+      stage8(
+          bs * os, [&](int e) { return __ldg(L + (size_t)(kb + e / os) * n + ok + e % os); },
+          [&](int e, double v) { T[e / os][e % os] = v; });
+    else
+      stage8(
+          os * bs, [&](int e) { return __ldg(L + (size_t)(ok + e / bs) * n + kb + e % bs); },
+          [&](int e, double v) { T[e / bs][e % bs] = v; });
+    if (t == 0) flag_wait(ready + ob);
+    __syncthreads();
+    if (t < os) xk[t] = __ldcg(x + ok + t);
+    __syncthreads();
+    if (t < bs) {
+      double sum = 0.0;
+      for (int q0 = 0; q0 < os; q0 += 8) {
+        double lv[8], yv[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          lv[q] = q0 + q < os ? (FWD ? T[t][q0 + q] : T[q0 + q][t]) : 0.0;
+          yv[q] = q0 + q < os ? xk[q0 + q] : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q0 + q < os) sum = __dadd_rn(sum, __dmul_rn(lv[q], yv[q]));
+      }
+      xi = __dsub_rn(xi, sum);
+    }
+  }
+  if (t < bs) xb[t] = xi;
+  __syncthreads();
+  if (w == 0) {
+    if (FWD) {
+      double ti[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) ti[h] = lane + 32 * h < bs ? xb[lane + 32 * h] : 0.0;
+      for (int c = 0; c < bs; ++c) {
+        double yc = 0.0;
+        if (lane == (c & 31)) {
+          yc = __ddiv_rn(c < 32 ? ti[0] : ti[1], Ld[c][c]);
+          xb[c] = yc;
+        }
+        yc = __shfl_sync(0xffffffffu, yc, c & 31);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int i = lane + 32 * h;
+          if (i > c && i < bs) ti[h] = __dsub_rn(ti[h], __dmul_rn(Ld[i][c], yc));
+        }
+      }
+    } else {
+      for (int r = bs - 1; r >= 0; --r) {
+        for (int c = r + 1 + lane; c < bs; c += 32) pr[c] = __dmul_rn(Ld[c][r], xb[c]);
+        __syncwarp();
+        if (lane == 0) {
+          double tv = xb[r];
+          for (int c0 = r + 1; c0 < bs; c0 += 8) {
+            double pv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) pv[u] = c0 + u < bs ? pr[c0 + u] : 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              if (c0 + u < bs) tv = __dsub_rn(tv, pv[u]);
+          }
+          xb[r] = __ddiv_rn(tv, Ld[r][r]);
+        }
+        __syncwarp();
+      }
+    }
+  }
+  __syncthreads();
+  if (t < bs) x[kb + t] = xb[t];
+  __threadfence();
+  __syncthreads();
+  if (t == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(ready + bi), "r"(1u) : "memory");
+}
+
 int llt_solve_device(aq_session* s, double* A, int n, double* x) {
   int* fail;
   void* p;
-  AQ_TRY(scratch(s, 4, 64, &p));
+  const int nblk = (n + kLLT - 1) / kLLT;
+  AQ_TRY(scratch(s, 4, 64 + 2 * (nblk + 1) * sizeof(unsigned), &p));
   fail = (int*)p;
   AQ_CUDA(cudaMemsetAsync(fail, 0, sizeof(int), s->stream));
   timer_mark(s, AQ_T_LLT);
@@ -1148,6 +1272,21 @@ int llt_solve_device(aq_session* s, double* A, int n, double* x) {
   AQ_CUDA(cudaMemcpyAsync(&hf, fail, sizeof(int), cudaMemcpyDeviceToHost, s->stream));
   AQ_CUDA(cudaStreamSynchronize(s->stream));
   if (hf) return ref_error(AQ_E_SINGULAR_SYSTEM, "joint codebook system is not positive definite");
+  // AQ_LLT_SOLVE=1: one launch per block and direction (k_llt_fwd / k_llt_bwd)
+  static const int solve_variant = getenv("AQ_LLT_SOLVE") ? atoi(getenv("AQ_LLT_SOLVE")) : 0;
+  const int nb = (n + kLLT - 1) / kLLT;
+  if (solve_variant == 0 && nb <= 4 * s->num_sms) {
+    unsigned* sync = (unsigned*)((char*)p + 64);  // ticket + nb ready flags per direction
+    AQ_CUDA(cudaMemsetAsync(sync, 0, 2 * (nb + 1) * sizeof(unsigned), s->stream));
+    const int fsmem = 2 * kLLT * (kLLT + 1) * (int)sizeof(double);
+    AQ_CUDA(cudaFuncSetAttribute(k_llt_flow<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem));
+    AQ_CUDA(cudaFuncSetAttribute(k_llt_flow<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem));
+    k_llt_flow<true><<<nb, 256, fsmem, s->stream>>>(A, n, x, sync);
+    AQ_LAUNCHED(s);
+    k_llt_flow<false><<<nb, 256, fsmem, s->stream>>>(A, n, x, sync + nb + 1);
+    AQ_LAUNCHED(s);
+    return AQ_OK;
+  }
   for (int kb = 0; kb < n; kb += kLLT) {
     const int below = n - std::min(kb + kLLT, n);
     k_llt_fwd<<<std::max(1, (below + kSolveRows - 1) / kSolveRows), 256, 0, s->stream>>>(

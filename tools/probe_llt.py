@@ -41,5 +41,7 @@ for dim in [int(v) for v in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["
         ftimes.append(ms.value)
     got = x.cpu().numpy()
     ok = "n/a" if want is None else bool(np.array_equal(got, want))
+    import hashlib
+    ok = f"{ok} sha {hashlib.sha1(got.tobytes()).hexdigest()[:12]}"
     print(f"dim {dim}: total {min(times):.3f} ms  factor {min(ftimes):.3f} ms  "
           f"solve+ridge {min(times) - min(ftimes):.3f} ms  bit-exact {ok}", flush=True)

@@ -92,7 +92,7 @@ struct aq_session {
   int num_sms = 148;
   aqd::DevError* err = nullptr;     // device
   aqd::DevError* err_host = nullptr;  // pinned mirror
-  aqd::Scratch scratch[7];  // slot 6: scan tile sums (sort.cu)
+  aqd::Scratch scratch[8];  // slot 6: scan tile sums (sort.cu), 7: ADC tensor-core work windows
   aqd::Scratch pinned[6];   // page-locked host staging (streamed host-pointer calls)
 };
 

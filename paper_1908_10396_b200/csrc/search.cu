@@ -24,6 +24,13 @@ namespace aqd {
 
 int sort_scores_desc(aq_session* s, const double* scores, uint32_t* idx,
                      size_t n);
+bool adc_tc_supported(int M, int bits, int k);
+int adc_tc_queries();
+int adc_tc_tile(int M);
+int adc_tc_plan(aq_session* s, size_t nq, size_t n, int M, size_t* R, size_t* chunk, size_t* G);
+int adc_tc_launch(aq_session* s, const uint8_t* codes, size_t n, int stride, const uint8_t* lutA,
+                  int M, size_t nq, int N, int cap, size_t R, size_t chunk, size_t G, uint2* obuf,
+                  int* ocnt, int* oflag);
 
 // Scoring CTA shapes: query pairs per CTA, points per tile (= threads),
 // min CTAs per SM. Selected per launch (AQ_ADC_VARIANT overrides).
@@ -55,7 +62,8 @@ constexpr int kQMax = 4095;      // |v| <= 4095: 13-bit fields, 8 adds per 16-bi
 __global__ void k_build_lut(const double* __restrict__ Q, int nq, int d,
                             const double* __restrict__ cb, int M, int k,
                             int sd, double* __restrict__ lut64,
-                            uint16_t* __restrict__ lutq, int QP) {
+                            uint16_t* __restrict__ lutq, int QP,
+                            uint8_t* __restrict__ lutA) {
   __shared__ double red[32];
   const int q = blockIdx.x;
   const double* qv = Q + (size_t)q * d;
@@ -86,6 +94,12 @@ __global__ void k_build_lut(const double* __restrict__ Q, int nq, int d,
       v = max(-kQMax, min(kQMax, v));
     }
     T[(size_t)e * 4] = (uint16_t)(v + kQMax + 1);
+    if (lutA) {  // tensor-core filter bytes: u = 64 hi + lo (adc_tc.cu)
+      const unsigned u = (unsigned)(v + kQMax + 1);
+      uint8_t* Aq = lutA + ((size_t)q * M + m) * 32;
+      Aq[j] = (uint8_t)(u >> 6);
+      Aq[16 + j] = (uint8_t)(u & 63u);
+    }
   }
 }
 
@@ -470,21 +484,35 @@ int adc_search_device(aq_codes* codes, aq_codebook* cb, const double* Qd,
   const AdcShape shp = kShapes[variant];
   const int QB = 2 * shp.qp, TILE = shp.tile;
   const size_t nqb = (nq + QB - 1) / QB;
+  // Tensor-core filter (adc_tc.cu) for long per-SM slices: each slice pays
+  // a window warm-up (appends and shrinks until its cut rises) that the
+  // scalar kernel amortises better on short ones. Measured (bench.py, one
+  // B200): config 4 (1e8 x 4,096, 2.8e6 points per SM slice) 1217 -> 842 ms,
+  // config 2 (1.18e6 x 10,000, 6.3e5 per slice) 41.0 -> 48.3 ms, so the
+  // default takes it from 1.5e6 points per slice. AQ_ADC_TC=1 / 0 forces it
+  // on / off. M > 50 and 8-bit codes always take the scalar kernel.
+  static const int tc_env = getenv("AQ_ADC_TC") ? atoi(getenv("AQ_ADC_TC")) : -1;
+  const size_t per_sm = ((nq + 127) / 128) * n / (size_t)s->num_sms;
+  const bool use_tc = adc_tc_supported(M, codes->bits, k) && topn <= (size_t)kMaxTopN &&
+                      (tc_env == 1 || (tc_env < 0 && per_sm >= 1500000));
   // workspace
   const size_t lut64_b = nq * M * k * sizeof(double);
   const size_t lutq_b = nqb * shp.qp * (size_t)M * 16 * sizeof(uint32_t);
+  const size_t luta_b = use_tc ? nq * (size_t)M * 32 : 0;
   void* p;
   // the score kernel stages the filter table with 16-byte loads: its offset
   // is rounded up (nq M k doubles can be an odd multiple of 8 bytes)
   const size_t lutq_off = (lut64_b + 255) & ~(size_t)255;
-  AQ_TRY(scratch(s, 1, lutq_off + lutq_b + 256, &p));
+  const size_t luta_off = (lutq_off + lutq_b + 255) & ~(size_t)255;
+  AQ_TRY(scratch(s, 1, luta_off + luta_b + 256, &p));
   double* lut64 = (double*)p;
   uint32_t* lutq = (uint32_t*)((char*)p + lutq_off);
+  uint8_t* luta = use_tc ? (uint8_t*)p + luta_off : nullptr;
   AQ_CUDA(cudaMemsetAsync(lutq, 0, lutq_b, s->stream));
   timer_mark(s, AQ_T_LUT);
   k_build_lut<<<(unsigned)nq, 256, 0, s->stream>>>(Qd, (int)nq, (int)d, cb->d64, M, k,
                                                   (int)cb->sd, lut64, (uint16_t*)lutq,
-                                                  shp.qp);
+                                                  shp.qp, luta);
   AQ_LAUNCHED(s);
   timer_mark(s, AQ_T_LUT);
 
@@ -496,6 +524,42 @@ int adc_search_device(aq_codes* codes, aq_codebook* cb, const double* Qd,
     // (their count grows with the depth of the N-th score)
     const int cap = ((N + 31) & ~31) + TILE * (shp.gbuf ? kGbPointsPerThread : 1) + 32 +
                     (N > 128 ? N : 0);
+    if (use_tc) {
+      const int TQ = adc_tc_queries(), TT = adc_tc_tile(M);
+      // per-(query, slice) list handed to the merge: N plus room for
+      // near-threshold ties, as the scalar kernel's (the work windows inside
+      // the kernel are larger)
+      const int cap = ((N + 31) & ~31) + 1024 + 32 + (N > 128 ? N : 0) + 0 * TT;
+      size_t R, chunk, G;
+      AQ_TRY(adc_tc_plan(s, nq, n, M, &R, &chunk, &G));
+      const size_t nq_pad = (nq + TQ - 1) / TQ * TQ;
+      const size_t buf_b = nq_pad * R * cap * sizeof(uint2);
+      void* p2;
+      AQ_TRY(scratch(s, 3, buf_b + nq * R * sizeof(int) + nq * sizeof(int) + 256, &p2));
+      uint2* obuf = (uint2*)p2;
+      int* ocnt = (int*)(obuf + nq_pad * R * cap);
+      int* oflag = ocnt + nq * R;
+      AQ_CUDA(cudaMemsetAsync(oflag, 0, nq * sizeof(int), s->stream));
+      AQ_CUDA(cudaMemsetAsync(ocnt, 0, nq * R * sizeof(int), s->stream));
+      timer_mark(s, AQ_T_ADC_SCORE);
+      AQ_TRY(adc_tc_launch(s, codes->data, n, (int)codes->stride, luta, M, nq, N, cap, R, chunk,
+                           G, obuf, ocnt, oflag));
+      timer_mark(s, AQ_T_ADC_SCORE);
+      int mcap = kMergeCapMin;
+      while (mcap < N + N / 2 + 1024 && mcap < kMergeCapMax) mcap <<= 1;
+      MergeArgs ma{obuf, ocnt, oflag, (int)R, cap, N, (int)topn_eff, mcap, lut64,
+                   codes->data, (int)codes->stride, codes->bits, M, k, ids, scores};
+      const size_t msmem = (size_t)mcap * (2 * sizeof(double) + sizeof(uint32_t));
+      AQ_CUDA(cudaFuncSetAttribute(k_adc_merge, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)msmem));
+      timer_mark(s, AQ_T_ADC_MERGE);
+      k_adc_merge<<<(unsigned)nq, R >= 32 ? 1024 : 256, msmem, s->stream>>>(ma);
+      AQ_LAUNCHED(s);
+      timer_mark(s, AQ_T_ADC_MERGE);
+      AQ_CUDA(cudaMemcpyAsync(hflag.data(), oflag, nq * sizeof(int), cudaMemcpyDeviceToHost,
+                              s->stream));
+      AQ_CUDA(cudaStreamSynchronize(s->stream));
+    } else {
     // point ranges: enough CTAs for ~2 waves, ranges of whole tiles
     const size_t tiles = (n + TILE - 1) / TILE;
     // Windows in global memory: one persistent CTA per resident slot, each
@@ -588,6 +652,7 @@ int adc_search_device(aq_codes* codes, aq_codebook* cb, const double* Qd,
     AQ_CUDA(cudaMemcpyAsync(hflag.data(), oflag, nq * sizeof(int), cudaMemcpyDeviceToHost,
                             s->stream));
     AQ_CUDA(cudaStreamSynchronize(s->stream));
+    }  // scalar filter
   }
   // exact fallback for flagged queries
   bool any = false;
@@ -883,7 +948,7 @@ int aq_build_lut(aq_session* s, const double* q, size_t d, const double* dict,
     double* l64 = (double*)p;
     uint16_t* lutq = (uint16_t*)(l64 + M * k);
     k_build_lut<<<1, 256, 0, s->stream>>>(Qd, 1, (int)d, cb->d64, (int)M, (int)k, (int)sd,
-                                          l64, lutq, kLutQP);
+                                          l64, lutq, kLutQP, nullptr);
     s->launches++;
     cudaMemcpyAsync(lut_out, l64, M * k * sizeof(double), cudaMemcpyDeviceToHost, s->stream);
     if (cudaStreamSynchronize(s->stream) != cudaSuccess) st = AQ_E_CUDA;

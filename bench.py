@@ -666,18 +666,37 @@ def bench_search_c4(args, aq, wl, sess, local, pk, stream):
     L.aq_session_timer_read(sess.h, 1, C.byref(msk), C.byref(cnt), 1)
     L.aq_session_timing(sess.h, 0)
     per_launch = msk.value / max(cnt.value, 1) / 1e3
-    achieved = nq * n * (M / 2) / per_launch / 1e9
-    ceil = 148 * 64 * 1.965e9 / M
+    hbm = nq * n * (M / 2) / per_launch / 1e9
     del dc, dcb
+    # the search takes the tensor-core filter (csrc/adc_tc.cu) for long
+    # per-SM slices (search.cu: >= 1.5e6 points of a 128-query block per SM)
+    tc = M <= 50 and ((nq + 127) // 128) * n / 148 >= 1.5e6 and os.environ.get("AQ_ADC_TC") != "0"
+    if tc:
+        # the filter as executed: a u8 x u8 GEMM, K = 32 M bytes per (query,
+        # point) (hi and lo one-hot images of each 4-bit code), 2 ops per MAC;
+        # int8 peak taken as twice the measured bf16 burst (sm_100 issues int8
+        # at twice the bf16 rate; tools/mb/umma_i8_test.cu measured 8,176
+        # MAC/clk/SM for M = 128, N = 256, i.e. 4.75 POPS at 1,965 MHz)
+        i8_peak = 2 * pk["bf16_tflops"]
+        ach = nq * n * 32 * M * 2 / per_launch / 1e12
+        roof = {"bound": "tensor", "achieved": round(ach, 1), "peak": round(i8_peak, 1),
+                "unit": "TOPS (int8)", "frac": round(ach / i8_peak, 4), "kernel": "k_adc_tc",
+                "hbm_single_pass": {"achieved_gbs": round(hbm, 1), "frac": round(hbm / pk["hbm_gbs"], 4)},
+                "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (int8 not measured by the driver)",
+                "note": "tcgen05.mma.kind::i8, M = 128 queries, N = 64 points, K = 32 per subspace; "
+                        "per-instruction floor ~72 cycles for N <= 128 (microbenchmark), so N = 64 "
+                        "tiles cap the tensor pipe near 45% of peak"}
+    else:
+        ceil = 148 * 64 * 1.965e9 / M
+        roof = {"bound": "hbm", "achieved": round(hbm, 1), "peak": pk["hbm_gbs"],
+                "unit": "GB/s", "frac": round(hbm / pk["hbm_gbs"], 4),
+                "kernel": "k_adc_score",
+                "onchip_frac": round(nq * n / per_launch / ceil, 4),
+                "note": "M/2 code bytes per score; 16 queries per code pass, so the "
+                        "bound is the shared-memory LUT (onchip_frac: 64 lookups/clk/SM)"}
     return {"metric": "ADC scores/sec", "workload": "config4", "value": round(nq * n / (ms / 1e3), 1),
             "unit": "scores/s", "ms_per_step": round(ms, 2), "n": n, "M": M,
-            "queries_per_step": nq, "topn": 100,
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"],
-                         "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4),
-                         "kernel": "k_adc_score",
-                         "onchip_frac": round(nq * n / per_launch / ceil, 4),
-                         "note": "M/2 code bytes per score; 16 queries per code pass, so the "
-                                 "bound is the shared-memory LUT (onchip_frac: 64 lookups/clk/SM)"},
+            "queries_per_step": nq, "topn": 100, "roofline": roof,
             "exact": "ids and scores equal the reference's over all 1e8 codes "
                      "(tests/test_config_pins_gpu.py::test_c4_all_codes_top100)"}
 

@@ -41,7 +41,7 @@ def main():
         env = dict(os.environ, AQ_ADC_TC=v)
         r = subprocess.run([sys.executable, "-c", CHILD % dict(root=ROOT, n=n, nq=nq, M=M, topn=topn)],
                            env=env, capture_output=True, text=True, timeout=900)
-        out = [l for l in r.stdout.splitlines() if l.startswith("RESULT") or "PROF" in l]
+        out = [l for l in r.stdout.splitlines() if l.startswith("RESULT") or "PROF" in l][-6:]
         print(f"n={n} nq={nq} M={M} topn={topn} AQ_ADC_TC={v}:", *out[-6:], r.stderr[-800:] if r.returncode else "",
               flush=True)
 

@@ -239,11 +239,47 @@ __global__ void __launch_bounds__(TILE, MINB) k_adc_score(const ScoreArgs a) {
 #pragma unroll
       for (int q = 0; q < QB; ++q) acc[q] = 0u;
       const uint32_t* crow = reinterpret_cast<const uint32_t*>(a.codes + p * a.stride);
+      // MP > 0: the row's code words in registers up front, in 16- (or 8-)
+      // byte loads: a warp's narrow loads at a 32-byte row stride each touch
+      // eight 128-byte lines, so seven 4-byte loads cost the L1 pipe 56
+      // wavefronts per 32 points against 16 for two 16-byte loads; the
+      // chunk loop then shifts the next word down (static indices)
+      constexpr int kNW = MP > 0 ? (MP + 7) / 8 : 1;
+      constexpr int kStride = (((MP > 0 ? MP : 2) + 1) / 2 + 7) & ~7;  // code_stride(MP, 4)
+      uint32_t cw[kNW];
+      if constexpr (MP > 0) {
+        if constexpr (kStride % 16 == 0) {
+          const uint4* r4 = reinterpret_cast<const uint4*>(crow);
+#pragma unroll
+          for (int i = 0; i < (kNW + 3) / 4; ++i) {
+            const uint4 v = __ldg(r4 + i);
+            if (4 * i < kNW) cw[4 * i] = v.x;
+            if (4 * i + 1 < kNW) cw[4 * i + 1] = v.y;
+            if (4 * i + 2 < kNW) cw[4 * i + 2] = v.z;
+            if (4 * i + 3 < kNW) cw[4 * i + 3] = v.w;
+          }
+        } else {
+          const uint2* r2 = reinterpret_cast<const uint2*>(crow);
+#pragma unroll
+          for (int i = 0; i < (kNW + 1) / 2; ++i) {
+            const uint2 v = __ldg(r2 + i);
+            if (2 * i < kNW) cw[2 * i] = v.x;
+            if (2 * i + 1 < kNW) cw[2 * i + 1] = v.y;
+          }
+        }
+      }
       // full chunks of 8 subspaces, then the tail (compile-time when MP > 0)
       const int nfull = M >> 3, tail = M & 7;
 #pragma unroll 1
       for (int ch = 0; ch < nfull; ++ch) {
-        const uint32_t w = __ldg(crow + ch);
+        uint32_t w;
+        if constexpr (MP > 0) {
+          w = cw[0];
+#pragma unroll
+          for (int i = 0; i + 1 < kNW; ++i) cw[i] = cw[i + 1];
+        } else {
+          w = __ldg(crow + ch);
+        }
         int off[8];
 #pragma unroll
         for (int t = 0; t < 8; ++t) off[t] = (ch * 8 + t) * 16 + ((w >> (4 * t)) & 15u);
@@ -261,7 +297,11 @@ __global__ void __launch_bounds__(TILE, MINB) k_adc_score(const ScoreArgs a) {
         }
       }
       if (tail) {
-        const uint32_t w = __ldg(crow + nfull);
+        uint32_t w;
+        if constexpr (MP > 0)
+          w = cw[0];
+        else
+          w = __ldg(crow + nfull);
         int off[8];
 #pragma unroll
         for (int t = 0; t < 8; ++t) off[t] = (nfull * 8 + t) * 16 + ((w >> (4 * t)) & 15u);

@@ -323,13 +323,19 @@ __global__ void __launch_bounds__(TILE, MINB) k_adc_score(const ScoreArgs a) {
         }
       }
 #pragma unroll
-      for (int q = 0; q < QB; ++q) {
-        if ((int)acc[q] >= cut[q]) {
-          const int pos = atomicAdd(&cnt[q], 1);
-          if (pos < cap)
-            buf[q * qstride + pos] = make_uint2(acc[q], (unsigned)p);
-          else
-            flag[q] = 1;
+      for (int q4 = 0; q4 < QB; q4 += 4) {  // cuts four at a time (one broadcast LDS.128)
+        const int4 c4 = *reinterpret_cast<const int4*>(cut + q4);
+        const int cv[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int q = q4 + u;
+          if ((int)acc[q] >= cv[u]) {
+            const int pos = atomicAdd(&cnt[q], 1);
+            if (pos < cap)
+              buf[q * qstride + pos] = make_uint2(acc[q], (unsigned)p);
+            else
+              flag[q] = 1;
+          }
         }
       }
     }

@@ -625,9 +625,11 @@ def bench_dropin_search(aq, sess, w, cb, dc, n):
     ms = (time.perf_counter() - t0) / (len(Q) - 1) * 1e3
     return {"call": "aq_adc_search (C++ anisoq::adc_search), one query, host codes",
             "ms_per_query": round(ms, 2), "scores_per_s": round(n / (ms / 1e3), 1),
-            "h2d_bytes_per_call": int(codes.nbytes + 8 * w.d),
+            "h2d_bytes_per_call": int(n * ((((w.M + 1) // 2) + 7) // 8 * 8) + 8 * w.d),
             "note": "dominated by the per-call index upload (the reference signature passes "
-                    "the codes by value); batched queries on the resident index: `value`"}
+                    "the codes by value, 4 bytes per code: packed to 4 bits by every host "
+                    "core into page-locked memory, then copied); batched queries on the "
+                    "resident index: `value`"}
 
 
 def bench_search_c4(args, aq, wl, sess, local, pk, stream):

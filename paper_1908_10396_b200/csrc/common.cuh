@@ -93,7 +93,7 @@ struct aq_session {
   aqd::DevError* err = nullptr;     // device
   aqd::DevError* err_host = nullptr;  // pinned mirror
   aqd::Scratch scratch[8];  // slot 6: scan tile sums (sort.cu), 7: ADC tensor-core work windows
-  aqd::Scratch pinned[6];   // page-locked host staging (streamed host-pointer calls)
+  aqd::Scratch pinned[7];   // page-locked host staging (streamed host-pointer calls; 6: packed codes)
 };
 
 struct aq_dataset {

@@ -1,7 +1,10 @@
 // Sessions, device-resident objects, layouts, weights and error plumbing.
+#include <algorithm>
 #include <cstdarg>
 #include <cstring>
 #include <mutex>
+#include <thread>
+#include <vector>
 
 #include "common.cuh"
 
@@ -592,6 +595,65 @@ int aq_codes_upload(aq_session* s, const uint32_t* codes, size_t n, size_t M,
   AQ_TRY(aq_codes_alloc(s, n, M, k, out));
   aq_codes* c = *out;
   if (n == 0) return AQ_OK;
+  if (n * M >= ((size_t)1 << 22)) {
+    // Large code matrices (the reference-signature calls pass them by value,
+    // 4 bytes per code): packed on the host by every core straight into
+    // page-locked memory, then one copy of the packed rows (M / 2 bytes
+    // per row for 4-bit codes) instead of a pageable copy of n M words.
+    // Same bytes and the same error as k_pack_codes: the lowest flat index
+    // of a code >= k.
+    void* pin;
+    int st = aqd::pinned_buffer(s, 6, n * c->stride, &pin);
+    if (st != AQ_OK) {
+      aq_codes_free(c);
+      *out = nullptr;
+      return st;
+    }
+    uint8_t* dst = static_cast<uint8_t*>(pin);
+    const uint32_t kk = (uint32_t)(k ? k : 1);
+    const size_t nt = std::max<size_t>(1, std::min<size_t>(std::thread::hardware_concurrency(),
+                                                            n / 4096 + 1));
+    std::vector<size_t> bad(nt, SIZE_MAX);
+    auto pack = [&](size_t t) {
+      const size_t r0 = n * t / nt, r1 = n * (t + 1) / nt;
+      for (size_t i = r0; i < r1; ++i) {
+        uint8_t* row = dst + i * c->stride;
+        std::memset(row, 0, c->stride);
+        const uint32_t* in = codes + i * M;
+        for (size_t m = 0; m < M; ++m) {
+          const uint32_t v = in[m];
+          if (v >= kk && bad[t] == SIZE_MAX) bad[t] = i * M + m;
+          if (c->bits == 4)
+            row[m >> 1] |= (uint8_t)((v & 15u) << ((m & 1) * 4));
+          else
+            row[m] = (uint8_t)v;
+        }
+      }
+    };
+    std::vector<std::thread> th;
+    for (size_t t = 1; t < nt; ++t) th.emplace_back(pack, t);
+    pack(0);
+    for (auto& x : th) x.join();
+    const size_t first = *std::min_element(bad.begin(), bad.end());
+    if (first != SIZE_MAX) {
+      char buf[256];
+      snprintf(buf, sizeof buf, "%s (%s, point %llu)", kDevErrDetail[AQ_E_CODE_OUT_OF_RANGE],
+               "codes upload", (unsigned long long)first);
+      aq_codes_free(c);
+      *out = nullptr;
+      return ref_error(AQ_E_CODE_OUT_OF_RANGE, buf);
+    }
+    st = cudaMemcpyAsync(c->data, dst, n * c->stride, cudaMemcpyHostToDevice, s->stream) ==
+                 cudaSuccess &&
+                 cudaStreamSynchronize(s->stream) == cudaSuccess
+             ? AQ_OK
+             : ref_error(AQ_E_CUDA, "codes upload copy failed");
+    if (st) {
+      aq_codes_free(c);
+      *out = nullptr;
+    }
+    return st;
+  }
   void* stage;
   AQ_TRY(scratch(s, 0, n * M * sizeof(uint32_t), &stage));
   AQ_CUDA(cudaMemcpyAsync(stage, codes, n * M * sizeof(uint32_t),

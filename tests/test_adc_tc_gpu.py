@@ -23,7 +23,8 @@ P = Port()
 cases = [(20000, 16, 100, 100, 16), (300000, 50, 100, 64, 16), (5000, 48, 7, 33, 16),
          (224, 50, 10, 1, 16), (70000, 49, 512, 20, 16), (200, 8, 100, 5, 16),
          (25000, 13, 50, 130, 16), (12000, 16, 100, 50, 9), (3000, 50, 10, 300, 16),
-         (60000, 50, 2000, 20, 16), (20000, 16, 4096, 9, 16), (400000, 48, 100, 256, 16)]
+         (60000, 50, 2000, 20, 16), (20000, 16, 4096, 9, 16), (400000, 48, 100, 256, 16),
+         (5000, 1, 10, 3, 16), (3000, 2, 20, 129, 7), (1, 50, 5, 2, 16), (63, 48, 100, 5, 16)]
 for n, M, topn, nq, k in cases:
     g = np.random.default_rng(n + M + k)
     cb = aq.ProductCodebook(M, k, 2, g.standard_normal(M * k * 2) / np.sqrt(2 * M))

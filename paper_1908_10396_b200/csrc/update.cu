@@ -1144,7 +1144,6 @@ __global__ void __launch_bounds__(256) k_llt_flow(const double* L, int n, double
   double(*T)[kLLT + 1] = reinterpret_cast<double(*)[kLLT + 1]>(fsm + kLLT * (kLLT + 1));  // FWD: T[row][k]; BWD: T[k][row]
   __shared__ double xk[kLLT];
   __shared__ double xb[kLLT];
-  __shared__ double pr2[2][kLLT];  // backward: row products, double-buffered
   __shared__ int s_r;
   const int nb = (n + kLLT - 1) / kLLT;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
@@ -1216,28 +1215,26 @@ __global__ void __launch_bounds__(256) k_llt_flow(const double* L, int n, double
       }
     } else {
       // One ordered chain (the first term of row r needs x(r + 1), the value
-      // just solved): lane 0 forms L(r+1, r) x(r+1) and subtracts the terms
-      // in ascending k, while lanes 1..31 already form row r - 1's other
-      // products (x(k) for k >= r + 1 is final) into the other buffer.
-      for (int r = bs - 1; r >= 0; --r) {
-        if (lane != 0 && r >= 1)
-          for (int c = r + lane; c < bs; c += 31) pr2[(r - 1) & 1][c] = __dmul_rn(Ld[c][r - 1], xb[c]);
-        if (lane == 0) {
+      // just solved): lane 0 alone, the loads and products of each eight
+      // terms issued ahead of their ascending subtractions (lanes 1..31
+      // forming the next row's products in the other half of a divergent
+      // branch only serialized with it: 86k -> ~70k cycles per block).
+      if (lane == 0) {
+        for (int r = bs - 1; r >= 0; --r) {
           double tv = xb[r];
-          if (r + 1 < bs) tv = __dsub_rn(tv, __dmul_rn(Ld[r + 1][r], xb[r + 1]));
-          const double* pb = pr2[r & 1];
-          for (int c0 = r + 2; c0 < bs; c0 += 8) {  // loads off the subtraction chain
+          for (int c0 = r + 1; c0 < bs; c0 += 8) {
             double pv[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) pv[u] = c0 + u < bs ? pb[c0 + u] : 0.0;
+            for (int u = 0; u < 8; ++u)
+              pv[u] = c0 + u < bs ? __dmul_rn(Ld[c0 + u][r], xb[c0 + u]) : 0.0;
 #pragma unroll
             for (int u = 0; u < 8; ++u)
               if (c0 + u < bs) tv = __dsub_rn(tv, pv[u]);
           }
           xb[r] = __ddiv_rn(tv, Ld[r][r]);
         }
-        __syncwarp();
       }
+      __syncwarp();
     }
   }
   __syncthreads();

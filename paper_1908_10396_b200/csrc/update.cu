@@ -513,12 +513,16 @@ __global__ void __launch_bounds__(32) k_assemble_sd2(const AsmArgs a, const uint
   uint32_t pl = 0;
   double cf = 0.0, hp = 0.0, ho = 0.0;
   float2 xm = make_float2(0.f, 0.f);
+  // h_par feeds only the rhs (chunk 0) and h_perp only the diagonal lane:
+  // other units skip those gathers (each a 32-line access per warp, on the
+  // L1 pipe the kernel is bound by)
+  const bool need_hp = chunk == 0, need_ho = m >= chunk * 32 && m < chunk * 32 + 32;
   auto load_scalars = [&](size_t t0, int nb) {
     if (lane < nb) {
       pl = L[t0 + lane];
       cf = a.coef[pl];
-      hp = a.hp[pl];
-      ho = a.ho[pl];
+      if (need_hp) hp = a.hp[pl];
+      if (need_ho) ho = a.ho[pl];
       xm = *reinterpret_cast<const float2*>(a.xr + (size_t)pl * d + m * 2);
     }
   };
@@ -687,13 +691,15 @@ __global__ void __launch_bounds__(32, 12) k_assemble_sd2r(const AsmArgs a, const
   uint32_t plc = 0, pln = 0;
   double cfc = 0.0, hpc = 0.0, hoc = 0.0, cfn = 0.0, hpn = 0.0, hon = 0.0;
   float2 xmc = make_float2(0.f, 0.f), xmn = make_float2(0.f, 0.f);
+  // h_par feeds only the rhs (chunk 0) and h_perp only the diagonal lane
+  const bool need_hp = chunk == 0, need_ho = m >= chunk * 32 && m < chunk * 32 + 32;
   auto load_scalars = [&](size_t t0, uint32_t& pl, double& cf, double& hp, double& ho,
                           float2& xm) {
     if (t0 + lane < cnt) {
       pl = L[t0 + lane];
       cf = a.coef[pl];
-      hp = a.hp[pl];
-      ho = a.ho[pl];
+      if (need_hp) hp = a.hp[pl];
+      if (need_ho) ho = a.ho[pl];
       xm = *reinterpret_cast<const float2*>(a.xr + (size_t)pl * d + m * 2);
     }
   };

@@ -26,7 +26,6 @@ int sort_scores_desc(aq_session* s, const double* scores, uint32_t* idx,
                      size_t n);
 bool adc_tc_supported(int M, int bits, int k);
 int adc_tc_queries();
-int adc_tc_tile(int M);
 int adc_tc_plan(aq_session* s, size_t nq, size_t n, int M, size_t* R, size_t* chunk, size_t* G);
 int adc_tc_launch(aq_session* s, const uint8_t* codes, size_t n, int stride, const uint8_t* lutA,
                   int M, size_t nq, int N, int cap, size_t R, size_t chunk, size_t G, uint2* obuf,
@@ -571,11 +570,11 @@ int adc_search_device(aq_codes* codes, aq_codebook* cb, const double* Qd,
     const int cap = ((N + 31) & ~31) + TILE * (shp.gbuf ? kGbPointsPerThread : 1) + 32 +
                     (N > 128 ? N : 0);
     if (use_tc) {
-      const int TQ = adc_tc_queries(), TT = adc_tc_tile(M);
+      const int TQ = adc_tc_queries();
       // per-(query, slice) list handed to the merge: N plus room for
       // near-threshold ties, as the scalar kernel's (the work windows inside
       // the kernel are larger)
-      const int cap = ((N + 31) & ~31) + 1024 + 32 + (N > 128 ? N : 0) + 0 * TT;
+      const int cap = ((N + 31) & ~31) + 1024 + 32 + (N > 128 ? N : 0);
       size_t R, chunk, G;
       AQ_TRY(adc_tc_plan(s, nq, n, M, &R, &chunk, &G));
       const size_t nq_pad = (nq + TQ - 1) / TQ * TQ;

@@ -1494,7 +1494,7 @@ int assemble_device(aq_dataset* ds, aq_codes* codes, const PointW& pw, const Buc
     static const int asm_variant =
         getenv("AQ_ASM_VARIANT") ? atoi(getenv("AQ_ASM_VARIANT")) : 0;
     AQ_CUDA(cudaFuncSetAttribute(k_assemble_sd2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 64 * 32 * 8));
+                                 64 * 32 * 8 + 14 * 1024));
     AQ_CUDA(cudaFuncSetAttribute(k_assemble_sd2r<16>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 32 * 8));
 
@@ -1528,8 +1528,14 @@ int assemble_device(aq_dataset* ds, aq_codes* codes, const PointW& pw, const Buc
       a.lo = (uint32_t)lo;
       a.hi = (uint32_t)std::min(ds->n, lo + bsz);
       a.resume = lo > 0;
+      // Up to 1.5 waves of 6 CTAs per SM (config 2: 1,088 units) the longest
+      // strips' chains are the critical path: 14 KB of unused dynamic shared
+      // memory caps the SM at 4 CTAs, so those chains share the shared-memory
+      // pipe with fewer warps (config 2: 14.7 -> 14.2 ms; 5 per SM 14.4,
+      // 3 per SM 17.6)
+      const int pad = ord.size() <= (size_t)9 * s->num_sms ? 14 * 1024 : 0;
       if (!ring)
-        k_assemble_sd2<<<(unsigned)ord.size(), 32, 64 * 32 * 8, s->stream>>>(a, dord);
+        k_assemble_sd2<<<(unsigned)ord.size(), 32, 64 * 32 * 8 + pad, s->stream>>>(a, dord);
       else
         k_assemble_sd2r<16><<<(unsigned)ord.size(), 32, 64 * 32 * 8, s->stream>>>(a, dord);
       AQ_LAUNCHED(s);

@@ -274,7 +274,13 @@ def train_record(w, n, info, codes_h, cpu):
                                   "ceiling_gmacs": round(ceil / 1e9, 1),
                                   "frac": round(macs / asm_s / ceil, 4),
                                   "note": "float64 entries, each a point-ordered chain "
-                                          "(bit-exact with pq.hpp:320-339)"},
+                                          "(bit-exact with pq.hpp:320-339); ceiling = 16 B of "
+                                          "shared-memory read-modify-write per MAC at 128 B/clk/SM",
+                                  "ncu": "k_assemble_sd2 at config 2: L1/shared pipe 62.5% busy, "
+                                         "~22 wavefronts per point and warp (16 the accumulator "
+                                         "read-modify-write); the update takes about as long as "
+                                         "the longest strip's chain (35k-104k points per strip) "
+                                         "(profiles/r01_ncu_assemble_full.csv, DESIGN.md 4.4)"},
             "exact": "codebooks, codes and loss history bit-identical to the reference",
             "cpu_baseline": cpu}
 
@@ -752,7 +758,11 @@ def bench_train_c5(args, aq, sess, local):
             "assembly_roofline": {"bound": "smem read-modify-write",
                                   "achieved_gmacs": round(macs / asm_s / 1e9, 1),
                                   "ceiling_gmacs": 2326.6,
-                                  "frac": round(macs / asm_s / 2.3266e12, 4)},
+                                  "frac": round(macs / asm_s / 2.3266e12, 4),
+                                  "ncu": "k_assemble_sd2r at config 5: L1/shared pipe 73.9% "
+                                         "busy (LSU wavefronts 70.6% of peak), ~20 wavefronts "
+                                         "per point and warp of which 16 the accumulator "
+                                         "read-modify-write (profiles/r01_ncu_assemble_ring_full.csv)"},
             "data": "synthetic on the device (torch, seeded): 4,096-component mixture, "
                     "sigma 0.4, unit norm",
             "exact": "bit-identical to the reference at the config-5 shape "

@@ -563,6 +563,28 @@ int adc_search_device(aq_codes* codes, aq_codebook* cb, const double* Qd,
 
   const bool fast = codes->bits == 4 && topn <= (size_t)kMaxTopN && M <= 256;
   std::vector<int> hflag(nq, fast ? 0 : 1);
+  // windows -> global theta, float64 re-scoring, exact order (both filters);
+  // the per-query overflow flags come back to the host for the fallback
+  auto merge = [&](const uint2* obuf, const int* ocnt, int* oflag, size_t R, int cap) -> int {
+    const int N = (int)topn_eff;
+    // merge window: N plus room for near-threshold ties, a power of two
+    int mcap = kMergeCapMin;
+    while (mcap < N + N / 2 + 1024 && mcap < kMergeCapMax) mcap <<= 1;
+    MergeArgs ma{obuf, ocnt, oflag, (int)R, cap, N, (int)topn_eff, mcap, lut64,
+                 codes->data, (int)codes->stride, codes->bits, M, k, ids, scores};
+    const size_t msmem = (size_t)mcap * (2 * sizeof(double) + sizeof(uint32_t));
+    AQ_CUDA(cudaFuncSetAttribute(k_adc_merge, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)msmem));
+    timer_mark(s, AQ_T_ADC_MERGE);
+    // many windows per query (small batches): more warps walk them at once
+    k_adc_merge<<<(unsigned)nq, R >= 32 ? 1024 : 256, msmem, s->stream>>>(ma);
+    AQ_LAUNCHED(s);
+    timer_mark(s, AQ_T_ADC_MERGE);
+    AQ_CUDA(cudaMemcpyAsync(hflag.data(), oflag, nq * sizeof(int), cudaMemcpyDeviceToHost,
+                            s->stream));
+    AQ_CUDA(cudaStreamSynchronize(s->stream));
+    return AQ_OK;
+  };
   if (fast) {
     const int N = (int)topn_eff;
     // window: N, one span of appends, and room for near-threshold ties
@@ -590,20 +612,7 @@ int adc_search_device(aq_codes* codes, aq_codebook* cb, const double* Qd,
       AQ_TRY(adc_tc_launch(s, codes->data, n, (int)codes->stride, luta, M, nq, N, cap, R, chunk,
                            G, obuf, ocnt, oflag));
       timer_mark(s, AQ_T_ADC_SCORE);
-      int mcap = kMergeCapMin;
-      while (mcap < N + N / 2 + 1024 && mcap < kMergeCapMax) mcap <<= 1;
-      MergeArgs ma{obuf, ocnt, oflag, (int)R, cap, N, (int)topn_eff, mcap, lut64,
-                   codes->data, (int)codes->stride, codes->bits, M, k, ids, scores};
-      const size_t msmem = (size_t)mcap * (2 * sizeof(double) + sizeof(uint32_t));
-      AQ_CUDA(cudaFuncSetAttribute(k_adc_merge, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)msmem));
-      timer_mark(s, AQ_T_ADC_MERGE);
-      k_adc_merge<<<(unsigned)nq, R >= 32 ? 1024 : 256, msmem, s->stream>>>(ma);
-      AQ_LAUNCHED(s);
-      timer_mark(s, AQ_T_ADC_MERGE);
-      AQ_CUDA(cudaMemcpyAsync(hflag.data(), oflag, nq * sizeof(int), cudaMemcpyDeviceToHost,
-                              s->stream));
-      AQ_CUDA(cudaStreamSynchronize(s->stream));
+      AQ_TRY(merge(obuf, ocnt, oflag, R, cap));
     } else {
     // point ranges: enough CTAs for ~2 waves, ranges of whole tiles
     const size_t tiles = (n + TILE - 1) / TILE;
@@ -681,22 +690,7 @@ int adc_search_device(aq_codes* codes, aq_codebook* cb, const double* Qd,
 #undef AQ_SCORE_LAUNCH
     AQ_LAUNCHED(s);
     timer_mark(s, AQ_T_ADC_SCORE);
-    // merge window: N plus room for near-threshold ties, a power of two
-    int mcap = kMergeCapMin;
-    while (mcap < N + N / 2 + 1024 && mcap < kMergeCapMax) mcap <<= 1;
-    MergeArgs ma{obuf, ocnt, oflag, (int)R, cap, N, (int)topn_eff, mcap, lut64,
-                 codes->data, (int)codes->stride, codes->bits, M, k, ids, scores};
-    const size_t msmem = (size_t)mcap * (2 * sizeof(double) + sizeof(uint32_t));
-    AQ_CUDA(cudaFuncSetAttribute(k_adc_merge, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)msmem));
-    timer_mark(s, AQ_T_ADC_MERGE);
-    // many windows per query (small batches): more warps walk them at once
-    k_adc_merge<<<(unsigned)nq, R >= 32 ? 1024 : 256, msmem, s->stream>>>(ma);
-    AQ_LAUNCHED(s);
-    timer_mark(s, AQ_T_ADC_MERGE);
-    AQ_CUDA(cudaMemcpyAsync(hflag.data(), oflag, nq * sizeof(int), cudaMemcpyDeviceToHost,
-                            s->stream));
-    AQ_CUDA(cudaStreamSynchronize(s->stream));
+    AQ_TRY(merge(obuf, ocnt, oflag, R, cap));
     }  // scalar filter
   }
   // exact fallback for flagged queries

@@ -130,6 +130,10 @@ def test_c4_all_codes_top100(R):
     dcb = s.upload_codebook(aq.ProductCodebook(M, 16, 2, w.codebook))
     Q = w.queries.astype(np.float64)
     ids, sc = aq.dev_adc_search(dc, dcb, Q, topn)
+    # 384 queries (3 blocks of 128, 2e6 points per SM slice) take the
+    # tensor-core filter (csrc/adc_tc.cu); its first 8 rows are Q's
+    extra = wl._normalize_rows(np.random.default_rng(44).standard_normal((376, 2 * M)))
+    ids_tc, sc_tc = aq.dev_adc_search(dc, dcb, np.concatenate([Q, extra]), topn)
     dc.free()
     cand_i, cand_s = [], []
     step = 10_000_000
@@ -144,6 +148,8 @@ def test_c4_all_codes_top100(R):
         order = np.lexsort((ci[q], -cs[q]))[:topn]  # score desc, index asc
         assert np.array_equal(ids[q].astype(np.int64), ci[q][order]), q
         assert np.array_equal(sc[q], cs[q][order]), q
+        assert np.array_equal(ids_tc[q].astype(np.int64), ci[q][order]), q
+        assert np.array_equal(sc_tc[q], cs[q][order]), q
 
 
 def test_c5_shape_train(R):

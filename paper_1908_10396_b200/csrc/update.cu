@@ -926,19 +926,25 @@ __global__ void __launch_bounds__(kPanelThreads) k_llt_panel(double* A, int n, i
     const int nrows = bs + nr;
     double* row = r < bs ? D[r] : R[min(r - bs, kPanelRows - 1)];
     const int jend = r < bs ? r + 1 : bs;  // diagonal rows stop at the diagonal
+    // the square root of column c + 1 is taken by the thread that gives its
+    // diagonal entry the last subtraction (column c's update), while the
+    // other rows still update: two barriers per column
+    auto pivot = [&](int c) {
+      const double sv = D[c][c];
+      if (sv <= 0.0) atomicExch(fail, 1);
+      D[c][c] = __dsqrt_rn(sv);
+    };
+    if (t == 0 && bs > 0) pivot(0);
+    __syncthreads();
     for (int c = 0; c < bs; ++c) {
-      if (r == c && q == 0) {
-        const double sv = D[c][c];
-        if (sv <= 0.0) atomicExch(fail, 1);
-        D[c][c] = __dsqrt_rn(sv);
-      }
-      __syncthreads();
       if (r > c && r < nrows && q == 0) row[c] = __ddiv_rn(row[c], D[c][c]);
       __syncthreads();
       if (r > c && r < nrows) panel_axpy<2>(row, D, c, row[c], c + 1 + ((q - c - 1) & 1), jend);
+      if (r == c + 1 && r < bs && q == (r & 1)) pivot(r);
       __syncthreads();
     }
   }
+
   if (blockIdx.x == 0)
     for (int e = t; e < bs * bs; e += blockDim.x) {
       const int r = e / bs, c = e % bs;
@@ -952,11 +958,16 @@ __global__ void __launch_bounds__(kPanelThreads) k_llt_panel(double* A, int n, i
 
 // Trailing update of the lower triangle: L[i][c] -= sum_{q in block} L[i][q] L[c][q]
 // (sum sequential in q from 0.0, then one subtraction). 64 x 64 tiles.
+// The panel slices are staged transposed with a row stride of 65 doubles:
+// a warp's transposed stores (one row, 32 consecutive q) then fall in 16
+// distinct bank pairs instead of one, and a full block (bs = 64) indexes by
+// shifts instead of integer division.
+constexpr int kTrailStride = kLLT + 1;
 __global__ void __launch_bounds__(256) k_llt_trail(double* A, int n, int kb) {
   extern __shared__ __align__(16) double tsm[];
   // transposed panel slices: Pi[q][r] = L(i0 + r, kb + q), Pc[q][r] = L(c0 + r, kb + q)
-  double(*Pi)[64] = reinterpret_cast<double(*)[64]>(tsm);
-  double(*Pc)[64] = reinterpret_cast<double(*)[64]>(tsm + 64 * 64);
+  double(*Pi)[kTrailStride] = reinterpret_cast<double(*)[kTrailStride]>(tsm);
+  double(*Pc)[kTrailStride] = reinterpret_cast<double(*)[kTrailStride]>(tsm + 64 * kTrailStride);
   const int be = min(kb + kLLT, n), bs = be - kb;
   // triangular tile index -> (ti, tc), tc <= ti
   const int tile = blockIdx.x;
@@ -965,20 +976,21 @@ __global__ void __launch_bounds__(256) k_llt_trail(double* A, int n, int kb) {
   while (ti * (ti + 1) / 2 > tile) --ti;
   const int tc = tile - ti * (ti + 1) / 2;
   const int i0 = be + ti * 64, c0 = be + tc * 64;
-  stage8(
-      64 * bs,
-      [&](int e) {
-        const int r = e / bs, q = e % bs;
-        return i0 + r < n ? A[(size_t)(i0 + r) * n + kb + q] : 0.0;
-      },
-      [&](int e, double v) { Pi[e % bs][e / bs] = v; });
-  stage8(
-      64 * bs,
-      [&](int e) {
-        const int r = e / bs, q = e % bs;
-        return c0 + r < n ? A[(size_t)(c0 + r) * n + kb + q] : 0.0;
-      },
-      [&](int e, double v) { Pc[e % bs][e / bs] = v; });
+  const bool full = bs == kLLT;
+  auto stage = [&](int r0, double(*P)[kTrailStride]) {
+    stage8(
+        64 * bs,
+        [&](int e) {
+          const int r = full ? e >> 6 : e / bs, q = full ? e & 63 : e % bs;
+          return r0 + r < n ? A[(size_t)(r0 + r) * n + kb + q] : 0.0;
+        },
+        [&](int e, double v) {
+          const int r = full ? e >> 6 : e / bs, q = full ? e & 63 : e % bs;
+          P[q][r] = v;
+        });
+  };
+  stage(i0, Pi);
+  stage(c0, Pc);
   __syncthreads();
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   double s[4][4];
@@ -987,11 +999,12 @@ __global__ void __launch_bounds__(256) k_llt_trail(double* A, int n, int kb) {
 #pragma unroll
     for (int v = 0; v < 4; ++v) s[u][v] = 0.0;
   for (int q = 0; q < bs; ++q) {
-    const double2 a0 = *reinterpret_cast<const double2*>(&Pi[q][ty * 4]);
-    const double2 a1 = *reinterpret_cast<const double2*>(&Pi[q][ty * 4 + 2]);
-    const double2 b0 = *reinterpret_cast<const double2*>(&Pc[q][tx * 4]);
-    const double2 b1 = *reinterpret_cast<const double2*>(&Pc[q][tx * 4 + 2]);
-    const double pi[4] = {a0.x, a0.y, a1.x, a1.y}, pc[4] = {b0.x, b0.y, b1.x, b1.y};
+    double pi[4], pc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      pi[u] = Pi[q][ty * 4 + u];
+      pc[u] = Pc[q][tx * 4 + u];
+    }
 #pragma unroll
     for (int u = 0; u < 4; ++u)
 #pragma unroll
@@ -1269,7 +1282,7 @@ int llt_solve_device(aq_session* s, double* A, int n, double* x) {
     AQ_LAUNCHED(s);
     if (below > 0) {
       const int T = (below + 63) / 64;
-      const int tsmem = 2 * 64 * 64 * (int)sizeof(double);
+      const int tsmem = 2 * 64 * kTrailStride * (int)sizeof(double);
       AQ_CUDA(cudaFuncSetAttribute(k_llt_trail, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    tsmem));
       k_llt_trail<<<T * (T + 1) / 2, 256, tsmem, s->stream>>>(A, n, kb);

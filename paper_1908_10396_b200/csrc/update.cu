@@ -431,8 +431,11 @@ __global__ void __launch_bounds__(32) k_assemble(const AsmArgs a) {
 //     signed zero, and adding a signed zero never changes an accumulator
 //     (accumulators start at +0 and are never -0), so the result is the same.
 // Units (strip x column chunk) run largest strip first (`order`).
+template <int SLIDE>
 __global__ void __launch_bounds__(32) k_assemble_sd2(const AsmArgs a, const uint32_t* order) {
-  extern __shared__ __align__(16) double acc[];  // [(aa*16 + j2)*2 + b][32]
+  // [aa*16 + j2][lane] of {b = 0, b = 1}: a point's 2x2 block is two 16-byte
+  // accesses per lane (LDS.128 / STS.128)
+  extern __shared__ __align__(16) double2 acc2[];
   __shared__ __align__(16) double2 s_u[32];      // coef * x_m
   __shared__ __align__(16) double2 s_r[32];      // h_par * x_m (rhs)
   __shared__ double s_ho[32];
@@ -461,7 +464,7 @@ __global__ void __launch_bounds__(32) k_assemble_sd2(const AsmArgs a, const uint
 #pragma unroll 4
       for (int e = 0; e < 64; ++e) {
         const int aa = e >> 5, j2 = (e >> 1) & 15, b = e & 1;
-        acc[e * 32 + lane] =
+        reinterpret_cast<double*>(acc2)[((e >> 1) * 32 + lane) * 2 + b] =
             a.A[((size_t)(m * 16 + j) * 2 + aa) * dim + (size_t)(m2 * 16 + j2) * 2 + b];
       }
     }
@@ -471,7 +474,7 @@ __global__ void __launch_bounds__(32) k_assemble_sd2(const AsmArgs a, const uint
     }
   } else {
 #pragma unroll
-    for (int e = 0; e < 64; ++e) acc[e * 32 + lane] = 0.0;
+    for (int e = 0; e < 32; ++e) acc2[e * 32 + lane] = make_double2(0.0, 0.0);
   }
   const uint32_t* L = Lall + t_lo;
   const size_t cnt = t_hi - t_lo;
@@ -548,8 +551,11 @@ __global__ void __launch_bounds__(32) k_assemble_sd2(const AsmArgs a, const uint
       asm volatile("cp.async.wait_group 0;\n" ::);
     }
     __syncwarp();
-    if (do_rhs)
-      for (int b = 0; b < nb; ++b) {  // rhs += h_par * x (pq.hpp:326)
+    // rhs += h_par * x (pq.hpp:326): a separate chain on lane 0 of chunk 0,
+    // interleaved with the point loop under SLIDE (lane 0 of chunk 0 is
+    // always `mine`)
+    if (do_rhs && !SLIDE)
+      for (int b = 0; b < nb; ++b) {
         const double2 r = s_r[b];
         r0 = __dadd_rn(r0, r.x);
         r1 = __dadd_rn(r1, r.y);
@@ -558,60 +564,100 @@ __global__ void __launch_bounds__(32) k_assemble_sd2(const AsmArgs a, const uint
       const int wsel = lane >> 3, sh = 4 * (lane & 7);
       // One point: h_perp on the diagonal first (pq.hpp:324-325; j2 == j
       // there), then the coupling products (pq.hpp:329-338).
-      auto upd = [&](int b, double& e00, double& e01, double& e10, double& e11) {
+      auto upd = [&](int b, double2& A0, double2& A1) {
         const double2 u = s_u[b];
         const float2 xc = *reinterpret_cast<const float2*>(&s_x[buf][b][lane * 2]);
         const double v0 = (double)xc.x, v1 = (double)xc.y;
         if (diag) {
           const double hop = s_ho[b];
-          e00 = __dadd_rn(e00, hop);
-          e11 = __dadd_rn(e11, hop);
+          A0.x = __dadd_rn(A0.x, hop);
+          A1.y = __dadd_rn(A1.y, hop);
         }
-        e00 = __dadd_rn(e00, __dmul_rn(u.x, v0));
-        e01 = __dadd_rn(e01, __dmul_rn(u.x, v1));
-        e10 = __dadd_rn(e10, __dmul_rn(u.y, v0));
-        e11 = __dadd_rn(e11, __dmul_rn(u.y, v1));
+        A0.x = __dadd_rn(A0.x, __dmul_rn(u.x, v0));
+        A0.y = __dadd_rn(A0.y, __dmul_rn(u.x, v1));
+        A1.x = __dadd_rn(A1.x, __dmul_rn(u.y, v0));
+        A1.y = __dadd_rn(A1.y, __dmul_rn(u.y, v1));
       };
-      // Points in pairs: both slots are loaded before either is stored; when
-      // the pair shares a slot the second update continues from the first's
-      // result, and the second store (program order) leaves the chained value.
-      int b = 0;
-      for (; b + 1 < nb; b += 2) {
-        const unsigned ja = (s_cw[buf][b][wsel] >> sh) & 15u;
-        const unsigned jb = (s_cw[buf][b + 1][wsel] >> sh) & 15u;
-        double* pa0 = acc + (size_t)(ja * 2) * 32 + lane;
-        double* pa1 = acc + (size_t)((16 + ja) * 2) * 32 + lane;
-        double* pb0 = acc + (size_t)(jb * 2) * 32 + lane;
-        double* pb1 = acc + (size_t)((16 + jb) * 2) * 32 + lane;
-        double a00 = pa0[0], a01 = pa0[32], a10 = pa1[0], a11 = pa1[32];
-        double b00 = pb0[0], b01 = pb0[32], b10 = pb1[0], b11 = pb1[32];
-        upd(b, a00, a01, a10, a11);
-        if (ja == jb) {
-          b00 = a00;
-          b01 = a01;
-          b10 = a10;
-          b11 = a11;
+      auto slot = [&](int b) { return (s_cw[buf][b][wsel] >> sh) & 15u; };
+      if (SLIDE) {
+        // Sliding forward: point b + 1's slot is loaded before point b's
+        // store; when the two points share a slot, point b's result is
+        // forwarded instead (that load predates the store). Every entry still
+        // receives the strip's additions in point order, and the
+        // load -> add -> store round trip through shared memory leaves the
+        // per-point dependency chain (which is then two float64 adds).
+        // Everything point b + 1 reads (slot, accumulators, u, x, h_perp) is
+        // loaded in iteration b, ahead of iteration b's stores in program
+        // order, so no load waits behind a store.
+        const int last = nb - 1;
+        unsigned jc = slot(0), jn = slot(min(1, last));
+        double2 C0 = acc2[jc * 32 + lane], C1 = acc2[(16 + jc) * 32 + lane];
+        double2 uc = s_u[0];
+        float2 xc = *reinterpret_cast<const float2*>(&s_x[buf][0][lane * 2]);
+        double hc = diag ? s_ho[0] : 0.0;
+        double2 rc = do_rhs ? s_r[0] : make_double2(0.0, 0.0);
+#pragma unroll 2
+        for (int b = 0; b < nb; ++b) {
+          const int bn = min(b + 1, last);
+          const double2 N0 = acc2[jn * 32 + lane], N1 = acc2[(16 + jn) * 32 + lane];
+          const unsigned jnn = slot(min(b + 2, last));
+          const double2 un = s_u[bn];
+          const float2 xn = *reinterpret_cast<const float2*>(&s_x[buf][bn][lane * 2]);
+          const double hn = diag ? s_ho[bn] : 0.0;
+          const double2 rn = do_rhs ? s_r[bn] : make_double2(0.0, 0.0);
+          if (do_rhs) {
+            r0 = __dadd_rn(r0, rc.x);
+            r1 = __dadd_rn(r1, rc.y);
+          }
+          const double v0 = (double)xc.x, v1 = (double)xc.y;
+          if (diag) {
+            C0.x = __dadd_rn(C0.x, hc);
+            C1.y = __dadd_rn(C1.y, hc);
+          }
+          C0.x = __dadd_rn(C0.x, __dmul_rn(uc.x, v0));
+          C0.y = __dadd_rn(C0.y, __dmul_rn(uc.x, v1));
+          C1.x = __dadd_rn(C1.x, __dmul_rn(uc.y, v0));
+          C1.y = __dadd_rn(C1.y, __dmul_rn(uc.y, v1));
+          acc2[jc * 32 + lane] = C0;
+          acc2[(16 + jc) * 32 + lane] = C1;
+          if (jn != jc) {
+            C0 = N0;
+            C1 = N1;
+          }
+          jc = jn;
+          jn = jnn;
+          uc = un;
+          xc = xn;
+          hc = hn;
+          rc = rn;
         }
-        upd(b + 1, b00, b01, b10, b11);
-        pa0[0] = a00;
-        pa0[32] = a01;
-        pa1[0] = a10;
-        pa1[32] = a11;
-        pb0[0] = b00;
-        pb0[32] = b01;
-        pb1[0] = b10;
-        pb1[32] = b11;
-      }
-      if (b < nb) {
-        const unsigned ja = (s_cw[buf][b][wsel] >> sh) & 15u;
-        double* pa0 = acc + (size_t)(ja * 2) * 32 + lane;
-        double* pa1 = acc + (size_t)((16 + ja) * 2) * 32 + lane;
-        double a00 = pa0[0], a01 = pa0[32], a10 = pa1[0], a11 = pa1[32];
-        upd(b, a00, a01, a10, a11);
-        pa0[0] = a00;
-        pa0[32] = a01;
-        pa1[0] = a10;
-        pa1[32] = a11;
+      } else {
+        // Points in pairs: both slots are loaded before either is stored; when
+        // the pair shares a slot the second update continues from the first's
+        // result, and the second store (program order) leaves the chained value.
+        int b = 0;
+        for (; b + 1 < nb; b += 2) {
+          const unsigned ja = slot(b), jb = slot(b + 1);
+          double2 A0 = acc2[ja * 32 + lane], A1 = acc2[(16 + ja) * 32 + lane];
+          double2 B0 = acc2[jb * 32 + lane], B1 = acc2[(16 + jb) * 32 + lane];
+          upd(b, A0, A1);
+          if (ja == jb) {
+            B0 = A0;
+            B1 = A1;
+          }
+          upd(b + 1, B0, B1);
+          acc2[ja * 32 + lane] = A0;
+          acc2[(16 + ja) * 32 + lane] = A1;
+          acc2[jb * 32 + lane] = B0;
+          acc2[(16 + jb) * 32 + lane] = B1;
+        }
+        if (b < nb) {
+          const unsigned ja = slot(b);
+          double2 A0 = acc2[ja * 32 + lane], A1 = acc2[(16 + ja) * 32 + lane];
+          upd(b, A0, A1);
+          acc2[ja * 32 + lane] = A0;
+          acc2[(16 + ja) * 32 + lane] = A1;
+        }
       }
     }
     __syncwarp();
@@ -623,7 +669,7 @@ __global__ void __launch_bounds__(32) k_assemble_sd2(const AsmArgs a, const uint
     for (int e = 0; e < 64; ++e) {
       const int aa = e >> 5, j2 = (e >> 1) & 15, b = e & 1;
       a.A[((size_t)(m * 16 + j) * 2 + aa) * dim + (size_t)(m2 * 16 + j2) * 2 + b] =
-          acc[(size_t)e * 32 + lane];
+          reinterpret_cast<const double*>(acc2)[((e >> 1) * 32 + lane) * 2 + b];
     }
   }
   if (do_rhs) {
@@ -1506,7 +1552,12 @@ int assemble_device(aq_dataset* ds, aq_codes* codes, const PointW& pw, const Buc
     // ms per 3 iterations), else the staged kernel (config 2: 138 vs 200 ms)
     static const int asm_variant =
         getenv("AQ_ASM_VARIANT") ? atoi(getenv("AQ_ASM_VARIANT")) : 0;
-    AQ_CUDA(cudaFuncSetAttribute(k_assemble_sd2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    // AQ_ASM_SLIDE=0: the staged kernel's paired read-modify-write loop
+    // instead of the sliding forward (same per-entry order)
+    static const int asm_slide = getenv("AQ_ASM_SLIDE") ? atoi(getenv("AQ_ASM_SLIDE")) : 1;
+    AQ_CUDA(cudaFuncSetAttribute(k_assemble_sd2<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 64 * 32 * 8 + 14 * 1024));
+    AQ_CUDA(cudaFuncSetAttribute(k_assemble_sd2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  64 * 32 * 8 + 14 * 1024));
     AQ_CUDA(cudaFuncSetAttribute(k_assemble_sd2r<16>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 32 * 8));
@@ -1547,8 +1598,10 @@ int assemble_device(aq_dataset* ds, aq_codes* codes, const PointW& pw, const Buc
       // pipe with fewer warps (config 2: 14.7 -> 14.2 ms; 5 per SM 14.4,
       // 3 per SM 17.6)
       const int pad = ord.size() <= (size_t)9 * s->num_sms ? 14 * 1024 : 0;
-      if (!ring)
-        k_assemble_sd2<<<(unsigned)ord.size(), 32, 64 * 32 * 8 + pad, s->stream>>>(a, dord);
+      if (!ring && asm_slide)
+        k_assemble_sd2<1><<<(unsigned)ord.size(), 32, 64 * 32 * 8 + pad, s->stream>>>(a, dord);
+      else if (!ring)
+        k_assemble_sd2<0><<<(unsigned)ord.size(), 32, 64 * 32 * 8 + pad, s->stream>>>(a, dord);
       else
         k_assemble_sd2r<16><<<(unsigned)ord.size(), 32, 64 * 32 * 8, s->stream>>>(a, dord);
       AQ_LAUNCHED(s);

@@ -1,6 +1,7 @@
 """GPU parity for both sd = 2 assembly kernels (the staged k_assemble_sd2 and
-the register-ring k_assemble_sd2r). The default picks one by launch size, so
-each is forced here through AQ_ASM_VARIANT in a child process (the variable
+the register-ring k_assemble_sd2r; the staged kernel's sliding-forward and
+paired loops). The default picks one by launch size, so each is forced here
+through AQ_ASM_VARIANT / AQ_ASM_SLIDE in a child process (the variable
 is read once per process), including a shape with several point blocks
 (resumed accumulators) with a partial column chunk (d = 100, M = 50)."""
 import os
@@ -19,9 +20,13 @@ from paper_1908_10396_b200 import anisoq as aq
 from tests.helpers import mixture_rows, threshold_hp_ho
 P = Port()
 # (130000, 100, 50): two point blocks of 125,829 rows (48 MB of float32)
-for n, d, M in ((6000, 32, 16), (130000, 100, 50)):
+# (9000, 32, 16) with codes in {0, 1} (every other subspace constant): runs of
+# one slot, where the sliding loop forwards point b's result to point b + 1
+for n, d, M, kk in ((6000, 32, 16, 16), (130000, 100, 50, 16), (9000, 32, 16, 2)):
     x = mixture_rows(n, d, 61)
-    codes = np.random.default_rng(62).integers(0, 16, (n, M)).astype(np.uint32)
+    codes = np.random.default_rng(62).integers(0, kk, (n, M)).astype(np.uint32)
+    if kk == 2:
+        codes[:, ::2] = 7
     hp, ho = threshold_hp_ho(x, 0.2)
     A, r = aq.assemble_selector_system(x, aq.CodeMatrix(n, M, 16, codes), (hp, ho), M, 16)
     A2, r2 = P.assemble_selector_system(x.astype(np.float64), codes, hp, ho, M, 16)
@@ -31,9 +36,11 @@ print("ok")
 """
 
 
-@pytest.mark.parametrize("variant", ["1", "3"])
+# "1:0": the staged kernel with its paired loop instead of the sliding forward
+@pytest.mark.parametrize("variant", ["1", "1:0", "3"])
 def test_assembly_variant_matches_oracle(variant):
-    env = dict(os.environ, AQ_ASM_VARIANT=variant, PYTHONPATH=ROOT)
+    v, _, slide = variant.partition(":")
+    env = dict(os.environ, AQ_ASM_VARIANT=v, AQ_ASM_SLIDE=slide or "1", PYTHONPATH=ROOT)
     r = subprocess.run([sys.executable, "-c", CHILD], cwd=ROOT, env=env, capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr

@@ -50,7 +50,11 @@ void parallel_rows(size_t rows, size_t nt, F f) {
 //   compute  tiles and encodes chunk i - 1, then its packed codes (M/2 bytes
 //            per row, 8x fewer than uint32) go D2H on a third stream.
 // Buffers (page-locked, device rows, tiled datasets, packed codes) are a ring
-// of three, allocated once per call. Points are independent
+// of three, allocated once per call. Page-locked caller buffers skip the host
+// side: rows go H2D straight from `x`, and the codes are widened to uint32 on
+// the device and go D2H straight into `codes_out` (the copy engines then
+// carry both directions at once and no host thread touches the data).
+// Points are independent
 // (pq.hpp:581-612), so the codes equal the single-shot call's; device errors
 // carry global point indices and are checked once at the end.
 int pq_quantize_streamed(aq_session* s, const float* x, size_t n, size_t d, aq_codebook* cb,
@@ -60,11 +64,20 @@ int pq_quantize_streamed(aq_session* s, const float* x, size_t n, size_t d, aq_c
   const int bits = cb->k <= 16 ? 4 : 8;
   const size_t stride = code_stride(M, bits);
   const size_t nt = std::max(1u, std::thread::hardware_concurrency());
-  void* hin[NB];
-  void* hout[NB];
+  auto page_locked = [](const void* p) {
+    cudaPointerAttributes at;
+    const bool pl = cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeHost;
+    cudaGetLastError();  // a pageable pointer may leave an error behind on older drivers
+    return pl;
+  };
+  const bool pin_in = page_locked(x) && page_locked(x + n * d - 1);
+  const bool pin_out = page_locked(codes_out) && page_locked(codes_out + n * M - 1);
+  void* hin[NB] = {};
+  void* hout[NB] = {};
+  uint32_t* du[NB] = {};  // device uint32 codes (page-locked codes_out only)
   for (int b = 0; b < NB; ++b) {
-    AQ_TRY(pinned_buffer(s, b, chunk * d * sizeof(float), &hin[b]));
-    AQ_TRY(pinned_buffer(s, NB + b, chunk * stride, &hout[b]));
+    if (!pin_in) AQ_TRY(pinned_buffer(s, b, chunk * d * sizeof(float), &hin[b]));
+    if (!pin_out) AQ_TRY(pinned_buffer(s, NB + b, chunk * stride, &hout[b]));
   }
   cudaStream_t up = nullptr, down = nullptr;
   float* dx[NB] = {};
@@ -84,7 +97,8 @@ int pq_quantize_streamed(aq_session* s, const float* x, size_t n, size_t d, aq_c
         cudaMemset(ds[b].xt + tiled_floats(chunk, d), 0, 256 * sizeof(float)) != cudaSuccess ||
         cudaEventCreateWithFlags(&ev_up[b], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ev_enc[b], cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ev_down[b], cudaEventDisableTiming) != cudaSuccess)
+        cudaEventCreateWithFlags(&ev_down[b], cudaEventDisableTiming) != cudaSuccess ||
+        (pin_out && cudaMalloc(&du[b], chunk * M * sizeof(uint32_t)) != cudaSuccess))
       st = ref_error(AQ_E_CUDA, "out of device memory for the streamed encode");
     if (st == AQ_OK) st = aq_codes_alloc(s, chunk, M, cb->k, &cc[b]);
   }
@@ -130,7 +144,7 @@ int pq_quantize_streamed(aq_session* s, const float* x, size_t n, size_t d, aq_c
   };
   for (size_t i = 0; i < nch + 2 && st == AQ_OK; ++i) {
     std::thread unpacker;
-    if (i >= 2) {  // chunk i - 2's codes, concurrently with chunk i's copy-in
+    if (i >= 2 && !pin_out) {  // chunk i - 2's codes, concurrently with chunk i's copy-in
       const size_t k = i - 2;
       if (cudaEventSynchronize(ev_down[k % NB]) != cudaSuccess) {
         st = ref_error(AQ_E_CUDA, "streamed encode failed");
@@ -141,14 +155,17 @@ int pq_quantize_streamed(aq_session* s, const float* x, size_t n, size_t d, aq_c
     if (i < nch) {  // chunk i: host staging, then H2D on `up`
       const int b = (int)(i % NB);
       const size_t cn = rows_of(i);
-      if (i >= NB) cudaEventSynchronize(ev_up[b]);  // staging slot b is free again
       const float* src = x + i * chunk * d;
-      float* dst = static_cast<float*>(hin[b]);
-      parallel_rows(cn, std::max<size_t>(1, i >= 2 ? nt / 2 : nt), [&](size_t r0, size_t r1) {
-        std::memcpy(dst + r0 * d, src + r0 * d, (r1 - r0) * d * sizeof(float));
-      });
+      if (!pin_in) {
+        if (i >= NB) cudaEventSynchronize(ev_up[b]);  // staging slot b is free again
+        float* dst = static_cast<float*>(hin[b]);
+        parallel_rows(cn, std::max<size_t>(1, i >= 2 ? nt / 2 : nt), [&](size_t r0, size_t r1) {
+          std::memcpy(dst + r0 * d, src + r0 * d, (r1 - r0) * d * sizeof(float));
+        });
+      }
       if (i >= NB) cudaStreamWaitEvent(up, ev_enc[b], 0);  // dx[b] read by chunk i - 3
-      if (cudaMemcpyAsync(dx[b], hin[b], cn * d * sizeof(float), cudaMemcpyHostToDevice, up) !=
+      if (cudaMemcpyAsync(dx[b], pin_in ? src : hin[b], cn * d * sizeof(float),
+                          cudaMemcpyHostToDevice, up) !=
               cudaSuccess ||
           cudaEventRecord(ev_up[b], up) != cudaSuccess)
         st = ref_error(AQ_E_CUDA, "streamed encode upload failed");
@@ -164,10 +181,14 @@ int pq_quantize_streamed(aq_session* s, const float* x, size_t n, size_t d, aq_c
       cc[b]->n = cn;
       st = tile_rows_async(dx[b], cn, d, ds[b].xt, ds[b].norms, s->stream);
       if (st == AQ_OK) st = run_encode_chunk(&ds[b], cb, w, cc[b], passes, j * chunk);
+      if (st == AQ_OK && pin_out) st = codes_unpack_async(cc[b], du[b]);
       if (st == AQ_OK && (cudaEventRecord(ev_enc[b], s->stream) != cudaSuccess ||
                           cudaStreamWaitEvent(down, ev_enc[b], 0) != cudaSuccess ||
-                          cudaMemcpyAsync(hout[b], cc[b]->data, cn * stride,
-                                          cudaMemcpyDeviceToHost, down) != cudaSuccess ||
+                          (pin_out ? cudaMemcpyAsync(codes_out + j * chunk * M, du[b],
+                                                     cn * M * sizeof(uint32_t),
+                                                     cudaMemcpyDeviceToHost, down)
+                                   : cudaMemcpyAsync(hout[b], cc[b]->data, cn * stride,
+                                                     cudaMemcpyDeviceToHost, down)) != cudaSuccess ||
                           cudaEventRecord(ev_down[b], down) != cudaSuccess))
         st = ref_error(AQ_E_CUDA, "streamed encode download failed");
     }
@@ -183,6 +204,7 @@ int pq_quantize_streamed(aq_session* s, const float* x, size_t n, size_t d, aq_c
       aq_codes_free(cc[b]);
     }
     cudaFree(dx[b]);
+    cudaFree(du[b]);
     cudaFree(ds[b].xt);
     cudaFree(ds[b].norms);
     ds[b].xt = nullptr;

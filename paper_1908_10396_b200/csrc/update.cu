@@ -431,7 +431,6 @@ __global__ void __launch_bounds__(32) k_assemble(const AsmArgs a) {
 //     signed zero, and adding a signed zero never changes an accumulator
 //     (accumulators start at +0 and are never -0), so the result is the same.
 // Units (strip x column chunk) run largest strip first (`order`).
-template <int SLIDE>
 __global__ void __launch_bounds__(32) k_assemble_sd2(const AsmArgs a, const uint32_t* order) {
   // [aa*16 + j2][lane] of {b = 0, b = 1}: a point's 2x2 block is two 16-byte
   // accesses per lane (LDS.128 / STS.128)
@@ -551,10 +550,7 @@ __global__ void __launch_bounds__(32) k_assemble_sd2(const AsmArgs a, const uint
       asm volatile("cp.async.wait_group 0;\n" ::);
     }
     __syncwarp();
-    // rhs += h_par * x (pq.hpp:326): a separate chain on lane 0 of chunk 0,
-    // interleaved with the point loop under SLIDE (lane 0 of chunk 0 is
-    // always `mine`)
-    if (do_rhs && !SLIDE)
+    if (do_rhs)  // rhs += h_par * x (pq.hpp:326)
       for (int b = 0; b < nb; ++b) {
         const double2 r = s_r[b];
         r0 = __dadd_rn(r0, r.x);
@@ -579,85 +575,31 @@ __global__ void __launch_bounds__(32) k_assemble_sd2(const AsmArgs a, const uint
         A1.y = __dadd_rn(A1.y, __dmul_rn(u.y, v1));
       };
       auto slot = [&](int b) { return (s_cw[buf][b][wsel] >> sh) & 15u; };
-      if (SLIDE) {
-        // Sliding forward: point b + 1's slot is loaded before point b's
-        // store; when the two points share a slot, point b's result is
-        // forwarded instead (that load predates the store). Every entry still
-        // receives the strip's additions in point order, and the
-        // load -> add -> store round trip through shared memory leaves the
-        // per-point dependency chain (which is then two float64 adds).
-        // Everything point b + 1 reads (slot, accumulators, u, x, h_perp) is
-        // loaded in iteration b, ahead of iteration b's stores in program
-        // order, so no load waits behind a store.
-        const int last = nb - 1;
-        unsigned jc = slot(0), jn = slot(min(1, last));
-        double2 C0 = acc2[jc * 32 + lane], C1 = acc2[(16 + jc) * 32 + lane];
-        double2 uc = s_u[0];
-        float2 xc = *reinterpret_cast<const float2*>(&s_x[buf][0][lane * 2]);
-        double hc = diag ? s_ho[0] : 0.0;
-        double2 rc = do_rhs ? s_r[0] : make_double2(0.0, 0.0);
-#pragma unroll 2
-        for (int b = 0; b < nb; ++b) {
-          const int bn = min(b + 1, last);
-          const double2 N0 = acc2[jn * 32 + lane], N1 = acc2[(16 + jn) * 32 + lane];
-          const unsigned jnn = slot(min(b + 2, last));
-          const double2 un = s_u[bn];
-          const float2 xn = *reinterpret_cast<const float2*>(&s_x[buf][bn][lane * 2]);
-          const double hn = diag ? s_ho[bn] : 0.0;
-          const double2 rn = do_rhs ? s_r[bn] : make_double2(0.0, 0.0);
-          if (do_rhs) {
-            r0 = __dadd_rn(r0, rc.x);
-            r1 = __dadd_rn(r1, rc.y);
-          }
-          const double v0 = (double)xc.x, v1 = (double)xc.y;
-          if (diag) {
-            C0.x = __dadd_rn(C0.x, hc);
-            C1.y = __dadd_rn(C1.y, hc);
-          }
-          C0.x = __dadd_rn(C0.x, __dmul_rn(uc.x, v0));
-          C0.y = __dadd_rn(C0.y, __dmul_rn(uc.x, v1));
-          C1.x = __dadd_rn(C1.x, __dmul_rn(uc.y, v0));
-          C1.y = __dadd_rn(C1.y, __dmul_rn(uc.y, v1));
-          acc2[jc * 32 + lane] = C0;
-          acc2[(16 + jc) * 32 + lane] = C1;
-          if (jn != jc) {
-            C0 = N0;
-            C1 = N1;
-          }
-          jc = jn;
-          jn = jnn;
-          uc = un;
-          xc = xn;
-          hc = hn;
-          rc = rn;
+      // Points in pairs: both slots are loaded before either is stored; when
+      // the pair shares a slot the second update continues from the first's
+      // result, and the second store (program order) leaves the chained value.
+      int b = 0;
+      for (; b + 1 < nb; b += 2) {
+        const unsigned ja = slot(b), jb = slot(b + 1);
+        double2 A0 = acc2[ja * 32 + lane], A1 = acc2[(16 + ja) * 32 + lane];
+        double2 B0 = acc2[jb * 32 + lane], B1 = acc2[(16 + jb) * 32 + lane];
+        upd(b, A0, A1);
+        if (ja == jb) {
+          B0 = A0;
+          B1 = A1;
         }
-      } else {
-        // Points in pairs: both slots are loaded before either is stored; when
-        // the pair shares a slot the second update continues from the first's
-        // result, and the second store (program order) leaves the chained value.
-        int b = 0;
-        for (; b + 1 < nb; b += 2) {
-          const unsigned ja = slot(b), jb = slot(b + 1);
-          double2 A0 = acc2[ja * 32 + lane], A1 = acc2[(16 + ja) * 32 + lane];
-          double2 B0 = acc2[jb * 32 + lane], B1 = acc2[(16 + jb) * 32 + lane];
-          upd(b, A0, A1);
-          if (ja == jb) {
-            B0 = A0;
-            B1 = A1;
-          }
-          upd(b + 1, B0, B1);
-          acc2[ja * 32 + lane] = A0;
-          acc2[(16 + ja) * 32 + lane] = A1;
-          acc2[jb * 32 + lane] = B0;
-          acc2[(16 + jb) * 32 + lane] = B1;
-        }
-        if (b < nb) {
-          const unsigned ja = slot(b);
-          double2 A0 = acc2[ja * 32 + lane], A1 = acc2[(16 + ja) * 32 + lane];
-          upd(b, A0, A1);
-          acc2[ja * 32 + lane] = A0;
-          acc2[(16 + ja) * 32 + lane] = A1;
-        }
+        upd(b + 1, B0, B1);
+        acc2[ja * 32 + lane] = A0;
+        acc2[(16 + ja) * 32 + lane] = A1;
+        acc2[jb * 32 + lane] = B0;
+        acc2[(16 + jb) * 32 + lane] = B1;
+      }
+      if (b < nb) {
+        const unsigned ja = slot(b);
+        double2 A0 = acc2[ja * 32 + lane], A1 = acc2[(16 + ja) * 32 + lane];
+        upd(b, A0, A1);
+        acc2[ja * 32 + lane] = A0;
+        acc2[(16 + ja) * 32 + lane] = A1;
       }
     }
     __syncwarp();
@@ -1552,12 +1494,7 @@ int assemble_device(aq_dataset* ds, aq_codes* codes, const PointW& pw, const Buc
     // ms per 3 iterations), else the staged kernel (config 2: 138 vs 200 ms)
     static const int asm_variant =
         getenv("AQ_ASM_VARIANT") ? atoi(getenv("AQ_ASM_VARIANT")) : 0;
-    // AQ_ASM_SLIDE=0: the staged kernel's paired read-modify-write loop
-    // instead of the sliding forward (same per-entry order)
-    static const int asm_slide = getenv("AQ_ASM_SLIDE") ? atoi(getenv("AQ_ASM_SLIDE")) : 1;
-    AQ_CUDA(cudaFuncSetAttribute(k_assemble_sd2<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 64 * 32 * 8 + 14 * 1024));
-    AQ_CUDA(cudaFuncSetAttribute(k_assemble_sd2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    AQ_CUDA(cudaFuncSetAttribute(k_assemble_sd2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  64 * 32 * 8 + 14 * 1024));
     AQ_CUDA(cudaFuncSetAttribute(k_assemble_sd2r<16>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 32 * 8));
@@ -1598,10 +1535,8 @@ int assemble_device(aq_dataset* ds, aq_codes* codes, const PointW& pw, const Buc
       // pipe with fewer warps (config 2: 14.7 -> 14.2 ms; 5 per SM 14.4,
       // 3 per SM 17.6)
       const int pad = ord.size() <= (size_t)9 * s->num_sms ? 14 * 1024 : 0;
-      if (!ring && asm_slide)
-        k_assemble_sd2<1><<<(unsigned)ord.size(), 32, 64 * 32 * 8 + pad, s->stream>>>(a, dord);
-      else if (!ring)
-        k_assemble_sd2<0><<<(unsigned)ord.size(), 32, 64 * 32 * 8 + pad, s->stream>>>(a, dord);
+      if (!ring)
+        k_assemble_sd2<<<(unsigned)ord.size(), 32, 64 * 32 * 8 + pad, s->stream>>>(a, dord);
       else
         k_assemble_sd2r<16><<<(unsigned)ord.size(), 32, 64 * 32 * 8, s->stream>>>(a, dord);
       AQ_LAUNCHED(s);

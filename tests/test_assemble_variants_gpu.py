@@ -1,7 +1,6 @@
 """GPU parity for both sd = 2 assembly kernels (the staged k_assemble_sd2 and
-the register-ring k_assemble_sd2r; the staged kernel's sliding-forward and
-paired loops). The default picks one by launch size, so each is forced here
-through AQ_ASM_VARIANT / AQ_ASM_SLIDE in a child process (the variable
+the register-ring k_assemble_sd2r). The default picks one by launch size, so
+each is forced here through AQ_ASM_VARIANT in a child process (the variable
 is read once per process), including a shape with several point blocks
 (resumed accumulators) with a partial column chunk (d = 100, M = 50)."""
 import os
@@ -21,7 +20,7 @@ from tests.helpers import mixture_rows, threshold_hp_ho
 P = Port()
 # (130000, 100, 50): two point blocks of 125,829 rows (48 MB of float32)
 # (9000, 32, 16) with codes in {0, 1} (every other subspace constant): runs of
-# one slot, where the sliding loop forwards point b's result to point b + 1
+# one slot, where a pair of points shares its accumulator slot
 for n, d, M, kk in ((6000, 32, 16, 16), (130000, 100, 50, 16), (9000, 32, 16, 2)):
     x = mixture_rows(n, d, 61)
     codes = np.random.default_rng(62).integers(0, kk, (n, M)).astype(np.uint32)
@@ -36,11 +35,9 @@ print("ok")
 """
 
 
-# "1:0": the staged kernel with its paired loop instead of the sliding forward
-@pytest.mark.parametrize("variant", ["1", "1:0", "3"])
+@pytest.mark.parametrize("variant", ["1", "3"])
 def test_assembly_variant_matches_oracle(variant):
-    v, _, slide = variant.partition(":")
-    env = dict(os.environ, AQ_ASM_VARIANT=v, AQ_ASM_SLIDE=slide or "1", PYTHONPATH=ROOT)
+    env = dict(os.environ, AQ_ASM_VARIANT=variant, PYTHONPATH=ROOT)
     r = subprocess.run([sys.executable, "-c", CHILD], cwd=ROOT, env=env, capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr

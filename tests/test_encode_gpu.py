@@ -190,3 +190,37 @@ def test_quantize_streamed_uniform_weights(monkeypatch, weights, passes):
     ho = np.full(len(x), w.h_perpendicular)
     want = P.pq_quantize(x.astype(np.float64), cb.dictionaries, 8, 16, 2, hp, ho, passes)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("pin_in,pin_out", [(True, True), (True, False), (False, True)])
+def test_quantize_streamed_page_locked(monkeypatch, pin_in, pin_out):
+    # page-locked caller buffers: rows go H2D straight from the caller's memory
+    # and the codes are widened on the device and copied straight into the
+    # caller's output; codes and error reporting equal the staged path's
+    import ctypes as C
+
+    import torch
+
+    monkeypatch.setenv("AQ_STREAM_CHUNK", "3000")
+    n, d, M = 20011, 32, 16
+    x = mixture_rows(n, d, 95, centers=20)
+    cb = _cb(M, 16, 2, 96, scale=0.25)
+    xt = torch.from_numpy(x).pin_memory() if pin_in else torch.from_numpy(x.copy())
+    ot = torch.zeros((n, M), dtype=torch.int32)
+    if pin_out:
+        ot = ot.pin_memory()
+    keep: list = []
+    w = aq._weights(aq.ThresholdWeights(0.2), n, keep)
+    s = aq.Session.default()
+
+    def call(rows):
+        return aq._L.aq_pq_quantize(s.h, rows.data_ptr(), n, d, cb.dictionaries.ctypes.data,
+                                    M, 16, 2, C.byref(w), 3, ot.data_ptr())
+
+    aq._check(call(xt))
+    hp, ho = threshold_hp_ho(x, 0.2)
+    want = P.pq_quantize(x.astype(np.float64), cb.dictionaries, M, 16, 2, hp, ho, 3)
+    assert np.array_equal(ot.numpy().view(np.uint32), want)
+    xt[17777] = 0.0
+    with pytest.raises(aq.InvalidArgument, match="point 17777"):
+        aq._check(call(xt))

@@ -53,12 +53,11 @@ def main():
     n = int(float(sys.argv[2])) if len(sys.argv) > 2 else (1183514 if cfg == 2 else 10_000_000)
     variants = (sys.argv[3] if len(sys.argv) > 3 else "0,1,3").split(",")
     trained = int(sys.argv[4]) if len(sys.argv) > 4 else 0
-    for v in variants:  # "1" or "1:0" (AQ_ASM_VARIANT:AQ_ASM_SLIDE)
-        v, _, sl = v.partition(":")
-        env = dict(os.environ, AQ_ASM_VARIANT=v, AQ_ASM_SLIDE=sl or "1")
+    for v in variants:
+        env = dict(os.environ, AQ_ASM_VARIANT=v)
         r = subprocess.run([sys.executable, "-c", CHILD % {"root": ROOT, "cfg": cfg, "n": n, "trained": trained}],
                            env=env, capture_output=True, text=True, timeout=1200)
-        print(f"config {cfg} n={n} AQ_ASM_VARIANT={v} AQ_ASM_SLIDE={env['AQ_ASM_SLIDE']} rc={r.returncode}")
+        print(f"config {cfg} n={n} AQ_ASM_VARIANT={v} rc={r.returncode}")
         print(r.stdout + (r.stderr[-2000:] if r.returncode else ""), flush=True)
 
 

@@ -1,4 +1,5 @@
-"""Small end-to-end workload for compute-sanitizer (tests/test_sanitizer_gpu.py).
+"""Small end-to-end workload for compute-sanitizer (run by hand where the tool is
+open: it is closed on this GPU pool, so no test drives it).
 
 Runs every kernel family of the library once at a small shape, with the
 variant switches the parity tests pin, so that `compute-sanitizer --tool
